@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""bench.py -- the driver's benchmark contract for bandgm_b200.
+
+Workload (default, ``--workload cfg3``): BASELINE.json configs[3], the
+end-to-end learning step -- B=256 series of length n=65536, precision
+Q = L L^T with lower bandwidth k=16, tau2 = 0.01; per step one fused forward
++ reverse pass (Cholesky, solves, log-det, inverse subset, dL, d tau2).  It is
+the config whose suite is the metric's "fwd+bwd banded Chol/solve/inv-subset"
+(configs[1] is forward-only).  Metric: band-rows/s = B*n*ranks / step time.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun every rank processes its own B-matrix batch (weak scaling:
+the batch partitioner hands each GPU whole, independent matrices) and the
+per-step scalars (sum loss, sum d tau2) are all-reduced over NCCL.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (B, n, k, description)
+    "cfg3": dict(B=256, n=65536, k=16, tau2=0.01,
+                 desc="configs[3]: Gaussian log-likelihood + dL + dtau2, B=256 n=65536 k=16 fp64"),
+    "cfg3_small": dict(B=64, n=8192, k=16, tau2=0.01, desc="configs[3] shape at reduced B, n (smoke)"),
+}
+
+# Algorithmic bytes per band-row of each fused kernel:
+# forward reads L (w doubles) + y, writes Lp (w) + w-vector;
+# reverse reads L, Lp (w each) + w-vector, writes L_bar (w).
+def alg_bytes_per_row(kernel: str, k: int) -> float:
+    w = k + 1
+    if "fwd" in kernel:
+        return 8.0 * (2 * w + 2)
+    if "bwd" in kernel:
+        return 8.0 * (3 * w + 1)
+    if "mlik_seg" in kernel:
+        return 8.0 * (5 * w + 3)
+    return float("nan")
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------- inputs
+def make_inputs(B, n, k, seed, device):
+    """Config-3 inputs on the device: L diag U[1,2], off-diag
+    N(0, 0.1^2); y = L^-T z + eps, z ~ N(0,1), eps ~ N(0, 0.1^2)."""
+    import torch
+    import paper_1902_10078_b200 as bgm
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    L = bgm.Bands.empty(B, n, k, 0, tile=32, device=device)
+    L.data.normal_(0.0, 0.1, generator=g)
+    L.data[:, :, 0, :].uniform_(1.0, 2.0, generator=g)
+    for r in range(1, k + 1):
+        L.data[:, n - r:, r, :] = 0.0  # corner cells
+    if B % 32:
+        L.data.view(-1, 32)[:, :]  # padded slots stay as generated; kernels never read them
+    z = bgm.Vecs.empty(B, n, device=device)
+    z.data.normal_(0.0, 1.0, generator=g)
+    x = bgm.solve_vec(L, z, transpose_l=True)
+    eps = torch.empty_like(x.data).normal_(0.0, 0.1, generator=g)
+    y = bgm.Vecs(x.data + eps, B, n, 32)
+    return L, y
+
+
+# --------------------------------------------------------------------- cpu legs
+def cpu_run(L_ref, y_ref, tau2, which=None):
+    import oracle as orc
+
+    kind = which or ("reference" if orc.available("reference") else "restatement")
+    o = orc.Oracle(kind)
+    t0 = time.perf_counter()
+    _, _, _, st, _ = o.marginal_likelihood_grad(L_ref, y_ref, tau2)
+    dt = time.perf_counter() - t0
+    assert (st == 0).all()
+    return dt, ("reference" if kind == "reference" else "port"), o.threads()
+
+
+def host_sample(L, y, m):
+    """First m matrices in the reference layout, on the host."""
+    import numpy as np
+    import paper_1902_10078_b200 as bgm
+
+    Ls = bgm.Bands(L.data[: (m + 31) // 32].contiguous(), m, L.n, L.lower, L.upper, 32)
+    ys = bgm.Vecs(y.data[: (m + 31) // 32].contiguous(), m, y.n, 32)
+    return np.ascontiguousarray(Ls.numpy()), np.ascontiguousarray(ys.numpy())
+
+
+def sample_size(cores, B):
+    # ~0.2 s of single-core work per config-3 matrix: a few matrices per core
+    # keeps the sample near 10-30 s of CPU time and well under a minute wall.
+    return int(max(8, min(B, 4 * cores)))
+
+
+# --------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg3")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--segment-rows", type=int, default=0)
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+    B, n, k, tau2 = wl["B"], wl["n"], wl["k"], wl["tau2"]
+    metric = "band-rows/s (B*n/s) fwd+bwd banded Chol/solve/inv-subset; % of roofline"
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return reference_arm(args, wl, metric, world, rank)
+
+    import torch
+    import torch.distributed as dist
+    import paper_1902_10078_b200 as bgm
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = bgm.library()
+    if args.segment_rows:
+        bgm.set_segment_rows(args.segment_rows)
+
+    L, y = make_inputs(B, n, k, seed=1234 + 7919 * rank, device=dev)
+    loss = torch.empty(B, dtype=torch.float64, device=dev)
+    tbar = torch.empty(B, dtype=torch.float64, device=dev)
+    lbar = L.like()
+    st = bgm.api.new_status(B, dev)
+    out = (loss, lbar, tbar, st)
+    red = torch.zeros(2, dtype=torch.float64, device=dev)
+
+    def step():
+        bgm.marginal_likelihood_grad(L, y, tau2, check=False, out=out)
+        red[0] = loss.sum()
+        red[1] = tbar.sum()
+        if world > 1:
+            dist.all_reduce(red)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    st.raise_first()
+
+    # ---------------- timed region: device-resident inputs
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    rows_total = B * n * world
+    value = rows_total / (ms / 1e3)
+
+    # ---------------- per-kernel attribution (CUDA events on the launch stream)
+    lib.bgm_timing_enable(1)
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    kernels = []
+    cnt = lib.bgm_timing_read(-1, None, 0, None, None)
+    for i in range(cnt):
+        name = C.create_string_buffer(128)
+        tot = C.c_double()
+        c = C.c_int64()
+        lib.bgm_timing_read(i, name, 128, C.byref(tot), C.byref(c))
+        kernels.append((name.value.decode(), tot.value, c.value))
+    lib.bgm_timing_enable(0)
+    launches_per_step = sum(c for _, _, c in kernels) / max(args.steps, 1)
+    dom = max(kernels, key=lambda t: t[1]) if kernels else ("?", float("nan"), 1)
+    dom_ms = dom[1] / dom[2]
+    peak, peak_src = load_peaks()
+    bpr = alg_bytes_per_row(dom[0], k)
+    achieved = bpr * B * n / (dom_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom[0], "achieved": round(achieved, 1), "peak": peak,
+                "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "traffic": None, "alg_bytes_per_row": bpr,
+                "kernel_ms": {kname: round(t / c, 4) for kname, t, c in kernels}}
+
+    # ---------------- e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_run(args, L, y, tau2, out, world, dev)
+
+    # ---------------- CPU baseline (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = os.cpu_count() or 1
+        m = sample_size(cores, B)
+        Lh, yh = host_sample(L, y, m)
+        dt, kind, thr = cpu_run(Lh, yh, tau2)
+        cpu = {"value": round(m * n / dt, 1), "unit": "band-rows/s", "cores": thr, "kind": kind,
+               "sample": f"{m} of the {B} config-3 matrices (n={n}, k={k}), oracle marginal_likelihood_grad, "
+                         f"{dt:.2f} s wall on {thr} threads"}
+
+    if rank == 0:
+        line = {
+            "metric": metric, "value": round(value, 1), "unit": "band-rows/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded on device; BASELINE.md §4 construction)",
+            "config": {"workload": args.workload, "desc": wl["desc"], "batch_per_gpu": B, "n": n, "k": k,
+                       "tau2": tau2, "parallelism": f"batch-sharded x{world}",
+                       "l2": "inputs (%.2f GB/GPU) exceed the 126 MB L2; no flush needed" % (B * n * (k + 1) * 8 / 1e9)},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(round(launches_per_step * args.steps)),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_run(args, L, y, tau2, out, world, dev):
+    """Same metric through the public API from pinned HOST buffers: each step
+    copies L and y host->device, runs the step, and reads loss, tau2_bar and
+    the full L_bar back device->host."""
+    import torch
+    import torch.distributed as dist
+    import paper_1902_10078_b200 as bgm
+
+    loss, lbar, tbar, st = out
+    hL = torch.empty(L.data.shape, dtype=L.data.dtype, pin_memory=True)
+    hy = torch.empty(y.data.shape, dtype=y.data.dtype, pin_memory=True)
+    hL.copy_(L.data)
+    hy.copy_(y.data)
+    dL = bgm.Bands(torch.empty_like(L.data), L.batch, L.n, L.lower, L.upper, 32)
+    dy = bgm.Vecs(torch.empty_like(y.data), y.batch, y.n, 32)
+    hLb = torch.empty(lbar.data.shape, dtype=torch.float64, pin_memory=True)
+    hloss = torch.empty(loss.shape, dtype=torch.float64, pin_memory=True)
+    htb = torch.empty(tbar.shape, dtype=torch.float64, pin_memory=True)
+
+    def step():
+        dL.data.copy_(hL, non_blocking=True)
+        dy.data.copy_(hy, non_blocking=True)
+        bgm.marginal_likelihood_grad(dL, dy, tau2, check=False, out=out)
+        hLb.copy_(lbar.data, non_blocking=True)
+        hloss.copy_(loss, non_blocking=True)
+        htb.copy_(tbar, non_blocking=True)
+
+    steps = max(2, min(args.steps, 5))
+    step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s = torch.cuda.current_stream()
+    e0.record(s)
+    for _ in range(steps):
+        step()
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    h2d = hL.numel() * 8 + hy.numel() * 8
+    d2h = hLb.numel() * 8 + hloss.numel() * 8 + htb.numel() * 8
+    return {"value": round(L.batch * L.n * world / (ms / 1e3), 1), "unit": "band-rows/s",
+            "ms_per_step": round(ms, 3), "steps": steps, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+
+def reference_arm(args, wl, metric, world, rank):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref,
+    compiled verbatim; the C restatement if that is absent) on the host cores,
+    each step a bounded sample of the workload.  Rank 0 only."""
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle as orc
+    from tests import common as cm
+
+    B, n, k, tau2 = wl["B"], wl["n"], wl["k"], wl["tau2"]
+    cores = os.cpu_count() or 1
+    m = sample_size(cores, B)
+    rng = np.random.default_rng(99)
+    L = cm.config_factor(rng, m, n, k)
+    y = rng.normal(0.0, 1.0, (m, n))
+    kind = "reference" if orc.available("reference") else "restatement"
+    for _ in range(max(args.warmup, 1) if m * n * (k + 1) < 5e8 else 1):
+        cpu_run(L[: max(1, m // 8)], y[: max(1, m // 8)], tau2, kind)
+    times = []
+    steps = max(1, min(args.steps, 3))
+    thr = 1
+    for _ in range(steps):
+        dt, kk, thr = cpu_run(L, y, tau2, kind)
+        times.append(dt)
+    dt = statistics.median(times)
+    value = m * n / dt
+    line = {"impl": "reference", "metric": metric, "value": round(value, 1), "unit": "band-rows/s",
+            "n_gpus": world, "steps": steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded numpy; BASELINE.md §4 construction)",
+            "config": {"workload": args.workload, "desc": wl["desc"], "batch_per_gpu": B, "n": n, "k": k,
+                       "tau2": tau2},
+            "cpu_baseline": {"value": round(value, 1), "unit": "band-rows/s", "cores": thr,
+                             "kind": "reference" if kind == "reference" else "port",
+                             "sample": f"{m} config-3 matrices per step (n={n}, k={k}), median of {steps}"},
+            "e2e": {"value": round(value, 1), "unit": "band-rows/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,195 @@
+/*
+ * bandgm_b200 -- C ABI of the B200 (sm_100a) banded operator library.
+ *
+ * This is the drop-in boundary under the reference's C++ operator API
+ * (/root/reference/proj/include/bandgm/{kernels,grad}.hpp).  The reference
+ * exposes no C ABI of its own; each entry point below states the reference
+ * function it replaces.  The C++ drop-in layer
+ * (paper_1902_10078_b200/cpp/include/bandgm/*.hpp) and the Python host
+ * package call only these symbols.  INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ * -----------
+ * - All data pointers are DEVICE pointers; every call is asynchronous on
+ *   `stream` (0 = legacy default stream).  No torch types cross this ABI.
+ * - A batch of B independent n x n bands (`bgm_band`) is stored
+ *   batch-interleaved with interleave width `tile` (1 or 32):
+ *       element (b, r, j) -> ((b / tile) * n * w + j * w + r) * tile + b % tile
+ *   where w = lower + upper + 1 and r = i - j + upper is the storage row of
+ *   matrix entry (i, j) -- the reference storage convention (banded.hpp:1-11).
+ *   tile = 1 is exactly the reference's per-matrix column-major block, one
+ *   matrix after another; tile = 32 puts 32 matrices side by side so a warp
+ *   reads 32 matrices' copies of one cell in one 256-byte transaction.  The
+ *   allocation must cover round_up(B, tile) matrices.  Corner cells (storage
+ *   cells mapping outside the matrix) are written as exact zeros.
+ * - Vectors (`bgm_vec`): element (b, i) -> ((b / tile) * n + i) * tile + b % tile.
+ * - Symmetric bands are stored as their lower band (upper = 0) and read
+ *   mirrored; symmetric adjoints follow the reference's stored-cell
+ *   convention (grad.hpp:4-8).
+ * - Per-matrix error reporting: `status` (int32, device, length B; may be
+ *   NULL) receives BGM_OK or the op's error code, `row` (int64, device,
+ *   length B; may be NULL) the first failing row or -1 -- the row the
+ *   reference's exception would carry (errors.hpp:27-50).  The returned int
+ *   covers argument validation and launch errors only (synchronous part).
+ * - dtype: BGM_F64 everywhere; BGM_F32 is accepted by the factorization,
+ *   solve, log-det, inverse-subset and their adjoints (config 4's fp32 runs).
+ */
+#ifndef BANDGM_B200_H
+#define BANDGM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  BGM_OK = 0,
+  BGM_ERR_NOT_PD = 1,        /* NotPositiveDefinite  (errors.hpp:27-34) */
+  BGM_ERR_SINGULAR = 2,      /* SingularDiagonal     (errors.hpp:36-43) */
+  BGM_ERR_NONPOS_DIAG = 3,   /* NonPositiveDiagonal  (errors.hpp:45-50) */
+  BGM_ERR_DIM = 4,           /* DimensionMismatch    (errors.hpp:9-11)  */
+  BGM_ERR_ARG = 5,           /* malformed descriptor / unsupported combination */
+  BGM_ERR_CUDA = 6           /* launch or allocation failure */
+};
+
+enum { BGM_F64 = 0, BGM_F32 = 1 };
+
+typedef struct bgm_band {
+  void* data;
+  int64_t batch;
+  int64_t n;
+  int32_t lower;
+  int32_t upper;
+  int32_t tile;  /* 1 or 32 */
+  int32_t dtype; /* BGM_F64 / BGM_F32 */
+} bgm_band;
+
+typedef struct bgm_vec {
+  void* data;
+  int64_t batch;
+  int64_t n;
+  int32_t tile;
+  int32_t dtype;
+} bgm_vec;
+
+typedef void* bgm_stream; /* cudaStream_t */
+
+/* ---------------------------------------------------------------- info */
+int bgm_abi_version(void);
+const char* bgm_status_name(int status);
+/* Last CUDA error text seen by the library on this thread. */
+const char* bgm_last_error(void);
+
+/* -------------------------------------------------------- layout helpers */
+/* Re-lays a band batch between interleave widths (same n, lower, upper,
+ * dtype).  Used to move reference-layout blocks (tile 1) in and out. */
+int bgm_relayout_band(bgm_band src, bgm_band dst, bgm_stream stream);
+int bgm_relayout_vec(bgm_vec src, bgm_vec dst, bgm_stream stream);
+/* bandgm::transpose (banded.hpp:166; banded.cpp:159-167): dst (upper, lower)
+ * receives the transpose of src (lower, upper).  The products below read
+ * transposes in place, so this is only needed to materialize one. */
+int bgm_transpose_band(bgm_band src, bgm_band dst, bgm_stream stream);
+
+/* ---------------------------------------------------------------- forward */
+/* ops::cholesky (kernels.hpp:25; kernels_serial.cpp:12-32).  q: lower band
+ * (bw, 0) of a symmetric matrix; l: (bw, 0).  Error: BGM_ERR_NOT_PD. */
+int bgm_cholesky(bgm_band q, bgm_band l, int32_t* status, int64_t* row, bgm_stream stream);
+
+/* ops::solve_vec (kernels.hpp:30-31; kernels_serial.cpp:34-60).
+ * x = L^{-1} v, or L^{-T} v when transpose != 0.  Error: BGM_ERR_SINGULAR. */
+int bgm_solve_vec(bgm_band l, bgm_vec v, int transpose, bgm_vec x, int32_t* status, int64_t* row,
+                  bgm_stream stream);
+
+/* ops::log_det_from_cholesky (kernels.hpp:72; kernels.cpp:121-129).
+ * out: B values (device, l's dtype).  Error: BGM_ERR_NONPOS_DIAG. */
+int bgm_log_det(bgm_band l, void* out, int32_t* status, int64_t* row, bgm_stream stream);
+
+/* ops::sparse_inverse_subset (kernels.hpp:47; kernels_serial.cpp:80-104).
+ * s: lower store (bw, 0) of the band of (L L^T)^{-1}.  Error: BGM_ERR_SINGULAR. */
+int bgm_sparse_inverse_subset(bgm_band l, bgm_band s, int32_t* status, int64_t* row,
+                              bgm_stream stream);
+
+/* ops::product_band_band[_restricted] (kernels.hpp:50-57; kernels_detail.hpp:16-28).
+ * c = op(a) * op(b) restricted to c's band; op(x) = x^T when trans_x != 0
+ * (reads the transpose in place; the reference materializes it,
+ * banded.cpp:159-167).  c's band must already be clipped to n-1. */
+int bgm_product_band_band(bgm_band a, int trans_a, bgm_band b, int trans_b, bgm_band c,
+                          bgm_stream stream);
+
+/* ops::product_band_vec (kernels.hpp:61-62; kernels_detail.hpp:31-45). */
+int bgm_product_band_vec(bgm_band b, bgm_vec v, int transpose, bgm_vec y, bgm_stream stream);
+
+/* ops::outer_band (kernels.hpp:66-67; kernels_detail.hpp:48-54):
+ * out = scale * band(m v^T) on out's band. */
+int bgm_outer_band(bgm_vec m, bgm_vec v, double scale, bgm_band out, bgm_stream stream);
+
+/* ops::solve_mat (kernels.hpp:40-42; kernels_serial.cpp:62-78; PAPER Alg. 4).
+ * out's band (already clipped) is the requested (out_lower, out_upper). */
+int bgm_solve_mat(bgm_band l, bgm_band r, int transpose, bgm_band out, int32_t* status,
+                  int64_t* row, bgm_stream stream);
+
+/* ---------------------------------------------------------------- reverse */
+/* grad::vjp_cholesky (grad.hpp:24; grad.cpp:11-36).  l_bar is CONSUMED
+ * (overwritten), as the reference takes it by value and consumes it. */
+int bgm_vjp_cholesky(bgm_band l, bgm_band l_bar_consumed, bgm_band q_bar, bgm_stream stream);
+
+/* grad::vjp_solve_vec (grad.hpp:31-32; grad.cpp:38-49). */
+int bgm_vjp_solve_vec(bgm_band l, bgm_vec s, bgm_vec s_bar, int transpose, bgm_band l_bar,
+                      bgm_vec v_bar, int32_t* status, int64_t* row, bgm_stream stream);
+
+/* grad::vjp_sparse_inverse_subset (grad.hpp:46-47; grad.cpp:84-143). */
+int bgm_vjp_sparse_inverse_subset(bgm_band l, bgm_band s, bgm_band s_bar, bgm_band l_bar,
+                                  int32_t* status, int64_t* row, bgm_stream stream);
+
+/* grad::vjp_product_band_band (grad.hpp:55-56; grad.cpp:145-151). */
+int bgm_vjp_product_band_band(bgm_band a, bgm_band b, bgm_band p_bar, bgm_band a_bar,
+                              bgm_band b_bar, bgm_stream stream);
+
+/* grad::vjp_product_band_vec (grad.hpp:62-63; grad.cpp:153-162). */
+int bgm_vjp_product_band_vec(bgm_band b, bgm_vec v, bgm_vec p_bar, int transpose, bgm_band b_bar,
+                             bgm_vec v_bar, bgm_stream stream);
+
+/* grad::vjp_outer_band (grad.hpp:69-70; grad.cpp:164-170). */
+int bgm_vjp_outer_band(bgm_vec m, bgm_vec v, bgm_band o_bar, bgm_vec m_bar, bgm_vec v_bar,
+                       bgm_stream stream);
+
+/* grad::vjp_log_det_from_cholesky (grad.hpp:73; grad.cpp:172-176).
+ * c_bar: B device values (l's dtype). */
+int bgm_vjp_log_det(bgm_band l, const void* c_bar, bgm_band l_bar, bgm_stream stream);
+
+/* grad::vjp_solve_mat (grad.hpp:40-42; grad.cpp:51-82).  r_bar's band is
+ * band(r) clipped to n-1. */
+int bgm_vjp_solve_mat(bgm_band l, bgm_band s, bgm_band s_bar, int transpose, bgm_band l_bar,
+                      bgm_band r_bar, int32_t* status, int64_t* row, bgm_stream stream);
+
+/* ------------------------------------------------- config-3 learning step */
+/* Gaussian log marginal likelihood of y under N(0, Q^{-1} + tau2 I) with
+ * Q = band(L L^T), and its reverse pass, per matrix:
+ *   infer::marginal_likelihood_partial (inference.cpp:140-163) with every
+ *   node observed, precision_from_factor (inference.cpp:23-26), and the dL
+ *   chain grad::vjp_product_band_band(L, L^T, Q_bar) (grad.cpp:145-151).
+ * Outputs per matrix: loss[b], l_bar (band of L), tau2_bar[b].
+ * Fused: two sweeps (forward factor+solve, reverse inverse-subset + adjoint)
+ * instead of the reference's 2 x cholesky, 2 x vjp_cholesky, solve,
+ * vjp_solve and products.  Errors: BGM_ERR_NOT_PD (posterior factor). */
+int bgm_marginal_likelihood_grad(bgm_band l, bgm_vec y, double tau2, double* loss,
+                                 bgm_band l_bar, double* tau2_bar, int32_t* status, int64_t* row,
+                                 bgm_stream stream);
+
+/* ------------------------------------------------- instrumentation */
+/* Per-kernel CUDA-event timing on the launching stream (off by default).
+ * bgm_timing_enable(1) clears and starts recording; bgm_timing_read(i, ...)
+ * returns the number of distinct kernels and, for 0 <= i < that number, the
+ * i-th kernel's name, summed milliseconds and launch count. */
+int bgm_timing_enable(int on);
+int bgm_timing_read(int idx, char* name, int name_len, double* total_ms, int64_t* count);
+
+/* Tuning knob for the segment-parallel sweeps (0 = automatic). */
+int bgm_set_segment_rows(int64_t rows);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BANDGM_B200_H */

@@ -1,0 +1,15 @@
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "bandgm_b200.h"
+
+namespace bgm {
+
+// Segment-parallel config-3 kernels (bgm_mlik_fast.cu).  Returns a BGM_*
+// status when it handled the call, or -1 to fall back to the generic sweep.
+int mlik_fast(const bgm_band& l, const bgm_vec& y, double tau2, double* loss,
+              const bgm_band& lbar, double* tau2_bar, int32_t* status, int64_t* row,
+              int segment_rows, cudaStream_t s);
+
+}  // namespace bgm

@@ -1,0 +1,125 @@
+"""GPU parity: every operator and adjoint through the C ABI vs the oracle.
+
+Mirrors proj/tests/test_kernels.cpp and test_grad.cpp: the golden vectors
+(reference compiled verbatim), random shapes against the C restatement, the
+reference's error rows, both device layouts (tile 32 / tile 1) and fp32.
+Tolerance: north_star's 1e-9 relative (fp64), 1e-4 (fp32), metric of
+test_util.hpp:19-21 with floor 1e-12 max|ref|.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from tests import common as cm
+from tests.golden.cases import CASES, run_case
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "golden_v1.npz")
+TOL64 = 1e-9
+
+
+@pytest.fixture(scope="module")
+def golden():
+    return np.load(GOLDEN)
+
+
+@pytest.fixture(scope="module", params=[32, 1], ids=["tile32", "tile1"])
+def gpu(request, cuda):
+    from tests.gpu_adapter import GpuOracle
+    return GpuOracle(tile=request.param)
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_golden_cases(gpu, golden, name):
+    got = run_case(name, gpu)
+    for key, val in got.items():
+        want = golden[f"{name}/{key}"]
+        if key == "status":
+            assert np.array_equal(val, want)
+            continue
+        err = cm.max_rel_err(val, want)
+        assert err <= TOL64, f"{name}/{key}: max rel err {err:.3e}"
+
+
+def test_error_rows(gpu):
+    q = np.zeros((2, 4, 1))
+    q[:, :, 0] = 1.0
+    q[1, 2, 0] = -1.0  # test_kernels.cpp:48-58: first bad pivot at row 2
+    _, st, row = gpu.cholesky(q)
+    assert list(st) == [0, 1] and row[1] == 2
+    ind = np.array([[[1.0, 2.0], [1.0, 0.0]]])  # indefinite 2x2 -> row 1
+    _, st, row = gpu.cholesky(ind)
+    assert st[0] == 1 and row[0] == 1
+    l = np.zeros((1, 3, 2))
+    l[0, :, 0] = [1.0, 0.0, 1.0]  # test_kernels.cpp:102-115
+    _, st, row = gpu.solve_vec(l, np.ones((1, 3)), False)
+    assert st[0] == 2 and row[0] == 1
+    _, st, row = gpu.log_det(np.array([[[1.0], [-2.0]]]))  # test_kernels.cpp:237-245
+    assert st[0] == 3 and row[0] == 1
+
+
+def test_known_answers(gpu):
+    l, st, _ = gpu.cholesky(np.array([[[4.0, 2.0], [5.0, 0.0]]]))
+    assert np.allclose(l[0], [[2.0, 1.0], [2.0, 0.0]], rtol=0, atol=1e-15)
+    s, _, _ = gpu.sparse_inverse_subset(np.array([[[1.0, 1.0], [1.0, 0.0]]]))
+    assert np.allclose(s[0], [[2.0, -1.0], [1.0, 0.0]], rtol=0, atol=1e-15)
+    assert gpu.vjp_cholesky(np.array([[[2.0]]]), np.array([[[1.0]]]))[0, 0, 0] == 0.25
+    lb, _, _ = gpu.vjp_sparse_inverse_subset(np.array([[[1.0]]]), np.array([[[1.0]]]), np.array([[[1.0]]]))
+    assert lb[0, 0, 0] == -2.0
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_shapes_vs_restatement(gpu, oracle, seed):
+    rng = np.random.default_rng(100 + seed)
+    B = [1, 5, 37, 64, 3, 33][seed]
+    n = int(rng.integers(1, 60))
+    bw = int(min(rng.integers(0, 7), n - 1))
+    q = cm.random_spd_band(rng, B, n, bw)
+    pairs = []
+    l_o, st_o, _ = oracle.cholesky(q)
+    l_g, st_g, _ = gpu.cholesky(q)
+    assert np.array_equal(st_o, st_g)
+    pairs.append(("cholesky", l_g, l_o))
+    v = cm.random_vec(rng, B, n)
+    for t in (False, True):
+        pairs.append((f"solve{t}", gpu.solve_vec(l_o, v, t)[0], oracle.solve_vec(l_o, v, t)[0]))
+    pairs.append(("logdet", gpu.log_det(l_o)[0], oracle.log_det(l_o)[0]))
+    s_o = oracle.sparse_inverse_subset(l_o)[0]
+    pairs.append(("subset", gpu.sparse_inverse_subset(l_o)[0], s_o))
+    lbar = cm.random_band(rng, B, n, bw, 0)
+    pairs.append(("vjp_chol", gpu.vjp_cholesky(l_o, lbar), oracle.vjp_cholesky(l_o, lbar)))
+    pairs.append(("vjp_subset", gpu.vjp_sparse_inverse_subset(l_o, s_o, lbar)[0],
+                  oracle.vjp_sparse_inverse_subset(l_o, s_o, lbar)[0]))
+    for t in (False, True):
+        x = oracle.solve_vec(l_o, v, t)[0]
+        g = gpu.vjp_solve_vec(l_o, x, v, t)
+        o = oracle.vjp_solve_vec(l_o, x, v, t)
+        pairs += [(f"vjp_solve_l{t}", g[0], o[0]), (f"vjp_solve_v{t}", g[1], o[1])]
+    al, au = int(rng.integers(0, 4)), int(rng.integers(0, 4))
+    al, au = min(al, n - 1), min(au, n - 1)
+    a = cm.random_band(rng, B, n, al, au)
+    b = cm.random_band(rng, B, n, bw, min(2, n - 1))
+    bu = min(2, n - 1)
+    pairs.append(("product", gpu.product_band_band(a, al, au, b, bw, bu)[0],
+                  oracle.product_band_band(a, al, au, b, bw, bu)[0]))
+    pairs.append(("bandvec", gpu.product_band_vec(a, al, au, v, True), oracle.product_band_vec(a, al, au, v, True)))
+    for name, g, o in pairs:
+        err = cm.max_rel_err(g, o)
+        assert err <= TOL64, f"{name} (B={B}, n={n}, bw={bw}): {err:.3e}"
+
+
+def test_fp32_factorization_path(cuda, oracle):
+    from tests.gpu_adapter import GpuOracle
+    g32 = GpuOracle(tile=1, dtype=torch.float32)
+    rng = np.random.default_rng(7)
+    B, n, k = 4, 300, 8
+    L = cm.config_factor(rng, B, n, k, off_std=0.02 / np.sqrt(k))
+    q = cm.precision(oracle, L, k).astype(np.float32).astype(np.float64)
+    l_o = oracle.cholesky(q)[0]
+    l_g = g32.cholesky(q)[0]
+    assert cm.max_rel_err(l_g, l_o) < 1e-4
+    v = cm.random_vec(rng, B, n).astype(np.float32).astype(np.float64)
+    assert cm.max_rel_err(g32.solve_vec(l_o, v, True)[0], oracle.solve_vec(l_o, v, True)[0]) < 1e-4
+    assert cm.max_rel_err(g32.sparse_inverse_subset(l_o)[0], oracle.sparse_inverse_subset(l_o)[0]) < 1e-4
