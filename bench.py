@@ -115,18 +115,18 @@ def make_inputs(B, n, k, seed, device):
 
     g = torch.Generator(device=device)
     g.manual_seed(seed)
-    L = bgm.Bands.empty(B, n, k, 0, tile=32, device=device)
+    # tile-1 layout: each matrix is the reference's own (k+1) x n storage
+    # block, which is what the segment-parallel config-3 kernels stream.
+    L = bgm.Bands.empty(B, n, k, 0, tile=1, device=device)
     L.data.normal_(0.0, 0.1, generator=g)
-    L.data[:, :, 0, :].uniform_(1.0, 2.0, generator=g)
+    L.data[:, :, 0].uniform_(1.0, 2.0, generator=g)
     for r in range(1, k + 1):
-        L.data[:, n - r:, r, :] = 0.0  # corner cells
-    if B % 32:
-        L.data.view(-1, 32)[:, :]  # padded slots stay as generated; kernels never read them
-    z = bgm.Vecs.empty(B, n, device=device)
+        L.data[:, n - r:, r] = 0.0  # corner cells
+    z = bgm.Vecs.empty(B, n, tile=1, device=device)
     z.data.normal_(0.0, 1.0, generator=g)
     x = bgm.solve_vec(L, z, transpose_l=True)
     eps = torch.empty_like(x.data).normal_(0.0, 0.1, generator=g)
-    y = bgm.Vecs(x.data + eps, B, n, 32)
+    y = bgm.Vecs(x.data + eps, B, n, 1)
     return L, y
 
 
@@ -148,8 +148,8 @@ def host_sample(L, y, m):
     import numpy as np
     import paper_1902_10078_b200 as bgm
 
-    Ls = bgm.Bands(L.data[: (m + 31) // 32].contiguous(), m, L.n, L.lower, L.upper, 32)
-    ys = bgm.Vecs(y.data[: (m + 31) // 32].contiguous(), m, y.n, 32)
+    Ls = bgm.Bands(L.data[:m].contiguous(), m, L.n, L.lower, L.upper, 1)
+    ys = bgm.Vecs(y.data[:m].contiguous(), m, y.n, 1)
     return np.ascontiguousarray(Ls.numpy()), np.ascontiguousarray(ys.numpy())
 
 
@@ -310,8 +310,8 @@ def e2e_run(args, L, y, tau2, out, world, dev):
     hy = torch.empty(y.data.shape, dtype=y.data.dtype, pin_memory=True)
     hL.copy_(L.data)
     hy.copy_(y.data)
-    dL = bgm.Bands(torch.empty_like(L.data), L.batch, L.n, L.lower, L.upper, 32)
-    dy = bgm.Vecs(torch.empty_like(y.data), y.batch, y.n, 32)
+    dL = bgm.Bands(torch.empty_like(L.data), L.batch, L.n, L.lower, L.upper, L.tile)
+    dy = bgm.Vecs(torch.empty_like(y.data), y.batch, y.n, y.tile)
     hLb = torch.empty(lbar.data.shape, dtype=torch.float64, pin_memory=True)
     hloss = torch.empty(loss.shape, dtype=torch.float64, pin_memory=True)
     htb = torch.empty(tbar.shape, dtype=torch.float64, pin_memory=True)

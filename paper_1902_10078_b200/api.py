@@ -528,5 +528,12 @@ def set_segment_rows(rows: int) -> None:
     _call("bgm_set_segment_rows", C.c_int64(rows))
 
 
+def debug_repairs(reset: bool = True) -> int:
+    """Matrices re-run on the exact single-unit path since the last reset."""
+    v = C.c_int64(0)
+    _call("bgm_debug_repairs", C.byref(v), C.c_int(int(reset)))
+    return int(v.value)
+
+
 def new_status(batch: int, device=None) -> _Status:
     return _Status(batch, _device(device))

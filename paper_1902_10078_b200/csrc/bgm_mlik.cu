@@ -141,6 +141,8 @@ using namespace bgm;
 
 extern "C" {
 
+int bgm_debug_repairs(int64_t* count, int reset) { return mlik_repairs(count, reset); }
+
 int bgm_set_segment_rows(int64_t rows) {
   if (rows < 0) return BGM_ERR_ARG;
   g_segment_rows = int(rows);

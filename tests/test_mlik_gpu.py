@@ -27,3 +27,42 @@ def _check(gpu, oracle, B, n, k, tau2, seed):
 def test_mlik_matches_tape_composition(cuda, oracle, B, n, k, tau2):
     from tests.gpu_adapter import GpuOracle
     _check(GpuOracle(tile=32), oracle, B, n, k, tau2, seed=B * 1000 + n)
+
+
+# ---------------------------------------------------------------- fast path
+# k = 16 in the tile-1 layout routes to the segment-parallel sweeps
+# (bgm_mlik_fast.cu); small segment lengths force many segments + burn-in.
+@pytest.mark.parametrize("B,n,seg", [(2, 300, 0), (3, 1000, 64), (5, 2048, 128), (33, 777, 96),
+                                     (1, 17, 16), (4, 4096, 0)])
+def test_mlik_fast_segments(cuda, oracle, B, n, seg):
+    from paper_1902_10078_b200 import api
+    from tests.gpu_adapter import GpuOracle
+    api.set_segment_rows(seg)
+    try:
+        api.debug_repairs(reset=True)
+        _check(GpuOracle(tile=1), oracle, B, n, 16, 0.01, seed=B * 7 + n)
+        assert api.debug_repairs() == 0  # well-conditioned: every burn-in converged
+    finally:
+        api.set_segment_rows(0)
+
+
+def test_mlik_fast_repair_path(cuda, oracle):
+    """Slowly-mixing precision: segment burn-ins cannot converge, the
+    verification flags them and the exact single-unit path reruns the matrix."""
+    from paper_1902_10078_b200 import api
+    from tests.gpu_adapter import GpuOracle
+    rng = np.random.default_rng(5)
+    B, n, k, tau2 = 3, 1500, 16, 50.0
+    L = cm.config_factor(rng, B, n, k, off_std=0.6)
+    y = rng.normal(0, 1, (B, n))
+    lo, lb, tb, st, _ = oracle.marginal_likelihood_grad(L, y, tau2)
+    api.set_segment_rows(64)
+    try:
+        api.debug_repairs(reset=True)
+        lg, lbg, tbg, _, _ = GpuOracle(tile=1).marginal_likelihood_grad(L, y, tau2)
+        reps = api.debug_repairs()
+    finally:
+        api.set_segment_rows(0)
+    assert reps > 0
+    for name, g, o in (("loss", lg, lo), ("l_bar", lbg, lb), ("tau2_bar", tbg, tb)):
+        assert cm.max_rel_err(g, o) <= 1e-8, name
