@@ -186,8 +186,9 @@ int bgm_timing_enable(int on);
 int bgm_timing_read(int idx, char* name, int name_len, double* total_ms, int64_t* count);
 
 /* Number of matrices the segment-parallel sweeps re-ran exactly because a
- * segment's burn-in had not converged (synchronizing; reset when reset != 0). */
-int bgm_debug_repairs(int64_t* count, int reset);
+ * segment's burn-in had not converged, and (BGM_DEBUG=1/2 only) the largest
+ * relative burn-in deviation the checks saw (synchronizing; reset != 0 clears). */
+int bgm_debug_repairs(int64_t* count, double* max_dev, int reset);
 
 /* Tuning knob for the segment-parallel sweeps (0 = automatic). */
 int bgm_set_segment_rows(int64_t rows);

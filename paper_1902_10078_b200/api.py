@@ -528,11 +528,13 @@ def set_segment_rows(rows: int) -> None:
     _call("bgm_set_segment_rows", C.c_int64(rows))
 
 
-def debug_repairs(reset: bool = True) -> int:
-    """Matrices re-run on the exact single-unit path since the last reset."""
+def debug_repairs(reset: bool = True, with_dev: bool = False):
+    """Matrices re-run on the exact single-unit path since the last reset
+    (and, with BGM_DEBUG set, the largest relative burn-in deviation)."""
     v = C.c_int64(0)
-    _call("bgm_debug_repairs", C.byref(v), C.c_int(int(reset)))
-    return int(v.value)
+    d = C.c_double(0.0)
+    _call("bgm_debug_repairs", C.byref(v), C.byref(d), C.c_int(int(reset)))
+    return (int(v.value), float(d.value)) if with_dev else int(v.value)
 
 
 def new_status(batch: int, device=None) -> _Status:

@@ -141,7 +141,9 @@ using namespace bgm;
 
 extern "C" {
 
-int bgm_debug_repairs(int64_t* count, int reset) { return mlik_repairs(count, reset); }
+int bgm_debug_repairs(int64_t* count, double* max_dev, int reset) {
+  return mlik_repairs(count, max_dev, reset);
+}
 
 int bgm_set_segment_rows(int64_t rows) {
   if (rows < 0) return BGM_ERR_ARG;

@@ -1,6 +1,13 @@
 """GPU parity of the fused config-3 learning step against the reference's
 tape composition (oracle: inference.cpp:140-163 + tape.cpp:435-451 +
-grad.cpp:145-151, restated bit-exactly in oracle/bandgm_oracle.c)."""
+grad.cpp:145-151, restated bit-exactly in oracle/bandgm_oracle.c).
+
+Metric: |a-b| / max(|a|, |b|, floor), floor = 1e-6 max|ref| for the
+gradient arrays.  The fused sweep and the reference tape reach L_bar by
+different (equally accurate) operation orders; entries that cancel to below
+~1e-6 of the array maximum then differ by rounding (~1e-16 max), which a
+1e-12 floor would report as ~1e-9 "relative" error.  test_exact.py pins both
+implementations against an extended-precision evaluation instead."""
 import numpy as np
 import pytest
 
@@ -8,6 +15,7 @@ from tests import common as cm
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-9
+FLOOR = 1e-6
 
 
 def _check(gpu, oracle, B, n, k, tau2, seed):
@@ -18,8 +26,10 @@ def _check(gpu, oracle, B, n, k, tau2, seed):
     assert np.all(st == 0)
     lg, lbg, tbg, _, _ = gpu.marginal_likelihood_grad(L, y, tau2)
     for name, g, o in (("loss", lg, lo), ("l_bar", lbg, lb), ("tau2_bar", tbg, tb)):
-        err = cm.max_rel_err(g, o)
+        err = cm.max_rel_err(g, o, floor_scale=FLOOR)
         assert err <= TOL, f"{name} B={B} n={n} k={k}: {err:.3e}"
+        # normwise agreement, as the survey also asks to report
+        assert np.linalg.norm(g - o) <= 1e-12 * np.linalg.norm(o), name
 
 
 @pytest.mark.parametrize("B,n,k,tau2", [(1, 1, 0, 0.5), (3, 50, 1, 0.3), (5, 400, 4, 0.01),
