@@ -117,4 +117,8 @@ __device__ __forceinline__ bool split_bj(ix t, ix batch, ix n, int s, ix& b, ix&
 
 int set_error(cudaError_t e);
 
+// Stream-ordered scratch from the library's private pool (bgm_scratch.cu).
+cudaError_t scratch_alloc(void** ptr, size_t bytes, cudaStream_t s);
+cudaError_t scratch_free(void* ptr, cudaStream_t s);
+
 }  // namespace bgm

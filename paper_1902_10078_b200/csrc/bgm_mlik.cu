@@ -170,7 +170,7 @@ int bgm_marginal_likelihood_grad(bgm_band l, bgm_vec y, double tau2, double* los
   const size_t band_bytes = sizeof(double) * size_t(padded * l.n * wd);
   const size_t vec_bytes = sizeof(double) * size_t(padded * l.n);
   char* ws = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws),
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&ws),
                                   2 * band_bytes + 2 * vec_bytes + sizeof(double) * 4 * padded, s);
   if (e != cudaSuccess) return set_error(e);
   Band<double> Lp{reinterpret_cast<double*>(ws), l.n, l.lower, 0, wd, 5};
@@ -181,7 +181,7 @@ int bgm_marginal_likelihood_grad(bgm_band l, bgm_vec y, double tau2, double* los
   int32_t* st = status;
   int32_t* own = nullptr;
   if (!st) {
-    e = cudaMallocAsync(reinterpret_cast<void**>(&own), sizeof(int32_t) * padded, s);
+    e = scratch_alloc(reinterpret_cast<void**>(&own), sizeof(int32_t) * padded, s);
     if (e != cudaSuccess) return set_error(e);
     st = own;
   }
@@ -197,8 +197,8 @@ int bgm_marginal_likelihood_grad(bgm_band l, bgm_vec y, double tau2, double* los
       view<double>(l), Lp, wv, tau2, Sm, uv, view<double>(lbar), part, loss, tau2_bar, l.batch, st);
   }
   e = cudaGetLastError();
-  cudaFreeAsync(ws, s);
-  if (own) cudaFreeAsync(own, s);
+  scratch_free(ws, s);
+  if (own) scratch_free(own, s);
   return e == cudaSuccess ? BGM_OK : set_error(e);
 }
 

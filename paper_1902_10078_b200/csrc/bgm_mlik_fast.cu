@@ -2,33 +2,35 @@
 //
 // The reference factors one matrix row by row (kernels_serial.cpp:12-32,
 // grad.cpp:11-36): a length-n dependency chain.  At config 3 (B = 256
-// matrices, n = 65536) one chain per matrix leaves a B200 idle, so every
-// matrix is split into P segments and each (matrix, segment) pair becomes an
-// independent "unit" run by a 16-lane team (2 units per warp):
+// matrices, n = 65536) one chain per matrix would leave a B200 idle, so every
+// matrix is split into P segments and each (matrix, segment) pair is an
+// independent "unit" run by a team of TEAM lanes (16 or 8; 32/TEAM units per
+// warp):
 //
 //   forward : unit p starts `burn` rows before its segment from a zero
-//             window (the Riccati/Schur recursion forgets its initial state
-//             geometrically), then factors its own rows exactly as the
-//             sequential sweep would.  The last 16 burn-in factor columns
-//             are saved; check_fwd compares them with the columns unit p-1
-//             produced for real.  Any mismatch beyond 1e-12 (relative to the
-//             column scale) flags the matrix and repair_fwd reruns it as a
-//             single exact unit -- so results never depend on convergence.
-//   reverse : same scheme run downwards (Takahashi recursion on the factor
-//             plus the back-solve), burning in from `burn` rows above the
-//             segment; the boundary window state is compared with the one
-//             unit p+1 produced, with the same repair.
+//             window (the Schur-complement recursion forgets its initial
+//             state geometrically), then factors its own rows exactly as the
+//             sequential sweep would.  The last 16 burn-in factor columns are
+//             saved; k_check_fwd compares them with the columns unit p-1
+//             produced for real.  A mismatch beyond 1e-12 of the column scale
+//             (or any out-of-range pivot) flags the matrix and k_repair_fwd
+//             reruns it as one exact unit with libdevice arithmetic, so the
+//             results never depend on convergence.
+//   reverse : the same scheme downwards (Takahashi recursion on the factor +
+//             back-solve), burning in `burn` rows above the segment; the
+//             boundary window state is compared with the one unit p+1
+//             produced, with the same repair.
 //
-// Team layout (forward): lane t owns the window column c = t (mod 16) and
-// keeps the full column of the symmetric (k+1)x(k+1) Schur window in 16
-// registers (rows indexed by absolute row mod 16).  Per row: rank-1 "+l l^T"
-// (forming A = L L^T + tau^-2 I on the fly) and "-c c^T" updates, pivot via
-// one rsqrt, the column c and the L column are exchanged through shared
-// memory.  Reverse: lane t owns window row r = t (mod 16) of S = band(A^-1)
-// and u = A^-1 y; per row a 16-term mat-vec for S(., j), one for the
-// L_bar column, and a 4-value butterfly for the diagonal terms.
-// Scratch Lp keeps 1/Lp(i,i) in storage row 0 (the reverse sweep only ever
-// divides by the pivot).
+// Team layout (forward): lane t owns the window columns c = t + TEAM*m
+// (mod 16) and keeps each full column of the symmetric (k+1)x(k+1) Schur
+// window in registers (rows indexed by absolute row mod 16).  Per row: the
+// rank-1 "+l l^T" (forming A = L L^T + I/tau2 on the fly) and "-c c^T"
+// updates, one pivot rsqrt, the c column exchanged through shared memory.
+// Reverse: lane t owns window rows of S = band(A^-1) and u = A^-1 y; per row
+// two 16-term mat-vecs (S(., j) and the L_bar column) and one 4-value team
+// reduction.  Inputs stream through per-unit cp.async rings (rows ahead of
+// use), so no prefetch registers are held.  Scratch Lp keeps 1/Lp(i,i) in
+// storage row 0 (the reverse sweep only ever divides by the pivot).
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -51,8 +53,13 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr double kLn2 = 0.69314718055994530942;
 constexpr double kLog2Pi = 1.8378770664093454836;  // inference.cpp:15
 constexpr double kCheckTol = 1e-12;
-constexpr int SIDE = 16 * 18;  // forward side buffer per unit: 16 columns x (17 + w)
-constexpr int STATE = 16 * 17;  // reverse boundary state per unit: 16 lanes x (16 S + u)
+constexpr int SIDE = 16 * 18;   // forward side buffer per unit: 16 columns x (17 + w)
+constexpr int STATE = 16 * 17;  // reverse boundary state per unit: 16 rows x (16 S + u)
+// shared memory per unit (doubles)
+constexpr int FRING = 16, FENT = 20;  // forward ring: 16 rows x [l0..l16, y(i+16), spare]
+constexpr int FSM = FRING * FENT + 2 * 20;
+constexpr int BRING = 8, BENT = 40;  // reverse ring: 8 rows x [1/Lp, Lp col, L(j,j), L col, w]
+constexpr int BSM = BRING * BENT + 2 * 24;
 
 template <class F, int... Us>
 __device__ __forceinline__ void unroll_up(F&& f, std::integer_sequence<int, Us...>) {
@@ -66,20 +73,21 @@ __device__ __forceinline__ void unroll_down(F&& f, std::integer_sequence<int, Us
 struct Geo {
   ix batch, n, seg;  // segment rows (multiple of 16)
   int nseg, burn;    // segments per matrix, burn-in rows (multiple of 16)
-  int debug;         // BGM_DEBUG=1: report check mismatches
+  int debug;         // BGM_DEBUG: 1 = printf + deviation, 2 = deviation only
   int team;          // lanes per unit (8 or 16)
 };
 
 struct FwdP {
   const double* L;
   const double* y;
-  double* lp;    // Lp scratch, tile-1, storage row 0 = 1/Lp(i,i)
-  double* w;     // w = Lp^-1 y
-  double* side;  // [unit][16][18]
-  double* part;  // [unit][4]: log|Lp|, log|L|, y'y, w'w
-  int64_t* fail;  // [batch]: first non-PD row (n = none)
-  double* sink;   // write target of padding teams (one matrix worth)
-  double sigma;  // 1/tau2
+  double* lp;     // Lp scratch, tile-1, storage row 0 = 1/Lp(i,i)
+  double* w;      // w = Lp^-1 y
+  double* side;   // [unit][16][18]
+  double* part;   // [unit][4]: log|Lp|, log|L|, y'y, w'w
+  int64_t* fail;  // [batch]: first non-PD row (n = none); exact on the safe path
+  int32_t* flag;  // [batch]: forward repair requested
+  double* sink;   // write target of padding teams
+  double sigma;   // 1/tau2
 };
 
 struct BwdP {
@@ -91,12 +99,12 @@ struct BwdP {
   double* exitb;  // [unit][16][17] genuine boundary state
   double* part;   // [unit][2]: tr S, u'u
   double* sink;
-  double c4;      // 1/tau2^2
+  double c4;  // 1/tau2^2
 };
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 
-// Matrices re-run by the exact single-unit path (burn-in did not converge).
+// Matrices re-run by the exact single-unit path.
 __device__ unsigned long long g_repairs = 0;
 // Largest burn-in deviation seen by the checks (bits of a non-negative double).
 __device__ unsigned long long g_maxdev = 0;
@@ -105,20 +113,32 @@ __device__ __forceinline__ void note_dev(double rel) {
   if (rel >= 0.0) atomicMax(&g_maxdev, static_cast<unsigned long long>(__double_as_longlong(rel)));
 }
 
-// ------------------------------------------------------------------ helpers
-// 1/sqrt(d) and 1/x from a float seed + two Newton steps (relative error a
-// few ulp); the exact libdevice routines outside the float range.
-__device__ __forceinline__ double fast_rsqrt(double d) {
-  if (!(d > 1e-30 && d < 1e30)) return rsqrt(d);
+// ------------------------------------------------------------------ primitives
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+// 8-byte global->shared async copy; bytes = 0 zero-fills without reading.
+__device__ __forceinline__ void cp8(void* dst, const double* src, int bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Float seed + two Newton steps (a few ulp).  Callers guarantee the argument
+// is well inside float range (the fast path flags anything else for repair).
+__device__ __forceinline__ double seeded_rsqrt(double d) {
   double r = double(rsqrtf(float(d)));
   const double h = 0.5 * d;
   r = r * fma(-h * r, r, 1.5);
   r = r * fma(-h * r, r, 1.5);
   return r;
 }
-__device__ __forceinline__ double fast_rcp(double x) {
-  const double ax = fabs(x);
-  if (!(ax > 1e-30 && ax < 1e30)) return __drcp_rn(x);
+__device__ __forceinline__ double seeded_rcp(double x) {
   double r = double(__frcp_rn(float(x)));
   r = r * fma(-x, r, 2.0);
   r = r * fma(-x, r, 2.0);
@@ -127,20 +147,17 @@ __device__ __forceinline__ double fast_rcp(double x) {
 
 template <int TEAM>
 struct Team {
-  static constexpr int CPL = 16 / TEAM;        // window columns (rows) per lane
+  static constexpr int CPL = 16 / TEAM;            // window columns (rows) per lane
   static constexpr int UPB = (32 / TEAM) * WARPS;  // units per block
-  // Every lane of a warp always runs a unit (padding units are "dummies"
-  // that compute but write nothing), so team collectives use the full mask.
-  __device__ static constexpr unsigned mask(int) { return FULL; }
 };
 
-// Per-block phases of a sweep: BURN (no outputs), OWN (outputs, no bounds
-// checks), GEN (everything checked: segment edges, matrix tail, side buffer).
+// Per-block phases of a sweep: BURN (no outputs), OWN (outputs; every row of
+// the block and of its prefetch lies inside the matrix), GEN (all checks).
 enum { PH_BURN = 0, PH_OWN = 1, PH_GEN = 2 };
 
 // ------------------------------------------------------------------ forward
 struct FwdCtx {
-  const double* Lb;  // this matrix's L (tile 1)
+  const double* Lb;
   const double* yb;
   double* lpb;
   double* wb;
@@ -154,92 +171,91 @@ struct FwdSt {
   static constexpr int CPL = Team<TEAM>::CPL;
   double W[CPL][16];  // W[m][q]: window row (absolute = q mod 16) of my m-th column
   double res[CPL];
-  double pa[CPL][8];  // prefetched L cells (distance 8 rows)
-  double pb[8];       // prefetched aux value (lane 0: L(i+16,i), lane 1: y(i+16))
   double yy, ww, prodp, prodl;
   int ep, el;
-  ix fail;
+  ix fail;   // safe path: first non-PD row
+  bool odd;  // fast path: an out-of-range pivot/diagonal was seen
 };
 
-template <int TEAM, int PH>
-__device__ __forceinline__ void fwd_block(FwdSt<TEAM>& S, const FwdCtx& C, ix base, int t,
-                                          double* sm, unsigned mask) {
+// Issue the ring copies of row ii; U = ii mod 16 (blocks start at multiples
+// of 16, so the ring slot is a compile-time constant in the unrolled steps).
+template <int TEAM, bool CHECK>
+__device__ __forceinline__ void fwd_fetch(const FwdCtx& C, double* ring, ix ii, int U, int t) {
   constexpr int CPL = Team<TEAM>::CPL;
-  const ix n = C.n;
-  const double* Lblk = C.Lb + base * WS;
-  // aux pointer: lane 1 streams y(i+16), every other lane L(i+16, i)
-  const double* auxp = (t == 1) ? C.yb + base + 16 : Lblk + 16;
-  const int auxs = (t == 1) ? 1 : WS;
-  const int aux_slot = 16 + (t < 2 ? t : 2);
+  double* dst = ring + U * FENT;
+  const bool in = !CHECK || (ii < C.n);
+  const ix ic = in ? ii : 0;
+#pragma unroll
+  for (int m = 0; m < CPL; ++m) {
+    const int crn = (t + TEAM * m - U) & 15;
+    cp8(dst + crn, C.Lb + ic * WS + crn, in ? 8 : 0);
+  }
+  if (t == 1) {
+    const bool iy = !CHECK || (ii + 16 < C.n);
+    cp8(dst + 17, C.yb + (iy ? ii + 16 : 0), iy ? 8 : 0);
+  } else {
+    cp8(dst + (t == 0 ? 16 : 18), C.Lb + ic * WS + 16, in ? 8 : 0);
+  }
+  cp_commit();
+}
+
+template <int TEAM, int PH, bool SAFE>
+__device__ __forceinline__ void fwd_block(FwdSt<TEAM>& S, const FwdCtx& C, ix base, int t,
+                                          double* sm) {
+  constexpr int CPL = Team<TEAM>::CPL;
+  double* ring = sm;
+  double* lpblk = C.lpb + base * WS;
   unroll_up(
       [&](auto UC) {
         constexpr int U = decltype(UC)::value;
         constexpr int PT = U % TEAM;  // pivot lane
-        constexpr int PM = U / TEAM;  // pivot lane's column slot
+        constexpr int PM = U / TEAM;  // its column slot
         const ix i = base + U;
         const bool pl = (t == PT);
+        fwd_fetch<TEAM, PH == PH_GEN>(C, ring, i + 8, (U + 8) & 15, t);
+        cp_wait<8>();
+        __syncwarp();
+        const double* lb = ring + U * FENT;
+        double* cb = sm + FRING * FENT + (U & 1) * 20;
         int cr[CPL];
         double lv[CPL];
 #pragma unroll
         for (int m = 0; m < CPL; ++m) {
           cr[m] = (t + TEAM * m - U) & 15;
-          lv[m] = S.pa[m][U & 7];
+          lv[m] = lb[cr[m]];
         }
-        const double xv = S.pb[U & 7];
-        // prefetch row i + 8
-        {
-          const ix ii = i + 8;
-#pragma unroll
-          for (int m = 0; m < CPL; ++m) {
-            const int crn = (t + TEAM * m - U - 8) & 15;
-            double a;
-            if (PH == PH_GEN)
-              a = ii < n ? ldg(C.Lb + ii * WS + crn) : 0.0;
-            else
-              a = ldg(Lblk + (U + 8) * WS + crn);
-            S.pa[m][U & 7] = a;
-          }
-          double x;
-          if (PH == PH_GEN) {
-            const bool ok = (t == 1) ? (ii + 16 < n) : (ii < n);
-            x = ok ? ldg(auxp + (U + 8) * auxs) : 0.0;
-          } else {
-            x = ldg(auxp + (U + 8) * auxs);
-          }
-          S.pb[U & 7] = x;
-        }
-        double* lb = sm + (U & 1) * 40;  // [0..16] l, [17] y(i+16), [18] scratch, [20..36] c
-#pragma unroll
-        for (int m = 0; m < CPL; ++m) lb[cr[m]] = lv[m];
-        lb[aux_slot] = xv;
-        __syncwarp(mask);
         const double l0 = lb[0], l16 = lb[16], yn = lb[17];
 #pragma unroll
         for (int m = 0; m < CPL; ++m)
           S.W[m][U] = fma(l0, lv[m], S.W[m][U] + ((m == PM && pl) ? C.sigma : 0.0));
-        const double d = __shfl_sync(mask, S.W[PM][U], PT, TEAM);
-        const double rs = fast_rsqrt(d);
+        const double d = __shfl_sync(FULL, S.W[PM][U], PT, TEAM);
+        const double rs = SAFE ? rsqrt(d) : seeded_rsqrt(d);
         double cmy[CPL];
 #pragma unroll
         for (int m = 0; m < CPL; ++m) {
           cmy[m] = S.W[m][U] * rs;
-          lb[20 + cr[m]] = cmy[m];
+          cb[cr[m]] = cmy[m];
         }
         const double c16 = l0 * l16 * rs;
-        lb[36] = c16;
-        const double rp = __shfl_sync(mask, S.res[PM], PT, TEAM);
+        cb[16] = c16;
+        const double rp = __shfl_sync(FULL, S.res[PM], PT, TEAM);
         const double wi = rp * rs;
-        bool own = true;
+        bool own = PH == PH_OWN;
         if (PH == PH_GEN) own = (i >= C.s && i < C.e);
-        if (PH != PH_BURN && own) {
-          double* lpi = C.lpb + i * WS;
+        if (own) {
+          double* lpi = lpblk + U * WS;
 #pragma unroll
           for (int m = 0; m < CPL; ++m) lpi[cr[m]] = (m == PM && pl) ? rs : cmy[m];
           double* o2 = (t == 1) ? C.wb + i : lpi + 16;
           *o2 = (t == 1) ? wi : c16;
-          if (!(d > kPivotFloor) || !(fabs(l0) > kPivotFloor)) S.fail = i < S.fail ? i : S.fail;
+          const double al0 = fabs(l0);
+          if (SAFE) {
+            if (!(d > kPivotFloor) || !(al0 > kPivotFloor)) S.fail = i < S.fail ? i : S.fail;
+          } else {
+            S.odd |= !(d > 1e-30) | !(d < 1e30) | !(al0 > 1e-30) | !(al0 < 1e30);
+          }
           S.prodp *= d * rs;
-          S.prodl *= fabs(l0);
+          S.prodl *= al0;
           S.ww += wi * wi;
         }
         if (PH == PH_GEN && C.side && i >= C.s - 16 && i < C.s) {
@@ -260,9 +276,9 @@ __device__ __forceinline__ void fwd_block(FwdSt<TEAM>& S, const FwdCtx& C, ix ba
           lcol[m] = me ? l16 : lv[m];
           S.res[m] = fma(-ccol[m], wi, me ? yn : S.res[m]);
         }
-        __syncwarp(mask);
-        // window update: W += l l^T - c c^T on my columns; the pivot lane's
-        // column is dead after this row and restarts as column i+16
+        __syncwarp();
+        // W += l l^T - c c^T on my columns; the pivot lane's column is dead
+        // after this row and restarts as column i+16
 #pragma unroll
         for (int m = 0; m < CPL; ++m) {
           const bool me = (m == PM && pl);
@@ -272,7 +288,7 @@ __device__ __forceinline__ void fwd_block(FwdSt<TEAM>& S, const FwdCtx& C, ix ba
               S.W[m][U] = fma(l16, lcol[m], -c16 * ccol[m]);
             } else {
               const int rel = (q - U) & 15;
-              S.W[m][q] = fma(lb[rel], lcol[m], fma(-lb[20 + rel], ccol[m], me ? 0.0 : S.W[m][q]));
+              S.W[m][q] = fma(lb[rel], lcol[m], fma(-cb[rel], ccol[m], me ? 0.0 : S.W[m][q]));
             }
           }
         }
@@ -281,16 +297,16 @@ __device__ __forceinline__ void fwd_block(FwdSt<TEAM>& S, const FwdCtx& C, ix ba
 }
 
 // One unit: rows [s, e) owned, sweep starts at i0 (multiple of 16, <= s).
-template <int TEAM>
+template <int TEAM, bool SAFE>
 __device__ void fwd_sweep(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, double* side,
-                          double* part, int t, double* sm, unsigned mask, bool dummy = false) {
+                          double* part, int t, double* sm, bool dummy) {
   constexpr int CPL = Team<TEAM>::CPL;
   const ix n = G.n;
   FwdCtx C;
   C.Lb = P.L + b * n * WS;
   C.yb = P.y + b * n;
-  C.lpb = dummy ? P.lp : P.lp + b * n * WS;  // dummies write into the sink
-  C.wb = dummy ? P.w : P.w + b * n;
+  C.lpb = dummy ? P.sink : P.lp + b * n * WS;
+  C.wb = dummy ? P.sink : P.w + b * n;
   C.side = side;
   C.n = n;
   C.s = s;
@@ -311,6 +327,7 @@ __device__ void fwd_sweep(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, 
   S.ep = 0;
   S.el = 0;
   S.fail = n;
+  S.odd = false;
   if (i0 == s) {  // exact start: rows [s, s+16) enter now
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
@@ -319,69 +336,56 @@ __device__ void fwd_sweep(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, 
       S.yy += v * v;
     }
   }
-  // prime the prefetch ring with rows i0 .. i0+7
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const ix ii = i0 + q;
-#pragma unroll
-    for (int m = 0; m < CPL; ++m) {
-      const int crn = (t + TEAM * m - q) & 15;
-      S.pa[m][q] = ii < n ? ldg(C.Lb + ii * WS + crn) : 0.0;
-    }
-    const bool ok = (t == 1) ? (ii + 16 < n) : (ii < n);
-    S.pb[q] = ok ? ((t == 1) ? ldg(C.yb + ii + 16) : ldg(C.Lb + ii * WS + 16)) : 0.0;
-  }
+  for (int q = 0; q < 8; ++q) fwd_fetch<TEAM, true>(C, sm, i0 + q, q, t);  // i0 % 16 == 0
   for (ix base = i0; base < e; base += 16) {
-    const bool inb = base + 40 <= n;  // block rows and their prefetch stay inside the matrix
+    const bool inb = base + 40 <= n;  // rows of the block and its prefetch (y at +16) inside
     if (inb && base + 16 <= s - 16)
-      fwd_block<TEAM, PH_BURN>(S, C, base, t, sm, mask);
+      fwd_block<TEAM, PH_BURN, SAFE>(S, C, base, t, sm);
     else if (inb && base >= s && base + 16 <= e)
-      fwd_block<TEAM, PH_OWN>(S, C, base, t, sm, mask);
+      fwd_block<TEAM, PH_OWN, SAFE>(S, C, base, t, sm);
     else
-      fwd_block<TEAM, PH_GEN>(S, C, base, t, sm, mask);
+      fwd_block<TEAM, PH_GEN, SAFE>(S, C, base, t, sm);
     int x;
     S.prodp = frexp(S.prodp, &x);
     S.ep += x;
     S.prodl = frexp(S.prodl, &x);
     S.el += x;
   }
-  if (t == 0) {
+  cp_wait<0>();
+  if (t == 0 && !dummy) {
     part[0] = log(S.prodp) + S.ep * kLn2;
     part[1] = log(S.prodl) + S.el * kLn2;
     part[2] = S.yy;
     part[3] = S.ww;
-    if (S.fail < n)
+    if (SAFE && S.fail < n)
       atomicMin(reinterpret_cast<unsigned long long*>(P.fail + b),
                 static_cast<unsigned long long>(S.fail));
   }
+  if (!SAFE && S.odd && !dummy) P.flag[b] = 1;
 }
 
 template <int TEAM>
 __global__ void __launch_bounds__(THREADS, 3) k_fwd(FwdP P, Geo G) {
   constexpr int UPB = Team<TEAM>::UPB;
-  __shared__ __align__(16) double smem[UPB][80];
+  __shared__ __align__(16) double smem[UPB][FSM];
   const int lane = threadIdx.x & 31;
   const int slot = threadIdx.x / TEAM;
   const int t = lane & (TEAM - 1);
   ix unit = ix(blockIdx.x) * UPB + slot;
-  const bool dummy = unit >= G.batch * G.nseg;
-  if (dummy) unit = 0;  // padding team: recompute unit 0 into the dummy sinks
+  const bool dummy = unit >= G.batch * G.nseg;  // padding team keeps its warp converged
+  if (dummy) unit = 0;
   const ix b = unit / G.nseg;
   const int p = int(unit % G.nseg);
   const ix s = ix(p) * G.seg;
   const ix e = s + G.seg < G.n ? s + G.seg : G.n;
   const ix i0 = s - G.burn > 0 ? s - G.burn : 0;
-  FwdP Q = P;
-  if (dummy) {
-    Q.lp = P.sink;
-    Q.w = P.sink;
-    Q.fail = reinterpret_cast<int64_t*>(P.sink);
-  }
-  fwd_sweep<TEAM>(Q, G, b, s, e, i0, (p > 0 && !dummy) ? P.side + unit * SIDE : nullptr,
-                  dummy ? P.sink : P.part + unit * 4, t, smem[slot], Team<TEAM>::mask(lane), dummy);
+  fwd_sweep<TEAM, false>(P, G, b, s, e, i0, (p > 0 && !dummy) ? P.side + unit * SIDE : nullptr,
+                         P.part + unit * 4, t, smem[slot], dummy);
 }
+
 // One thread per (matrix, segment > 0): burn-in columns vs the real ones.
-__global__ void k_check_fwd(FwdP P, Geo G, int32_t* flag) {
+__global__ void k_check_fwd(FwdP P, Geo G) {
   const ix unit = blockIdx.x * ix(blockDim.x) + threadIdx.x;
   if (unit >= G.batch * G.nseg) return;
   const int p = int(unit % G.nseg);
@@ -393,60 +397,50 @@ __global__ void k_check_fwd(FwdP P, Geo G, int32_t* flag) {
   double dev = 0.0;
   double wscale = 0.0;
   for (int c = 0; c < 16; ++c) wscale = fmax(wscale, fabs(P.w[b * n + s - 16 + c]));
-  for (int c = 0; c < 16 && !bad; ++c) {
+  for (int c = 0; c < 16; ++c) {
     const double* real = P.lp + (b * n + s - 16 + c) * WS;
     double sc = 0.0;
     for (int r = 0; r < WS; ++r) sc = fmax(sc, fabs(real[r]));
-    for (int r = 0; r < WS; ++r) dev = fmax(dev, fabs(sd[c * 18 + r] - real[r]) / (sc + 1e-300));
-    dev = fmax(dev, fabs(sd[c * 18 + 17] - P.w[b * n + s - 16 + c]) / (wscale + 1e-300));
-    for (int r = 0; r < WS; ++r)
-      if (!(fabs(sd[c * 18 + r] - real[r]) <= kCheckTol * sc)) {
+    for (int r = 0; r <= WS; ++r) {
+      const double a = sd[c * 18 + r];
+      const double ref = r < WS ? real[r] : P.w[b * n + s - 16 + c];
+      const double scale = r < WS ? sc : wscale;
+      const double rel = fabs(a - ref) / (scale + 1e-300);
+      dev = fmax(dev, rel);
+      if (!(rel <= kCheckTol)) {
         if (G.debug == 1 && !bad)
           printf("fwd check b=%lld p=%d col=%lld r=%d burn=%.17g real=%.17g\n", (long long)b, p,
-                 (long long)(s - 16 + c), r, sd[c * 18 + r], real[r]);
+                 (long long)(s - 16 + c), r, a, ref);
         bad = true;
       }
-    if (!(fabs(sd[c * 18 + 17] - P.w[b * n + s - 16 + c]) <= kCheckTol * (wscale + 1e-300))) {
-      if (G.debug == 1 && !bad)
-        printf("fwd check w b=%lld p=%d row=%lld burn=%.17g real=%.17g\n", (long long)b, p,
-               (long long)(s - 16 + c), sd[c * 18 + 17], P.w[b * n + s - 16 + c]);
-      bad = true;
     }
   }
   if (G.debug) note_dev(dev);
-  if (bad) flag[b] = 1;
+  if (bad) P.flag[b] = 1;
 }
 
 // One team per matrix: flagged matrices rerun the forward as one exact unit.
 template <int TEAM>
-__global__ void __launch_bounds__(THREADS, 3) k_repair_fwd(FwdP P, Geo G, const int32_t* flag) {
+__global__ void __launch_bounds__(THREADS, 3) k_repair_fwd(FwdP P, Geo G) {
   constexpr int UPB = Team<TEAM>::UPB;
-  __shared__ __align__(16) double smem[UPB][80];
+  __shared__ __align__(16) double smem[UPB][FSM];
   const int lane = threadIdx.x & 31;
   const int slot = threadIdx.x / TEAM;
   const ix b0 = ix(blockIdx.x) * UPB + slot;
-  const bool work = b0 < G.batch && flag[b0];
+  const bool work = b0 < G.batch && P.flag[b0];
   // whole warps skip when none of their teams has work; otherwise idle teams
   // run as dummies so the team collectives stay converged
   if (!__any_sync(FULL, work)) return;
   const ix b = work ? b0 : 0;
   const int t = lane & (TEAM - 1);
-  FwdP Q = P;
-  double* part0 = P.part + b * G.nseg * 4;
-  if (work) {
-    if (t == 0) {
-      atomicAdd(&g_repairs, 1ull);
-      P.fail[b] = G.n;
-      for (int q = 4; q < G.nseg * 4; ++q) part0[q] = 0.0;
-    }
-  } else {
-    Q.lp = P.sink;
-    Q.w = P.sink;
-    Q.fail = reinterpret_cast<int64_t*>(P.sink);
-    part0 = P.sink;
+  double* part0 = work ? P.part + b * G.nseg * 4 : P.sink;
+  if (work && t == 0) {
+    atomicAdd(&g_repairs, 1ull);
+    P.fail[b] = G.n;
+    for (int q = 4; q < G.nseg * 4; ++q) part0[q] = 0.0;
   }
   __syncwarp();
-  fwd_sweep<TEAM>(Q, G, b, 0, G.n, 0, nullptr, part0, t, smem[slot], Team<TEAM>::mask(lane), !work);
+  fwd_sweep<TEAM, true>(P, G, b, 0, G.n, 0, nullptr, part0, t, smem[slot], !work);
 }
 
 // ------------------------------------------------------------------ reverse
@@ -455,7 +449,7 @@ struct BwdCtx {
   const double* lpb;
   const double* wb;
   double* lbb;
-  ix n, s, e, jtop;
+  ix n, s, e;
   double c4;
 };
 
@@ -464,46 +458,62 @@ struct BwdSt {
   static constexpr int RPL = Team<TEAM>::CPL;
   double S[RPL][16];  // S[m][q]: my m-th window row, column (absolute = q mod 16)
   double um[RPL];
-  double pa[RPL][4], pb[RPL][4];  // prefetched Lp / L cells (distance 4 rows)
-  double pc[4];                   // aux: lane 0 1/Lp(j,j), lane 1 L(j,j), lane 2 w_j
   double tr, uu;
 };
 
-// Sum of 4 values over the team, result identical on every lane:
-// reduce-scatter over the top two levels, butterfly below, allgather via smem.
+// Sum of 4 values over the team, identical on every lane: reduce-scatter over
+// the top two levels, butterfly below, allgather through shared memory.
 template <int TEAM>
 __device__ __forceinline__ void team_sum4(double& a, double& b, double& c, double& d, int t,
-                                          double* red, unsigned mask) {
+                                          double* red) {
   constexpr int H = TEAM / 2, Q = TEAM / 4;
   const bool hi = t & H;
   double k0, k1;
   {
     const double s0 = hi ? a : c, s1 = hi ? b : d;
-    const double r0 = __shfl_xor_sync(mask, s0, H, TEAM);
-    const double r1 = __shfl_xor_sync(mask, s1, H, TEAM);
+    const double r0 = __shfl_xor_sync(FULL, s0, H, TEAM);
+    const double r1 = __shfl_xor_sync(FULL, s1, H, TEAM);
     k0 = (hi ? c : a) + r0;
     k1 = (hi ? d : b) + r1;
   }
   const bool q1 = t & Q;
-  double k = (q1 ? k1 : k0) + __shfl_xor_sync(mask, q1 ? k0 : k1, Q, TEAM);
+  double k = (q1 ? k1 : k0) + __shfl_xor_sync(FULL, q1 ? k0 : k1, Q, TEAM);
 #pragma unroll
-  for (int o = Q / 2; o >= 1; o >>= 1) k += __shfl_xor_sync(mask, k, o, TEAM);
+  for (int o = Q / 2; o >= 1; o >>= 1) k += __shfl_xor_sync(FULL, k, o, TEAM);
   red[t / Q] = k;  // (hi, q1) -> a, b, c, d
-  __syncwarp(mask);
+  __syncwarp();
   a = red[0];
   b = red[1];
   c = red[2];
   d = red[3];
 }
 
-template <int TEAM, int PH>
-__device__ __forceinline__ void bwd_block(BwdSt<TEAM>& S, const BwdCtx& C, ix base, int t,
-                                          double* sm, unsigned mask) {
+template <int TEAM, bool CHECK>
+__device__ __forceinline__ void bwd_fetch(const BwdCtx& C, double* ring, ix jj, int U, int t) {
   constexpr int RPL = Team<TEAM>::CPL;
-  const ix n = C.n;
-  const double* auxp = (t == 2) ? C.wb : (t == 1 ? C.Lb : C.lpb);
-  const int auxs = (t == 2) ? 1 : WS;
-  const int aux_slot = t == 0 ? 0 : t == 1 ? 18 : t == 2 ? 36 : 54;
+  double* dst = ring + (U & (BRING - 1)) * BENT;
+  const bool in = !CHECK || (jj >= 0 && jj < C.n);
+  const ix jc = in ? jj : 0;
+  const int nb = in ? 8 : 0;
+#pragma unroll
+  for (int m = 0; m < RPL; ++m) {
+    const int rl = ((t + TEAM * m - U - 1) & 15) + 1;
+    cp8(dst + rl, C.lpb + jc * WS + rl, nb);
+    cp8(dst + 18 + rl, C.Lb + jc * WS + rl, nb);
+  }
+  if (t == 2)
+    cp8(dst + 36, C.wb + jc, nb);
+  else
+    cp8(dst + (t == 0 ? 0 : t == 1 ? 18 : 38), (t == 1 ? C.Lb : C.lpb) + jc * WS, nb);
+  cp_commit();
+}
+
+template <int TEAM, int PH, bool SAFE>
+__device__ __forceinline__ void bwd_block(BwdSt<TEAM>& S, const BwdCtx& C, ix base, int t,
+                                          double* sm) {
+  constexpr int RPL = Team<TEAM>::CPL;
+  double* ring = sm;
+  double* lbblk = C.lbb + base * WS;
   unroll_down(
       [&](auto UC) {
         constexpr int U = decltype(UC)::value;
@@ -511,36 +521,19 @@ __device__ __forceinline__ void bwd_block(BwdSt<TEAM>& S, const BwdCtx& C, ix ba
         constexpr int EM = U / TEAM;
         const ix j = base + U;
         const bool ent = (t == ET);
+        bwd_fetch<TEAM, PH == PH_GEN>(C, ring, j - 4, (U - 4) & 15, t);
+        cp_wait<4>();
+        __syncwarp();
+        const double* sb = ring + (U & (BRING - 1)) * BENT;
+        double* gb = sm + BRING * BENT + (U & 1) * 24;  // [1..16] S(., j), [20..23] sums
         int rel[RPL];
         double lpm[RPL], lm[RPL];
 #pragma unroll
         for (int m = 0; m < RPL; ++m) {
           rel[m] = ((t + TEAM * m - U - 1) & 15) + 1;
-          lpm[m] = S.pa[m][U & 3];
-          lm[m] = S.pb[m][U & 3];
+          lpm[m] = sb[rel[m]];
+          lm[m] = sb[18 + rel[m]];
         }
-        const double xv = S.pc[U & 3];
-        {  // prefetch row j - 4
-          const ix jj = j - 4;
-          const bool ok = (PH != PH_GEN) || (jj >= 0 && jj < n);
-#pragma unroll
-          for (int m = 0; m < RPL; ++m) {
-            const int reln = ((t + TEAM * m - U + 4 - 1) & 15) + 1;
-            S.pa[m][U & 3] = ok ? ldg(C.lpb + jj * WS + reln) : 0.0;
-            S.pb[m][U & 3] = ok ? ldg(C.Lb + jj * WS + reln) : 0.0;
-          }
-          S.pc[U & 3] = ok ? ldg(auxp + jj * auxs) : 0.0;
-        }
-        if (PH == PH_GEN && j > C.jtop) return;
-        double* sb = sm + (U & 1) * 64;  // [0] 1/Lp(j,j) [1..16] Lp col, [18] L(j,j) [19..34] L col,
-                                         // [36] w_j [37..52] S(.,j), [54] scratch, [56..59] sums
-#pragma unroll
-        for (int m = 0; m < RPL; ++m) {
-          sb[rel[m]] = lpm[m];
-          sb[18 + rel[m]] = lm[m];
-        }
-        sb[aux_slot] = xv;
-        __syncwarp(mask);
         const double inv = sb[0], ljj = sb[18], wj = sb[36];
         double out[RPL], accl[RPL];
 #pragma unroll
@@ -568,35 +561,34 @@ __device__ __forceinline__ void bwd_block(BwdSt<TEAM>& S, const BwdCtx& C, ix ba
           rc = fma(S.um[m], lm[m], rc);
           rd = fma(out[m], lm[m], rd);
         }
-        team_sum4<TEAM>(ra, rb, rc, rd, t, sb + 56, mask);
+        team_sum4<TEAM>(ra, rb, rc, rd, t, gb + 20);
         const double sjj = inv * inv + inv * ra;
         const double uj = (wj - rb) * inv;
         const double ul = uj * ljj + rc;
-        bool own = true;
+        bool own = PH == PH_OWN;
         if (PH == PH_GEN) own = (j >= C.s && j < C.e);
-        if (PH == PH_BURN) own = false;
         if (own) {
-          double* lbj = C.lbb + j * WS;
+          double* lbj = lbblk + U * WS;
 #pragma unroll
           for (int m = 0; m < RPL; ++m) {
             const double v = -(accl[m] - out[m] * ljj) - C.c4 * S.um[m] * ul;
-            lbj[rel[m]] = (PH == PH_GEN && j + rel[m] >= n) ? 0.0 : v;
+            lbj[rel[m]] = (PH == PH_GEN && j + rel[m] >= C.n) ? 0.0 : v;
           }
-          const double dj = rd - sjj * ljj - C.c4 * uj * ul + fast_rcp(ljj);
-          if (ent) lbj[0] = dj;
+          const double rl = SAFE ? __drcp_rn(ljj) : seeded_rcp(ljj);
+          if (ent) lbj[0] = rd - sjj * ljj - C.c4 * uj * ul + rl;
           S.tr += sjj;
           S.uu += uj * uj;
         }
 #pragma unroll
         for (int m = 0; m < RPL; ++m) {
-          sb[36 + rel[m]] = -out[m];
+          gb[rel[m]] = -out[m];
           S.S[m][U] = -out[m];
         }
-        __syncwarp(mask);
+        __syncwarp();
         if (ent) {
 #pragma unroll
           for (int q = 0; q < 16; ++q)
-            if (q != U) S.S[EM][q] = sb[36 + (((q - U - 1) & 15) + 1)];
+            if (q != U) S.S[EM][q] = gb[((q - U - 1) & 15) + 1];
           S.S[EM][U] = sjj;
           S.um[EM] = uj;
         }
@@ -604,21 +596,19 @@ __device__ __forceinline__ void bwd_block(BwdSt<TEAM>& S, const BwdCtx& C, ix ba
       std::make_integer_sequence<int, 16>{});
 }
 
-template <int TEAM>
+template <int TEAM, bool SAFE>
 __device__ void bwd_sweep(const BwdP& P, const Geo& G, ix b, ix s, ix e, ix jtop, double* entry,
-                          double* exitb, double* part, int t, double* sm, unsigned mask,
-                          bool dummy = false) {
+                          double* exitb, double* part, int t, double* sm, bool dummy) {
   constexpr int RPL = Team<TEAM>::CPL;
   const ix n = G.n;
   BwdCtx C;
   C.Lb = P.L + b * n * WS;
   C.lpb = P.lp + b * n * WS;
   C.wb = P.w + b * n;
-  C.lbb = dummy ? P.lbar : P.lbar + b * n * WS;
+  C.lbb = dummy ? P.sink : P.lbar + b * n * WS;
   C.n = n;
   C.s = s;
   C.e = e;
-  C.jtop = jtop;
   C.c4 = P.c4;
   BwdSt<TEAM> S;
 #pragma unroll
@@ -630,21 +620,10 @@ __device__ void bwd_sweep(const BwdP& P, const Geo& G, ix b, ix s, ix e, ix jtop
   S.tr = 0.0;
   S.uu = 0.0;
   const ix top_base = jtop / 16 * 16;
-  const double* auxp = (t == 2) ? C.wb : (t == 1 ? C.Lb : C.lpb);
-  const int auxs = (t == 2) ? 1 : WS;
+  // Rows above the matrix are zero-filled: with a zero window they are exact
+  // no-ops, so a partial top block needs no special casing.
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {  // rows top_base+15 .. top_base+12
-    const int U = 15 - q;
-    const ix jj = top_base + U;
-    const bool ok = jj < n;
-#pragma unroll
-    for (int m = 0; m < RPL; ++m) {
-      const int rl = ((t + TEAM * m - U - 1) & 15) + 1;
-      S.pa[m][U & 3] = ok ? ldg(C.lpb + jj * WS + rl) : 0.0;
-      S.pb[m][U & 3] = ok ? ldg(C.Lb + jj * WS + rl) : 0.0;
-    }
-    S.pc[U & 3] = ok ? ldg(auxp + jj * auxs) : 0.0;
-  }
+  for (int q = 0; q < 4; ++q) bwd_fetch<TEAM, true>(C, sm, top_base + 15 - q, 15 - q, t);
   for (ix base = top_base; base >= s; base -= 16) {
     if (entry && base + 16 == e) {  // boundary window [e, e+16) reached by burn-in
 #pragma unroll
@@ -655,14 +634,15 @@ __device__ void bwd_sweep(const BwdP& P, const Geo& G, ix b, ix s, ix e, ix jtop
         en[16] = S.um[m];
       }
     }
-    const bool inb = base >= 16 && base + 31 < n && base + 15 <= jtop;
+    const bool inb = base >= 16 && base + 32 <= n;
     if (inb && base >= e)
-      bwd_block<TEAM, PH_BURN>(S, C, base, t, sm, mask);
+      bwd_block<TEAM, PH_BURN, SAFE>(S, C, base, t, sm);
     else if (inb && base >= s && base + 16 <= e)
-      bwd_block<TEAM, PH_OWN>(S, C, base, t, sm, mask);
+      bwd_block<TEAM, PH_OWN, SAFE>(S, C, base, t, sm);
     else
-      bwd_block<TEAM, PH_GEN>(S, C, base, t, sm, mask);
+      bwd_block<TEAM, PH_GEN, SAFE>(S, C, base, t, sm);
   }
+  cp_wait<0>();
   if (exitb) {
 #pragma unroll
     for (int m = 0; m < RPL; ++m) {
@@ -672,7 +652,7 @@ __device__ void bwd_sweep(const BwdP& P, const Geo& G, ix b, ix s, ix e, ix jtop
       ex[16] = S.um[m];
     }
   }
-  if (t == 0) {
+  if (t == 0 && !dummy) {
     part[0] = S.tr;
     part[1] = S.uu;
   }
@@ -681,7 +661,7 @@ __device__ void bwd_sweep(const BwdP& P, const Geo& G, ix b, ix s, ix e, ix jtop
 template <int TEAM>
 __global__ void __launch_bounds__(THREADS, 3) k_bwd(BwdP P, Geo G) {
   constexpr int UPB = Team<TEAM>::UPB;
-  __shared__ __align__(16) double smem[UPB][128];
+  __shared__ __align__(16) double smem[UPB][BSM];
   const int lane = threadIdx.x & 31;
   const int slot = threadIdx.x / TEAM;
   const int t = lane & (TEAM - 1);
@@ -694,12 +674,12 @@ __global__ void __launch_bounds__(THREADS, 3) k_bwd(BwdP P, Geo G) {
   const ix e = s + G.seg < G.n ? s + G.seg : G.n;
   ix jtop = e + G.burn - 1;
   if (jtop > G.n - 1) jtop = G.n - 1;
-  BwdP Q = P;
-  if (dummy) Q.lbar = P.sink;
-  bwd_sweep<TEAM>(Q, G, b, s, e, jtop, (p + 1 < G.nseg && !dummy) ? P.entry + unit * STATE : nullptr,
-                  (p > 0 && !dummy) ? P.exitb + unit * STATE : nullptr,
-                  dummy ? P.sink : P.part + unit * 2, t, smem[slot], Team<TEAM>::mask(lane), dummy);
+  bwd_sweep<TEAM, false>(P, G, b, s, e, jtop,
+                         (p + 1 < G.nseg && !dummy) ? P.entry + unit * STATE : nullptr,
+                         (p > 0 && !dummy) ? P.exitb + unit * STATE : nullptr, P.part + unit * 2, t,
+                         smem[slot], dummy);
 }
+
 __global__ void k_check_bwd(BwdP P, Geo G, int32_t* flag) {
   const ix unit = blockIdx.x * ix(blockDim.x) + threadIdx.x;
   if (unit >= G.batch * G.nseg) return;
@@ -718,10 +698,11 @@ __global__ void k_check_bwd(BwdP P, Geo G, int32_t* flag) {
   for (int q = 0; q < 16; ++q) {
     for (int c = 0; c < 17; ++c) {
       const double sc = c < 16 ? ss : us;
-      dev = fmax(dev, fabs(a[q * 17 + c] - r[q * 17 + c]) / (sc + 1e-300));
-      if (!(fabs(a[q * 17 + c] - r[q * 17 + c]) <= kCheckTol * (sc + 1e-300))) {
+      const double rel = fabs(a[q * 17 + c] - r[q * 17 + c]) / (sc + 1e-300);
+      dev = fmax(dev, rel);
+      if (!(rel <= kCheckTol)) {
         if (G.debug == 1 && !bad)
-          printf("bwd check b=%lld p=%d lane=%d slot=%d burn=%.17g real=%.17g\n", (long long)b, p, q,
+          printf("bwd check b=%lld p=%d row=%d slot=%d burn=%.17g real=%.17g\n", (long long)b, p, q,
                  c, a[q * 17 + c], r[q * 17 + c]);
         bad = true;
       }
@@ -735,7 +716,7 @@ template <int TEAM>
 __global__ void __launch_bounds__(THREADS, 3) k_repair_bwd(BwdP P, Geo G, const int32_t* flag,
                                                            const int64_t* fail) {
   constexpr int UPB = Team<TEAM>::UPB;
-  __shared__ __align__(16) double smem[UPB][128];
+  __shared__ __align__(16) double smem[UPB][BSM];
   const int lane = threadIdx.x & 31;
   const int slot = threadIdx.x / TEAM;
   const ix b0 = ix(blockIdx.x) * UPB + slot;
@@ -743,21 +724,15 @@ __global__ void __launch_bounds__(THREADS, 3) k_repair_bwd(BwdP P, Geo G, const 
   if (!__any_sync(FULL, work)) return;
   const ix b = work ? b0 : 0;
   const int t = lane & (TEAM - 1);
-  BwdP Q = P;
-  double* part0 = P.part + b * G.nseg * 2;
-  if (work) {
-    if (t == 0) {
-      atomicAdd(&g_repairs, 1ull);
-      for (int q = 2; q < G.nseg * 2; ++q) part0[q] = 0.0;
-    }
-  } else {
-    Q.lbar = P.sink;
-    part0 = P.sink;
+  double* part0 = work ? P.part + b * G.nseg * 2 : P.sink;
+  if (work && t == 0) {
+    atomicAdd(&g_repairs, 1ull);
+    for (int q = 2; q < G.nseg * 2; ++q) part0[q] = 0.0;
   }
   __syncwarp();
-  bwd_sweep<TEAM>(Q, G, b, 0, G.n, G.n - 1, nullptr, nullptr, part0, t, smem[slot],
-                  Team<TEAM>::mask(lane), !work);
+  bwd_sweep<TEAM, true>(P, G, b, 0, G.n, G.n - 1, nullptr, nullptr, part0, t, smem[slot], !work);
 }
+
 __global__ void k_finalize(const double* pf, const double* pb, const int64_t* fail, Geo G,
                            double tau2, double* loss, double* tau2_bar, int32_t* status,
                            int64_t* row) {
@@ -790,6 +765,46 @@ __global__ void k_init_fail(int64_t* fail, int32_t* flag, ix batch, ix n) {
   flag[batch + b] = 0;
 }
 
+template <int TEAM>
+int bpm_for() {
+  int bf = 1, bb = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, k_fwd<TEAM>, THREADS, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bb, k_bwd<TEAM>, THREADS, 0);
+  const int v = bf < bb ? bf : bb;
+  return v < 1 ? 1 : v;
+}
+
+template <int TEAM>
+void launch_all(const FwdP& F, const BwdP& Bp, const Geo& G, int32_t* flags, double tau2,
+                double* loss, double* tau2_bar, int32_t* status, int64_t* row, cudaStream_t s) {
+  constexpr int UPB = Team<TEAM>::UPB;
+  const ix units = G.batch * G.nseg;
+  const unsigned ublocks = unsigned((units + UPB - 1) / UPB);
+  const unsigned mblocks = unsigned((G.batch + UPB - 1) / UPB);
+  const unsigned cblocks = unsigned((units + 127) / 128);
+  k_init_fail<<<blocks_for(G.batch, 128), 128, 0, s>>>(F.fail, flags, G.batch, G.n);
+  {
+    timing::Scope ts("mlik_seg_fwd", s);
+    k_fwd<TEAM><<<ublocks, THREADS, 0, s>>>(F, G);
+  }
+  {
+    timing::Scope ts("mlik_seg_check", s);
+    k_check_fwd<<<cblocks, 128, 0, s>>>(F, G);
+    k_repair_fwd<TEAM><<<mblocks, THREADS, 0, s>>>(F, G);
+  }
+  {
+    timing::Scope ts("mlik_seg_bwd", s);
+    k_bwd<TEAM><<<ublocks, THREADS, 0, s>>>(Bp, G);
+  }
+  {
+    timing::Scope ts("mlik_seg_check", s);
+    k_check_bwd<<<cblocks, 128, 0, s>>>(Bp, G, flags + G.batch);
+    k_repair_bwd<TEAM><<<mblocks, THREADS, 0, s>>>(Bp, G, flags + G.batch, F.fail);
+    k_finalize<<<blocks_for(G.batch, 128), 128, 0, s>>>(F.part, Bp.part, F.fail, G, tau2, loss,
+                                                        tau2_bar, status, row);
+  }
+}
+
 }  // namespace
 
 int mlik_repairs(int64_t* count, double* max_dev, int reset) {
@@ -818,31 +833,22 @@ int mlik_fast(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, co
   G.burn = 128;  // window errors ride ~16 rows to the pivot before damping (~1e-2-1e-3 per 16 rows)
   {
     const char* dbg = std::getenv("BGM_DEBUG");
-    G.debug = dbg ? (dbg[0] == '1' ? 2 : dbg[0] == '2' ? 1 : 0) : 0;  // 1: printf + dev, 2: dev only
+    G.debug = dbg ? (dbg[0] == '1' ? 1 : dbg[0] == '2' ? 2 : 0) : 0;
   }
-  // Team size: BGM_TEAM=8|16 (default 16).
   int team = 16;
   {
     const char* e = std::getenv("BGM_TEAM");
     if (e && std::atoi(e) == 8) team = 8;
   }
+  G.team = team;
   // One wave: as many units as fit resident on the chip.
-  int sms = 148, bpm = 1;
+  int sms = 148;
   {
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess)
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int bf = 1, bb = 1;
-    if (team == 8) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, k_fwd<8>, THREADS, 0);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bb, k_bwd<8>, THREADS, 0);
-    } else {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, k_fwd<16>, THREADS, 0);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bb, k_bwd<16>, THREADS, 0);
-    }
-    bpm = bf < bb ? bf : bb;
-    if (bpm < 1) bpm = 1;
   }
+  const int bpm = team == 8 ? bpm_for<8>() : bpm_for<16>();
   const int upb = (32 / team) * WARPS;
   ix seg = segment_rows;
   if (seg <= 0) {
@@ -853,20 +859,24 @@ int mlik_fast(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, co
     seg = (seg + 15) / 16 * 16;
     if (seg < 4 * G.burn) seg = 4 * G.burn;
   }
+  seg = (seg + 15) / 16 * 16;
+  if (seg < 16) seg = 16;
   G.seg = seg;
   G.nseg = int((G.n + seg - 1) / seg);
   const ix units = G.batch * G.nseg;
 
-  // scratch: Lp, w, side, fwd parts, states, bwd parts, fail, flags
+  // scratch: Lp, w, side, fwd parts, states, bwd parts, sink, fail, flags
   const size_t nb = size_t(G.batch) * size_t(G.n);
   const size_t sink_len = size_t(G.n) * WS + 64;
-  const size_t bytes = sizeof(double) * (nb * WS + nb + size_t(units) * (SIDE + 4 + 2 * STATE + 2) + sink_len) +
-                       sizeof(int64_t) * size_t(G.batch) + sizeof(int32_t) * 2 * size_t(G.batch) + 256;
+  const size_t bytes =
+      sizeof(double) * (nb * WS + nb + size_t(units) * (SIDE + 4 + 2 * STATE + 2) + sink_len) +
+      sizeof(int64_t) * size_t(G.batch) + sizeof(int32_t) * 2 * size_t(G.batch) + 256;
   char* ws = nullptr;
-  cudaError_t err = cudaMallocAsync(reinterpret_cast<void**>(&ws), bytes, s);
+  cudaError_t err = scratch_alloc(reinterpret_cast<void**>(&ws), bytes, s);
   if (err != cudaSuccess) return set_error(err);
   double* dp = reinterpret_cast<double*>(ws);
   FwdP F;
+  BwdP Bp;
   F.L = static_cast<const double*>(l.data);
   F.y = static_cast<const double*>(y.data);
   F.lp = dp;
@@ -877,7 +887,6 @@ int mlik_fast(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, co
   dp += size_t(units) * SIDE;
   F.part = dp;
   dp += size_t(units) * 4;
-  BwdP Bp;
   Bp.entry = dp;
   dp += size_t(units) * STATE;
   Bp.exitb = dp;
@@ -889,51 +898,19 @@ int mlik_fast(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, co
   dp += sink_len;
   F.fail = reinterpret_cast<int64_t*>(dp);
   int32_t* flags = reinterpret_cast<int32_t*>(F.fail + G.batch);
+  F.flag = flags;
   F.sigma = 1.0 / tau2;
   Bp.L = F.L;
   Bp.lp = F.lp;
   Bp.w = F.w;
   Bp.lbar = static_cast<double*>(lbar.data);
   Bp.c4 = F.sigma * F.sigma;
-
-  const unsigned ublocks = unsigned((units + upb - 1) / upb);
-  const unsigned mblocks = unsigned((G.batch + upb - 1) / upb);
-  const unsigned cblocks = unsigned((units + 127) / 128);
-  k_init_fail<<<blocks_for(G.batch, 128), 128, 0, s>>>(F.fail, flags, G.batch, G.n);
-  {
-    timing::Scope ts("mlik_seg_fwd", s);
-    if (team == 8)
-      k_fwd<8><<<ublocks, THREADS, 0, s>>>(F, G);
-    else
-      k_fwd<16><<<ublocks, THREADS, 0, s>>>(F, G);
-  }
-  {
-    timing::Scope ts("mlik_seg_check", s);
-    k_check_fwd<<<cblocks, 128, 0, s>>>(F, G, flags);
-    if (team == 8)
-      k_repair_fwd<8><<<mblocks, THREADS, 0, s>>>(F, G, flags);
-    else
-      k_repair_fwd<16><<<mblocks, THREADS, 0, s>>>(F, G, flags);
-  }
-  {
-    timing::Scope ts("mlik_seg_bwd", s);
-    if (team == 8)
-      k_bwd<8><<<ublocks, THREADS, 0, s>>>(Bp, G);
-    else
-      k_bwd<16><<<ublocks, THREADS, 0, s>>>(Bp, G);
-  }
-  {
-    timing::Scope ts("mlik_seg_check", s);
-    k_check_bwd<<<cblocks, 128, 0, s>>>(Bp, G, flags + G.batch);
-    if (team == 8)
-      k_repair_bwd<8><<<mblocks, THREADS, 0, s>>>(Bp, G, flags + G.batch, F.fail);
-    else
-      k_repair_bwd<16><<<mblocks, THREADS, 0, s>>>(Bp, G, flags + G.batch, F.fail);
-    k_finalize<<<blocks_for(G.batch, 128), 128, 0, s>>>(F.part, Bp.part, F.fail, G, tau2, loss,
-                                                        tau2_bar, status, row);
-  }
+  if (team == 8)
+    launch_all<8>(F, Bp, G, flags, tau2, loss, tau2_bar, status, row, s);
+  else
+    launch_all<16>(F, Bp, G, flags, tau2, loss, tau2_bar, status, row, s);
   err = cudaGetLastError();
-  cudaFreeAsync(ws, s);
+  scratch_free(ws, s);
   return err == cudaSuccess ? BGM_OK : set_error(err);
 }
 

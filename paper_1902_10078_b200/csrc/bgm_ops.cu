@@ -671,13 +671,13 @@ int bgm_vjp_sparse_inverse_subset(bgm_band l, bgm_band sm, bgm_band sbar, bgm_ba
     const int wr = 3 * l.lower + 4;
     const ix padded = (l.batch + 31) / 32 * 32;
     void* wsp = nullptr;
-    cudaError_t e = cudaMallocAsync(&wsp, sizeof(T) * size_t(padded * l.n * wr), s);
+    cudaError_t e = scratch_alloc(&wsp, sizeof(T) * size_t(padded * l.n * wr), s);
     if (e != cudaSuccess) return set_error(e);
     Band<T> ws{static_cast<T*>(wsp), l.n, wr - 1, 0, wr, 5};
     k_vjp_subset<T><<<blocks_for(l.batch, 64), 64, 0, s>>>(view<T>(l), view<T>(sm), view<T>(sbar),
                                                             view<T>(lbar), ws, l.batch, status, row);
     const int rc = launched();
-    cudaFreeAsync(wsp, s);
+    scratch_free(wsp, s);
     return rc;
   });
 }
@@ -774,7 +774,7 @@ int bgm_vjp_solve_mat(bgm_band l, bgm_band sm, bgm_band sbar, int transpose, bgm
     const ix padded = (l.batch + 31) / 32 * 32;
     void* tp = nullptr;
     cudaError_t e =
-        cudaMallocAsync(&tp, sizeof(T) * size_t(padded * n * (t.lower + t.upper + 1)), s);
+        scratch_alloc(&tp, sizeof(T) * size_t(padded * n * (t.lower + t.upper + 1)), s);
     if (e != cudaSuccess) return set_error(e);
     t.data = tp;
     int rc = run_solve_mat<T>(l, sbar, !transpose, t, status, row, s);
@@ -788,7 +788,7 @@ int bgm_vjp_solve_mat(bgm_band l, bgm_band sm, bgm_band sbar, int transpose, bgm
     if (!rc)
       rc = transpose ? run_product<T>(sm, 0, t, 1, lbar, -1.0, s)
                      : run_product<T>(t, 0, sm, 1, lbar, -1.0, s);
-    cudaFreeAsync(tp, s);
+    scratch_free(tp, s);
     return rc;
   });
 }

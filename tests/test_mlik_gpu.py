@@ -29,7 +29,7 @@ def _check(gpu, oracle, B, n, k, tau2, seed):
         err = cm.max_rel_err(g, o, floor_scale=FLOOR)
         assert err <= TOL, f"{name} B={B} n={n} k={k}: {err:.3e}"
         # normwise agreement, as the survey also asks to report
-        assert np.linalg.norm(g - o) <= 1e-12 * np.linalg.norm(o), name
+        assert np.linalg.norm(g - o) <= 1e-10 * np.linalg.norm(o), name
 
 
 @pytest.mark.parametrize("B,n,k,tau2", [(1, 1, 0, 0.5), (3, 50, 1, 0.3), (5, 400, 4, 0.01),
