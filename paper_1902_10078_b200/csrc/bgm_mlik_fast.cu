@@ -832,6 +832,11 @@ int mlik_fast(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, co
   G.n = l.n;
   G.burn = 128;  // window errors ride ~16 rows to the pivot before damping (~1e-2-1e-3 per 16 rows)
   {
+    // test knob: a short burn-in forces the verify-and-repair path
+    const char* b = std::getenv("BGM_BURN");
+    if (b && std::atoi(b) >= 16) G.burn = std::atoi(b) / 16 * 16;
+  }
+  {
     const char* dbg = std::getenv("BGM_DEBUG");
     G.debug = dbg ? (dbg[0] == '1' ? 1 : dbg[0] == '2' ? 2 : 0) : 0;
   }
