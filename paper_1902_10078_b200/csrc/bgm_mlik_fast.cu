@@ -57,9 +57,11 @@ constexpr int SIDE = 16 * 18;   // forward side buffer per unit: 16 columns x (1
 constexpr int STATE = 16 * 17;  // reverse boundary state per unit: 16 rows x (16 S + u)
 // shared memory per unit (doubles)
 constexpr int FRING = 16, FENT = 20;  // forward ring: 16 rows x [l0..l16, y(i+16), spare]
-constexpr int FSM = FRING * FENT + 2 * 20;
+// Per-unit strides are padded to 8 banks (mod 32) apart so the 2-4 units of a
+// warp never hit the same shared-memory banks.
+constexpr int FSM = FRING * FENT + 2 * 20 + 4;  // 364 doubles = 728 words = 24 (mod 32)
 constexpr int BRING = 8, BENT = 40;  // reverse ring: 8 rows x [1/Lp, Lp col, L(j,j), L col, w]
-constexpr int BSM = BRING * BENT + 2 * 24;
+constexpr int BSM = BRING * BENT + 2 * 24 + 4;  // 372 doubles = 744 words = 8 (mod 32)
 
 template <class F, int... Us>
 __device__ __forceinline__ void unroll_up(F&& f, std::integer_sequence<int, Us...>) {
@@ -122,6 +124,15 @@ __device__ __forceinline__ void cp8(void* dst, const double* src, int bytes) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
                "r"(bytes)
                : "memory");
+}
+// Same, issued only by lanes with `pred` set (others stay idle instead of
+// all hitting one scratch address).
+__device__ __forceinline__ void cp8_if(bool pred, void* dst, const double* src, int bytes) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %3, 0;\n"
+      " @p cp.async.ca.shared.global [%0], [%1], 8, %2;\n}\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(int(pred))
+      : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
@@ -190,12 +201,10 @@ __device__ __forceinline__ void fwd_fetch(const FwdCtx& C, double* ring, ix ii, 
     const int crn = (t + TEAM * m - U) & 15;
     cp8(dst + crn, C.Lb + ic * WS + crn, in ? 8 : 0);
   }
-  if (t == 1) {
-    const bool iy = !CHECK || (ii + 16 < C.n);
-    cp8(dst + 17, C.yb + (iy ? ii + 16 : 0), iy ? 8 : 0);
-  } else {
-    cp8(dst + (t == 0 ? 16 : 18), C.Lb + ic * WS + 16, in ? 8 : 0);
-  }
+  // aux: lane 0 streams L(ii+16, ii), lane 1 y(ii+16); other lanes issue nothing
+  const bool iy = !CHECK || (ii + 16 < C.n);
+  cp8_if(t < 2, dst + 16 + t, t == 1 ? C.yb + (iy ? ii + 16 : 0) : C.Lb + ic * WS + 16,
+         (t == 1 ? iy : in) ? 8 : 0);
   cp_commit();
 }
 
@@ -340,9 +349,9 @@ __device__ void fwd_sweep(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, 
   for (int q = 0; q < 8; ++q) fwd_fetch<TEAM, true>(C, sm, i0 + q, q, t);  // i0 % 16 == 0
   for (ix base = i0; base < e; base += 16) {
     const bool inb = base + 40 <= n;  // rows of the block and its prefetch (y at +16) inside
-    if (inb && base + 16 <= s - 16)
-      fwd_block<TEAM, PH_BURN, SAFE>(S, C, base, t, sm);
-    else if (inb && base >= s && base + 16 <= e)
+    // burn-in blocks (~2% of rows) share the general variant: one hot
+    // specialised loop body keeps the instruction cache warm
+    if (inb && base >= s && base + 16 <= e)
       fwd_block<TEAM, PH_OWN, SAFE>(S, C, base, t, sm);
     else
       fwd_block<TEAM, PH_GEN, SAFE>(S, C, base, t, sm);
@@ -501,10 +510,8 @@ __device__ __forceinline__ void bwd_fetch(const BwdCtx& C, double* ring, ix jj, 
     cp8(dst + rl, C.lpb + jc * WS + rl, nb);
     cp8(dst + 18 + rl, C.Lb + jc * WS + rl, nb);
   }
-  if (t == 2)
-    cp8(dst + 36, C.wb + jc, nb);
-  else
-    cp8(dst + (t == 0 ? 0 : t == 1 ? 18 : 38), (t == 1 ? C.Lb : C.lpb) + jc * WS, nb);
+  // aux: lane 0 streams 1/Lp(jj,jj), lane 1 L(jj,jj), lane 2 w_jj
+  cp8_if(t < 3, dst + 18 * t, t == 2 ? C.wb + jc : (t == 1 ? C.Lb : C.lpb) + jc * WS, nb);
   cp_commit();
 }
 
@@ -635,9 +642,7 @@ __device__ void bwd_sweep(const BwdP& P, const Geo& G, ix b, ix s, ix e, ix jtop
       }
     }
     const bool inb = base >= 16 && base + 32 <= n;
-    if (inb && base >= e)
-      bwd_block<TEAM, PH_BURN, SAFE>(S, C, base, t, sm);
-    else if (inb && base >= s && base + 16 <= e)
+    if (inb && base >= s && base + 16 <= e)
       bwd_block<TEAM, PH_OWN, SAFE>(S, C, base, t, sm);
     else
       bwd_block<TEAM, PH_GEN, SAFE>(S, C, base, t, sm);
