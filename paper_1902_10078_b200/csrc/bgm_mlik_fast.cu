@@ -49,6 +49,12 @@ constexpr int K = 16;
 constexpr int WS = K + 1;  // storage rows per column
 constexpr int WARPS = 4;
 constexpr int THREADS = 32 * WARPS;
+// Resident blocks per SM each sweep is register-tuned for (ptxas -v: the
+// reverse sweep fits 4 blocks spill-free, the forward needs 3 for no spills).
+template <int TEAM>
+struct MinBlocks {
+  static constexpr int fwd = 3, bwd = 4;
+};
 constexpr unsigned FULL = 0xffffffffu;
 constexpr double kLn2 = 0.69314718055994530942;
 constexpr double kLog2Pi = 1.8378770664093454836;  // inference.cpp:15
@@ -375,7 +381,7 @@ __device__ void fwd_sweep(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, 
 }
 
 template <int TEAM>
-__global__ void __launch_bounds__(THREADS, 3) k_fwd(FwdP P, Geo G) {
+__global__ void __launch_bounds__(THREADS, MinBlocks<TEAM>::fwd) k_fwd(FwdP P, Geo G) {
   constexpr int UPB = Team<TEAM>::UPB;
   __shared__ __align__(16) double smem[UPB][FSM];
   const int lane = threadIdx.x & 31;
@@ -430,7 +436,7 @@ __global__ void k_check_fwd(FwdP P, Geo G) {
 
 // One team per matrix: flagged matrices rerun the forward as one exact unit.
 template <int TEAM>
-__global__ void __launch_bounds__(THREADS, 3) k_repair_fwd(FwdP P, Geo G) {
+__global__ void __launch_bounds__(THREADS, MinBlocks<TEAM>::fwd) k_repair_fwd(FwdP P, Geo G) {
   constexpr int UPB = Team<TEAM>::UPB;
   __shared__ __align__(16) double smem[UPB][FSM];
   const int lane = threadIdx.x & 31;
@@ -664,7 +670,7 @@ __device__ void bwd_sweep(const BwdP& P, const Geo& G, ix b, ix s, ix e, ix jtop
 }
 
 template <int TEAM>
-__global__ void __launch_bounds__(THREADS, 3) k_bwd(BwdP P, Geo G) {
+__global__ void __launch_bounds__(THREADS, MinBlocks<TEAM>::bwd) k_bwd(BwdP P, Geo G) {
   constexpr int UPB = Team<TEAM>::UPB;
   __shared__ __align__(16) double smem[UPB][BSM];
   const int lane = threadIdx.x & 31;
@@ -718,7 +724,7 @@ __global__ void k_check_bwd(BwdP P, Geo G, int32_t* flag) {
 }
 
 template <int TEAM>
-__global__ void __launch_bounds__(THREADS, 3) k_repair_bwd(BwdP P, Geo G, const int32_t* flag,
+__global__ void __launch_bounds__(THREADS, MinBlocks<TEAM>::bwd) k_repair_bwd(BwdP P, Geo G, const int32_t* flag,
                                                            const int64_t* fail) {
   constexpr int UPB = Team<TEAM>::UPB;
   __shared__ __align__(16) double smem[UPB][BSM];
@@ -738,26 +744,28 @@ __global__ void __launch_bounds__(THREADS, 3) k_repair_bwd(BwdP P, Geo G, const 
   bwd_sweep<TEAM, true>(P, G, b, 0, G.n, G.n - 1, nullptr, nullptr, part0, t, smem[slot], !work);
 }
 
-__global__ void k_finalize(const double* pf, const double* pb, const int64_t* fail, Geo G,
-                           double tau2, double* loss, double* tau2_bar, int32_t* status,
+__global__ void k_finalize(const double* pf, const double* pb, const int64_t* fail, Geo Gf,
+                           Geo Gb, double tau2, double* loss, double* tau2_bar, int32_t* status,
                            int64_t* row) {
   const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
-  if (b >= G.batch) return;
+  if (b >= Gf.batch) return;
   double ldp = 0, ldl = 0, yy = 0, ww = 0, tr = 0, uu = 0;
-  for (int p = 0; p < G.nseg; ++p) {
-    const double* f = pf + (b * G.nseg + p) * 4;
+  for (int p = 0; p < Gf.nseg; ++p) {
+    const double* f = pf + (b * Gf.nseg + p) * 4;
     ldp += f[0];
     ldl += f[1];
     yy += f[2];
     ww += f[3];
-    tr += pb[(b * G.nseg + p) * 2];
-    uu += pb[(b * G.nseg + p) * 2 + 1];
   }
-  const double nn = double(G.n), inv = 1.0 / tau2, c4 = inv * inv;
+  for (int p = 0; p < Gb.nseg; ++p) {
+    tr += pb[(b * Gb.nseg + p) * 2];
+    uu += pb[(b * Gb.nseg + p) * 2 + 1];
+  }
+  const double nn = double(Gf.n), inv = 1.0 / tau2, c4 = inv * inv;
   // log|Lp| = sum log Lp(i,i); log|L_Q| = sum log|L(i,i)| (chol(L L^T) = L)
   loss[b] = -0.5 * nn * kLog2Pi - ldp + ldl - 0.5 * nn * log(tau2) - 0.5 * yy * inv + 0.5 * ww * c4;
   tau2_bar[b] = -nn * 0.5 * inv + 0.5 * yy * c4 + 0.5 * c4 * tr - ww * c4 * inv + 0.5 * uu * c4 * c4;
-  const bool ok = fail[b] >= G.n;
+  const bool ok = fail[b] >= Gf.n;
   if (status) status[b] = ok ? BGM_OK : BGM_ERR_NOT_PD;
   if (row) row[b] = ok ? -1 : fail[b];
 }
@@ -771,43 +779,56 @@ __global__ void k_init_fail(int64_t* fail, int32_t* flag, ix batch, ix n) {
 }
 
 template <int TEAM>
-int bpm_for() {
-  int bf = 1, bb = 1;
+void resident(int& bf, int& bb) {
+  bf = bb = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, k_fwd<TEAM>, THREADS, 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bb, k_bwd<TEAM>, THREADS, 0);
-  const int v = bf < bb ? bf : bb;
-  return v < 1 ? 1 : v;
+  if (bf < 1) bf = 1;
+  if (bb < 1) bb = 1;
 }
 
 template <int TEAM>
-void launch_all(const FwdP& F, const BwdP& Bp, const Geo& G, int32_t* flags, double tau2,
-                double* loss, double* tau2_bar, int32_t* status, int64_t* row, cudaStream_t s) {
+void launch_all(const FwdP& F, const BwdP& Bp, const Geo& Gf, const Geo& Gb, int32_t* flags,
+                double tau2, double* loss, double* tau2_bar, int32_t* status, int64_t* row,
+                cudaStream_t s) {
   constexpr int UPB = Team<TEAM>::UPB;
-  const ix units = G.batch * G.nseg;
-  const unsigned ublocks = unsigned((units + UPB - 1) / UPB);
-  const unsigned mblocks = unsigned((G.batch + UPB - 1) / UPB);
-  const unsigned cblocks = unsigned((units + 127) / 128);
-  k_init_fail<<<blocks_for(G.batch, 128), 128, 0, s>>>(F.fail, flags, G.batch, G.n);
+  const ix uf = Gf.batch * Gf.nseg, ub = Gb.batch * Gb.nseg;
+  const unsigned mblocks = unsigned((Gf.batch + UPB - 1) / UPB);
+  k_init_fail<<<blocks_for(Gf.batch, 128), 128, 0, s>>>(F.fail, flags, Gf.batch, Gf.n);
   {
     timing::Scope ts("mlik_seg_fwd", s);
-    k_fwd<TEAM><<<ublocks, THREADS, 0, s>>>(F, G);
+    k_fwd<TEAM><<<unsigned((uf + UPB - 1) / UPB), THREADS, 0, s>>>(F, Gf);
   }
   {
     timing::Scope ts("mlik_seg_check", s);
-    k_check_fwd<<<cblocks, 128, 0, s>>>(F, G);
-    k_repair_fwd<TEAM><<<mblocks, THREADS, 0, s>>>(F, G);
+    k_check_fwd<<<unsigned((uf + 127) / 128), 128, 0, s>>>(F, Gf);
+    k_repair_fwd<TEAM><<<mblocks, THREADS, 0, s>>>(F, Gf);
   }
   {
     timing::Scope ts("mlik_seg_bwd", s);
-    k_bwd<TEAM><<<ublocks, THREADS, 0, s>>>(Bp, G);
+    k_bwd<TEAM><<<unsigned((ub + UPB - 1) / UPB), THREADS, 0, s>>>(Bp, Gb);
   }
   {
     timing::Scope ts("mlik_seg_check", s);
-    k_check_bwd<<<cblocks, 128, 0, s>>>(Bp, G, flags + G.batch);
-    k_repair_bwd<TEAM><<<mblocks, THREADS, 0, s>>>(Bp, G, flags + G.batch, F.fail);
-    k_finalize<<<blocks_for(G.batch, 128), 128, 0, s>>>(F.part, Bp.part, F.fail, G, tau2, loss,
-                                                        tau2_bar, status, row);
+    k_check_bwd<<<unsigned((ub + 127) / 128), 128, 0, s>>>(Bp, Gb, flags + Gb.batch);
+    k_repair_bwd<TEAM><<<mblocks, THREADS, 0, s>>>(Bp, Gb, flags + Gb.batch, F.fail);
+    k_finalize<<<blocks_for(Gf.batch, 128), 128, 0, s>>>(F.part, Bp.part, F.fail, Gf, Gb, tau2,
+                                                         loss, tau2_bar, status, row);
   }
+}
+
+// Segment length giving one resident wave of units (or the caller's choice).
+ix segment_for(ix n, ix batch, ix capacity, int burn, ix requested) {
+  ix seg = requested;
+  if (seg <= 0) {
+    ix per = capacity / batch;
+    if (per < 1) per = 1;
+    seg = (n + per - 1) / per;
+    seg = (seg + 15) / 16 * 16;
+    if (seg < 4 * burn) seg = 4 * burn;
+  }
+  seg = (seg + 15) / 16 * 16;
+  return seg < 16 ? 16 : seg;
 }
 
 }  // namespace
@@ -845,42 +866,40 @@ int mlik_fast(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, co
     const char* dbg = std::getenv("BGM_DEBUG");
     G.debug = dbg ? (dbg[0] == '1' ? 1 : dbg[0] == '2' ? 2 : 0) : 0;
   }
-  int team = 16;
+  int team = 8;
   {
     const char* e = std::getenv("BGM_TEAM");
-    if (e && std::atoi(e) == 8) team = 8;
+    if (e && std::atoi(e) == 16) team = 16;
   }
   G.team = team;
-  // One wave: as many units as fit resident on the chip.
+  // One resident wave per sweep: forward and reverse are segmented
+  // independently, each to its own occupancy.
   int sms = 148;
   {
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess)
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int bpm = team == 8 ? bpm_for<8>() : bpm_for<16>();
+  int bf = 1, bb = 1;
+  if (team == 8)
+    resident<8>(bf, bb);
+  else
+    resident<16>(bf, bb);
   const int upb = (32 / team) * WARPS;
-  ix seg = segment_rows;
-  if (seg <= 0) {
-    const ix capacity = ix(sms) * bpm * upb;
-    ix per = capacity / G.batch;
-    if (per < 1) per = 1;
-    seg = (G.n + per - 1) / per;
-    seg = (seg + 15) / 16 * 16;
-    if (seg < 4 * G.burn) seg = 4 * G.burn;
-  }
-  seg = (seg + 15) / 16 * 16;
-  if (seg < 16) seg = 16;
-  G.seg = seg;
-  G.nseg = int((G.n + seg - 1) / seg);
-  const ix units = G.batch * G.nseg;
+  Geo Gf = G, Gb = G;
+  Gf.seg = segment_for(G.n, G.batch, ix(sms) * bf * upb, G.burn, segment_rows);
+  Gb.seg = segment_for(G.n, G.batch, ix(sms) * bb * upb, G.burn, segment_rows);
+  Gf.nseg = int((G.n + Gf.seg - 1) / Gf.seg);
+  Gb.nseg = int((G.n + Gb.seg - 1) / Gb.seg);
+  const ix uf = G.batch * Gf.nseg, ub = G.batch * Gb.nseg;
 
-  // scratch: Lp, w, side, fwd parts, states, bwd parts, sink, fail, flags
+  // scratch: Lp, w, side + fwd parts (per fwd unit), states + bwd parts (per
+  // bwd unit), sink, fail, flags
   const size_t nb = size_t(G.batch) * size_t(G.n);
   const size_t sink_len = size_t(G.n) * WS + 64;
-  const size_t bytes =
-      sizeof(double) * (nb * WS + nb + size_t(units) * (SIDE + 4 + 2 * STATE + 2) + sink_len) +
-      sizeof(int64_t) * size_t(G.batch) + sizeof(int32_t) * 2 * size_t(G.batch) + 256;
+  const size_t bytes = sizeof(double) * (nb * WS + nb + size_t(uf) * (SIDE + 4) +
+                                         size_t(ub) * (2 * STATE + 2) + sink_len) +
+                       sizeof(int64_t) * size_t(G.batch) + sizeof(int32_t) * 2 * size_t(G.batch) + 256;
   char* ws = nullptr;
   cudaError_t err = scratch_alloc(reinterpret_cast<void**>(&ws), bytes, s);
   if (err != cudaSuccess) return set_error(err);
@@ -894,15 +913,15 @@ int mlik_fast(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, co
   F.w = dp;
   dp += nb;
   F.side = dp;
-  dp += size_t(units) * SIDE;
+  dp += size_t(uf) * SIDE;
   F.part = dp;
-  dp += size_t(units) * 4;
+  dp += size_t(uf) * 4;
   Bp.entry = dp;
-  dp += size_t(units) * STATE;
+  dp += size_t(ub) * STATE;
   Bp.exitb = dp;
-  dp += size_t(units) * STATE;
+  dp += size_t(ub) * STATE;
   Bp.part = dp;
-  dp += size_t(units) * 2;
+  dp += size_t(ub) * 2;
   F.sink = dp;
   Bp.sink = dp;
   dp += sink_len;
@@ -916,9 +935,9 @@ int mlik_fast(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, co
   Bp.lbar = static_cast<double*>(lbar.data);
   Bp.c4 = F.sigma * F.sigma;
   if (team == 8)
-    launch_all<8>(F, Bp, G, flags, tau2, loss, tau2_bar, status, row, s);
+    launch_all<8>(F, Bp, Gf, Gb, flags, tau2, loss, tau2_bar, status, row, s);
   else
-    launch_all<16>(F, Bp, G, flags, tau2, loss, tau2_bar, status, row, s);
+    launch_all<16>(F, Bp, Gf, Gb, flags, tau2, loss, tau2_bar, status, row, s);
   err = cudaGetLastError();
   scratch_free(ws, s);
   return err == cudaSuccess ? BGM_OK : set_error(err);
