@@ -200,14 +200,13 @@ def main():
     lbar = L.like()
     st = bgm.api.new_status(B, dev)
     out = (loss, lbar, tbar, st)
-    red = torch.zeros(2, dtype=torch.float64, device=dev)
+    from paper_1902_10078_b200.dist import reduce_totals
 
     def step():
+        # fused sweeps on this rank's matrices, then the one 2 x fp64 NCCL
+        # all-reduce of (sum loss, sum d tau2) when world > 1
         bgm.marginal_likelihood_grad(L, y, tau2, check=False, out=out)
-        red[0] = loss.sum()
-        red[1] = tbar.sum()
-        if world > 1:
-            dist.all_reduce(red)
+        return reduce_totals([loss, tbar])
 
     for _ in range(max(args.warmup, 3)):
         step()

@@ -5,7 +5,8 @@
  * (/root/reference/proj/include/bandgm/{kernels,grad}.hpp).  The reference
  * exposes no C ABI of its own; each entry point below states the reference
  * function it replaces.  The C++ drop-in layer
- * (paper_1902_10078_b200/cpp/include/bandgm/*.hpp) and the Python host
+ * (paper_1902_10078_b200/cpp/include/bandgm/{banded,errors,kernels,grad}.hpp)
+ * and the Python host
  * package call only these symbols.  INTEGRATION.md shows the bindings.
  *
  * Conventions
@@ -189,6 +190,10 @@ int bgm_timing_read(int idx, char* name, int name_len, double* total_ms, int64_t
  * segment's burn-in had not converged, and (BGM_DEBUG=1/2 only) the largest
  * relative burn-in deviation the checks saw (synchronizing; reset != 0 clears). */
 int bgm_debug_repairs(int64_t* count, double* max_dev, int reset);
+
+/* Calling thread only: route every operator to the one-thread-per-matrix
+ * kernels that restate the reference loops (the drop-in's ops::serial::*). */
+int bgm_force_generic(int on);
 
 /* Tuning knob for the segment-parallel sweeps (0 = automatic). */
 int bgm_set_segment_rows(int64_t rows);

@@ -8,13 +8,28 @@
 namespace bgm {
 namespace fast {
 
+namespace {
+thread_local bool t_force_generic = false;
+}
+
 bool disabled() {
   static const bool off = [] {
     const char* e = std::getenv("BGM_GENERIC_ONLY");
     return e && e[0] == '1';
   }();
-  return off;
+  return off || t_force_generic;
 }
+
+}  // namespace fast
+}  // namespace bgm
+
+extern "C" int bgm_force_generic(int on) {
+  bgm::fast::t_force_generic = on != 0;
+  return BGM_OK;
+}
+
+namespace bgm {
+namespace fast {
 
 bool cholesky(const bgm_band&, const bgm_band&, int32_t*, int64_t*, cudaStream_t) { return false; }
 bool solve_vec(const bgm_band&, const bgm_vec&, int, const bgm_vec&, int32_t*, int64_t*,

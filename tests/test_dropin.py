@@ -1,0 +1,48 @@
+"""The C++ drop-in boundary.
+
+CPU: libbandgm_dropin.so exports the reference's C++ operator API
+(bandgm::ops::*, bandgm::grad::* -- mangled names) and links the C ABI.
+GPU: the reference's own tape.cpp + gradcheck.cpp, compiled verbatim against
+the drop-in headers (oracle/_ref/dropin_check), pass the reference's
+finite-difference suites and known answers while every kernel runs on the
+B200.
+"""
+import os
+import shutil
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIB = os.path.join(ROOT, "paper_1902_10078_b200", "libbandgm_dropin.so")
+PROOF = os.path.join(ROOT, "oracle", "_ref", "dropin_check")
+
+API = ["bandgm::ops::cholesky(bandgm::SymmetricBandedMatrix const&)",
+       "bandgm::ops::solve_vec(bandgm::BandedMatrix const&, Eigen::VectorXd const&, bool)",
+       "bandgm::ops::sparse_inverse_subset(bandgm::BandedMatrix const&)",
+       "bandgm::ops::product_band_band_restricted(bandgm::BandedMatrix const&, bandgm::BandedMatrix const&, long, long)",
+       "bandgm::ops::log_det_from_cholesky(bandgm::BandedMatrix const&)",
+       "bandgm::grad::vjp_cholesky(bandgm::BandedMatrix const&, bandgm::BandedMatrix)",
+       "bandgm::grad::vjp_sparse_inverse_subset(bandgm::BandedMatrix const&, bandgm::SymmetricBandedMatrix const&, bandgm::SymmetricBandedMatrix const&)",
+       "bandgm::ops::serial::cholesky_ref(bandgm::SymmetricBandedMatrix const&)"]
+
+
+@pytest.mark.skipif(shutil.which("nm") is None, reason="nm missing")
+def test_dropin_exports_reference_api():
+    if not os.path.exists(LIB):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "paper_1902_10078_b200", "cpp")], check=True)
+    out = subprocess.run(["nm", "-DC", "--defined-only", LIB], capture_output=True, text=True).stdout
+    for sym in API:
+        assert sym in out, sym
+    undef = subprocess.run(["nm", "-DC", "--undefined-only", LIB], capture_output=True, text=True).stdout
+    assert "bgm_cholesky" in undef and "bgm_vjp_cholesky" in undef  # goes through the C ABI
+
+
+@pytest.mark.gpu
+def test_reference_tape_and_gradcheck_on_the_dropin(cuda):
+    if not os.path.exists(PROOF):
+        pytest.skip("oracle/_ref/dropin_check not built (needs /root/reference at build time)")
+    r = subprocess.run([PROOF], capture_output=True, text=True, timeout=900)
+    print(r.stdout[-3000:])
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert r.stdout.count("[PASS]") >= 27
