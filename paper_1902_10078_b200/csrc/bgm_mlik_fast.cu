@@ -794,14 +794,20 @@ void launch_all(const FwdP& F, const BwdP& Bp, const Geo& Gf, const Geo& Gb, int
   constexpr int UPB = Team<TEAM>::UPB;
   const ix uf = Gf.batch * Gf.nseg, ub = Gb.batch * Gb.nseg;
   const unsigned mblocks = unsigned((Gf.batch + UPB - 1) / UPB);
-  k_init_fail<<<blocks_for(Gf.batch, 128), 128, 0, s>>>(F.fail, flags, Gf.batch, Gf.n);
+  {
+    timing::Scope ts("mlik_init", s);
+    k_init_fail<<<blocks_for(Gf.batch, 128), 128, 0, s>>>(F.fail, flags, Gf.batch, Gf.n);
+  }
   {
     timing::Scope ts("mlik_seg_fwd", s);
     k_fwd<TEAM><<<unsigned((uf + UPB - 1) / UPB), THREADS, 0, s>>>(F, Gf);
   }
   {
-    timing::Scope ts("mlik_seg_check", s);
+    timing::Scope ts("mlik_check_fwd", s);
     k_check_fwd<<<unsigned((uf + 127) / 128), 128, 0, s>>>(F, Gf);
+  }
+  {
+    timing::Scope ts("mlik_repair_fwd", s);
     k_repair_fwd<TEAM><<<mblocks, THREADS, 0, s>>>(F, Gf);
   }
   {
@@ -809,9 +815,15 @@ void launch_all(const FwdP& F, const BwdP& Bp, const Geo& Gf, const Geo& Gb, int
     k_bwd<TEAM><<<unsigned((ub + UPB - 1) / UPB), THREADS, 0, s>>>(Bp, Gb);
   }
   {
-    timing::Scope ts("mlik_seg_check", s);
+    timing::Scope ts("mlik_check_bwd", s);
     k_check_bwd<<<unsigned((ub + 127) / 128), 128, 0, s>>>(Bp, Gb, flags + Gb.batch);
+  }
+  {
+    timing::Scope ts("mlik_repair_bwd", s);
     k_repair_bwd<TEAM><<<mblocks, THREADS, 0, s>>>(Bp, Gb, flags + Gb.batch, F.fail);
+  }
+  {
+    timing::Scope ts("mlik_finalize", s);
     k_finalize<<<blocks_for(Gf.batch, 128), 128, 0, s>>>(F.part, Bp.part, F.fail, Gf, Gb, tau2,
                                                          loss, tau2_bar, status, row);
   }

@@ -1,0 +1,64 @@
+"""Host-buffer entry points: the call a user with data in host memory makes.
+
+The reference's API is host-resident (Eigen storage).  For batches, the
+drop-in keeps that contract and hides the PCIe traffic behind compute: the
+batch is cut into chunks of whole matrices and each chunk runs
+H2D copy -> fused sweeps -> D2H copy on its own stream, so chunk c's
+transfers overlap chunk c+/-1's kernels (PCIe Gen5 is full duplex, so H2D of
+one chunk and D2H of another also overlap).
+"""
+from __future__ import annotations
+
+import torch
+
+from .api import Bands, Vecs, marginal_likelihood_grad, new_status
+
+
+def marginal_likelihood_grad_host(L_host: torch.Tensor, y_host: torch.Tensor, tau2: float,
+                                  out_host=None, chunk: int = 32, streams: int = 3, device=None):
+    """Config-3 learning step on host buffers.
+
+    L_host: (B, n, k+1) float64, the reference storage block per matrix
+    (ideally pinned); y_host: (B, n).  Returns host (loss[B], l_bar, tau2_bar[B]).
+    """
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    B, n, w = L_host.shape
+    k = w - 1
+    if out_host is None:
+        pin = L_host.is_pinned()
+        out_host = (torch.empty(B, dtype=torch.float64, pin_memory=pin),
+                    torch.empty_like(L_host, pin_memory=pin),
+                    torch.empty(B, dtype=torch.float64, pin_memory=pin))
+    loss_h, lbar_h, tbar_h = out_host
+    chunk = max(1, min(chunk, B))
+    pool = [torch.cuda.Stream(device=dev) for _ in range(max(1, streams))]
+    # per-stream device buffers, reused round-robin
+    bufs = []
+    for _ in pool:
+        bufs.append((torch.empty((chunk, n, w), dtype=torch.float64, device=dev),
+                     torch.empty((chunk, n), dtype=torch.float64, device=dev),
+                     torch.empty((chunk, n, w), dtype=torch.float64, device=dev),
+                     torch.empty(chunk, dtype=torch.float64, device=dev),
+                     torch.empty(chunk, dtype=torch.float64, device=dev),
+                     new_status(chunk, dev)))
+    cur = torch.cuda.current_stream(dev)
+    for s in pool:
+        s.wait_stream(cur)
+    for ci, a in enumerate(range(0, B, chunk)):
+        b = min(B, a + chunk)
+        m = b - a
+        s = pool[ci % len(pool)]
+        dL, dy, dLb, dloss, dtb, st = bufs[ci % len(pool)]
+        with torch.cuda.stream(s):
+            dL[:m].copy_(L_host[a:b], non_blocking=True)
+            dy[:m].copy_(y_host[a:b], non_blocking=True)
+            Lb = Bands(dL[:m], m, n, k, 0, 1)
+            Yv = Vecs(dy[:m], m, n, 1)
+            Lbar = Bands(dLb[:m], m, n, k, 0, 1)
+            marginal_likelihood_grad(Lb, Yv, tau2, check=False, out=(dloss[:m], Lbar, dtb[:m], st))
+            lbar_h[a:b].copy_(dLb[:m], non_blocking=True)
+            loss_h[a:b].copy_(dloss[:m], non_blocking=True)
+            tbar_h[a:b].copy_(dtb[:m], non_blocking=True)
+    for s in pool:
+        cur.wait_stream(s)
+    return loss_h, lbar_h, tbar_h
