@@ -122,7 +122,7 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------- inputs
-def make_inputs(B, n, k, seed, device):
+def make_inputs(B, n, k, seed, device, tile=32):
     """Config-3 inputs on the device: L diag U[1,2], off-diag
     N(0, 0.1^2); y = L^-T z + eps, z ~ N(0,1), eps ~ N(0, 0.1^2)."""
     import torch
@@ -130,8 +130,8 @@ def make_inputs(B, n, k, seed, device):
 
     g = torch.Generator(device=device)
     g.manual_seed(seed)
-    # tile-1 layout: each matrix is the reference's own (k+1) x n storage
-    # block, which is what the segment-parallel config-3 kernels stream.
+    # generated in the tile-1 layout (the reference's own (k+1) x n storage
+    # block per matrix)
     L = bgm.Bands.empty(B, n, k, 0, tile=1, device=device)
     L.data.normal_(0.0, 0.1, generator=g)
     L.data[:, :, 0].uniform_(1.0, 2.0, generator=g)
@@ -142,7 +142,11 @@ def make_inputs(B, n, k, seed, device):
     x = bgm.solve_vec(L, z, transpose_l=True)
     eps = torch.empty_like(x.data).normal_(0.0, 0.1, generator=g)
     y = bgm.Vecs(x.data + eps, B, n, 1)
-    return L, y
+    if tile == 1:
+        return L, y
+    # tile 32 (default): 32 matrices interleaved per cell, the layout of the
+    # one-thread-per-unit sweeps (coalesced 256-byte warp accesses)
+    return L.to_tile(32), y.to_tile(32)
 
 
 # --------------------------------------------------------------------- cpu legs
@@ -163,9 +167,8 @@ def host_sample(L, y, m):
     import numpy as np
     import paper_1902_10078_b200 as bgm
 
-    Ls = bgm.Bands(L.data[:m].contiguous(), m, L.n, L.lower, L.upper, 1)
-    ys = bgm.Vecs(y.data[:m].contiguous(), m, y.n, 1)
-    return np.ascontiguousarray(Ls.numpy()), np.ascontiguousarray(ys.numpy())
+    Lr, yr = L.to_reference(), y.to_reference()
+    return (np.ascontiguousarray(Lr[:m].cpu().numpy()), np.ascontiguousarray(yr[:m].cpu().numpy()))
 
 
 def sample_size(cores, B):
@@ -185,6 +188,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--segment-rows", type=int, default=0)
+    ap.add_argument("--tile", type=int, choices=[1, 32], default=32,
+                    help="device layout: 32 = interleaved (one-thread-per-unit sweeps), 1 = reference layout (team sweeps)")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     B, n, k, tau2 = wl["B"], wl["n"], wl["k"], wl["tau2"]
@@ -209,7 +214,7 @@ def main():
     if args.segment_rows:
         bgm.set_segment_rows(args.segment_rows)
 
-    L, y = make_inputs(B, n, k, seed=1234 + 7919 * rank, device=dev)
+    L, y = make_inputs(B, n, k, seed=1234 + 7919 * rank, device=dev, tile=args.tile)
     loss = torch.empty(B, dtype=torch.float64, device=dev)
     tbar = torch.empty(B, dtype=torch.float64, device=dev)
     lbar = L.like()
@@ -310,7 +315,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded on device; BASELINE.md §4 construction)",
             "config": {"workload": args.workload, "desc": wl["desc"], "batch_per_gpu": B, "n": n, "k": k,
-                       "tau2": tau2, "parallelism": f"batch-sharded x{world}",
+                       "tau2": tau2, "parallelism": f"batch-sharded x{world}", "layout_tile": L.tile,
                        "l2": "inputs (%.2f GB/GPU) exceed the 126 MB L2; no flush needed" % (B * n * (k + 1) * 8 / 1e9)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(round(launches_per_step * args.steps)),
@@ -334,18 +339,20 @@ def e2e_run(args, L, y, tau2, out, world, dev):
 
     loss, lbar, tbar, st = out
     # the user's data: pinned host buffers in the reference storage layout
-    hL = torch.empty(L.data.shape, dtype=L.data.dtype, pin_memory=True)
-    hy = torch.empty(y.data.shape, dtype=y.data.dtype, pin_memory=True)
-    hL.copy_(L.data)
-    hy.copy_(y.data)
+    Lr, yr = L.to_reference(), y.to_reference()
+    hL = torch.empty(Lr.shape, dtype=Lr.dtype, pin_memory=True)
+    hy = torch.empty(yr.shape, dtype=yr.dtype, pin_memory=True)
+    hL.copy_(Lr)
+    hy.copy_(yr)
+    del Lr, yr
     hout = (torch.empty(L.batch, dtype=torch.float64, pin_memory=True),
-            torch.empty(lbar.data.shape, dtype=torch.float64, pin_memory=True),
+            torch.empty(hL.shape, dtype=torch.float64, pin_memory=True),
             torch.empty(L.batch, dtype=torch.float64, pin_memory=True))
     hLb = hout[1]
 
     def step():
         # public host-buffer API: chunked H2D -> fused sweeps -> D2H, overlapped
-        hloss, _, htb = marginal_likelihood_grad_host(hL, hy, tau2, out_host=hout)
+        hloss, _, htb = marginal_likelihood_grad_host(hL, hy, tau2, out_host=hout, tile=L.tile)
         if world > 1:
             reduce_totals([hloss.to(dev, non_blocking=True), htb.to(dev, non_blocking=True)])
 

@@ -205,6 +205,15 @@ class Bands:
     def numpy(self) -> np.ndarray:
         return self.to_reference().cpu().numpy()
 
+    def to_tile(self, tile: int, out: "Bands | None" = None) -> "Bands":
+        """Copy into the `tile` interleave (1 = reference layout, 32)."""
+        if out is None:
+            out = Bands.empty(self.batch, self.n, self.lower, self.upper, tile, self.dtype, self.data.device)
+        if out.tile != tile or (out.batch, out.n, out.lower, out.upper) != (self.batch, self.n, self.lower, self.upper):
+            raise DimensionMismatch("to_tile: output does not match")
+        _call("bgm_relayout_band", self.desc(), out.desc(), _stream())
+        return out
+
     def transpose(self) -> "Bands":
         """bandgm::transpose (banded.cpp:159-167), materialized."""
         out = self.like(self.upper, self.lower)
@@ -285,6 +294,14 @@ class Vecs:
 
     def numpy(self) -> np.ndarray:
         return self.to_reference().cpu().numpy()
+
+    def to_tile(self, tile: int, out: "Vecs | None" = None) -> "Vecs":
+        if out is None:
+            out = Vecs.empty(self.batch, self.n, tile, self.dtype, self.data.device)
+        if out.tile != tile or (out.batch, out.n) != (self.batch, self.n):
+            raise DimensionMismatch("to_tile: output does not match")
+        _call("bgm_relayout_vec", self.desc(), out.desc(), _stream())
+        return out
 
 
 # --------------------------------------------------------------------- status

@@ -142,7 +142,12 @@ using namespace bgm;
 extern "C" {
 
 int bgm_debug_repairs(int64_t* count, double* max_dev, int reset) {
-  return mlik_repairs(count, max_dev, reset);
+  int64_t c = 0;
+  const int rc = mlik_repairs(&c, max_dev, reset);
+  if (rc != BGM_OK) return rc;
+  const int rc2 = t1::repairs(&c, reset);
+  if (count) *count = c;
+  return rc2;
 }
 
 int bgm_set_segment_rows(int64_t rows) {
@@ -162,7 +167,9 @@ int bgm_marginal_likelihood_grad(bgm_band l, bgm_vec y, double tau2, double* los
     return BGM_ERR_DIM;
   if (l.batch == 0 || l.n == 0) return BGM_OK;
   auto s = static_cast<cudaStream_t>(stream);
-  const int rc = mlik_fast(l, y, tau2, loss, lbar, tau2_bar, status, row, g_segment_rows, s);
+  int rc = mlik_t1(l, y, tau2, loss, lbar, tau2_bar, status, row, g_segment_rows, s);
+  if (rc >= 0) return rc;
+  rc = mlik_fast(l, y, tau2, loss, lbar, tau2_bar, status, row, g_segment_rows, s);
   if (rc >= 0) return rc;
   // Generic path: one thread per matrix, scratch for Lp, w, S, u.
   const ix padded = (l.batch + 31) / 32 * 32;

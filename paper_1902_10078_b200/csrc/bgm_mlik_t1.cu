@@ -1,0 +1,624 @@
+// Config-3 sweeps, one thread per (matrix, segment): tile-32 layout.
+//
+// Same mathematics, segmentation, burn-in, verification and exact repair as
+// bgm_mlik_fast.cu (see its header), but each unit is a single thread:
+//   * a warp is 32 consecutive matrices of one 32-matrix tile working on the
+//     same segment, so every L / Lp / L_bar / y access is one coalesced
+//     256-byte warp transaction in the batch-interleaved layout;
+//   * the (K+1)x(K+1) Schur window (forward) and the KxK inverse-subset
+//     window (reverse) live in shared memory as packed lower triangles laid
+//     out [entry][thread] (conflict-free), and are shifted physically as they
+//     are updated -- every live entry is read and written once per row;
+//   * no shuffles, no warp barriers, no per-lane roles: the code is a compact
+//     rolled loop and lanes never diverge (units of one warp share a segment).
+// Per row the forward does the two rank-1 updates of the window (l l^T and
+// -c c^T, ~K^2 FMAs) and the reverse the two K-term mat-vecs (S(., j) and the
+// L_bar column) off one read of each window entry.  Both are bound by shared
+// memory bandwidth at ~2(K+1)K/2 accesses per row.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+
+#include "bgm_common.cuh"
+#include "bgm_fast.cuh"
+#include "bgm_mlik.cuh"
+#include "bgm_timing.cuh"
+
+namespace bgm {
+namespace t1 {
+namespace {
+
+constexpr double kLn2 = 0.69314718055994530942;
+constexpr double kLog2Pi = 1.8378770664093454836;  // inference.cpp:15
+constexpr double kCheckTol = 1e-12;
+// One warp per block: shared memory, not threads, bounds residency.  Window
+// entries of one thread are kThreads doubles apart ([entry][thread]).
+constexpr int kThreads = 32;
+
+template <int K>
+struct Shape {
+  static constexpr int W = K + 1;                // storage rows per column
+  static constexpr int NF = W * (W + 1) / 2;     // forward window entries (packed)
+  static constexpr int NB = K * (K + 1) / 2;     // reverse window entries (packed)
+  static constexpr int SIDE = K * (W + 1);       // forward check: K columns x (W + w)
+  static constexpr int STATE = NB + K;           // reverse check: window + u
+};
+
+__host__ __device__ constexpr int tri(int a, int b) { return a * (a + 1) / 2 + b; }  // a >= b
+
+struct Geo {
+  ix batch, n, seg;
+  int nseg, burn, debug;
+  ix tiles;  // ceil(batch / 32)
+};
+
+struct FwdP {
+  const double* L;  // tile 32
+  const double* y;  // tile 32
+  double* lp;       // Lp scratch (tile 32), storage row 0 = 1/Lp(i,i)
+  double* w;        // w = Lp^-1 y (tile 32)
+  double* side;     // [unit][SIDE]
+  double* part;     // [unit][4]
+  int64_t* fail;
+  int32_t* flag;
+  double sigma;
+};
+
+struct BwdP {
+  const double* L;
+  const double* lp;
+  const double* w;
+  double* lbar;
+  double* entry;  // [unit][STATE]
+  double* exitb;  // [unit][STATE]
+  double* part;   // [unit][2]
+  double c4;
+};
+
+__device__ unsigned long long g_repairs_t1 = 0;
+
+// Unit = (tile, segment, lane): thread index layout  [tile][segment][lane].
+struct Unit {
+  ix b;      // matrix
+  int p;     // segment
+  ix id;     // unit id = b * nseg + p (part / side / state slots)
+  bool live; // b < batch
+};
+__device__ __forceinline__ Unit unit_of(const Geo& G, ix gtid) {
+  const ix lane = gtid & 31, warp = gtid >> 5;
+  const ix tile = warp / G.nseg;
+  Unit u;
+  u.p = int(warp % G.nseg);
+  u.b = tile * 32 + lane;
+  u.live = tile < G.tiles && u.b < G.batch;
+  u.id = u.b * G.nseg + u.p;
+  return u;
+}
+
+// tile-32 addressing: band cell (r, j) of matrix b / vector element i
+__device__ __forceinline__ ix boff(ix b, ix n, int W, ix j, int r) {
+  return (((b >> 5) * n + j) * W + r) * 32 + (b & 31);
+}
+__device__ __forceinline__ ix voff(ix b, ix n, ix i) { return ((b >> 5) * n + i) * 32 + (b & 31); }
+
+template <bool SAFE>
+__device__ __forceinline__ double rsq(double d) {
+  if (SAFE) return rsqrt(d);
+  double r = double(rsqrtf(float(d)));
+  const double h = 0.5 * d;
+  r = r * fma(-h * r, r, 1.5);
+  return r * fma(-h * r, r, 1.5);
+}
+template <bool SAFE>
+__device__ __forceinline__ double rcp(double x) {
+  if (SAFE) return __drcp_rn(x);
+  double r = double(__frcp_rn(float(x)));
+  r = r * fma(-x, r, 2.0);
+  return r * fma(-x, r, 2.0);
+}
+
+// Warp-wide L2 prefetch of the contiguous per-tile block of one column
+// (all 32 matrices' copies of W cells) -- one bulk request from lane 0.
+__device__ __forceinline__ void l2_prefetch(const double* p, unsigned bytes) {
+  if ((threadIdx.x & 31) == 0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// ------------------------------------------------------------------ forward
+// Rows [s, e) owned, sweep from i0.  win: this thread's window.
+template <int K, bool SAFE>
+__device__ void fwd_unit(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, double* side,
+                         double* part, double* win, bool write) {
+  constexpr int ts = kThreads;
+  using Sh = Shape<K>;
+  constexpr int W = Sh::W;
+  const ix n = G.n;
+  auto Wr = [&](int a, int c) -> double& { return win[tri(a, c) * ts]; };
+#pragma unroll 1
+  for (int q = 0; q < Sh::NF; ++q) win[q * ts] = 0.0;
+  double res[W];  // solve residuals of window rows i .. i+K
+#pragma unroll
+  for (int a = 0; a < W; ++a) res[a] = (i0 + a < n) ? P.y[voff(b, n, i0 + a)] : 0.0;
+  double yy = 0.0, ww = 0.0, prodp = 1.0, prodl = 1.0;
+  int ep = 0, el = 0;
+  ix fail = n;
+  bool odd = false;
+#pragma unroll
+  for (int a = 0; a < W; ++a)
+    if (i0 + a >= s && i0 + a < e) yy += res[a] * res[a];
+  double lcur[W];
+#pragma unroll
+  for (int r = 0; r < W; ++r) lcur[r] = (i0 + r < n) ? P.L[boff(b, n, W, i0, r)] : 0.0;
+#pragma unroll 1
+  for (ix i = i0; i < e; ++i) {
+    // prefetch next column of L (one row ahead covers HBM latency: a row
+    // costs ~K^2 shared-memory accesses per lane)
+    double lnext[W];
+#pragma unroll
+    for (int r = 0; r < W; ++r) lnext[r] = (i + 1 + r < n) ? P.L[boff(b, n, W, i + 1, r)] : 0.0;
+    const double ynew = (i + W < n) ? P.y[voff(b, n, i + W)] : 0.0;
+    const double* l = lcur;
+    // pivot column of the window (row K is fresh: zero before this row)
+    const double d = Wr(0, 0) + fma(l[0], l[0], P.sigma);
+    const double rs = rsq<SAFE>(d);
+    double c[W];
+    c[0] = d * rs;
+#pragma unroll
+    for (int a = 1; a < K; ++a) c[a] = fma(l[a], l[0], Wr(a, 0)) * rs;
+    c[K] = l[K] * l[0] * rs;
+    const double wi = res[0] * rs;
+    const bool own = i >= s;
+    if (write && own) {
+      P.lp[boff(b, n, W, i, 0)] = rs;
+#pragma unroll
+      for (int a = 1; a < W; ++a) P.lp[boff(b, n, W, i, a)] = c[a];
+      P.w[voff(b, n, i)] = wi;
+      const double al = fabs(l[0]);
+      if (SAFE) {
+        if (!(d > kPivotFloor) || !(al > kPivotFloor)) fail = i < fail ? i : fail;
+      } else {
+        odd |= !(d > 1e-30) | !(d < 1e30) | !(al > 1e-30) | !(al < 1e30);
+      }
+      prodp *= c[0];
+      prodl *= al;
+      ww += wi * wi;
+      if ((i & 7) == 7) {
+        int x;
+        prodp = frexp(prodp, &x);
+        ep += x;
+        prodl = frexp(prodl, &x);
+        el += x;
+      }
+    } else if (write && side && i >= s - K) {
+      double* sd = side + (i - (s - K)) * (W + 1);
+      sd[0] = rs;
+#pragma unroll
+      for (int a = 1; a < W; ++a) sd[a] = c[a];
+      sd[W] = wi;
+    }
+    if (i + W >= s && i + W < e) yy += ynew * ynew;
+    // residuals: shift and eliminate w_i
+#pragma unroll
+    for (int a = 1; a < W; ++a) res[a - 1] = fma(-c[a], wi, res[a]);
+    res[K] = ynew;
+    // window: W'(a-1, c-1) = W(a, c) + l_a l_c - c_a c_c, rows 1..K-1 read,
+    // row K fresh; increasing packed index = in-place memmove order
+#pragma unroll
+    for (int a = 1; a < K; ++a) {
+#pragma unroll
+      for (int cc = 1; cc <= a; ++cc)
+        Wr(a - 1, cc - 1) = fma(l[a], l[cc], fma(-c[a], c[cc], Wr(a, cc)));
+    }
+#pragma unroll
+    for (int cc = 1; cc <= K; ++cc) Wr(K - 1, cc - 1) = fma(l[K], l[cc], -c[K] * c[cc]);
+#pragma unroll
+    for (int cc = 0; cc <= K; ++cc) Wr(K, cc) = 0.0;
+#pragma unroll
+    for (int r = 0; r < W; ++r) lcur[r] = lnext[r];
+  }
+  if (write) {
+    part[0] = log(prodp) + ep * kLn2;
+    part[1] = log(prodl) + el * kLn2;
+    part[2] = yy;
+    part[3] = ww;
+    if (SAFE && fail < n)
+      atomicMin(reinterpret_cast<unsigned long long*>(P.fail + b), static_cast<unsigned long long>(fail));
+    if (!SAFE && odd) P.flag[b] = 1;
+  }
+}
+
+template <int K>
+__global__ void k_fwd(FwdP P, Geo G) {
+  extern __shared__ double sm[];
+  const ix gt = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  const Unit u = unit_of(G, gt);
+  if (!u.live) return;
+  const ix s = ix(u.p) * G.seg;
+  const ix e = s + G.seg < G.n ? s + G.seg : G.n;
+  const ix i0 = s - G.burn > 0 ? s - G.burn : 0;
+  fwd_unit<K, false>(P, G, u.b, s, e, i0, u.p > 0 ? P.side + u.id * Shape<K>::SIDE : nullptr,
+                     P.part + u.id * 4, sm + threadIdx.x, true);
+}
+
+template <int K>
+__global__ void k_check_fwd(FwdP P, Geo G) {
+  using Sh = Shape<K>;
+  constexpr int W = Sh::W;
+  const ix id = blockIdx.x * ix(blockDim.x) + threadIdx.x;  // unit id = b * nseg + p
+  if (id >= G.batch * G.nseg) return;
+  const int p = int(id % G.nseg);
+  if (p == 0) return;
+  const ix b = id / G.nseg, n = G.n, s = ix(p) * G.seg;
+  const double* sd = P.side + id * Sh::SIDE;
+  double wscale = 0.0;
+  for (int c = 0; c < K; ++c) wscale = fmax(wscale, fabs(P.w[voff(b, n, s - K + c)]));
+  bool bad = false;
+  for (int c = 0; c < K; ++c) {
+    const ix col = s - K + c;
+    double sc = 0.0;
+    for (int r = 0; r < W; ++r) sc = fmax(sc, fabs(P.lp[boff(b, n, W, col, r)]));
+    for (int r = 0; r <= W; ++r) {
+      const double ref = r < W ? P.lp[boff(b, n, W, col, r)] : P.w[voff(b, n, col)];
+      const double rel = fabs(sd[c * (W + 1) + r] - ref) / ((r < W ? sc : wscale) + 1e-300);
+      if (!(rel <= kCheckTol)) {
+        if (G.debug && !bad)
+          printf("t1 fwd check b=%lld p=%d col=%lld r=%d burn=%.17g real=%.17g\n", (long long)b, p,
+                 (long long)col, r, sd[c * (W + 1) + r], ref);
+        bad = true;
+      }
+    }
+  }
+  if (bad) P.flag[b] = 1;
+}
+
+// One thread per matrix: flagged matrices rerun as one exact sweep.
+template <int K>
+__global__ void k_repair_fwd(FwdP P, Geo G) {
+  extern __shared__ double sm[];
+  const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (b >= G.batch || !P.flag[b]) return;
+  atomicAdd(&g_repairs_t1, 1ull);
+  P.fail[b] = G.n;
+  double* part0 = P.part + b * G.nseg * 4;
+  for (int q = 4; q < G.nseg * 4; ++q) part0[q] = 0.0;
+  fwd_unit<K, true>(P, G, b, 0, G.n, 0, nullptr, part0, sm + threadIdx.x, true);
+}
+
+// ------------------------------------------------------------------ reverse
+// Window: S over rows j+1 .. j+K (index x <-> row j+1+x), packed lower
+// triangle; u over the same rows.
+template <int K, bool SAFE>
+__device__ void bwd_unit(const BwdP& P, const Geo& G, ix b, ix s, ix e, ix jtop, double* entry,
+                         double* exitb, double* part, double* win) {
+  constexpr int ts = kThreads;
+  using Sh = Shape<K>;
+  constexpr int W = Sh::W;
+  const ix n = G.n;
+  auto Sr = [&](int x, int y) -> double& { return win[tri(x, y) * ts]; };
+#pragma unroll 1
+  for (int q = 0; q < Sh::NB; ++q) win[q * ts] = 0.0;
+  double u[K];
+#pragma unroll
+  for (int x = 0; x < K; ++x) u[x] = 0.0;
+  double tr = 0.0, uu = 0.0;
+  auto save = [&](double* dst) {
+#pragma unroll 1
+    for (int q = 0; q < Sh::NB; ++q) dst[q] = win[q * ts];
+#pragma unroll
+    for (int x = 0; x < K; ++x) dst[Sh::NB + x] = u[x];
+  };
+  constexpr int kAhead = 4;  // rows of L2 prefetch ahead of the sweep
+  auto prefetch = [&](ix j) {
+    if (j >= 0 && j < n) {
+      l2_prefetch(P.lp + boff(b & ~ix(31), n, W, j, 0), W * 256);
+      l2_prefetch(P.L + boff(b & ~ix(31), n, W, j, 0), W * 256);
+    }
+  };
+#pragma unroll 1
+  for (int d = 0; d < kAhead; ++d) prefetch(jtop - d);
+#pragma unroll 1
+  for (ix j = jtop; j >= s; --j) {
+    if (entry && j == e - 1) save(entry);  // boundary window [e, e+K) reached by burn-in
+    prefetch(j - kAhead);
+    double lpc[W], lc[W];
+#pragma unroll
+    for (int r = 0; r < W; ++r) {
+      const bool cell = j + r < n;  // input corner cells are not trusted
+      lpc[r] = cell ? P.lp[boff(b, n, W, j, r)] : 0.0;
+      lc[r] = cell ? P.L[boff(b, n, W, j, r)] : 0.0;
+    }
+    const double wc = P.w[voff(b, n, j)];
+    const double inv = lpc[0], ljj = lc[0];
+    // mat-vecs against the window: out = S lp(1..K), accl = S L(1..K).  Each
+    // entry is read once and immediately written to its place in the next
+    // window, (x, y) -> (x+1, y+1); decreasing packed index = memmove order.
+    double out[K], accl[K];
+#pragma unroll
+    for (int x = 0; x < K; ++x) out[x] = accl[x] = 0.0;
+#pragma unroll
+    for (int x = K - 1; x >= 0; --x) {
+#pragma unroll
+      for (int y = x; y >= 0; --y) {
+        const double sv = Sr(x, y);
+        if (x < K - 1) Sr(x + 1, y + 1) = sv;
+        out[x] = fma(sv, lpc[y + 1], out[x]);
+        accl[x] = fma(sv, lc[y + 1], accl[x]);
+        if (y != x) {
+          out[y] = fma(sv, lpc[x + 1], out[y]);
+          accl[y] = fma(sv, lc[x + 1], accl[y]);
+        }
+      }
+    }
+    double ra = 0.0, rb = 0.0, rc = 0.0, rd = 0.0;
+#pragma unroll
+    for (int x = 0; x < K; ++x) {
+      out[x] *= inv;
+      ra = fma(lpc[x + 1], out[x], ra);
+      rb = fma(lpc[x + 1], u[x], rb);
+      rc = fma(u[x], lc[x + 1], rc);
+      rd = fma(out[x], lc[x + 1], rd);
+    }
+    const double sjj = inv * inv + inv * ra;
+    const double uj = (wc - rb) * inv;
+    const double ul = uj * ljj + rc;
+    if (j < e) {
+      P.lbar[boff(b, n, W, j, 0)] = rd - sjj * ljj - P.c4 * uj * ul + rcp<SAFE>(ljj);
+#pragma unroll
+      for (int x = 0; x < K; ++x)
+        P.lbar[boff(b, n, W, j, x + 1)] =
+            (j + 1 + x < n) ? -(accl[x] - out[x] * ljj) - P.c4 * u[x] * ul : 0.0;
+      tr += sjj;
+      uu += uj * uj;
+    }
+    // new window rows j .. j+K-1: row/column 0 is the new one
+    Sr(0, 0) = sjj;
+#pragma unroll
+    for (int x = 1; x < K; ++x) Sr(x, 0) = -out[x - 1];
+#pragma unroll
+    for (int x = K - 1; x >= 1; --x) u[x] = u[x - 1];
+    u[0] = uj;
+  }
+  if (exitb) save(exitb);
+  part[0] = tr;
+  part[1] = uu;
+}
+
+template <int K>
+__global__ void k_bwd(BwdP P, Geo G) {
+  extern __shared__ double sm[];
+  const ix gt = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  const Unit u = unit_of(G, gt);
+  if (!u.live) return;
+  const ix s = ix(u.p) * G.seg;
+  const ix e = s + G.seg < G.n ? s + G.seg : G.n;
+  ix jtop = e + G.burn - 1;
+  if (jtop > G.n - 1) jtop = G.n - 1;
+  bwd_unit<K, false>(P, G, u.b, s, e, jtop,
+                     u.p + 1 < G.nseg ? P.entry + u.id * Shape<K>::STATE : nullptr,
+                     u.p > 0 ? P.exitb + u.id * Shape<K>::STATE : nullptr, P.part + u.id * 2,
+                     sm + threadIdx.x);
+}
+
+template <int K>
+__global__ void k_check_bwd(BwdP P, Geo G, int32_t* flag) {
+  using Sh = Shape<K>;
+  const ix id = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (id >= G.batch * G.nseg) return;
+  const int p = int(id % G.nseg);
+  if (p + 1 >= G.nseg) return;
+  const ix b = id / G.nseg;
+  const double* a = P.entry + id * Sh::STATE;
+  const double* r = P.exitb + (id + 1) * Sh::STATE;
+  double ss = 0.0, us = 0.0;
+  for (int q = 0; q < Sh::NB; ++q) ss = fmax(ss, fabs(r[q]));
+  for (int q = Sh::NB; q < Sh::STATE; ++q) us = fmax(us, fabs(r[q]));
+  bool bad = false;
+  for (int q = 0; q < Sh::STATE; ++q) {
+    const double rel = fabs(a[q] - r[q]) / ((q < Sh::NB ? ss : us) + 1e-300);
+    if (!(rel <= kCheckTol)) {
+      if (G.debug && !bad)
+        printf("t1 bwd check b=%lld p=%d slot=%d burn=%.17g real=%.17g\n", (long long)b, p, q, a[q],
+               r[q]);
+      bad = true;
+    }
+  }
+  if (bad) flag[b] = 1;
+}
+
+template <int K>
+__global__ void k_repair_bwd(BwdP P, Geo G, const int32_t* flag, const int64_t* fail) {
+  extern __shared__ double sm[];
+  const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (b >= G.batch || !flag[b] || fail[b] < G.n) return;
+  atomicAdd(&g_repairs_t1, 1ull);
+  double* part0 = P.part + b * G.nseg * 2;
+  for (int q = 2; q < G.nseg * 2; ++q) part0[q] = 0.0;
+  bwd_unit<K, true>(P, G, b, 0, G.n, G.n - 1, nullptr, nullptr, part0, sm + threadIdx.x);
+}
+
+__global__ void k_finalize(const double* pf, const double* pb, const int64_t* fail, Geo Gf, Geo Gb,
+                           double tau2, double* loss, double* tau2_bar, int32_t* status,
+                           int64_t* row) {
+  const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (b >= Gf.batch) return;
+  double ldp = 0, ldl = 0, yy = 0, ww = 0, tr = 0, uu = 0;
+  for (int p = 0; p < Gf.nseg; ++p) {
+    const double* f = pf + (b * Gf.nseg + p) * 4;
+    ldp += f[0];
+    ldl += f[1];
+    yy += f[2];
+    ww += f[3];
+  }
+  for (int p = 0; p < Gb.nseg; ++p) {
+    tr += pb[(b * Gb.nseg + p) * 2];
+    uu += pb[(b * Gb.nseg + p) * 2 + 1];
+  }
+  const double nn = double(Gf.n), inv = 1.0 / tau2, c4 = inv * inv;
+  loss[b] = -0.5 * nn * kLog2Pi - ldp + ldl - 0.5 * nn * log(tau2) - 0.5 * yy * inv + 0.5 * ww * c4;
+  tau2_bar[b] = -nn * 0.5 * inv + 0.5 * yy * c4 + 0.5 * c4 * tr - ww * c4 * inv + 0.5 * uu * c4 * c4;
+  const bool ok = fail[b] >= Gf.n;
+  if (status) status[b] = ok ? BGM_OK : BGM_ERR_NOT_PD;
+  if (row) row[b] = ok ? -1 : fail[b];
+}
+
+__global__ void k_init(int64_t* fail, int32_t* flag, ix batch, ix n) {
+  const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (b >= batch) return;
+  fail[b] = n;
+  flag[b] = 0;
+  flag[batch + b] = 0;
+}
+
+
+ix seg_for(ix n, ix tiles, ix warps_resident, int burn, ix requested) {
+  ix seg = requested;
+  if (seg <= 0) {
+    ix per = warps_resident / (tiles > 0 ? tiles : 1);
+    if (per < 1) per = 1;
+    seg = (n + per - 1) / per;
+    if (seg < 2 * burn) seg = 2 * burn;
+  }
+  return seg < 1 ? 1 : seg;
+}
+
+template <int K>
+int run(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, const bgm_band& lbar,
+        double* tau2_bar, int32_t* status, int64_t* row, int segment_rows, cudaStream_t s) {
+  using Sh = Shape<K>;
+  Geo G;
+  G.batch = l.batch;
+  G.n = l.n;
+  G.tiles = (l.batch + 31) / 32;
+  G.burn = 128;
+  if (const char* bv = std::getenv("BGM_BURN"))
+    if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
+  G.debug = std::getenv("BGM_DEBUG") != nullptr;
+  const size_t smf = sizeof(double) * Sh::NF * kThreads, smb = sizeof(double) * Sh::NB * kThreads;
+  static bool attrs = false;
+  if (!attrs) {
+    cudaFuncSetAttribute(k_fwd<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smf));
+    cudaFuncSetAttribute(k_repair_fwd<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smf));
+    cudaFuncSetAttribute(k_bwd<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smb));
+    cudaFuncSetAttribute(k_repair_bwd<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smb));
+    attrs = true;
+  }
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int bf = 1, bb = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, k_fwd<K>, kThreads, smf);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bb, k_bwd<K>, kThreads, smb);
+  Geo Gf = G, Gb = G;
+  Gf.seg = seg_for(G.n, G.tiles, ix(sms) * (bf > 0 ? bf : 1), G.burn, segment_rows);
+  Gb.seg = seg_for(G.n, G.tiles, ix(sms) * (bb > 0 ? bb : 1), G.burn, segment_rows);
+  Gf.nseg = int((G.n + Gf.seg - 1) / Gf.seg);
+  Gb.nseg = int((G.n + Gb.seg - 1) / Gb.seg);
+  const ix uf = G.batch * Gf.nseg, ub = G.batch * Gb.nseg;
+
+  const size_t nb = size_t(G.tiles) * 32 * size_t(G.n);
+  const size_t bytes = sizeof(double) * (nb * Sh::W + nb + size_t(uf) * (Sh::SIDE + 4) +
+                                         size_t(ub) * (2 * Sh::STATE + 2)) +
+                       sizeof(int64_t) * size_t(G.batch) + sizeof(int32_t) * 2 * size_t(G.batch) + 256;
+  char* ws = nullptr;
+  cudaError_t err = scratch_alloc(reinterpret_cast<void**>(&ws), bytes, s);
+  if (err != cudaSuccess) return set_error(err);
+  double* dp = reinterpret_cast<double*>(ws);
+  FwdP F;
+  BwdP Bp;
+  F.L = static_cast<const double*>(l.data);
+  F.y = static_cast<const double*>(y.data);
+  F.lp = dp;
+  dp += nb * Sh::W;
+  F.w = dp;
+  dp += nb;
+  F.side = dp;
+  dp += size_t(uf) * Sh::SIDE;
+  F.part = dp;
+  dp += size_t(uf) * 4;
+  Bp.entry = dp;
+  dp += size_t(ub) * Sh::STATE;
+  Bp.exitb = dp;
+  dp += size_t(ub) * Sh::STATE;
+  Bp.part = dp;
+  dp += size_t(ub) * 2;
+  F.fail = reinterpret_cast<int64_t*>(dp);
+  int32_t* flags = reinterpret_cast<int32_t*>(F.fail + G.batch);
+  F.flag = flags;
+  F.sigma = 1.0 / tau2;
+  Bp.L = F.L;
+  Bp.lp = F.lp;
+  Bp.w = F.w;
+  Bp.lbar = static_cast<double*>(lbar.data);
+  Bp.c4 = F.sigma * F.sigma;
+
+  const unsigned gf = unsigned(G.tiles * Gf.nseg), gb = unsigned(G.tiles * Gb.nseg);
+  const unsigned mb = unsigned((G.batch + kThreads - 1) / kThreads);
+  {
+    timing::Scope ts("mlik_init", s);
+    k_init<<<blocks_for(G.batch, 128), 128, 0, s>>>(F.fail, flags, G.batch, G.n);
+  }
+  {
+    timing::Scope ts("mlik_t1_fwd", s);
+    k_fwd<K><<<gf, kThreads, smf, s>>>(F, Gf);
+  }
+  {
+    timing::Scope ts("mlik_check_fwd", s);
+    k_check_fwd<K><<<unsigned((uf + 127) / 128), 128, 0, s>>>(F, Gf);
+  }
+  {
+    timing::Scope ts("mlik_repair_fwd", s);
+    k_repair_fwd<K><<<mb, kThreads, smf, s>>>(F, Gf);
+  }
+  {
+    timing::Scope ts("mlik_t1_bwd", s);
+    k_bwd<K><<<gb, kThreads, smb, s>>>(Bp, Gb);
+  }
+  {
+    timing::Scope ts("mlik_check_bwd", s);
+    k_check_bwd<K><<<unsigned((ub + 127) / 128), 128, 0, s>>>(Bp, Gb, flags + G.batch);
+  }
+  {
+    timing::Scope ts("mlik_repair_bwd", s);
+    k_repair_bwd<K><<<mb, kThreads, smb, s>>>(Bp, Gb, flags + G.batch, F.fail);
+  }
+  {
+    timing::Scope ts("mlik_finalize", s);
+    k_finalize<<<blocks_for(G.batch, 128), 128, 0, s>>>(F.part, Bp.part, F.fail, Gf, Gb, tau2, loss,
+                                                        tau2_bar, status, row);
+  }
+  err = cudaGetLastError();
+  scratch_free(ws, s);
+  return err == cudaSuccess ? BGM_OK : set_error(err);
+}
+
+}  // namespace
+
+int repairs(int64_t* count, int reset) {
+  unsigned long long v = 0;
+  cudaError_t e = cudaMemcpyFromSymbol(&v, g_repairs_t1, sizeof v);
+  if (e != cudaSuccess) return set_error(e);
+  if (count) *count += int64_t(v);
+  if (reset) {
+    v = 0;
+    e = cudaMemcpyToSymbol(g_repairs_t1, &v, sizeof v);
+    if (e != cudaSuccess) return set_error(e);
+  }
+  return BGM_OK;
+}
+
+}  // namespace t1
+
+// tile-32 inputs with a supported bandwidth -> one-thread-per-unit sweeps
+int mlik_t1(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, const bgm_band& lbar,
+            double* tau2_bar, int32_t* status, int64_t* row, int segment_rows, cudaStream_t s) {
+  if (fast::disabled()) return -1;
+  if (l.tile != 32 || y.tile != 32 || lbar.tile != 32) return -1;
+  switch (l.lower) {
+    case 16: return t1::run<16>(l, y, tau2, loss, lbar, tau2_bar, status, row, segment_rows, s);
+    case 8: return t1::run<8>(l, y, tau2, loss, lbar, tau2_bar, status, row, segment_rows, s);
+    case 4: return t1::run<4>(l, y, tau2, loss, lbar, tau2_bar, status, row, segment_rows, s);
+    default: return -1;
+  }
+}
+
+}  // namespace bgm

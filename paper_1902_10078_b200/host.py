@@ -15,11 +15,16 @@ from .api import Bands, Vecs, marginal_likelihood_grad, new_status
 
 
 def marginal_likelihood_grad_host(L_host: torch.Tensor, y_host: torch.Tensor, tau2: float,
-                                  out_host=None, chunk: int = 32, streams: int = 3, device=None):
+                                  out_host=None, chunk: int = 32, streams: int = 3, device=None,
+                                  tile: int = 32):
     """Config-3 learning step on host buffers.
 
     L_host: (B, n, k+1) float64, the reference storage block per matrix
     (ideally pinned); y_host: (B, n).  Returns host (loss[B], l_bar, tau2_bar[B]).
+    With tile 32 each chunk is re-interleaved on the device (32 matrices side
+    by side) for the one-thread-per-unit sweeps and L_bar is brought back to
+    the reference layout before the copy out; tile 1 feeds the reference
+    layout to the kernels directly.
     """
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     B, n, w = L_host.shape
@@ -30,7 +35,11 @@ def marginal_likelihood_grad_host(L_host: torch.Tensor, y_host: torch.Tensor, ta
                     torch.empty_like(L_host, pin_memory=pin),
                     torch.empty(B, dtype=torch.float64, pin_memory=pin))
     loss_h, lbar_h, tbar_h = out_host
+    if tile not in (1, 32):
+        raise ValueError("tile must be 1 or 32")
     chunk = max(1, min(chunk, B))
+    if tile == 32:
+        chunk = (chunk + 31) // 32 * 32
     pool = [torch.cuda.Stream(device=dev) for _ in range(max(1, streams))]
     # per-stream device buffers, reused round-robin
     bufs = []
@@ -40,7 +49,9 @@ def marginal_likelihood_grad_host(L_host: torch.Tensor, y_host: torch.Tensor, ta
                      torch.empty((chunk, n, w), dtype=torch.float64, device=dev),
                      torch.empty(chunk, dtype=torch.float64, device=dev),
                      torch.empty(chunk, dtype=torch.float64, device=dev),
-                     new_status(chunk, dev)))
+                     new_status(chunk, dev),
+                     (Bands.empty(chunk, n, k, 0, 32, device=dev), Vecs.empty(chunk, n, 32, device=dev),
+                      Bands.empty(chunk, n, k, 0, 32, device=dev)) if tile == 32 else None))
     cur = torch.cuda.current_stream(dev)
     for s in pool:
         s.wait_stream(cur)
@@ -48,17 +59,32 @@ def marginal_likelihood_grad_host(L_host: torch.Tensor, y_host: torch.Tensor, ta
         b = min(B, a + chunk)
         m = b - a
         s = pool[ci % len(pool)]
-        dL, dy, dLb, dloss, dtb, st = bufs[ci % len(pool)]
+        dL, dy, dLb, dloss, dtb, st, t32 = bufs[ci % len(pool)]
         with torch.cuda.stream(s):
             dL[:m].copy_(L_host[a:b], non_blocking=True)
             dy[:m].copy_(y_host[a:b], non_blocking=True)
             Lb = Bands(dL[:m], m, n, k, 0, 1)
             Yv = Vecs(dy[:m], m, n, 1)
             Lbar = Bands(dLb[:m], m, n, k, 0, 1)
-            marginal_likelihood_grad(Lb, Yv, tau2, check=False, out=(dloss[:m], Lbar, dtb[:m], st))
+            if t32 is None:
+                marginal_likelihood_grad(Lb, Yv, tau2, check=False, out=(dloss[:m], Lbar, dtb[:m], st))
+            else:
+                L32, y32, Lbar32 = (_prefix(x, m) for x in t32)
+                Lb.to_tile(32, L32)
+                Yv.to_tile(32, y32)
+                marginal_likelihood_grad(L32, y32, tau2, check=False, out=(dloss[:m], Lbar32, dtb[:m], st))
+                Lbar32.to_tile(1, Lbar)
             lbar_h[a:b].copy_(dLb[:m], non_blocking=True)
             loss_h[a:b].copy_(dloss[:m], non_blocking=True)
             tbar_h[a:b].copy_(dtb[:m], non_blocking=True)
     for s in pool:
         cur.wait_stream(s)
     return loss_h, lbar_h, tbar_h
+
+
+def _prefix(x, m):
+    """The first m matrices of a tile-32 container (whole tiles + a partial one)."""
+    t = (m + 31) // 32
+    if isinstance(x, Bands):
+        return Bands(x.data[:t], m, x.n, x.lower, x.upper, 32)
+    return Vecs(x.data[:t], m, x.n, 32)

@@ -136,5 +136,10 @@ class GpuOracle:
         L = np.asarray(L)
         Lb = bgm.Bands.from_reference(L, L.shape[2] - 1, 0, tile=self.tile)
         Y = bgm.Vecs.from_reference(np.asarray(y), tile=self.tile)
-        loss, lbar, tbar = bgm.marginal_likelihood_grad(Lb, Y, tau2, check=False)
-        return self._np(loss), self._np(lbar), self._np(tbar), None, None
+        B = L.shape[0]
+        st = api.new_status(B, Lb.data.device)
+        out = (torch.empty(B, dtype=torch.float64, device=Lb.data.device), Lb.like(),
+               torch.empty(B, dtype=torch.float64, device=Lb.data.device), st)
+        loss, lbar, tbar = bgm.marginal_likelihood_grad(Lb, Y, tau2, check=False, out=out)
+        return (self._np(loss), self._np(lbar), self._np(tbar), st.st[:B].cpu().numpy(),
+                st.row[:B].cpu().numpy())

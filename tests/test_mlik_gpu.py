@@ -40,23 +40,29 @@ def test_mlik_matches_tape_composition(cuda, oracle, B, n, k, tau2):
 
 
 # ---------------------------------------------------------------- fast path
-# k = 16 in the tile-1 layout routes to the segment-parallel sweeps
-# (bgm_mlik_fast.cu); small segment lengths force many segments + burn-in.
+# k = 16 in the tile-1 layout routes to the team sweeps (bgm_mlik_fast.cu),
+# k in {4, 8, 16} in the tile-32 layout to the one-thread-per-unit sweeps
+# (bgm_mlik_t1.cu); small segment lengths force many segments + burn-in.
+FAST = [(1, 16), (32, 16), (32, 8), (32, 4)]
+
+
+@pytest.mark.parametrize("tile,k", FAST)
 @pytest.mark.parametrize("B,n,seg", [(2, 300, 0), (3, 1000, 64), (5, 2048, 128), (33, 777, 96),
-                                     (1, 17, 16), (4, 4096, 0)])
-def test_mlik_fast_segments(cuda, oracle, B, n, seg):
+                                     (1, 17, 16), (4, 4096, 0), (70, 1200, 0)])
+def test_mlik_fast_segments(cuda, oracle, B, n, seg, tile, k):
     from paper_1902_10078_b200 import api
     from tests.gpu_adapter import GpuOracle
     api.set_segment_rows(seg)
     try:
         api.debug_repairs(reset=True)
-        _check(GpuOracle(tile=1), oracle, B, n, 16, 0.01, seed=B * 7 + n)
+        _check(GpuOracle(tile=tile), oracle, B, n, k, 0.01, seed=B * 7 + n + k)
         assert api.debug_repairs() == 0  # well-conditioned: every burn-in converged
     finally:
         api.set_segment_rows(0)
 
 
-def test_mlik_fast_repair_path(cuda, oracle, monkeypatch):
+@pytest.mark.parametrize("tile", [1, 32])
+def test_mlik_fast_repair_path(cuda, oracle, monkeypatch, tile):
     """A 16-row burn-in cannot converge: the verification flags every
     segment boundary and the exact single-unit path reruns each matrix.
     Results must still match the reference."""
@@ -72,10 +78,30 @@ def test_mlik_fast_repair_path(cuda, oracle, monkeypatch):
     api.set_segment_rows(64)
     try:
         api.debug_repairs(reset=True)
-        lg, lbg, tbg, _, _ = GpuOracle(tile=1).marginal_likelihood_grad(L, y, tau2)
+        lg, lbg, tbg, _, _ = GpuOracle(tile=tile).marginal_likelihood_grad(L, y, tau2)
         reps = api.debug_repairs()
     finally:
         api.set_segment_rows(0)
     assert reps > 0
     for name, g, o in (("loss", lg, lo), ("l_bar", lbg, lb), ("tau2_bar", tbg, tb)):
         assert cm.max_rel_err(g, o, floor_scale=FLOOR) <= TOL, name
+
+
+@pytest.mark.parametrize("tile", [1, 32])
+def test_mlik_fast_not_pd(cuda, oracle, tile):
+    """A zero on L's diagonal mid-matrix: the reference throws at the
+    log-det of L (inference.cpp:143); the fused step reports that row."""
+    from paper_1902_10078_b200 import api
+    from tests.gpu_adapter import GpuOracle
+    rng = np.random.default_rng(11)
+    B, n, k = 3, 900, 16
+    L = cm.config_factor(rng, B, n, k)
+    L[1, 500, 0] = 0.0
+    y = rng.normal(0, 1, (B, n))
+    api.set_segment_rows(128)
+    try:
+        _, _, _, st, row = GpuOracle(tile=tile).marginal_likelihood_grad(L, y, 0.01)
+    finally:
+        api.set_segment_rows(0)
+    assert st[0] == 0 and st[2] == 0
+    assert st[1] != 0 and row[1] == 500
