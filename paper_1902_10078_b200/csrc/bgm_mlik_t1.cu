@@ -19,6 +19,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "bgm_common.cuh"
 #include "bgm_fast.cuh"
@@ -39,10 +40,11 @@ constexpr int kThreads = 32;
 template <int K>
 struct Shape {
   static constexpr int W = K + 1;                // storage rows per column
-  static constexpr int NF = W * (W + 1) / 2;     // forward window entries (packed)
+  static constexpr int NF = K * (K + 1) / 2;     // forward window entries (rows 0..K-1; row K is always fresh)
   static constexpr int NB = K * (K + 1) / 2;     // reverse window entries (packed)
   static constexpr int SIDE = K * (W + 1);       // forward check: K columns x (W + w)
   static constexpr int STATE = NB + K;           // reverse check: window + u
+  static constexpr int BSLOT = 2 * W + 1;        // reverse prefetch slot: Lp, L columns + w
 };
 
 __host__ __device__ constexpr int tri(int a, int b) { return a * (a + 1) / 2 + b; }  // a >= b
@@ -118,12 +120,20 @@ __device__ __forceinline__ double rcp(double x) {
   return r * fma(-x, r, 2.0);
 }
 
-// Warp-wide L2 prefetch of the contiguous per-tile block of one column
-// (all 32 matrices' copies of W cells) -- one bulk request from lane 0.
+// L2 prefetch of a contiguous block (all 32 matrices' copies of a column).
 __device__ __forceinline__ void l2_prefetch(const double* p, unsigned bytes) {
-  if ((threadIdx.x & 31) == 0)
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
+
+__device__ __forceinline__ void cpa8(double* dst, const double* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+using Plain = std::false_type;  // interior rows: no cell of the row's columns leaves the matrix
+using Edge = std::true_type;    // last rows: corner cells masked
 
 // ------------------------------------------------------------------ forward
 // Rows [s, e) owned, sweep from i0.  win: this thread's window.
@@ -150,14 +160,21 @@ __device__ void fwd_unit(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, d
   double lcur[W];
 #pragma unroll
   for (int r = 0; r < W; ++r) lcur[r] = (i0 + r < n) ? P.L[boff(b, n, W, i0, r)] : 0.0;
-#pragma unroll 1
-  for (ix i = i0; i < e; ++i) {
+  const ix cstep = ix(W) * 32;  // one column of one tile
+  constexpr int kAhead = 4;
+  auto row = [&](ix i, auto edge) {
+    constexpr bool EDGE = decltype(edge)::value;
+    const double* Lq = P.L + boff(b, n, W, i + 1, 0);
+    if ((threadIdx.x & 31) == 0) {  // L2 fill kAhead rows ahead of the loads below
+      if (i + 1 + kAhead < n) l2_prefetch(Lq + kAhead * cstep, W * 256);
+      if (i + W + kAhead < n) l2_prefetch(P.y + voff(b & ~ix(31), n, i + W + kAhead), 256);
+    }
     // prefetch next column of L (one row ahead covers HBM latency: a row
     // costs ~K^2 shared-memory accesses per lane)
     double lnext[W];
 #pragma unroll
-    for (int r = 0; r < W; ++r) lnext[r] = (i + 1 + r < n) ? P.L[boff(b, n, W, i + 1, r)] : 0.0;
-    const double ynew = (i + W < n) ? P.y[voff(b, n, i + W)] : 0.0;
+    for (int r = 0; r < W; ++r) lnext[r] = (!EDGE || i + 1 + r < n) ? Lq[r * 32] : 0.0;
+    const double ynew = (!EDGE || i + W < n) ? P.y[voff(b, n, i + W)] : 0.0;
     const double* l = lcur;
     // pivot column of the window (row K is fresh: zero before this row)
     const double d = Wr(0, 0) + fma(l[0], l[0], P.sigma);
@@ -170,9 +187,10 @@ __device__ void fwd_unit(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, d
     const double wi = res[0] * rs;
     const bool own = i >= s;
     if (write && own) {
-      P.lp[boff(b, n, W, i, 0)] = rs;
+      double* lpq = P.lp + (Lq - P.L) - cstep;
+      lpq[0] = rs;
 #pragma unroll
-      for (int a = 1; a < W; ++a) P.lp[boff(b, n, W, i, a)] = c[a];
+      for (int a = 1; a < W; ++a) lpq[a * 32] = c[a];
       P.w[voff(b, n, i)] = wi;
       const double al = fabs(l[0]);
       if (SAFE) {
@@ -202,8 +220,8 @@ __device__ void fwd_unit(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, d
 #pragma unroll
     for (int a = 1; a < W; ++a) res[a - 1] = fma(-c[a], wi, res[a]);
     res[K] = ynew;
-    // window: W'(a-1, c-1) = W(a, c) + l_a l_c - c_a c_c, rows 1..K-1 read,
-    // row K fresh; increasing packed index = in-place memmove order
+    // window: W'(a-1, c-1) = W(a, c) + l_a l_c - c_a c_c for rows 1..K-1,
+    // row K fresh (never stored); increasing packed index = memmove order
 #pragma unroll
     for (int a = 1; a < K; ++a) {
 #pragma unroll
@@ -213,10 +231,14 @@ __device__ void fwd_unit(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, d
 #pragma unroll
     for (int cc = 1; cc <= K; ++cc) Wr(K - 1, cc - 1) = fma(l[K], l[cc], -c[K] * c[cc]);
 #pragma unroll
-    for (int cc = 0; cc <= K; ++cc) Wr(K, cc) = 0.0;
-#pragma unroll
     for (int r = 0; r < W; ++r) lcur[r] = lnext[r];
-  }
+  };
+  // rows whose next column reaches past the matrix take the masked body
+  const ix split = n - 1 - K > i0 ? (n - 1 - K < e ? n - 1 - K : e) : i0;
+#pragma unroll 1
+  for (ix i = i0; i < split; ++i) row(i, Plain{});
+#pragma unroll 1
+  for (ix i = split; i < e; ++i) row(i, Edge{});
   if (write) {
     part[0] = log(prodp) + ep * kLn2;
     part[1] = log(prodl) + el * kLn2;
@@ -308,32 +330,48 @@ __device__ void bwd_unit(const BwdP& P, const Geo& G, ix b, ix s, ix e, ix jtop,
 #pragma unroll
     for (int x = 0; x < K; ++x) dst[Sh::NB + x] = u[x];
   };
-  constexpr int kAhead = 4;  // rows of L2 prefetch ahead of the sweep
-  auto prefetch = [&](ix j) {
-    if (j >= 0 && j < n) {
-      l2_prefetch(P.lp + boff(b & ~ix(31), n, W, j, 0), W * 256);
-      l2_prefetch(P.L + boff(b & ~ix(31), n, W, j, 0), W * 256);
+  // Lp / L columns of the current row live in registers; the next row's are
+  // loaded into the same registers as soon as the mat-vecs retire them (the
+  // row's tail covers the L2 latency; L2 is filled kAhead rows ahead).
+  constexpr int kAhead = 4;
+  auto l2_ahead = [&](ix j) {
+    if (j >= 0 && (threadIdx.x & 31) == 0) {
+      l2_prefetch(P.lp + boff(b, n, W, j, 0), W * 256);
+      l2_prefetch(P.L + boff(b, n, W, j, 0), W * 256);
+      l2_prefetch(P.w + voff(b, n, j), 256);
     }
   };
-#pragma unroll 1
-  for (int d = 0; d < kAhead; ++d) prefetch(jtop - d);
-#pragma unroll 1
-  for (ix j = jtop; j >= s; --j) {
-    if (entry && j == e - 1) save(entry);  // boundary window [e, e+K) reached by burn-in
-    prefetch(j - kAhead);
-    double lpc[W], lc[W];
+  double lpc[W], lc[W], wc;
+  auto load = [&](ix j, bool mask) {
+    const double* lpq = P.lp + boff(b, n, W, j, 0);
+    const double* lq = P.L + boff(b, n, W, j, 0);
 #pragma unroll
     for (int r = 0; r < W; ++r) {
-      const bool cell = j + r < n;  // input corner cells are not trusted
-      lpc[r] = cell ? P.lp[boff(b, n, W, j, r)] : 0.0;
-      lc[r] = cell ? P.L[boff(b, n, W, j, r)] : 0.0;
+      const bool cell = !mask || j + r < n;  // input corner cells are not trusted
+      lpc[r] = cell ? lpq[r * 32] : 0.0;
+      lc[r] = cell ? lq[r * 32] : 0.0;
     }
-    const double wc = P.w[voff(b, n, j)];
-    const double inv = lpc[0], ljj = lc[0];
+    wc = P.w[voff(b, n, j)];
+  };
+#pragma unroll 1
+  for (int d = 1; d <= kAhead; ++d) l2_ahead(jtop - d);
+  load(jtop, true);
+  auto row = [&](ix j, auto edge) {
+    constexpr bool EDGE = decltype(edge)::value;
+    if (entry && j == e - 1) save(entry);  // boundary window [e, e+K) reached by burn-in
+    l2_ahead(j - 1 - kAhead);
+    const double inv = lpc[0], ljj = lc[0], wj = wc;
+    double rb = 0.0, rc = 0.0;
+#pragma unroll
+    for (int x = 0; x < K; ++x) {
+      rb = fma(lpc[x + 1], u[x], rb);
+      rc = fma(u[x], lc[x + 1], rc);
+    }
     // mat-vecs against the window: out = S lp(1..K), accl = S L(1..K).  Each
     // entry is read once and immediately written to its place in the next
     // window, (x, y) -> (x+1, y+1); decreasing packed index = memmove order.
-    double out[K], accl[K];
+    // Row x completes out[x]; the lp / L dots over out are folded in there.
+    double out[K], accl[K], ra = 0.0, rd = 0.0;
 #pragma unroll
     for (int x = 0; x < K; ++x) out[x] = accl[x] = 0.0;
 #pragma unroll
@@ -349,25 +387,24 @@ __device__ void bwd_unit(const BwdP& P, const Geo& G, ix b, ix s, ix e, ix jtop,
           accl[y] = fma(sv, lc[x + 1], accl[y]);
         }
       }
-    }
-    double ra = 0.0, rb = 0.0, rc = 0.0, rd = 0.0;
-#pragma unroll
-    for (int x = 0; x < K; ++x) {
-      out[x] *= inv;
       ra = fma(lpc[x + 1], out[x], ra);
-      rb = fma(lpc[x + 1], u[x], rb);
-      rc = fma(u[x], lc[x + 1], rc);
-      rd = fma(out[x], lc[x + 1], rd);
+      rd = fma(lc[x + 1], out[x], rd);
     }
+    if (j > s) load(j - 1, EDGE);  // lp / L registers are free from here on
+    ra *= inv;
+    rd *= inv;
+#pragma unroll
+    for (int x = 0; x < K; ++x) out[x] *= inv;
     const double sjj = inv * inv + inv * ra;
-    const double uj = (wc - rb) * inv;
+    const double uj = (wj - rb) * inv;
     const double ul = uj * ljj + rc;
     if (j < e) {
-      P.lbar[boff(b, n, W, j, 0)] = rd - sjj * ljj - P.c4 * uj * ul + rcp<SAFE>(ljj);
+      double* lbq = P.lbar + boff(b, n, W, j, 0);
+      lbq[0] = rd - sjj * ljj - P.c4 * uj * ul + rcp<SAFE>(ljj);
 #pragma unroll
       for (int x = 0; x < K; ++x)
-        P.lbar[boff(b, n, W, j, x + 1)] =
-            (j + 1 + x < n) ? -(accl[x] - out[x] * ljj) - P.c4 * u[x] * ul : 0.0;
+        lbq[(x + 1) * 32] =
+            (!EDGE || j + 1 + x < n) ? -(accl[x] - out[x] * ljj) - P.c4 * u[x] * ul : 0.0;
       tr += sjj;
       uu += uj * uj;
     }
@@ -378,7 +415,12 @@ __device__ void bwd_unit(const BwdP& P, const Geo& G, ix b, ix s, ix e, ix jtop,
 #pragma unroll
     for (int x = K - 1; x >= 1; --x) u[x] = u[x - 1];
     u[0] = uj;
-  }
+  };
+  const ix split = n - 1 - K;  // rows above take the masked body
+#pragma unroll 1
+  for (ix j = jtop; j >= s && j > split; --j) row(j, Edge{});
+#pragma unroll 1
+  for (ix j = (jtop < split ? jtop : split); j >= s; --j) row(j, Plain{});
   if (exitb) save(exitb);
   part[0] = tr;
   part[1] = uu;
