@@ -136,7 +136,9 @@ using Plain = std::false_type;  // interior rows: no cell of the row's columns l
 using Edge = std::true_type;    // last rows: corner cells masked
 
 // ------------------------------------------------------------------ forward
-// Rows [s, e) owned, sweep from i0.  win: this thread's window.
+// Rows [s, e) owned, sweep from i0.  win: this thread's window (rows 0..K-1
+// of the (K+1)-row Schur window; row K is always fresh), followed by a
+// two-column cp.async slot for the paired body.
 template <int K, bool SAFE>
 __device__ void fwd_unit(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, double* side,
                          double* part, double* win, bool write) {
@@ -145,11 +147,19 @@ __device__ void fwd_unit(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, d
   constexpr int W = Sh::W;
   const ix n = G.n;
   auto Wr = [&](int a, int c) -> double& { return win[tri(a, c) * ts]; };
+  double* slot = win + Sh::NF * ts;  // [2 columns][W][thread], then [2 y][thread]
+  // per-thread bases: cell (r, column i) at Lt[i * cstep + r * 32], y_i at yt[i * 32]
+  const ix cstep = ix(W) * 32;  // one column of one tile
+  const ix tile0 = (b >> 5) * n, lane = b & 31;
+  const double* Lt = P.L + tile0 * cstep + lane;
+  const double* yt = P.y + tile0 * 32 + lane;
+  double* lpt = P.lp + tile0 * cstep + lane;
+  double* wt = P.w + tile0 * 32 + lane;
 #pragma unroll 1
   for (int q = 0; q < Sh::NF; ++q) win[q * ts] = 0.0;
   double res[W];  // solve residuals of window rows i .. i+K
 #pragma unroll
-  for (int a = 0; a < W; ++a) res[a] = (i0 + a < n) ? P.y[voff(b, n, i0 + a)] : 0.0;
+  for (int a = 0; a < W; ++a) res[a] = (i0 + a < n) ? yt[(i0 + a) * 32] : 0.0;
   double yy = 0.0, ww = 0.0, prodp = 1.0, prodl = 1.0;
   int ep = 0, el = 0;
   ix fail = n;
@@ -157,42 +167,19 @@ __device__ void fwd_unit(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, d
 #pragma unroll
   for (int a = 0; a < W; ++a)
     if (i0 + a >= s && i0 + a < e) yy += res[a] * res[a];
-  double lcur[W];
-#pragma unroll
-  for (int r = 0; r < W; ++r) lcur[r] = (i0 + r < n) ? P.L[boff(b, n, W, i0, r)] : 0.0;
-  const ix cstep = ix(W) * 32;  // one column of one tile
   constexpr int kAhead = 4;
-  auto row = [&](ix i, auto edge) {
-    constexpr bool EDGE = decltype(edge)::value;
-    const double* Lq = P.L + boff(b, n, W, i + 1, 0);
-    if ((threadIdx.x & 31) == 0) {  // L2 fill kAhead rows ahead of the loads below
-      if (i + 1 + kAhead < n) l2_prefetch(Lq + kAhead * cstep, W * 256);
-      if (i + W + kAhead < n) l2_prefetch(P.y + voff(b & ~ix(31), n, i + W + kAhead), 256);
-    }
-    // prefetch next column of L (one row ahead covers HBM latency: a row
-    // costs ~K^2 shared-memory accesses per lane)
-    double lnext[W];
-#pragma unroll
-    for (int r = 0; r < W; ++r) lnext[r] = (!EDGE || i + 1 + r < n) ? Lq[r * 32] : 0.0;
-    const double ynew = (!EDGE || i + W < n) ? P.y[voff(b, n, i + W)] : 0.0;
-    const double* l = lcur;
-    // pivot column of the window (row K is fresh: zero before this row)
-    const double d = Wr(0, 0) + fma(l[0], l[0], P.sigma);
-    const double rs = rsq<SAFE>(d);
-    double c[W];
-    c[0] = d * rs;
-#pragma unroll
-    for (int a = 1; a < K; ++a) c[a] = fma(l[a], l[0], Wr(a, 0)) * rs;
-    c[K] = l[K] * l[0] * rs;
-    const double wi = res[0] * rs;
-    const bool own = i >= s;
-    if (write && own) {
-      double* lpq = P.lp + (Lq - P.L) - cstep;
+
+  // Column i finished: Lp column (row 0 = 1/piv), w_i, the log-det / norm
+  // accumulators; burn-in rows just before s go to the verification buffer.
+  auto emit = [&](ix i, double d, double rs, const double* c, double wi, double l0) {
+    if (!write) return;
+    if (i >= s) {
+      double* lpq = lpt + i * cstep;
       lpq[0] = rs;
 #pragma unroll
       for (int a = 1; a < W; ++a) lpq[a * 32] = c[a];
-      P.w[voff(b, n, i)] = wi;
-      const double al = fabs(l[0]);
+      wt[i * 32] = wi;
+      const double al = fabs(l0);
       if (SAFE) {
         if (!(d > kPivotFloor) || !(al > kPivotFloor)) fail = i < fail ? i : fail;
       } else {
@@ -208,15 +195,123 @@ __device__ void fwd_unit(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, d
         prodl = frexp(prodl, &x);
         el += x;
       }
-    } else if (write && side && i >= s - K) {
+    } else if (side && i >= s - K) {
       double* sd = side + (i - (s - K)) * (W + 1);
       sd[0] = rs;
 #pragma unroll
       for (int a = 1; a < W; ++a) sd[a] = c[a];
       sd[W] = wi;
     }
-    if (i + W >= s && i + W < e) yy += ynew * ynew;
-    // residuals: shift and eliminate w_i
+  };
+  auto take_y = [&](ix r, double v) {
+    if (r >= s && r < e) yy += v * v;
+  };
+
+  // ---- paired body: columns i, i+1 in one pass over the window.  The two
+  // pivots only need window columns 0 and 1; every other entry is read and
+  // written once per two rows with both rank-2 corrections applied:
+  //   W''(a-2, b-2) = W(a, b) + l_a l_b - c_a c_b + m_{a-1} m_{b-1} - d_{a-1} d_{b-1}
+  // (l, c: column i and its Cholesky column; m, d: the same for column i+1).
+  auto fetch2 = [&](ix i) {  // L columns i, i+1 and y_{i+K+1}, y_{i+K+2} -> slot (interior only)
+    const double* Lq = Lt + i * cstep;
+#pragma unroll
+    for (int r = 0; r < W; ++r) {
+      cpa8(slot + r * ts, Lq + r * 32);
+      cpa8(slot + (W + r) * ts, Lq + cstep + r * 32);
+    }
+    cpa8(slot + 2 * W * ts, yt + (i + W) * 32);
+    cpa8(slot + (2 * W + 1) * ts, yt + (i + W + 1) * 32);
+    cpa_commit();
+  };
+  auto pair = [&](ix i) {
+    if ((threadIdx.x & 31) == 0 && i + W + 3 + 2 * kAhead < n) {
+      l2_prefetch(Lt + (i + 2 + 2 * kAhead) * cstep, 2 * W * 256);
+      l2_prefetch(yt + (i + W + 2 + 2 * kAhead) * 32, 512);
+    }
+    cpa_wait();
+    const double y1 = slot[2 * W * ts], y2 = slot[(2 * W + 1) * ts];
+    double l[W], m[W];
+#pragma unroll
+    for (int r = 0; r < W; ++r) {
+      l[r] = slot[r * ts];
+      m[r] = slot[(W + r) * ts];
+    }
+    // step i
+    const double d0 = Wr(0, 0) + fma(l[0], l[0], P.sigma);
+    const double rs0 = rsq<SAFE>(d0);
+    double c[W];
+    c[0] = d0 * rs0;
+#pragma unroll
+    for (int a = 1; a < K; ++a) c[a] = fma(l[a], l[0], Wr(a, 0)) * rs0;
+    c[K] = l[K] * l[0] * rs0;
+    const double w0 = res[0] * rs0;
+#pragma unroll
+    for (int a = 1; a < W; ++a) res[a - 1] = fma(-c[a], w0, res[a]);
+    res[K] = y1;
+    // step i+1: its pivot column is window column 1 after step i
+    // column 0 after step i: v(a') = W'(a', 0) = W(a'+1, 1) + l_{a'+1} l_1 - c_{a'+1} c_1
+    auto v = [&](int a1) {
+      return a1 + 1 < K ? fma(l[a1 + 1], l[1], fma(-c[a1 + 1], c[1], Wr(a1 + 1, 1)))
+                        : fma(l[K], l[1], -c[K] * c[1]);
+    };
+    const double d1 = v(0) + fma(m[0], m[0], P.sigma);
+    const double rs1 = rsq<SAFE>(d1);
+    double dd[W];
+    dd[0] = d1 * rs1;
+#pragma unroll
+    for (int a = 1; a < K; ++a) dd[a] = fma(m[a], m[0], v(a)) * rs1;
+    dd[K] = m[K] * m[0] * rs1;
+    const double w1 = res[0] * rs1;
+#pragma unroll
+    for (int a = 1; a < W; ++a) res[a - 1] = fma(-dd[a], w1, res[a]);
+    res[K] = y2;
+    // the slot's values have all been consumed: refill it two columns ahead
+    fetch2(i + 2);
+    // bulk: old rows 2..K-1, ascending packed index = in-place memmove order
+#pragma unroll
+    for (int a = 2; a < K; ++a) {
+#pragma unroll
+      for (int q = 2; q <= a; ++q) {
+        double t = fma(-c[a], c[q], Wr(a, q));
+        t = fma(l[a], l[q], t);
+        t = fma(-dd[a - 1], dd[q - 1], t);
+        Wr(a - 2, q - 2) = fma(m[a - 1], m[q - 1], t);
+      }
+    }
+    // old row K (fresh at step i) -> row K-2; row K+1 (fresh at step i+1) -> row K-1
+#pragma unroll
+    for (int q = 2; q <= K; ++q) {
+      double t = fma(l[K], l[q], -c[K] * c[q]);
+      t = fma(-dd[K - 1], dd[q - 1], t);
+      Wr(K - 2, q - 2) = fma(m[K - 1], m[q - 1], t);
+    }
+#pragma unroll
+    for (int q = 1; q <= K; ++q) Wr(K - 1, q - 1) = fma(m[K], m[q], -dd[K] * dd[q]);
+    emit(i, d0, rs0, c, w0, l[0]);
+    emit(i + 1, d1, rs1, dd, w1, m[0]);
+    take_y(i + W, y1);
+    take_y(i + W + 1, y2);
+  };
+
+  // ---- single-column body (tail rows, odd counts); L in registers
+  double lcur[W];
+  auto row = [&](ix i, auto edge) {
+    constexpr bool EDGE = decltype(edge)::value;
+    const double* Lq = Lt + (i + 1) * cstep;
+    double lnext[W];
+#pragma unroll
+    for (int r = 0; r < W; ++r) lnext[r] = (!EDGE || i + 1 + r < n) ? Lq[r * 32] : 0.0;
+    const double ynew = (!EDGE || i + W < n) ? yt[(i + W) * 32] : 0.0;
+    const double* l = lcur;
+    // pivot column of the window (row K is fresh: zero before this row)
+    const double d = Wr(0, 0) + fma(l[0], l[0], P.sigma);
+    const double rs = rsq<SAFE>(d);
+    double c[W];
+    c[0] = d * rs;
+#pragma unroll
+    for (int a = 1; a < K; ++a) c[a] = fma(l[a], l[0], Wr(a, 0)) * rs;
+    c[K] = l[K] * l[0] * rs;
+    const double wi = res[0] * rs;
 #pragma unroll
     for (int a = 1; a < W; ++a) res[a - 1] = fma(-c[a], wi, res[a]);
     res[K] = ynew;
@@ -230,15 +325,29 @@ __device__ void fwd_unit(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, d
     }
 #pragma unroll
     for (int cc = 1; cc <= K; ++cc) Wr(K - 1, cc - 1) = fma(l[K], l[cc], -c[K] * c[cc]);
+    emit(i, d, rs, c, wi, l[0]);
+    take_y(i + W, ynew);
 #pragma unroll
     for (int r = 0; r < W; ++r) lcur[r] = lnext[r];
   };
+
+  // pairs while both prefetched columns (i+2, i+3) and y_{i+K+2} are interior
+  ix i = i0;
+  const ix pair_end = n - 3 - K;  // pair(i) needs i + 3 + K < n
+  if (i + 1 < e && i < pair_end) {
+    fetch2(i);
+#pragma unroll 1
+    for (; i + 1 < e && i < pair_end; i += 2) pair(i);
+    cpa_wait();
+  }
+#pragma unroll
+  for (int r = 0; r < W; ++r) lcur[r] = (i < n && i + r < n) ? Lt[i * cstep + r * 32] : 0.0;
   // rows whose next column reaches past the matrix take the masked body
-  const ix split = n - 1 - K > i0 ? (n - 1 - K < e ? n - 1 - K : e) : i0;
+  const ix split = n - 1 - K > i ? (n - 1 - K < e ? n - 1 - K : e) : i;
 #pragma unroll 1
-  for (ix i = i0; i < split; ++i) row(i, Plain{});
+  for (; i < split; ++i) row(i, Plain{});
 #pragma unroll 1
-  for (ix i = split; i < e; ++i) row(i, Edge{});
+  for (; i < e; ++i) row(i, Edge{});
   if (write) {
     part[0] = log(prodp) + ep * kLn2;
     part[1] = log(prodl) + el * kLn2;
@@ -333,25 +442,31 @@ __device__ void bwd_unit(const BwdP& P, const Geo& G, ix b, ix s, ix e, ix jtop,
   // Lp / L columns of the current row live in registers; the next row's are
   // loaded into the same registers as soon as the mat-vecs retire them (the
   // row's tail covers the L2 latency; L2 is filled kAhead rows ahead).
+  const ix cstep = ix(W) * 32;
+  const ix tile0 = (b >> 5) * n, lane = b & 31;
+  const double* Lt = P.L + tile0 * cstep + lane;
+  const double* lpt = P.lp + tile0 * cstep + lane;
+  const double* wt = P.w + tile0 * 32 + lane;
+  double* lbt = P.lbar + tile0 * cstep + lane;
   constexpr int kAhead = 4;
   auto l2_ahead = [&](ix j) {
     if (j >= 0 && (threadIdx.x & 31) == 0) {
-      l2_prefetch(P.lp + boff(b, n, W, j, 0), W * 256);
-      l2_prefetch(P.L + boff(b, n, W, j, 0), W * 256);
-      l2_prefetch(P.w + voff(b, n, j), 256);
+      l2_prefetch(lpt + j * cstep, W * 256);
+      l2_prefetch(Lt + j * cstep, W * 256);
+      l2_prefetch(wt + j * 32, 256);
     }
   };
   double lpc[W], lc[W], wc;
   auto load = [&](ix j, bool mask) {
-    const double* lpq = P.lp + boff(b, n, W, j, 0);
-    const double* lq = P.L + boff(b, n, W, j, 0);
+    const double* lpq = lpt + j * cstep;
+    const double* lq = Lt + j * cstep;
 #pragma unroll
     for (int r = 0; r < W; ++r) {
       const bool cell = !mask || j + r < n;  // input corner cells are not trusted
       lpc[r] = cell ? lpq[r * 32] : 0.0;
       lc[r] = cell ? lq[r * 32] : 0.0;
     }
-    wc = P.w[voff(b, n, j)];
+    wc = wt[j * 32];
   };
 #pragma unroll 1
   for (int d = 1; d <= kAhead; ++d) l2_ahead(jtop - d);
@@ -399,7 +514,7 @@ __device__ void bwd_unit(const BwdP& P, const Geo& G, ix b, ix s, ix e, ix jtop,
     const double uj = (wj - rb) * inv;
     const double ul = uj * ljj + rc;
     if (j < e) {
-      double* lbq = P.lbar + boff(b, n, W, j, 0);
+      double* lbq = lbt + j * cstep;
       lbq[0] = rd - sjj * ljj - P.c4 * uj * ul + rcp<SAFE>(ljj);
 #pragma unroll
       for (int x = 0; x < K; ++x)
@@ -536,7 +651,7 @@ int run(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, const bg
   if (const char* bv = std::getenv("BGM_BURN"))
     if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
   G.debug = std::getenv("BGM_DEBUG") != nullptr;
-  const size_t smf = sizeof(double) * Sh::NF * kThreads, smb = sizeof(double) * Sh::NB * kThreads;
+  const size_t smf = sizeof(double) * (Sh::NF + 2 * Sh::W + 2) * kThreads, smb = sizeof(double) * Sh::NB * kThreads;
   static bool attrs = false;
   if (!attrs) {
     cudaFuncSetAttribute(k_fwd<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smf));
