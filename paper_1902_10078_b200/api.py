@@ -72,7 +72,8 @@ class _Vec(C.Structure):
 
 
 def library_path() -> str:
-    return os.path.join(HERE, "libbandgm_b200.so")
+    # BGM_LIBRARY: load an experiment build instead of the in-tree library
+    return os.environ.get("BGM_LIBRARY") or os.path.join(HERE, "libbandgm_b200.so")
 
 
 def library():

@@ -36,6 +36,15 @@ constexpr double kCheckTol = 1e-12;
 // One warp per block: shared memory, not threads, bounds residency.  Window
 // entries of one thread are kThreads doubles apart ([entry][thread]).
 constexpr int kThreads = 32;
+#ifndef T1_FWD_AHEAD
+#define T1_FWD_AHEAD 1  // forward L2 prefetch distance, in column pairs (measured best of 0-4)
+#endif
+#ifndef T1_BWD_PROGRESSIVE
+#define T1_BWD_PROGRESSIVE 0  // reverse: load the next row cell by cell inside the mat-vecs
+#endif
+#ifndef T1_BWD_AHEAD
+#define T1_BWD_AHEAD 2  // reverse L2 prefetch distance, in rows (measured best of 1-8)
+#endif
 
 template <int K>
 struct Shape {
@@ -167,7 +176,7 @@ __device__ void fwd_unit(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, d
 #pragma unroll
   for (int a = 0; a < W; ++a)
     if (i0 + a >= s && i0 + a < e) yy += res[a] * res[a];
-  constexpr int kAhead = 4;
+  constexpr int kAhead = T1_FWD_AHEAD;
 
   // Column i finished: Lp column (row 0 = 1/piv), w_i, the log-det / norm
   // accumulators; burn-in rows just before s go to the verification buffer.
@@ -440,15 +449,15 @@ __device__ void bwd_unit(const BwdP& P, const Geo& G, ix b, ix s, ix e, ix jtop,
     for (int x = 0; x < K; ++x) dst[Sh::NB + x] = u[x];
   };
   // Lp / L columns of the current row live in registers; the next row's are
-  // loaded into the same registers as soon as the mat-vecs retire them (the
-  // row's tail covers the L2 latency; L2 is filled kAhead rows ahead).
+  // loaded into the same registers cell by cell as the mat-vecs retire them
+  // (L2 is filled kAhead rows ahead).
   const ix cstep = ix(W) * 32;
   const ix tile0 = (b >> 5) * n, lane = b & 31;
   const double* Lt = P.L + tile0 * cstep + lane;
   const double* lpt = P.lp + tile0 * cstep + lane;
   const double* wt = P.w + tile0 * 32 + lane;
   double* lbt = P.lbar + tile0 * cstep + lane;
-  constexpr int kAhead = 4;
+  constexpr int kAhead = T1_BWD_AHEAD;
   auto l2_ahead = [&](ix j) {
     if (j >= 0 && (threadIdx.x & 31) == 0) {
       l2_prefetch(lpt + j * cstep, W * 256);
@@ -457,15 +466,16 @@ __device__ void bwd_unit(const BwdP& P, const Geo& G, ix b, ix s, ix e, ix jtop,
     }
   };
   double lpc[W], lc[W], wc;
+  // cell r of the next row's Lp / L columns (+ w) into the registers of the
+  // current row's, as soon as the current row has retired them
+  auto load_cell = [&](ix j, int r, bool mask) {
+    const bool cell = !mask || j + r < n;  // input corner cells are not trusted
+    lpc[r] = cell ? lpt[j * cstep + r * 32] : 0.0;
+    lc[r] = cell ? Lt[j * cstep + r * 32] : 0.0;
+  };
   auto load = [&](ix j, bool mask) {
-    const double* lpq = lpt + j * cstep;
-    const double* lq = Lt + j * cstep;
 #pragma unroll
-    for (int r = 0; r < W; ++r) {
-      const bool cell = !mask || j + r < n;  // input corner cells are not trusted
-      lpc[r] = cell ? lpq[r * 32] : 0.0;
-      lc[r] = cell ? lq[r * 32] : 0.0;
-    }
+    for (int r = 0; r < W; ++r) load_cell(j, r, mask);
     wc = wt[j * 32];
   };
 #pragma unroll 1
@@ -476,6 +486,11 @@ __device__ void bwd_unit(const BwdP& P, const Geo& G, ix b, ix s, ix e, ix jtop,
     if (entry && j == e - 1) save(entry);  // boundary window [e, e+K) reached by burn-in
     l2_ahead(j - 1 - kAhead);
     const double inv = lpc[0], ljj = lc[0], wj = wc;
+    const bool more = j > s;
+    if (more) {
+      load_cell(j - 1, 0, EDGE);
+      wc = wt[(j - 1) * 32];
+    }
     double rb = 0.0, rc = 0.0;
 #pragma unroll
     for (int x = 0; x < K; ++x) {
@@ -504,8 +519,13 @@ __device__ void bwd_unit(const BwdP& P, const Geo& G, ix b, ix s, ix e, ix jtop,
       }
       ra = fma(lpc[x + 1], out[x], ra);
       rd = fma(lc[x + 1], out[x], rd);
+      // rows x' < x only use cells <= x: cell x+1 of the next row can load now
+      if (T1_BWD_PROGRESSIVE && more) load_cell(j - 1, x + 1, EDGE);
     }
-    if (j > s) load(j - 1, EDGE);  // lp / L registers are free from here on
+    if (!T1_BWD_PROGRESSIVE && more) {
+#pragma unroll
+      for (int r = 1; r < W; ++r) load_cell(j - 1, r, EDGE);
+    }
     ra *= inv;
     rd *= inv;
 #pragma unroll
