@@ -381,32 +381,39 @@ __global__ void k_fwd(FwdP P, Geo G) {
                      P.part + u.id * 4, sm + threadIdx.x, true);
 }
 
+// One thread per (unit, column): the burn-in copy of the K columns before
+// the segment must equal the neighbour's genuine columns.
 template <int K>
 __global__ void k_check_fwd(FwdP P, Geo G) {
   using Sh = Shape<K>;
   constexpr int W = Sh::W;
-  const ix id = blockIdx.x * ix(blockDim.x) + threadIdx.x;  // unit id = b * nseg + p
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  const ix id = t / K;  // unit id = b * nseg + p
+  const int c = int(t % K);
   if (id >= G.batch * G.nseg) return;
   const int p = int(id % G.nseg);
   if (p == 0) return;
   const ix b = id / G.nseg, n = G.n, s = ix(p) * G.seg;
-  const double* sd = P.side + id * Sh::SIDE;
+  const double* sd = P.side + id * Sh::SIDE + c * (W + 1);
   double wscale = 0.0;
-  for (int c = 0; c < K; ++c) wscale = fmax(wscale, fabs(P.w[voff(b, n, s - K + c)]));
+  for (int q = 0; q < K; ++q) wscale = fmax(wscale, fabs(P.w[voff(b, n, s - K + q)]));
+  const ix col = s - K + c;
+  double ref[W + 1], sc = 0.0;
+#pragma unroll
+  for (int r = 0; r < W; ++r) {
+    ref[r] = P.lp[boff(b, n, W, col, r)];
+    sc = fmax(sc, fabs(ref[r]));
+  }
+  ref[W] = P.w[voff(b, n, col)];
   bool bad = false;
-  for (int c = 0; c < K; ++c) {
-    const ix col = s - K + c;
-    double sc = 0.0;
-    for (int r = 0; r < W; ++r) sc = fmax(sc, fabs(P.lp[boff(b, n, W, col, r)]));
-    for (int r = 0; r <= W; ++r) {
-      const double ref = r < W ? P.lp[boff(b, n, W, col, r)] : P.w[voff(b, n, col)];
-      const double rel = fabs(sd[c * (W + 1) + r] - ref) / ((r < W ? sc : wscale) + 1e-300);
-      if (!(rel <= kCheckTol)) {
-        if (G.debug && !bad)
-          printf("t1 fwd check b=%lld p=%d col=%lld r=%d burn=%.17g real=%.17g\n", (long long)b, p,
-                 (long long)col, r, sd[c * (W + 1) + r], ref);
-        bad = true;
-      }
+#pragma unroll
+  for (int r = 0; r <= W; ++r) {
+    const double rel = fabs(sd[r] - ref[r]) / ((r < W ? sc : wscale) + 1e-300);
+    if (!(rel <= kCheckTol)) {
+      if (G.debug && !bad)
+        printf("t1 fwd check b=%lld p=%d col=%lld r=%d burn=%.17g real=%.17g\n", (long long)b, p,
+               (long long)col, r, sd[r], ref[r]);
+      bad = true;
     }
   }
   if (bad) P.flag[b] = 1;
@@ -577,21 +584,39 @@ __global__ void k_bwd(BwdP P, Geo G) {
                      sm + threadIdx.x);
 }
 
+// One warp per unit boundary: the burn-in entry state of segment p must equal
+// segment p+1's genuine exit state (window + u), relative to their scales.
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 template <int K>
 __global__ void k_check_bwd(BwdP P, Geo G, int32_t* flag) {
   using Sh = Shape<K>;
-  const ix id = blockIdx.x * ix(blockDim.x) + threadIdx.x;
-  if (id >= G.batch * G.nseg) return;
+  const ix id = (blockIdx.x * ix(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (id >= G.batch * G.nseg) return;  // whole warps
   const int p = int(id % G.nseg);
   if (p + 1 >= G.nseg) return;
   const ix b = id / G.nseg;
   const double* a = P.entry + id * Sh::STATE;
   const double* r = P.exitb + (id + 1) * Sh::STATE;
   double ss = 0.0, us = 0.0;
-  for (int q = 0; q < Sh::NB; ++q) ss = fmax(ss, fabs(r[q]));
-  for (int q = Sh::NB; q < Sh::STATE; ++q) us = fmax(us, fabs(r[q]));
+  for (int q = lane; q < Sh::STATE; q += 32) {
+    if (q < Sh::NB) ss = fmax(ss, fabs(r[q]));
+    else us = fmax(us, fabs(r[q]));
+  }
+  ss = warp_max(ss);
+  us = warp_max(us);
   bool bad = false;
-  for (int q = 0; q < Sh::STATE; ++q) {
+  for (int q = lane; q < Sh::STATE; q += 32) {
     const double rel = fabs(a[q] - r[q]) / ((q < Sh::NB ? ss : us) + 1e-300);
     if (!(rel <= kCheckTol)) {
       if (G.debug && !bad)
@@ -614,23 +639,32 @@ __global__ void k_repair_bwd(BwdP P, Geo G, const int32_t* flag, const int64_t* 
   bwd_unit<K, true>(P, G, b, 0, G.n, G.n - 1, nullptr, nullptr, part0, sm + threadIdx.x);
 }
 
+// One warp per matrix: sums the per-segment partials, forms loss and d tau2.
 __global__ void k_finalize(const double* pf, const double* pb, const int64_t* fail, Geo Gf, Geo Gb,
                            double tau2, double* loss, double* tau2_bar, int32_t* status,
                            int64_t* row) {
-  const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
-  if (b >= Gf.batch) return;
+  const ix b = (blockIdx.x * ix(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (b >= Gf.batch) return;  // whole warps
   double ldp = 0, ldl = 0, yy = 0, ww = 0, tr = 0, uu = 0;
-  for (int p = 0; p < Gf.nseg; ++p) {
+  for (int p = lane; p < Gf.nseg; p += 32) {
     const double* f = pf + (b * Gf.nseg + p) * 4;
     ldp += f[0];
     ldl += f[1];
     yy += f[2];
     ww += f[3];
   }
-  for (int p = 0; p < Gb.nseg; ++p) {
+  for (int p = lane; p < Gb.nseg; p += 32) {
     tr += pb[(b * Gb.nseg + p) * 2];
     uu += pb[(b * Gb.nseg + p) * 2 + 1];
   }
+  ldp = warp_sum(ldp);
+  ldl = warp_sum(ldl);
+  yy = warp_sum(yy);
+  ww = warp_sum(ww);
+  tr = warp_sum(tr);
+  uu = warp_sum(uu);
+  if (lane) return;
   const double nn = double(Gf.n), inv = 1.0 / tau2, c4 = inv * inv;
   loss[b] = -0.5 * nn * kLog2Pi - ldp + ldl - 0.5 * nn * log(tau2) - 0.5 * yy * inv + 0.5 * ww * c4;
   tau2_bar[b] = -nn * 0.5 * inv + 0.5 * yy * c4 + 0.5 * c4 * tr - ww * c4 * inv + 0.5 * uu * c4 * c4;
@@ -740,7 +774,7 @@ int run(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, const bg
   }
   {
     timing::Scope ts("mlik_check_fwd", s);
-    k_check_fwd<K><<<unsigned((uf + 127) / 128), 128, 0, s>>>(F, Gf);
+    k_check_fwd<K><<<unsigned((uf * K + 127) / 128), 128, 0, s>>>(F, Gf);
   }
   {
     timing::Scope ts("mlik_repair_fwd", s);
@@ -752,7 +786,7 @@ int run(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, const bg
   }
   {
     timing::Scope ts("mlik_check_bwd", s);
-    k_check_bwd<K><<<unsigned((ub + 127) / 128), 128, 0, s>>>(Bp, Gb, flags + G.batch);
+    k_check_bwd<K><<<unsigned((ub * 32 + 127) / 128), 128, 0, s>>>(Bp, Gb, flags + G.batch);
   }
   {
     timing::Scope ts("mlik_repair_bwd", s);
@@ -760,7 +794,7 @@ int run(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, const bg
   }
   {
     timing::Scope ts("mlik_finalize", s);
-    k_finalize<<<blocks_for(G.batch, 128), 128, 0, s>>>(F.part, Bp.part, F.fail, Gf, Gb, tau2, loss,
+    k_finalize<<<blocks_for(G.batch * 32, 128), 128, 0, s>>>(F.part, Bp.part, F.fail, Gf, Gb, tau2, loss,
                                                         tau2_bar, status, row);
   }
   err = cudaGetLastError();
