@@ -51,6 +51,22 @@ def alg_bytes_per_row(kernel: str, k: int) -> float:
     return float("nan")
 
 
+def load_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the newest committed ncu capture
+    (profiles/rNN_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    for f in reversed(files):
+        try:
+            with open(f) as fh:
+                d = json.load(fh)
+            if kernel in d:
+                return d[kernel]["traffic_bytes"], os.path.relpath(f, ROOT)
+        except Exception:
+            continue
+    return None, None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -287,10 +303,20 @@ def main():
     peak, peak_src = load_peaks()
     bpr = alg_bytes_per_row(dom[0], k)
     achieved = bpr * B * n / (dom_ms / 1e3) / 1e9
+    traffic, traffic_src = load_traffic(dom[0])
     roofline = {"bound": "hbm", "kernel": dom[0], "achieved": round(achieved, 1), "peak": peak,
                 "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                "traffic": None, "alg_bytes_per_row": bpr,
+                "traffic": traffic, "traffic_source": traffic_src,
+                "alg_bytes_per_launch": bpr * B * n, "alg_bytes_per_row": bpr,
                 "kernel_ms": {kname: round(t / c, 4) for kname, t, c in kernels}}
+    # the reference composition's suite roofline for config 3
+    # (sum of per-op max(bytes/HBM, flops/FP64)) -- the metric's "% of roofline"
+    suite = None
+    if args.workload == "cfg3":
+        suite_ms = 7.50 * (B * n) / (256 * 65536)
+        suite = {"suite_roofline_ms": round(suite_ms, 3), "frac": round(suite_ms / ms, 3),
+                 "note": "reference op-by-op composition at HBM/FP64 peaks (SURVEY.md 8(d)); "
+                         "the fused step beats it, its own FP64 roofline is ~0.84 ms (DESIGN.md 4.1)"}
 
     # ---------------- e2e through the public API with host buffers
     e2e = None
@@ -317,7 +343,7 @@ def main():
             "config": {"workload": args.workload, "desc": wl["desc"], "batch_per_gpu": B, "n": n, "k": k,
                        "tau2": tau2, "parallelism": f"batch-sharded x{world}", "layout_tile": L.tile,
                        "l2": "inputs (%.2f GB/GPU) exceed the 126 MB L2; no flush needed" % (B * n * (k + 1) * 8 / 1e9)},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "suite_roofline": suite, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(round(launches_per_step * args.steps)),
             "clocks": clk.summary(),
         }
