@@ -4,6 +4,7 @@
 
 #include "bgm_common.cuh"
 #include "bgm_fast.cuh"
+#include "bgm_wide.cuh"
 
 namespace bgm {
 namespace fast {
@@ -31,13 +32,23 @@ extern "C" int bgm_force_generic(int on) {
 namespace bgm {
 namespace fast {
 
-bool cholesky(const bgm_band&, const bgm_band&, int32_t*, int64_t*, cudaStream_t) { return false; }
-bool solve_vec(const bgm_band&, const bgm_vec&, int, const bgm_vec&, int32_t*, int64_t*,
-               cudaStream_t) {
-  return false;
+bool cholesky(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, cudaStream_t s) {
+  if (disabled()) return false;
+  return wide::cholesky(q, l, st, row, s);
 }
-bool log_det(const bgm_band&, void*, int32_t*, int64_t*, cudaStream_t) { return false; }
-bool subset(const bgm_band&, const bgm_band&, int32_t*, int64_t*, cudaStream_t) { return false; }
+bool solve_vec(const bgm_band& l, const bgm_vec& v, int tr, const bgm_vec& x, int32_t* st, int64_t* row,
+               cudaStream_t s) {
+  if (disabled()) return false;
+  return wide::solve_vec(l, v, tr, x, st, row, s);
+}
+bool log_det(const bgm_band& l, void* out, int32_t* st, int64_t* row, cudaStream_t s) {
+  if (disabled()) return false;
+  return wide::log_det(l, out, st, row, s);
+}
+bool subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cudaStream_t s) {
+  if (disabled()) return false;
+  return wide::subset(l, sb, st, row, s);
+}
 bool product(const bgm_band&, int, const bgm_band&, int, const bgm_band&, cudaStream_t) {
   return false;
 }

@@ -29,6 +29,7 @@
 #include "bgm_common.cuh"
 #include "bgm_fast.cuh"
 #include "bgm_mlik.cuh"
+#include "bgm_wide.cuh"
 #include "bgm_timing.cuh"
 
 namespace bgm {
@@ -153,6 +154,7 @@ int bgm_debug_repairs(int64_t* count, double* max_dev, int reset) {
 int bgm_set_segment_rows(int64_t rows) {
   if (rows < 0) return BGM_ERR_ARG;
   g_segment_rows = int(rows);
+  wide::set_segment_rows(int(rows));
   return BGM_OK;
 }
 

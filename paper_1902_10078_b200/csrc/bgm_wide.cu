@@ -1,0 +1,886 @@
+// Wide-band (k = 64, 128) fast paths: one CTA per (matrix, segment).
+//
+// For wide bands the per-row work is a dense (k+1) x (k+1) rank-1 update,
+// too large for one thread and too small for a GEMM.  A CTA of P x P threads
+// holds the whole symmetric Schur window in REGISTERS: thread (tr, tc) owns
+// the TS x TS tile of window positions [tr*TS, tr*TS+TS) x [tc*TS, tc*TS+TS)
+// of an M x M circular grid (M = P*TS >= k+1).  Matrix row r lives at
+// position r mod M for as long as it is in the window, so the window slides
+// down the band with no data movement: the eliminated row's positions are
+// reused by the row entering k steps later.  Per row:
+//   (a) the entering row r = i+k is written into its positions from a
+//       shared-memory stage that cp.async fills one group of TS rows ahead;
+//   (b) the owner of position (i, i) takes the pivot           -- barrier
+//   (c) the owners of column i scale it into l = L(i.., i) and
+//       publish it (and write it to HBM)                        -- barrier
+//   (d) every thread applies W -= l l^T to its tile (TS*TS FMAs, l read
+//       from shared memory once per tile row / column).
+// Steps are unrolled by TS so every register index is static.
+//
+// Long matrices are cut into segments with a burn-in (the Schur complement
+// forgets its start state geometrically); a check kernel compares each
+// unit's burn-in copy of the K columns before its segment with the
+// neighbour's genuine columns, and flagged matrices are recomputed by a
+// single-unit sweep -- the same scheme as the config-3 sweeps.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+
+#include "bgm_common.cuh"
+#include "bgm_fast.cuh"
+#include "bgm_timing.cuh"
+
+namespace bgm {
+namespace wide {
+namespace {
+
+constexpr double kCheckTol = 1e-12;
+
+struct Geo {
+  ix batch, n, seg;
+  int nseg, burn;
+};
+
+template <class T>
+struct CholP {
+  Band<T> q;  // symmetric lower store
+  Band<T> l;  // output factor
+  T* side;    // [unit][K][K+1] burn-in copies of the K columns before the segment
+  int64_t* fail;
+  int32_t* flag;
+};
+
+template <class T>
+__device__ __forceinline__ void cpa(T* dst, const T* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  if (sizeof(T) == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <int K, int P, int TS>
+struct Shape {
+  static constexpr int M = P * TS;
+  static constexpr int NT = P * P;
+  static_assert(M >= K + 1, "window grid too small");
+};
+
+// One unit: rows [s, e) owned, sweep from i0 (a multiple of TS).  `side`
+// receives the columns [s-K, s) computed during burn-in (nullptr: none).
+template <class T, int K, int P, int TS>
+__device__ void chol_unit(const CholP<T>& C, ix b, ix n, ix s, ix e, ix i0, T* side) {
+  using Sh = Shape<K, P, TS>;
+  constexpr int M = Sh::M;
+  __shared__ T stage[2][TS][K + 1];  // entering rows of the current / next group
+  __shared__ T sh_l[M];
+  __shared__ T sh_piv[2];
+  const int tid = threadIdx.x, tr = tid / P, tc = tid % P;
+  const Band<T>& Q = C.q;
+  const Band<T>& L = C.l;
+
+  // window-relative index of position p when the window starts at the row
+  // whose position is im
+  auto relp = [](int p, int im) -> int {
+    const int r = p - im;
+    return r < 0 ? r + M : r;
+  };
+  auto rel = [&](int p, ix i) -> int { return relp(p, int(i % M)); };
+  // initial window: rows/cols [i0, i0+K) from Q (row i0+K enters at step i0)
+  T w[TS][TS];
+#pragma unroll
+  for (int a = 0; a < TS; ++a) {
+#pragma unroll
+    for (int c = 0; c < TS; ++c) {
+      const int ra = rel(tr * TS + a, i0), rc = rel(tc * TS + c, i0);
+      const ix r = i0 + ra, cc = i0 + rc;
+      T v = T(0);
+      if (ra < K && rc < K && r < n && cc < n) v = ra >= rc ? Q.cell(b, ra - rc, cc) : Q.cell(b, rc - ra, r);
+      w[a][c] = v;
+    }
+  }
+  // stage fill for the group starting at row g: rows g+K .. g+K+TS-1
+  auto fill = [&](int buf, ix g) {
+    for (int idx = tid; idx < TS * (K + 1); idx += Sh::NT) {
+      const int t = idx / (K + 1), d = idx % (K + 1);
+      const ix r = g + K + t, c = r - d;
+      if (r < n && c >= 0) cpa(&stage[buf][t][d], &Q.cell(b, d, c));
+      else stage[buf][t][d] = T(0);
+    }
+    cpa_commit();
+  };
+  fill(0, i0);
+  ix fail = n;
+  int buf = 0;
+#pragma unroll 1
+  for (ix g = i0; g < e; g += TS) {
+    const int gm = int(g % M);
+    cpa_wait0();
+    __syncthreads();  // stage[buf] complete; stage[buf^1] free
+    if (g + TS < e) fill(buf ^ 1, g + TS);
+#pragma unroll
+    for (int st = 0; st < TS; ++st) {
+      const ix i = g + st;
+      if (i >= e) break;  // uniform
+      const int im = gm + st < M ? gm + st : gm + st - M;  // position of row i
+      const int oi = im / TS;                               // its owner index (slot st)
+      // (a) row i+K enters at positions (i+K) mod M, slot (st+K) % TS
+      {
+        constexpr int sn_base = K % TS;
+        const int sn = (st + sn_base) % TS;  // static after unrolling
+        const int pn = im + K < M ? im + K : im + K - M;
+        const int on = pn / TS;
+        if (tr == on) {
+#pragma unroll
+          for (int c = 0; c < TS; ++c) {
+            const int rc = relp(tc * TS + c, im);
+            w[sn][c] = rc <= K ? stage[buf][st][K - rc] : T(0);
+          }
+        }
+        if (tc == on) {
+#pragma unroll
+          for (int a = 0; a < TS; ++a) {
+            const int ra = relp(tr * TS + a, im);
+            w[a][sn] = ra <= K ? stage[buf][st][K - ra] : T(0);
+          }
+        }
+      }
+      // (b) pivot
+      if (tr == oi && tc == oi) {
+        const T d = w[st][st];
+        if (!(double(d) > kPivotFloor) && i >= s) fail = fail < i ? fail : i;
+        const T piv = sqrt(d);
+        sh_piv[0] = piv;
+        sh_piv[1] = T(1) / piv;
+      }
+      __syncthreads();
+      // (c) column i -> l, published and stored
+      if (tc == oi) {
+        const T piv = sh_piv[0], rinv = sh_piv[1];
+#pragma unroll
+        for (int a = 0; a < TS; ++a) {
+          const int ra = relp(tr * TS + a, im);
+          const bool live = ra <= K && i + ra < n;
+          const T lv = ra == 0 ? piv : (live ? w[a][st] * rinv : T(0));
+          sh_l[tr * TS + a] = lv;
+          if (ra <= K) {
+            if (i >= s) L.cell(b, ra, i) = lv;  // corner cells (i+ra >= n) get 0
+            else if (side && i >= s - K) side[(i - (s - K)) * (K + 1) + ra] = lv;
+          }
+        }
+      }
+      __syncthreads();
+      // (d) rank-1 update of this thread's tile
+      T lc[TS];
+#pragma unroll
+      for (int c = 0; c < TS; ++c) lc[c] = sh_l[tc * TS + c];
+#pragma unroll
+      for (int a = 0; a < TS; ++a) {
+        const T lr = sh_l[tr * TS + a];
+#pragma unroll
+        for (int c = 0; c < TS; ++c) w[a][c] = fma(-lr, lc[c], w[a][c]);
+      }
+    }
+    buf ^= 1;
+  }
+  cpa_wait0();
+  if (fail < n) atomicMin(reinterpret_cast<unsigned long long*>(C.fail + b), static_cast<unsigned long long>(fail));
+}
+
+template <class T, int K, int P, int TS>
+__global__ void __launch_bounds__(P* P) k_chol(CholP<T> C, Geo G) {
+  const ix unit = blockIdx.x;
+  const ix b = unit / G.nseg;
+  const int p = int(unit % G.nseg);
+  if (b >= G.batch) return;
+  const ix s = ix(p) * G.seg;
+  const ix e = s + G.seg < G.n ? s + G.seg : G.n;
+  ix i0 = s - G.burn;
+  if (i0 < 0) i0 = 0;
+  i0 -= i0 % TS;
+  chol_unit<T, K, P, TS>(C, b, G.n, s, e, i0, p > 0 ? C.side + unit * ix(K) * (K + 1) : nullptr);
+}
+
+// thread per (unit, column of the K before the segment)
+template <class T, int K>
+__global__ void k_chol_check(CholP<T> C, Geo G) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  const ix unit = t / K;
+  const int c = int(t % K);
+  if (unit >= G.batch * G.nseg) return;
+  const int p = int(unit % G.nseg);
+  if (p == 0) return;
+  const ix b = unit / G.nseg, s = ix(p) * G.seg, col = s - K + c;
+  const T* sd = C.side + (unit * K + c) * (K + 1);
+  double sc = 0.0;
+  for (int r = 0; r <= K; ++r) sc = fmax(sc, fabs(double(C.l.cell(b, r, col))));
+  const double tol = sizeof(T) == 8 ? kCheckTol : 1e-5;
+  bool bad = false;
+  for (int r = 0; r <= K; ++r)
+    bad |= !(fabs(double(sd[r]) - double(C.l.cell(b, r, col))) <= tol * (sc + 1e-300));
+  if (bad) C.flag[b] = 1;
+}
+
+template <class T, int K, int P, int TS>
+__global__ void __launch_bounds__(P* P) k_chol_repair(CholP<T> C, Geo G) {
+  const ix b = blockIdx.x;
+  if (b >= G.batch || !C.flag[b]) return;
+  if (threadIdx.x == 0) C.fail[b] = G.n;
+  __syncthreads();
+  chol_unit<T, K, P, TS>(C, b, G.n, 0, G.n, 0, nullptr);
+}
+
+__global__ void fill_fail(int64_t* fail, ix batch, ix n) {
+  const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (b < batch) fail[b] = n;
+}
+
+__global__ void k_init(int64_t* fail, int32_t* flag, ix batch, ix n) {
+  const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (b >= batch) return;
+  fail[b] = n;
+  flag[b] = 0;
+}
+
+__global__ void k_status(const int64_t* fail, ix batch, ix n, int32_t* status, int64_t* row) {
+  const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (b >= batch) return;
+  const bool ok = fail[b] >= n;
+  report(status, row, b, ok ? BGM_OK : BGM_ERR_NOT_PD, ok ? -1 : fail[b]);
+}
+
+// ------------------------------------------------------------------ subset
+// Takahashi recursion, column form (kernels_serial.cpp:80-104 computes the
+// same band row-wise): with u_m = L(j+m, j) / L(j,j),
+//   S(j+a, j) = -sum_m S(j+a, j+m) u_m          (a = 1..K)
+//   S(j, j)   = 1/L(j,j)^2 - sum_m u_m S(j+m, j)
+// The window holds S over rows / columns j+1 .. j+K in the same circular
+// register tiles as the Cholesky; per row: u published -- barrier -- tile
+// partial mat-vecs -- barrier -- per-position sums (the new column) and the
+// diagonal dot -- barrier -- the new row / column j is written into its
+// positions (row j+K leaves the window).
+template <class T>
+struct SubP {
+  Band<T> l;
+  Band<T> s;  // output, symmetric lower store
+  T* side;    // [unit][K][K+1] burn-in copies of the K columns above the segment
+  int32_t* flag;
+};
+
+template <class T, int K, int P, int TS>
+__device__ void subset_unit(const SubP<T>& C, ix b, ix n, ix s, ix e, ix jtop, T* side) {
+  using Sh = Shape<K, P, TS>;
+  constexpr int M = Sh::M, NT = Sh::NT, NW = (NT + 31) / 32;
+  __shared__ T stage[2][TS][K + 1];  // L columns of the current / next group
+  __shared__ T sh_u[M];
+  __shared__ T sh_new[M];
+  __shared__ T sh_part[P][M];
+  __shared__ T sh_dot[NW];
+  const int tid = threadIdx.x, tr = tid / P, tc = tid % P;
+  const Band<T>& L = C.l;
+  const Band<T>& S = C.s;
+  auto relp = [](int p, int pj) -> int {
+    const int r = p - pj;
+    return r < 0 ? r + M : r;
+  };
+  T w[TS][TS];
+#pragma unroll
+  for (int a = 0; a < TS; ++a)
+#pragma unroll
+    for (int c = 0; c < TS; ++c) w[a][c] = T(0);
+  auto fill = [&](int buf, ix gb) {  // L columns gb .. gb+TS-1
+    for (int idx = tid; idx < TS * (K + 1); idx += NT) {
+      const int t = idx / (K + 1), m = idx % (K + 1);
+      const ix j = gb + t;
+      if (j >= 0 && j < n && j + m < n) cpa(&stage[buf][t][m], &L.cell(b, m, j));
+      else stage[buf][t][m] = T(0);
+    }
+    cpa_commit();
+  };
+  const ix gb0 = jtop - jtop % TS;
+  fill(0, gb0);
+  int buf = 0;
+#pragma unroll 1
+  for (ix gb = gb0; gb + TS > s; gb -= TS) {
+    const int gbm = int(gb % M);
+    cpa_wait0();
+    __syncthreads();
+    if (gb - TS + TS > s && gb - TS >= 0) fill(buf ^ 1, gb - TS);
+#pragma unroll
+    for (int st = TS - 1; st >= 0; --st) {
+      const ix j = gb + st;
+      if (j > jtop || j < s) continue;  // uniform
+      const int pj = gbm + st < M ? gbm + st : gbm + st - M;
+      const int oj = pj / TS;
+      const T inv = T(1) / stage[buf][st][0];
+      // (1) u by position
+      for (int p = tid; p < M; p += NT) {
+        const int r = relp(p, pj);
+        sh_u[p] = (r >= 1 && r <= K && j + r < n) ? stage[buf][st][r] * inv : T(0);
+      }
+      __syncthreads();
+      // (2) tile partial mat-vecs
+      {
+        T uc[TS];
+#pragma unroll
+        for (int c = 0; c < TS; ++c) uc[c] = sh_u[tc * TS + c];
+#pragma unroll
+        for (int a = 0; a < TS; ++a) {
+          T acc = T(0);
+#pragma unroll
+          for (int c = 0; c < TS; ++c) acc = fma(w[a][c], uc[c], acc);
+          sh_part[tc][tr * TS + a] = acc;
+        }
+      }
+      __syncthreads();
+      // (3) the new column, its store, and the diagonal dot
+      T dot = T(0);
+      for (int p = tid; p < M; p += NT) {
+        const int r = relp(p, pj);
+        T v = T(0);
+        if (r >= 1 && r <= K && j + r < n) {
+          T acc = T(0);
+#pragma unroll
+          for (int q = 0; q < P; ++q) acc += sh_part[q][p];
+          v = -acc;
+          dot = fma(sh_u[p], v, dot);
+        }
+        sh_new[p] = v;
+        if (r >= 1 && r <= K) {
+          if (j < e) S.cell(b, r, j) = v;  // corner cells get 0
+          else if (side && j < e + K) side[(j - e) * (K + 1) + r] = v;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      if ((tid & 31) == 0) sh_dot[tid >> 5] = dot;
+      __syncthreads();
+      // (4) S(j, j) and the new row / column j into its positions
+      T dsum = T(0);
+#pragma unroll
+      for (int q = 0; q < NW; ++q) dsum += sh_dot[q];
+      const T sjj = inv * inv - dsum;
+      if (tid == 0) {
+        if (j < e) S.cell(b, 0, j) = sjj;
+        else if (side && j < e + K) side[(j - e) * (K + 1)] = sjj;
+      }
+      if (tr == oj) {
+#pragma unroll
+        for (int c = 0; c < TS; ++c) {
+          const int p = tc * TS + c;
+          w[st][c] = p == pj ? sjj : sh_new[p];
+        }
+      }
+      if (tc == oj) {
+#pragma unroll
+        for (int a = 0; a < TS; ++a) {
+          const int p = tr * TS + a;
+          w[a][st] = p == pj ? sjj : sh_new[p];
+        }
+      }
+    }
+    buf ^= 1;
+  }
+  cpa_wait0();
+}
+
+template <class T, int K, int P, int TS>
+__global__ void __launch_bounds__(P* P) k_subset(SubP<T> C, Geo G) {
+  const ix unit = blockIdx.x;
+  const ix b = unit / G.nseg;
+  const int p = int(unit % G.nseg);
+  if (b >= G.batch) return;
+  const ix s = ix(p) * G.seg;
+  const ix e = s + G.seg < G.n ? s + G.seg : G.n;
+  ix jtop = e + G.burn - 1;
+  if (jtop > G.n - 1) jtop = G.n - 1;
+  subset_unit<T, K, P, TS>(C, b, G.n, s, e, jtop,
+                           p + 1 < G.nseg ? C.side + unit * ix(K) * (K + 1) : nullptr);
+}
+
+// thread per (unit, column of the K above the segment)
+template <class T, int K>
+__global__ void k_subset_check(SubP<T> C, Geo G) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  const ix unit = t / K;
+  const int c = int(t % K);
+  if (unit >= G.batch * G.nseg) return;
+  const int p = int(unit % G.nseg);
+  if (p + 1 >= G.nseg) return;
+  const ix b = unit / G.nseg;
+  const ix e = ix(p + 1) * G.seg, col = e + c;
+  if (col >= G.n) return;
+  const T* sd = C.side + (unit * K + c) * (K + 1);
+  double sc = 0.0;
+  for (int r = 0; r <= K; ++r) sc = fmax(sc, fabs(double(C.s.cell(b, r, col))));
+  const double tol = sizeof(T) == 8 ? kCheckTol : 1e-5;
+  bool bad = false;
+  for (int r = 0; r <= K; ++r)
+    bad |= !(fabs(double(sd[r]) - double(C.s.cell(b, r, col))) <= tol * (sc + 1e-300));
+  if (bad) C.flag[b] = 1;
+}
+
+template <class T, int K, int P, int TS>
+__global__ void __launch_bounds__(P* P) k_subset_repair(SubP<T> C, Geo G) {
+  const ix b = blockIdx.x;
+  if (b >= G.batch || !C.flag[b]) return;
+  subset_unit<T, K, P, TS>(C, b, G.n, 0, G.n, G.n - 1, nullptr);
+}
+
+// SingularDiagonal pre-check (kernels_serial.cpp:82-86): first row with
+// |L(i,i)| < 1e-300, one thread per (matrix, row).
+template <class T>
+__global__ void k_diag_check(Band<T> l, ix batch, int64_t* fail) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (t >= batch * l.n) return;
+  const ix b = t / l.n, i = t % l.n;
+  if (fabs(double(l.cell(b, 0, i))) < kPivotFloor)
+    atomicMin(reinterpret_cast<unsigned long long*>(fail + b), static_cast<unsigned long long>(i));
+}
+
+__global__ void k_status_code(const int64_t* fail, ix batch, ix n, int code, int32_t* status, int64_t* row) {
+  const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (b >= batch) return;
+  const bool ok = fail[b] >= n;
+  report(status, row, b, ok ? BGM_OK : code, ok ? -1 : fail[b]);
+}
+
+template <class KernelT>
+ix pick_seg(KernelT kern, int threads, const Geo& G, ix min_seg) {
+  int sms = 148, dev = 0, per = 1;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, 0);
+  if (per < 1) per = 1;
+  ix nseg = ix(sms) * per / (G.batch > 0 ? G.batch : 1);
+  if (nseg < 1) nseg = 1;
+  ix seg = (G.n + nseg - 1) / nseg;
+  return seg < min_seg ? min_seg : seg;
+}
+
+// ------------------------------------------------------------------ solves
+// One warp per (matrix, segment).  The unit's window of K+1 residuals
+// (L x = v, forward) or K solution values (L^T x = v, backward) lives in
+// shared memory at positions row mod M; the columns of L stream through a
+// cp.async ring D columns deep.  Forward row i: x_i = res_i / L(i,i), then
+// the lanes apply res_{i+a} -= L(i+a, i) x_i (right-looking, column i read
+// contiguously).  Backward row i: the lanes dot column i with the window,
+// a butterfly sum, x_i = (v_i - s) / L(i,i) (kernels_serial.cpp:34-60).
+template <class T>
+struct SolveP {
+  Band<T> l;
+  Vec<T> v, x;
+  T* side;  // [unit][K] burn-in copies of the K solution values next to the segment
+  int32_t* flag;
+};
+
+constexpr int kSolveWarps = 4;  // units per CTA
+constexpr int kSolveRing = 8;   // columns in flight per unit
+
+template <class T, int K, bool TR>
+__device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start, T* side, T* win,
+                           T (*ring)[K + 2]) {
+  constexpr int R = (K + 1 + 31) / 32, M = 32 * R, D = kSolveRing;
+  const int lane = threadIdx.x & 31;
+  const Band<T>& L = C.l;
+  auto pos = [](ix r) -> int { return int(r % M); };
+  // ring slot for column j: cells 0..K, then v_j (TR) or v_{j+K+1} (!TR)
+  auto issue = [&](ix j, int slot) {
+    if (j >= 0 && j < n) {
+      for (int a = lane; a <= K; a += 32)
+        if (j + a < n) cpa(&ring[slot][a], &L.cell(b, a, j));
+        else ring[slot][a] = T(0);
+      if (lane == 0) {
+        const ix vr = TR ? j : j + K + 1;
+        if (vr < n) cpa(&ring[slot][K + 1], &C.v(b, vr));
+        else ring[slot][K + 1] = T(0);
+      }
+    }
+    cpa_commit();
+  };
+  const int dir = TR ? -1 : 1;
+  const ix stop = TR ? s - 1 : e;
+  // window init
+  for (int p = lane; p < M; p += 32) win[p] = T(0);
+  __syncwarp();
+  if (!TR) {
+    for (int a = lane; a <= K; a += 32)
+      if (start + a < n) win[pos(start + a)] = C.v(b, start + a);
+  }
+  for (int d = 0; d < D - 1; ++d) issue(start + dir * d, d);
+  __syncwarp();
+  int slot = 0;
+#pragma unroll 1
+  for (ix i = start; i != stop; i += dir) {
+    issue(i + dir * (D - 1), (slot + D - 1) % D);
+    asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
+    __syncwarp();
+    const T* col = ring[slot];
+    T xi;
+    if (!TR) {
+      xi = win[pos(i)] / col[0];
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int a = lane + 32 * q + 1;
+        if (a <= K && i + a < n) {
+          const int p = pos(i + a);
+          win[p] = fma(-col[a], xi, win[p]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) win[pos(i + K + 1)] = col[K + 1];
+    } else {
+      T acc = T(0);
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int a = lane + 32 * q + 1;
+        if (a <= K && i + a < n) acc = fma(col[a], win[pos(i + a)], acc);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      xi = (col[K + 1] - acc) / col[0];
+      __syncwarp();
+      if (lane == 0) win[pos(i)] = xi;
+    }
+    if (lane == 0) {
+      if (i >= s && i < e) C.x(b, i) = xi;
+      else if (side) {
+        const ix o = TR ? i - e : i - (s - K);
+        if (o >= 0 && o < K) side[o] = xi;
+      }
+    }
+    __syncwarp();
+    slot = slot + 1 == D ? 0 : slot + 1;
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+template <class T, int K, bool TR>
+__global__ void __launch_bounds__(32 * kSolveWarps) k_solve(SolveP<T> C, Geo G) {
+  __shared__ T win[kSolveWarps][32 * ((K + 1 + 31) / 32)];
+  __shared__ T ring[kSolveWarps][kSolveRing][K + 2];
+  const int w = threadIdx.x >> 5;
+  const ix unit = blockIdx.x * ix(kSolveWarps) + w;
+  if (unit >= G.batch * G.nseg) return;  // whole warps
+  const ix b = unit / G.nseg;
+  const int p = int(unit % G.nseg);
+  const ix s = ix(p) * G.seg;
+  const ix e = s + G.seg < G.n ? s + G.seg : G.n;
+  ix start;
+  T* side = nullptr;
+  if (!TR) {
+    start = s - G.burn > 0 ? s - G.burn : 0;
+    if (p > 0) side = C.side + unit * K;
+  } else {
+    start = e + G.burn - 1 < G.n - 1 ? e + G.burn - 1 : G.n - 1;
+    if (p + 1 < G.nseg) side = C.side + unit * K;
+  }
+  solve_unit<T, K, TR>(C, b, G.n, s, e, start, side, win[w], ring[w]);
+}
+
+// thread per (unit, value): burn-in copy vs the neighbour's genuine values
+template <class T, int K, bool TR>
+__global__ void k_solve_check(SolveP<T> C, Geo G) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  const ix unit = t / K;
+  const int c = int(t % K);
+  if (unit >= G.batch * G.nseg) return;
+  const int p = int(unit % G.nseg);
+  if (TR ? p + 1 >= G.nseg : p == 0) return;
+  const ix b = unit / G.nseg;
+  const ix row = TR ? ix(p + 1) * G.seg + c : ix(p) * G.seg - K + c;
+  if (row >= G.n) return;
+  double sc = 0.0;
+  for (int q = 0; q < K; ++q) {
+    const ix r = TR ? ix(p + 1) * G.seg + q : ix(p) * G.seg - K + q;
+    if (r < G.n) sc = fmax(sc, fabs(double(C.x(b, r))));
+  }
+  const double tol = sizeof(T) == 8 ? kCheckTol : 1e-5;
+  if (!(fabs(double(C.side[unit * K + c]) - double(C.x(b, row))) <= tol * (sc + 1e-300))) C.flag[b] = 1;
+}
+
+template <class T, int K, bool TR>
+__global__ void __launch_bounds__(32 * kSolveWarps) k_solve_repair(SolveP<T> C, Geo G) {
+  __shared__ T win[kSolveWarps][32 * ((K + 1 + 31) / 32)];
+  __shared__ T ring[kSolveWarps][kSolveRing][K + 2];
+  const int w = threadIdx.x >> 5;
+  const ix b = blockIdx.x * ix(kSolveWarps) + w;
+  if (b >= G.batch || !C.flag[b]) return;  // whole warps
+  solve_unit<T, K, TR>(C, b, G.n, 0, G.n, TR ? G.n - 1 : 0, nullptr, win[w], ring[w]);
+}
+
+// first (forward) / last (backward sweep reaches it first) singular pivot
+template <class T>
+__global__ void k_singular(Band<T> l, ix batch, int tr, int64_t* fail) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (t >= batch * l.n) return;
+  const ix b = t / l.n, i = t % l.n;
+  if (fabs(double(l.cell(b, 0, i))) < kPivotFloor) {
+    if (!tr) atomicMin(reinterpret_cast<unsigned long long*>(fail + b), static_cast<unsigned long long>(i));
+    else atomicMax(reinterpret_cast<unsigned long long*>(fail + b), static_cast<unsigned long long>(i + 1));
+  }
+}
+
+__global__ void k_init_fail(int64_t* fail, int32_t* flag, ix batch, int64_t v) {
+  const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (b >= batch) return;
+  fail[b] = v;
+  flag[b] = 0;
+}
+
+__global__ void k_status_solve(const int64_t* fail, ix batch, ix n, int tr, int32_t* status, int64_t* row) {
+  const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (b >= batch) return;
+  const ix f = tr ? fail[b] - 1 : fail[b];  // backward: stored as row + 1, 0 = none
+  const bool ok = tr ? f < 0 : f >= n;
+  report(status, row, b, ok ? BGM_OK : BGM_ERR_SINGULAR, ok ? -1 : f);
+}
+
+// ------------------------------------------------------------------ log-det
+// kernels.cpp:121-129, any bandwidth / layout: thread per (matrix, chunk of
+// kLogChunk rows), then a per-matrix sum of the chunk partials in chunk order
+// (deterministic).  NonPositiveDiagonal reports the first failing row.
+constexpr int kLogChunk = 64;
+
+template <class T>
+__global__ void k_logdet_part(Band<T> l, ix batch, ix chunks, double* part, int64_t* fail) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  ix b, c;
+  if (!split_bj(t, batch, chunks, l.s, b, c)) return;
+  const ix i0 = c * kLogChunk;
+  const ix i1 = i0 + kLogChunk < l.n ? i0 + kLogChunk : l.n;
+  double acc = 0.0;
+  ix bad = -1;
+  for (ix i = i0; i < i1; ++i) {
+    const double d = double(l.cell(b, 0, i));
+    if (!(d > 0.0) && bad < 0) bad = i;
+    acc += log(d);
+  }
+  part[b * chunks + c] = acc;
+  if (bad >= 0) atomicMin(reinterpret_cast<unsigned long long*>(fail + b), static_cast<unsigned long long>(bad));
+}
+
+template <class T>
+__global__ void k_logdet_sum(const double* part, const int64_t* fail, ix batch, ix n, ix chunks, T* out,
+                             int32_t* status, int64_t* row) {
+  const ix b = (blockIdx.x * ix(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (b >= batch) return;  // whole warps
+  double acc = 0.0;
+  for (ix c = lane; c < chunks; c += 32) acc += part[b * chunks + c];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane) return;
+  const bool ok = fail[b] >= n;
+  if (ok) out[b] = T(acc);
+  report(status, row, b, ok ? BGM_OK : BGM_ERR_NONPOS_DIAG, ok ? -1 : fail[b]);
+}
+
+int g_segment_rows = 0;
+
+template <class T, int K, int P, int TS>
+bool run_chol(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, cudaStream_t s) {
+  using Sh = Shape<K, P, TS>;
+  Geo G;
+  G.batch = q.batch;
+  G.n = q.n;
+  G.burn = 2 * K;
+  if (const char* bv = std::getenv("BGM_WIDE_BURN"))
+    if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
+  int sms = 148, dev = 0, per = 1;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_chol<T, K, P, TS>, Sh::NT, 0);
+  if (per < 1) per = 1;
+  ix seg = g_segment_rows;
+  if (seg <= 0) {
+    ix units = ix(sms) * per;
+    ix nseg = units / (G.batch > 0 ? G.batch : 1);
+    if (nseg < 1) nseg = 1;
+    seg = (G.n + nseg - 1) / nseg;
+    if (seg < 4 * ix(G.burn)) seg = 4 * ix(G.burn);
+  }
+  seg = (seg + TS - 1) / TS * TS;
+  G.seg = seg;
+  G.nseg = int((G.n + seg - 1) / seg);
+  const ix units = G.batch * G.nseg;
+  const size_t bytes = sizeof(T) * size_t(units) * K * (K + 1) + sizeof(int64_t) * size_t(G.batch) +
+                       sizeof(int32_t) * size_t(G.batch) + 64;
+  char* ws = nullptr;
+  if (scratch_alloc(reinterpret_cast<void**>(&ws), bytes, s) != cudaSuccess) return false;
+  CholP<T> C;
+  C.q = view<T>(q);
+  C.l = view<T>(l);
+  C.side = reinterpret_cast<T*>(ws);
+  C.fail = reinterpret_cast<int64_t*>(ws + sizeof(T) * size_t(units) * K * (K + 1));
+  C.flag = reinterpret_cast<int32_t*>(C.fail + G.batch);
+  {
+    timing::Scope ts("wide_chol", s);
+    k_init<<<blocks_for(G.batch, 128), 128, 0, s>>>(C.fail, C.flag, G.batch, G.n);
+    k_chol<T, K, P, TS><<<unsigned(units), Sh::NT, 0, s>>>(C, G);
+    k_chol_check<T, K><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
+    k_chol_repair<T, K, P, TS><<<unsigned(G.batch), Sh::NT, 0, s>>>(C, G);
+    k_status<<<blocks_for(G.batch, 128), 128, 0, s>>>(C.fail, G.batch, G.n, st, row);
+  }
+  scratch_free(ws, s);
+  return true;
+}
+
+
+template <class T, int K, int P, int TS>
+bool run_subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cudaStream_t s) {
+  using Sh = Shape<K, P, TS>;
+  Geo G;
+  G.batch = l.batch;
+  G.n = l.n;
+  G.burn = 2 * K;
+  if (const char* bv = std::getenv("BGM_WIDE_BURN"))
+    if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
+  ix seg = g_segment_rows > 0 ? ix(g_segment_rows) : pick_seg(k_subset<T, K, P, TS>, Sh::NT, G, 4 * ix(G.burn));
+  seg = (seg + TS - 1) / TS * TS;
+  G.seg = seg;
+  G.nseg = int((G.n + seg - 1) / seg);
+  const ix units = G.batch * G.nseg;
+  const size_t side_bytes = sizeof(T) * size_t(units) * K * (K + 1);
+  const size_t bytes = side_bytes + sizeof(int64_t) * size_t(G.batch) + sizeof(int32_t) * size_t(G.batch) + 64;
+  char* ws = nullptr;
+  if (scratch_alloc(reinterpret_cast<void**>(&ws), bytes, s) != cudaSuccess) return false;
+  SubP<T> C;
+  C.l = view<T>(l);
+  C.s = view<T>(sb);
+  C.side = reinterpret_cast<T*>(ws);
+  int64_t* fail = reinterpret_cast<int64_t*>(ws + side_bytes);
+  C.flag = reinterpret_cast<int32_t*>(fail + G.batch);
+  {
+    timing::Scope ts("wide_subset", s);
+    k_init<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, C.flag, G.batch, G.n);
+    k_diag_check<T><<<blocks_for(G.batch * G.n, 256), 256, 0, s>>>(C.l, G.batch, fail);
+    k_subset<T, K, P, TS><<<unsigned(units), Sh::NT, 0, s>>>(C, G);
+    k_subset_check<T, K><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
+    k_subset_repair<T, K, P, TS><<<unsigned(G.batch), Sh::NT, 0, s>>>(C, G);
+    k_status_code<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, G.batch, G.n, BGM_ERR_SINGULAR, st, row);
+  }
+  scratch_free(ws, s);
+  return true;
+}
+
+template <class T, int K, bool TR>
+bool run_solve(const bgm_band& l, const bgm_vec& v, const bgm_vec& x, int32_t* st, int64_t* row, cudaStream_t s) {
+  Geo G;
+  G.batch = l.batch;
+  G.n = l.n;
+  G.burn = K;
+  if (const char* bv = std::getenv("BGM_WIDE_BURN"))
+    if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
+  ix seg = g_segment_rows;
+  if (seg <= 0) {
+    int sms = 148, dev = 0, per = 1;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_solve<T, K, TR>, 32 * kSolveWarps, 0);
+    ix nseg = ix(sms) * (per > 0 ? per : 1) * kSolveWarps / (G.batch > 0 ? G.batch : 1);
+    if (nseg < 1) nseg = 1;
+    seg = (G.n + nseg - 1) / nseg;
+    if (seg < 8 * ix(G.burn)) seg = 8 * ix(G.burn);
+  }
+  if (seg < K) seg = K;
+  G.seg = seg;
+  G.nseg = int((G.n + seg - 1) / seg);
+  const ix units = G.batch * G.nseg;
+  const size_t side_bytes = sizeof(T) * size_t(units) * K;
+  char* ws = nullptr;
+  if (scratch_alloc(reinterpret_cast<void**>(&ws), side_bytes + 12 * size_t(G.batch) + 64, s) != cudaSuccess)
+    return false;
+  SolveP<T> C;
+  C.l = view<T>(l);
+  C.v = view<T>(v);
+  C.x = view<T>(x);
+  C.side = reinterpret_cast<T*>(ws);
+  int64_t* fail = reinterpret_cast<int64_t*>(ws + (side_bytes + 7) / 8 * 8);
+  C.flag = reinterpret_cast<int32_t*>(fail + G.batch);
+  {
+    timing::Scope ts(TR ? "wide_solve_t" : "wide_solve", s);
+    k_init_fail<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, C.flag, G.batch, TR ? 0 : G.n);
+    k_singular<T><<<blocks_for(G.batch * G.n, 256), 256, 0, s>>>(C.l, G.batch, TR, fail);
+    k_solve<T, K, TR><<<unsigned((units + kSolveWarps - 1) / kSolveWarps), 32 * kSolveWarps, 0, s>>>(C, G);
+    k_solve_check<T, K, TR><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
+    k_solve_repair<T, K, TR><<<unsigned((G.batch + kSolveWarps - 1) / kSolveWarps), 32 * kSolveWarps, 0, s>>>(C, G);
+    k_status_solve<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, G.batch, G.n, TR, st, row);
+  }
+  scratch_free(ws, s);
+  return true;
+}
+
+template <class T>
+bool run_logdet(const bgm_band& l, void* out, int32_t* st, int64_t* row, cudaStream_t s) {
+  const ix chunks = (l.n + kLogChunk - 1) / kLogChunk;
+  char* ws = nullptr;
+  const size_t pb = sizeof(double) * size_t(l.batch) * chunks;
+  if (scratch_alloc(reinterpret_cast<void**>(&ws), pb + sizeof(int64_t) * size_t(l.batch) + 64, s) != cudaSuccess)
+    return false;
+  double* part = reinterpret_cast<double*>(ws);
+  int64_t* fail = reinterpret_cast<int64_t*>(ws + pb);
+  {
+    timing::Scope ts("log_det", s);
+    fill_fail<<<blocks_for(l.batch, 128), 128, 0, s>>>(fail, l.batch, l.n);
+    const Band<T> L = view<T>(l);
+    const ix work = ((l.batch + l.tile - 1) / l.tile * l.tile) * chunks;
+    k_logdet_part<T><<<blocks_for(work, 128), 128, 0, s>>>(L, l.batch, chunks, part, fail);
+    k_logdet_sum<T><<<blocks_for(l.batch * 32, 128), 128, 0, s>>>(part, fail, l.batch, l.n, chunks,
+                                                                static_cast<T*>(out), st, row);
+  }
+  scratch_free(ws, s);
+  return true;
+}
+}  // namespace
+
+bool cholesky(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, cudaStream_t s) {
+  if (q.lower != l.lower || q.upper != 0 || l.upper != 0 || q.batch == 0 || q.n == 0) return false;
+  if (q.n < 4 * q.lower) return false;  // short matrices: the generic sweep is fine
+  const bool f64 = q.dtype == BGM_F64;
+  switch (q.lower) {
+    case 64: return f64 ? run_chol<double, 64, 8, 9>(q, l, st, row, s) : run_chol<float, 64, 8, 9>(q, l, st, row, s);
+    case 128:
+      return f64 ? run_chol<double, 128, 16, 9>(q, l, st, row, s) : run_chol<float, 128, 16, 9>(q, l, st, row, s);
+    default: return false;
+  }
+}
+
+bool subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cudaStream_t s) {
+  if (l.lower != sb.lower || l.upper != 0 || sb.upper != 0 || l.batch == 0 || l.n == 0) return false;
+  if (l.n < 4 * l.lower) return false;
+  const bool f64 = l.dtype == BGM_F64;
+  switch (l.lower) {
+    case 64: return f64 ? run_subset<double, 64, 8, 9>(l, sb, st, row, s) : run_subset<float, 64, 8, 9>(l, sb, st, row, s);
+    case 128:
+      return f64 ? run_subset<double, 128, 16, 9>(l, sb, st, row, s)
+                 : run_subset<float, 128, 16, 9>(l, sb, st, row, s);
+    default: return false;
+  }
+}
+
+bool solve_vec(const bgm_band& l, const bgm_vec& v, int tr, const bgm_vec& x, int32_t* st, int64_t* row,
+               cudaStream_t s) {
+  if (l.upper != 0 || l.batch == 0 || l.n == 0 || l.n < 8 * l.lower) return false;
+  const bool f64 = l.dtype == BGM_F64;
+  switch (l.lower) {
+#define BGM_SOLVE(KK)                                                                           \
+  case KK:                                                                                      \
+    if (f64) return tr ? run_solve<double, KK, true>(l, v, x, st, row, s) : run_solve<double, KK, false>(l, v, x, st, row, s); \
+    return tr ? run_solve<float, KK, true>(l, v, x, st, row, s) : run_solve<float, KK, false>(l, v, x, st, row, s);
+    BGM_SOLVE(64)
+    BGM_SOLVE(128)
+#undef BGM_SOLVE
+    default: return false;
+  }
+}
+
+bool log_det(const bgm_band& l, void* out, int32_t* st, int64_t* row, cudaStream_t s) {
+  if (l.batch == 0 || l.n == 0) return false;
+  return l.dtype == BGM_F64 ? run_logdet<double>(l, out, st, row, s) : run_logdet<float>(l, out, st, row, s);
+}
+
+void set_segment_rows(int rows) { g_segment_rows = rows; }
+
+}  // namespace wide
+}  // namespace bgm

@@ -1,0 +1,21 @@
+// Wide-band (k = 64, 128) fast paths (bgm_wide.cu).  Each returns true when
+// it recognised the shape and launched, false to fall back to the generic
+// kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "bandgm_b200.h"
+
+namespace bgm {
+namespace wide {
+
+bool cholesky(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, cudaStream_t s);
+bool subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cudaStream_t s);
+bool solve_vec(const bgm_band& l, const bgm_vec& v, int tr, const bgm_vec& x, int32_t* st, int64_t* row,
+               cudaStream_t s);
+bool log_det(const bgm_band& l, void* out, int32_t* st, int64_t* row, cudaStream_t s);
+void set_segment_rows(int rows);
+
+}  // namespace wide
+}  // namespace bgm
