@@ -34,12 +34,12 @@ namespace fast {
 
 bool cholesky(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, cudaStream_t s) {
   if (disabled()) return false;
-  return wide::cholesky(q, l, st, row, s);
+  return narrow::cholesky(q, l, st, row, s) || wide::cholesky(q, l, st, row, s);
 }
 bool solve_vec(const bgm_band& l, const bgm_vec& v, int tr, const bgm_vec& x, int32_t* st, int64_t* row,
                cudaStream_t s) {
   if (disabled()) return false;
-  return wide::solve_vec(l, v, tr, x, st, row, s);
+  return narrow::solve_vec(l, v, tr, x, st, row, s) || wide::solve_vec(l, v, tr, x, st, row, s);
 }
 bool log_det(const bgm_band& l, void* out, int32_t* st, int64_t* row, cudaStream_t s) {
   if (disabled()) return false;
@@ -47,7 +47,7 @@ bool log_det(const bgm_band& l, void* out, int32_t* st, int64_t* row, cudaStream
 }
 bool subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cudaStream_t s) {
   if (disabled()) return false;
-  return wide::subset(l, sb, st, row, s);
+  return narrow::subset(l, sb, st, row, s) || wide::subset(l, sb, st, row, s);
 }
 bool product(const bgm_band&, int, const bgm_band&, int, const bgm_band&, cudaStream_t) {
   return false;

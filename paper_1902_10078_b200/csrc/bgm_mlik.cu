@@ -155,6 +155,7 @@ int bgm_set_segment_rows(int64_t rows) {
   if (rows < 0) return BGM_ERR_ARG;
   g_segment_rows = int(rows);
   wide::set_segment_rows(int(rows));
+  narrow::set_segment_rows(int(rows));
   return BGM_OK;
 }
 

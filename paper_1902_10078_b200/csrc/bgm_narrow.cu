@@ -1,0 +1,617 @@
+// Narrow-band (k <= 16) fast paths for the per-operator API: cholesky,
+// solve_vec (L and L^T) and the Takahashi subset, tile-32 layout.
+//
+// Same organisation as the config-3 sweeps (bgm_mlik_t1.cu): one thread per
+// (matrix, segment), a warp = the 32 matrices of one tile on one segment, so
+// every band-cell access is one coalesced 256-byte warp transaction; the
+// recurrence state lives in registers (solves) or in a per-thread packed
+// triangle in shared memory laid out [entry][thread] (cholesky, subset),
+// shifted physically as it is updated.  Segments start with a burn-in from a
+// zero state; a check kernel compares each unit's burn-in copy of the K
+// values / columns next to its segment with the neighbour's genuine ones and
+// flagged matrices are recomputed by a single-unit sweep.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+
+#include "bgm_common.cuh"
+#include "bgm_fast.cuh"
+#include "bgm_timing.cuh"
+
+namespace bgm {
+namespace narrow {
+namespace {
+
+constexpr int kThreads = 32;     // one warp per CTA: shared memory bounds residency
+constexpr int kBurnMin = 64;     // burn-in rows: max(kBurnMin, kBurnGen * K)
+constexpr int kBurnGen = 16;
+constexpr double kCheckTol = 1e-12;
+
+__host__ __device__ constexpr int tri(int a, int b) { return a * (a + 1) / 2 + b; }
+
+struct Geo {
+  ix batch, n, seg, tiles;
+  int nseg, burn;
+};
+
+struct Unit {
+  ix b, id;
+  int p;
+  bool live;
+};
+__device__ __forceinline__ Unit unit_of(const Geo& G) {
+  const ix gt = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  const ix warp = gt >> 5, tile = warp / G.nseg;
+  Unit u;
+  u.p = int(warp % G.nseg);
+  u.b = tile * 32 + (gt & 31);
+  u.live = tile < G.tiles && u.b < G.batch;
+  u.id = u.b * G.nseg + u.p;
+  return u;
+}
+
+// tile-32 base pointer of matrix b: cell (r, column j) at base[(j * w + r) * 32]
+template <class T>
+__device__ __forceinline__ T* bbase(const Band<T>& B, ix b) {
+  return B.p + (b >> 5) * B.n * B.w * 32 + (b & 31);
+}
+template <class T>
+__device__ __forceinline__ T* vbase(const Vec<T>& V, ix b) {
+  return V.p + (b >> 5) * V.n * 32 + (b & 31);
+}
+
+template <class T>
+__device__ __forceinline__ double dabs(T x) {
+  return fabs(double(x));
+}
+
+// ------------------------------------------------------------------ cholesky
+// Right-looking: the window W holds the trailing Schur complement rows
+// i .. i+K-1 (packed, rows 0..K-1); row i+K enters fresh as Q(i+K, i..i+K).
+template <class T>
+struct CholP {
+  Band<T> q, l;
+  T* side;  // [unit][K][K+1]
+  int64_t* fail;
+  int32_t* flag;
+};
+
+template <class T, int K>
+__device__ void chol_unit(const CholP<T>& C, ix b, ix n, ix s, ix e, ix i0, T* side, T* win) {
+  constexpr int W = K + 1, ts = kThreads;
+  auto Wr = [&](int a, int c) -> T& { return win[tri(a, c) * ts]; };
+  const T* qb = bbase(C.q, b);
+  T* lb = bbase(C.l, b);
+  const ix cs = ix(W) * 32;  // column stride
+  // window rows i0 .. i0+K-1 from Q
+#pragma unroll 1
+  for (int a = 0; a < K; ++a)
+    for (int c = 0; c <= a; ++c)
+      Wr(a, c) = (i0 + a < n) ? qb[(i0 + c) * cs + (a - c) * 32] : T(0);
+  auto load_row = [&](ix r, T* out) {  // Q(r, r-K .. r) -> out[0..K] (column r-K+c)
+#pragma unroll
+    for (int c = 0; c <= K; ++c) out[c] = (r < n) ? qb[(r - K + c) * cs + (K - c) * 32] : T(0);
+  };
+  T qn[W];
+  load_row(i0 + K, qn);
+  ix fail = n;
+#pragma unroll 1
+  for (ix i = i0; i < e; ++i) {
+    T q[W];
+#pragma unroll
+    for (int c = 0; c <= K; ++c) q[c] = qn[c];
+    load_row(i + K + 1, qn);  // one row ahead
+    const T d = Wr(0, 0);
+    if (!(double(d) > kPivotFloor) && i >= s) fail = fail < i ? fail : i;
+    const T piv = sqrt(d), rinv = T(1) / piv;
+    T l[W];
+    l[0] = piv;
+#pragma unroll
+    for (int a = 1; a < K; ++a) l[a] = Wr(a, 0) * rinv;
+    l[K] = (i + K < n) ? q[0] * rinv : T(0);
+    if (i >= s) {
+      T* col = lb + i * cs;
+#pragma unroll
+      for (int a = 0; a <= K; ++a) col[a * 32] = (i + a < n) ? l[a] : T(0);
+    } else if (side && i >= s - K) {
+      T* sd = side + (i - (s - K)) * W;
+#pragma unroll
+      for (int a = 0; a <= K; ++a) sd[a] = l[a];
+    }
+#pragma unroll
+    for (int a = 1; a < K; ++a) {
+#pragma unroll
+      for (int c = 1; c <= a; ++c) Wr(a - 1, c - 1) = fma(-l[a], l[c], Wr(a, c));
+    }
+#pragma unroll
+    for (int c = 1; c <= K; ++c) Wr(K - 1, c - 1) = fma(-l[K], l[c], q[c]);
+  }
+  if (fail < n) atomicMin(reinterpret_cast<unsigned long long*>(C.fail + b), static_cast<unsigned long long>(fail));
+}
+
+template <class T, int K>
+__global__ void k_chol(CholP<T> C, Geo G) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* sm = reinterpret_cast<T*>(smraw);
+  const Unit u = unit_of(G);
+  if (!u.live) return;
+  const ix s = ix(u.p) * G.seg, e = s + G.seg < G.n ? s + G.seg : G.n;
+  const ix i0 = s - G.burn > 0 ? s - G.burn : 0;
+  chol_unit<T, K>(C, u.b, G.n, s, e, i0, u.p > 0 ? C.side + u.id * ix(K) * (K + 1) : nullptr,
+                  sm + threadIdx.x);
+}
+
+template <class T, int K>
+__global__ void k_chol_check(CholP<T> C, Geo G) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  const ix id = t / K;
+  const int c = int(t % K);
+  if (id >= G.batch * G.nseg) return;
+  const int p = int(id % G.nseg);
+  if (p == 0) return;
+  const ix b = id / G.nseg, col = ix(p) * G.seg - K + c;
+  const T* sd = C.side + (id * K + c) * (K + 1);
+  double sc = 0.0;
+  for (int r = 0; r <= K; ++r) sc = fmax(sc, dabs(C.l.cell(b, r, col)));
+  const double tol = sizeof(T) == 8 ? kCheckTol : 1e-5;
+  bool bad = false;
+  for (int r = 0; r <= K; ++r) bad |= !(fabs(double(sd[r]) - double(C.l.cell(b, r, col))) <= tol * (sc + 1e-300));
+  if (bad) C.flag[b] = 1;
+}
+
+template <class T, int K>
+__global__ void k_chol_repair(CholP<T> C, Geo G) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* sm = reinterpret_cast<T*>(smraw);
+  const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (b >= G.batch || !C.flag[b]) return;
+  C.fail[b] = G.n;
+  chol_unit<T, K>(C, b, G.n, 0, G.n, 0, nullptr, sm + threadIdx.x);
+}
+
+// ------------------------------------------------------------------ solves
+template <class T>
+struct SolveP {
+  Band<T> l;
+  Vec<T> v, x;
+  T* side;  // [unit][K]
+  int32_t* flag;
+};
+
+// Forward: res[a] = residual of row i+a; x_i = res[0] / L(i,i) (the
+// reference divides, kernels_serial.cpp:47).  Backward: x window x[a] =
+// x_{i+1+a}; x_i = (v_i - sum_a L(i+1+a, i) x[a]) / L(i,i).
+template <class T, int K, bool TR>
+__device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start, T* side) {
+  constexpr int W = K + 1;
+  const T* lb = bbase(C.l, b);
+  const T* vb = vbase(C.v, b);
+  T* xb = vbase(C.x, b);
+  const ix cs = ix(W) * 32;
+  auto load_col = [&](ix j, T* out, T& vv) {
+    const bool in = j >= 0 && j < n;
+#pragma unroll
+    for (int a = 0; a <= K; ++a) out[a] = (in && j + a < n) ? lb[j * cs + a * 32] : T(0);
+    const ix vr = TR ? j : j + K + 1;
+    vv = (vr >= 0 && vr < n) ? vb[vr * 32] : T(0);
+  };
+  T win[W];
+  if (!TR) {
+#pragma unroll
+    for (int a = 0; a <= K; ++a) win[a] = (start + a < n) ? vb[(start + a) * 32] : T(0);
+  } else {
+#pragma unroll
+    for (int a = 0; a <= K; ++a) win[a] = T(0);
+  }
+  T cn[W], vn;
+  load_col(start, cn, vn);
+  const int dir = TR ? -1 : 1;
+  const ix stop = TR ? s - 1 : e;
+#pragma unroll 1
+  for (ix i = start; i != stop; i += dir) {
+    T col[W], vv = vn;
+#pragma unroll
+    for (int a = 0; a <= K; ++a) col[a] = cn[a];
+    load_col(i + dir, cn, vn);
+    T xi;
+    if (!TR) {
+      xi = win[0] / col[0];
+#pragma unroll
+      for (int a = 1; a <= K; ++a) win[a - 1] = fma(-col[a], xi, win[a]);
+      win[K] = vv;  // v_{i+K+1}
+    } else {
+      T acc = T(0);
+#pragma unroll
+      for (int a = 1; a <= K; ++a) acc = fma(col[a], win[a - 1], acc);
+      xi = (vv - acc) / col[0];
+#pragma unroll
+      for (int a = K - 1; a >= 1; --a) win[a] = win[a - 1];
+      win[0] = xi;
+    }
+    if (i >= s && i < e) xb[i * 32] = xi;
+    else if (side) {
+      const ix o = TR ? i - e : i - (s - K);
+      if (o >= 0 && o < K) side[o] = xi;
+    }
+  }
+}
+
+template <class T, int K, bool TR>
+__global__ void k_solve(SolveP<T> C, Geo G) {
+  const Unit u = unit_of(G);
+  if (!u.live) return;
+  const ix s = ix(u.p) * G.seg, e = s + G.seg < G.n ? s + G.seg : G.n;
+  ix start;
+  T* side = nullptr;
+  if (!TR) {
+    start = s - G.burn > 0 ? s - G.burn : 0;
+    if (u.p > 0) side = C.side + u.id * K;
+  } else {
+    start = e + G.burn - 1 < G.n - 1 ? e + G.burn - 1 : G.n - 1;
+    if (u.p + 1 < G.nseg) side = C.side + u.id * K;
+  }
+  solve_unit<T, K, TR>(C, u.b, G.n, s, e, start, side);
+}
+
+template <class T, int K, bool TR>
+__global__ void k_solve_check(SolveP<T> C, Geo G) {
+  const ix id = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (id >= G.batch * G.nseg) return;
+  const int p = int(id % G.nseg);
+  if (TR ? p + 1 >= G.nseg : p == 0) return;
+  const ix b = id / G.nseg;
+  const ix r0 = TR ? ix(p + 1) * G.seg : ix(p) * G.seg - K;
+  double sc = 0.0;
+  for (int c = 0; c < K; ++c)
+    if (r0 + c < G.n) sc = fmax(sc, dabs(C.x(b, r0 + c)));
+  const double tol = sizeof(T) == 8 ? kCheckTol : 1e-5;
+  bool bad = false;
+  for (int c = 0; c < K; ++c)
+    if (r0 + c < G.n) bad |= !(fabs(double(C.side[id * K + c]) - double(C.x(b, r0 + c))) <= tol * (sc + 1e-300));
+  if (bad) C.flag[b] = 1;
+}
+
+template <class T, int K, bool TR>
+__global__ void k_solve_repair(SolveP<T> C, Geo G) {
+  const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (b >= G.batch || !C.flag[b]) return;
+  solve_unit<T, K, TR>(C, b, G.n, 0, G.n, TR ? G.n - 1 : 0, nullptr);
+}
+
+template <class T>
+__global__ void k_singular(Band<T> l, ix batch, int tr, int64_t* fail) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  ix b, i;
+  if (!split_bj(t, batch, l.n, l.s, b, i)) return;
+  if (dabs(l.cell(b, 0, i)) < kPivotFloor) {
+    if (!tr) atomicMin(reinterpret_cast<unsigned long long*>(fail + b), static_cast<unsigned long long>(i));
+    else atomicMax(reinterpret_cast<unsigned long long*>(fail + b), static_cast<unsigned long long>(i + 1));
+  }
+}
+
+// ------------------------------------------------------------------ subset
+// Column-form Takahashi (see bgm_wide.cu): window S over rows j+1 .. j+K,
+// packed lower triangle [entry][thread], index x <-> row j+1+x.
+template <class T>
+struct SubP {
+  Band<T> l, s;
+  T* side;  // [unit][K][K+1]
+  int32_t* flag;
+};
+
+template <class T, int K>
+__device__ void subset_unit(const SubP<T>& C, ix b, ix n, ix s, ix e, ix jtop, T* side, T* win) {
+  constexpr int W = K + 1, ts = kThreads;
+  auto Sr = [&](int x, int y) -> T& { return win[tri(x, y) * ts]; };
+  const T* lb = bbase(C.l, b);
+  T* sb = bbase(C.s, b);
+  const ix cs = ix(W) * 32;
+#pragma unroll 1
+  for (int q = 0; q < K * (K + 1) / 2; ++q) win[q * ts] = T(0);
+  auto load_col = [&](ix j, T* out) {
+    const bool in = j >= 0 && j < n;
+#pragma unroll
+    for (int a = 0; a <= K; ++a) out[a] = (in && j + a < n) ? lb[j * cs + a * 32] : T(0);
+  };
+  T cn[W];
+  load_col(jtop, cn);
+#pragma unroll 1
+  for (ix j = jtop; j >= s; --j) {
+    T lc[W];
+#pragma unroll
+    for (int a = 0; a <= K; ++a) lc[a] = cn[a];
+    load_col(j - 1, cn);
+    const T inv = T(1) / lc[0];
+    T out[K];
+#pragma unroll
+    for (int x = 0; x < K; ++x) out[x] = T(0);
+    // out = S(window) lc(1..K); entries shifted (x,y) -> (x+1,y+1) in place
+#pragma unroll
+    for (int x = K - 1; x >= 0; --x) {
+#pragma unroll
+      for (int y = x; y >= 0; --y) {
+        const T sv = Sr(x, y);
+        if (x < K - 1) Sr(x + 1, y + 1) = sv;
+        out[x] = fma(sv, lc[y + 1], out[x]);
+        if (y != x) out[y] = fma(sv, lc[x + 1], out[y]);
+      }
+    }
+    T dot = T(0);
+#pragma unroll
+    for (int x = 0; x < K; ++x) {
+      out[x] = -out[x] * inv;  // S(j+1+x, j)
+      dot = fma(lc[x + 1], out[x], dot);
+    }
+    const T sjj = inv * inv - inv * dot;
+    Sr(0, 0) = sjj;
+#pragma unroll
+    for (int x = 1; x < K; ++x) Sr(x, 0) = out[x - 1];
+    if (j < e) {
+      T* col = sb + j * cs;
+      col[0] = sjj;
+#pragma unroll
+      for (int x = 0; x < K; ++x) col[(x + 1) * 32] = (j + 1 + x < n) ? out[x] : T(0);
+    } else if (side && j < e + K) {
+      T* sd = side + (j - e) * W;
+      sd[0] = sjj;
+#pragma unroll
+      for (int x = 0; x < K; ++x) sd[x + 1] = (j + 1 + x < n) ? out[x] : T(0);
+    }
+  }
+}
+
+template <class T, int K>
+__global__ void k_subset(SubP<T> C, Geo G) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* sm = reinterpret_cast<T*>(smraw);
+  const Unit u = unit_of(G);
+  if (!u.live) return;
+  const ix s = ix(u.p) * G.seg, e = s + G.seg < G.n ? s + G.seg : G.n;
+  const ix jtop = e + G.burn - 1 < G.n - 1 ? e + G.burn - 1 : G.n - 1;
+  subset_unit<T, K>(C, u.b, G.n, s, e, jtop, u.p + 1 < G.nseg ? C.side + u.id * ix(K) * (K + 1) : nullptr,
+                    sm + threadIdx.x);
+}
+
+template <class T, int K>
+__global__ void k_subset_check(SubP<T> C, Geo G) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  const ix id = t / K;
+  const int c = int(t % K);
+  if (id >= G.batch * G.nseg) return;
+  const int p = int(id % G.nseg);
+  if (p + 1 >= G.nseg) return;
+  const ix b = id / G.nseg, col = ix(p + 1) * G.seg + c;
+  if (col >= G.n) return;
+  const T* sd = C.side + (id * K + c) * (K + 1);
+  double sc = 0.0;
+  for (int r = 0; r <= K; ++r) sc = fmax(sc, dabs(C.s.cell(b, r, col)));
+  const double tol = sizeof(T) == 8 ? kCheckTol : 1e-5;
+  bool bad = false;
+  for (int r = 0; r <= K; ++r) bad |= !(fabs(double(sd[r]) - double(C.s.cell(b, r, col))) <= tol * (sc + 1e-300));
+  if (bad) C.flag[b] = 1;
+}
+
+template <class T, int K>
+__global__ void k_subset_repair(SubP<T> C, Geo G) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* sm = reinterpret_cast<T*>(smraw);
+  const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (b >= G.batch || !C.flag[b]) return;
+  subset_unit<T, K>(C, b, G.n, 0, G.n, G.n - 1, nullptr, sm + threadIdx.x);
+}
+
+template <class T>
+__global__ void k_diag_small(Band<T> l, ix batch, int64_t* fail) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  ix b, i;
+  if (!split_bj(t, batch, l.n, l.s, b, i)) return;
+  if (dabs(l.cell(b, 0, i)) < kPivotFloor)
+    atomicMin(reinterpret_cast<unsigned long long*>(fail + b), static_cast<unsigned long long>(i));
+}
+
+// ------------------------------------------------------------------ common
+__global__ void k_init(int64_t* fail, int32_t* flag, ix batch, int64_t v) {
+  const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (b >= batch) return;
+  fail[b] = v;
+  flag[b] = 0;
+}
+
+__global__ void k_report(const int64_t* fail, ix batch, ix n, int code, int backward, int32_t* status,
+                         int64_t* row) {
+  const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (b >= batch) return;
+  const ix f = backward ? fail[b] - 1 : fail[b];
+  const bool ok = backward ? f < 0 : f >= n;
+  report(status, row, b, ok ? BGM_OK : code, ok ? -1 : f);
+}
+
+int g_segment_rows = 0;
+
+int burn_rows(int K) {
+  int burn = kBurnGen * K > kBurnMin ? kBurnGen * K : kBurnMin;
+  if (const char* bv = std::getenv("BGM_NARROW_BURN"))
+    if (std::atoi(bv) >= 1) burn = std::atoi(bv);
+  return burn;
+}
+
+template <class KernelT>
+Geo make_geo(KernelT kern, size_t smem, ix batch, ix n, int burn) {
+  Geo G;
+  G.batch = batch;
+  G.n = n;
+  G.tiles = (batch + 31) / 32;
+  G.burn = burn;
+  int sms = 148, dev = 0, per = 1;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, smem);
+  if (per < 1) per = 1;
+  ix seg = g_segment_rows;
+  if (seg <= 0) {
+    ix nseg = ix(sms) * per / G.tiles;
+    if (nseg < 1) nseg = 1;
+    seg = (n + nseg - 1) / nseg;
+    if (seg < 4 * ix(burn)) seg = 4 * ix(burn);
+  }
+  if (seg < 1) seg = 1;
+  G.seg = seg;
+  G.nseg = int((n + seg - 1) / seg);
+  return G;
+}
+
+struct Scratch {
+  char* p = nullptr;
+  cudaStream_t s;
+  ~Scratch() {
+    if (p) scratch_free(p, s);
+  }
+};
+
+template <class T, int K>
+bool run_chol(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, cudaStream_t s) {
+  const size_t smem = sizeof(T) * (K * (K + 1) / 2) * kThreads;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_chol<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_chol_repair<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = true;
+  }
+  const int burn = burn_rows(K);
+  const Geo G = make_geo(k_chol<T, K>, smem, q.batch, q.n, burn);
+  const ix units = G.batch * G.nseg;
+  const size_t side = sizeof(T) * size_t(units) * K * (K + 1);
+  Scratch ws;
+  ws.s = s;
+  if (scratch_alloc(reinterpret_cast<void**>(&ws.p), side + 12 * size_t(G.batch) + 64, s) != cudaSuccess) return false;
+  CholP<T> C;
+  C.q = view<T>(q);
+  C.l = view<T>(l);
+  C.side = reinterpret_cast<T*>(ws.p);
+  C.fail = reinterpret_cast<int64_t*>(ws.p + (side + 7) / 8 * 8);
+  C.flag = reinterpret_cast<int32_t*>(C.fail + G.batch);
+  k_init<<<blocks_for(G.batch, 128), 128, 0, s>>>(C.fail, C.flag, G.batch, G.n);
+  {
+    timing::Scope t("narrow_chol", s);
+    k_chol<T, K><<<unsigned(G.tiles * G.nseg), kThreads, smem, s>>>(C, G);
+  }
+  k_chol_check<T, K><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
+  k_chol_repair<T, K><<<blocks_for(G.batch, kThreads), kThreads, smem, s>>>(C, G);
+  k_report<<<blocks_for(G.batch, 128), 128, 0, s>>>(C.fail, G.batch, G.n, BGM_ERR_NOT_PD, 0, st, row);
+  return true;
+}
+
+template <class T, int K, bool TR>
+bool run_solve(const bgm_band& l, const bgm_vec& v, const bgm_vec& x, int32_t* st, int64_t* row, cudaStream_t s) {
+  const int burn = burn_rows(K);
+  const Geo G = make_geo(k_solve<T, K, TR>, 0, l.batch, l.n, burn);
+  const ix units = G.batch * G.nseg;
+  const size_t side = sizeof(T) * size_t(units) * K;
+  Scratch ws;
+  ws.s = s;
+  if (scratch_alloc(reinterpret_cast<void**>(&ws.p), side + 12 * size_t(G.batch) + 64, s) != cudaSuccess) return false;
+  SolveP<T> C;
+  C.l = view<T>(l);
+  C.v = view<T>(v);
+  C.x = view<T>(x);
+  C.side = reinterpret_cast<T*>(ws.p);
+  int64_t* fail = reinterpret_cast<int64_t*>(ws.p + (side + 7) / 8 * 8);
+  C.flag = reinterpret_cast<int32_t*>(fail + G.batch);
+  k_init<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, C.flag, G.batch, TR ? 0 : G.n);
+  k_singular<T><<<blocks_for(G.tiles * 32 * G.n, 256), 256, 0, s>>>(C.l, G.batch, TR, fail);
+  {
+    timing::Scope t(TR ? "narrow_solve_t" : "narrow_solve", s);
+    k_solve<T, K, TR><<<unsigned(G.tiles * G.nseg), kThreads, 0, s>>>(C, G);
+  }
+  k_solve_check<T, K, TR><<<blocks_for(units, 128), 128, 0, s>>>(C, G);
+  k_solve_repair<T, K, TR><<<blocks_for(G.batch, kThreads), kThreads, 0, s>>>(C, G);
+  k_report<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, G.batch, G.n, BGM_ERR_SINGULAR, TR, st, row);
+  return true;
+}
+
+template <class T, int K>
+bool run_subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cudaStream_t s) {
+  const size_t smem = sizeof(T) * (K * (K + 1) / 2) * kThreads;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_subset<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_subset_repair<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = true;
+  }
+  const int burn = burn_rows(K);
+  const Geo G = make_geo(k_subset<T, K>, smem, l.batch, l.n, burn);
+  const ix units = G.batch * G.nseg;
+  const size_t side = sizeof(T) * size_t(units) * K * (K + 1);
+  Scratch ws;
+  ws.s = s;
+  if (scratch_alloc(reinterpret_cast<void**>(&ws.p), side + 12 * size_t(G.batch) + 64, s) != cudaSuccess) return false;
+  SubP<T> C;
+  C.l = view<T>(l);
+  C.s = view<T>(sb);
+  C.side = reinterpret_cast<T*>(ws.p);
+  int64_t* fail = reinterpret_cast<int64_t*>(ws.p + (side + 7) / 8 * 8);
+  C.flag = reinterpret_cast<int32_t*>(fail + G.batch);
+  k_init<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, C.flag, G.batch, G.n);
+  k_diag_small<T><<<blocks_for(G.tiles * 32 * G.n, 256), 256, 0, s>>>(C.l, G.batch, fail);
+  {
+    timing::Scope t("narrow_subset", s);
+    k_subset<T, K><<<unsigned(G.tiles * G.nseg), kThreads, smem, s>>>(C, G);
+  }
+  k_subset_check<T, K><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
+  k_subset_repair<T, K><<<blocks_for(G.batch, kThreads), kThreads, smem, s>>>(C, G);
+  k_report<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, G.batch, G.n, BGM_ERR_SINGULAR, 0, st, row);
+  return true;
+}
+
+bool shape_ok(const bgm_band& b) {
+  // tile 32 (coalesced per-cell warp accesses) and long enough to segment
+  return b.tile == 32 && b.upper == 0 && b.batch > 0 && b.n >= 64 && b.lower >= 1 && b.lower <= 16;
+}
+
+}  // namespace
+
+#define BGM_NARROW_K(X) X(1) X(2) X(3) X(4) X(8) X(16)
+
+bool cholesky(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, cudaStream_t s) {
+  if (!shape_ok(q) || l.tile != 32 || l.lower != q.lower) return false;
+  const bool f64 = q.dtype == BGM_F64;
+  switch (q.lower) {
+#define C_(KK) \
+  case KK: return f64 ? run_chol<double, KK>(q, l, st, row, s) : run_chol<float, KK>(q, l, st, row, s);
+    BGM_NARROW_K(C_)
+#undef C_
+    default: return false;
+  }
+}
+
+bool solve_vec(const bgm_band& l, const bgm_vec& v, int tr, const bgm_vec& x, int32_t* st, int64_t* row,
+               cudaStream_t s) {
+  if (!shape_ok(l) || v.tile != 32 || x.tile != 32) return false;
+  const bool f64 = l.dtype == BGM_F64;
+  switch (l.lower) {
+#define S_(KK)                                                                                              \
+  case KK:                                                                                                  \
+    if (f64) return tr ? run_solve<double, KK, true>(l, v, x, st, row, s) : run_solve<double, KK, false>(l, v, x, st, row, s); \
+    return tr ? run_solve<float, KK, true>(l, v, x, st, row, s) : run_solve<float, KK, false>(l, v, x, st, row, s);
+    BGM_NARROW_K(S_)
+#undef S_
+    default: return false;
+  }
+}
+
+bool subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cudaStream_t s) {
+  if (!shape_ok(l) || sb.tile != 32 || sb.lower != l.lower) return false;
+  const bool f64 = l.dtype == BGM_F64;
+  switch (l.lower) {
+#define U_(KK) \
+  case KK: return f64 ? run_subset<double, KK>(l, sb, st, row, s) : run_subset<float, KK>(l, sb, st, row, s);
+    BGM_NARROW_K(U_)
+#undef U_
+    default: return false;
+  }
+}
+
+void set_segment_rows(int rows) { g_segment_rows = rows; }
+
+}  // namespace narrow
+}  // namespace bgm

@@ -18,4 +18,13 @@ bool log_det(const bgm_band& l, void* out, int32_t* st, int64_t* row, cudaStream
 void set_segment_rows(int rows);
 
 }  // namespace wide
+
+// Narrow-band (k <= 16, tile 32) fast paths (bgm_narrow.cu).
+namespace narrow {
+bool cholesky(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, cudaStream_t s);
+bool solve_vec(const bgm_band& l, const bgm_vec& v, int tr, const bgm_vec& x, int32_t* st, int64_t* row,
+               cudaStream_t s);
+bool subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cudaStream_t s);
+void set_segment_rows(int rows);
+}  // namespace narrow
 }  // namespace bgm
