@@ -410,6 +410,141 @@ __global__ void k_diag_small(Band<T> l, ix batch, int64_t* fail) {
     atomicMin(reinterpret_cast<unsigned long long*>(fail + b), static_cast<unsigned long long>(i));
 }
 
+// ------------------------------------------------------------------ vjp_cholesky
+// grad.cpp:11-36 (Giles' reverse sweep).  Row i of q_bar solves
+//   q_i = 1/2 r_i / L(i,i),   q_j = (r_j - 2 q_i L(i,j) - sum_{j<j'<i} q_j' L(j',j)) / L(j,j)
+// (r = the current l_bar row i; left-looking, so column j of L is read
+// contiguously), then the rows above are updated l_bar(j,k) -= q_j L(i,k)
+// (k <= j; k = j is the reference's diagonal update).  Window: l_bar over
+// rows [i-K, i] x cols [i-K, row], packed [entry][thread], index (x, y) =
+// (row - (i-K), col - (i-K)); each step drops row i and takes column i-K-1
+// of the input.
+template <class T>
+struct VcholP {
+  Band<T> l, lb, qb;
+  T* side;  // [unit][K][K+1]
+  int32_t* flag;
+};
+
+template <class T, int K>
+__device__ void vchol_unit(const VcholP<T>& C, ix b, ix n, ix s, ix e, ix start, T* side, T* win) {
+  constexpr int W = K + 1, ts = kThreads;
+  auto Wb = [&](int x, int y) -> T& { return win[tri(x, y) * ts]; };
+  const T* lbase = bbase(C.l, b);
+  const T* gbase = bbase(C.lb, b);
+  T* qbase = bbase(C.qb, b);
+  const ix cs = ix(W) * 32;
+  auto L = [&](ix r, ix c) -> T {  // L(r, c), 0 <= r - c <= K
+    return (c >= 0 && r < n) ? lbase[c * cs + (r - c) * 32] : T(0);
+  };
+  // window for row `start`: input l_bar rows [start-K, start], cols [start-K, row]
+#pragma unroll 1
+  for (int x = 0; x <= K; ++x)
+    for (int y = 0; y <= x; ++y) {
+      const ix r = start - K + x, c = start - K + y;
+      Wb(x, y) = (c >= 0 && r < n) ? gbase[c * cs + (x - y) * 32] : T(0);
+    }
+#pragma unroll 1
+  for (ix i = start; i >= s; --i) {
+    T r[W], lr[W], q[W];
+#pragma unroll
+    for (int y = 0; y <= K; ++y) {
+      r[y] = Wb(K, y);
+      lr[y] = L(i, i - K + y);
+    }
+    q[K] = T(0.5) * r[K] / lr[K];
+#pragma unroll
+    for (int x = K - 1; x >= 0; --x) {
+      const ix j = i - K + x;
+      if (j < 0) {
+        q[x] = T(0);
+        continue;
+      }
+      const T* colj = lbase + j * cs;
+      T acc = fma(T(-2) * q[K], lr[x], r[x]);
+#pragma unroll
+      for (int x2 = x + 1; x2 < K; ++x2) acc = fma(-q[x2], colj[(x2 - x) * 32], acc);
+      q[x] = acc / colj[0];
+    }
+    // q_bar row i (stored at cell (i - j, j)), or the burn-in copy
+    if (i < e) {
+#pragma unroll
+      for (int x = 0; x <= K; ++x)
+        if (i - K + x >= 0) qbase[(i - K + x) * cs + (K - x) * 32] = q[x];
+    } else if (side && i < e + K) {
+      T* sd = side + (i - e) * W;
+#pragma unroll
+      for (int x = 0; x <= K; ++x) sd[x] = q[x];
+    }
+    // rank-1 update of rows [i-K, i-1] and the shift to row i-1's window:
+    // (x, y) -> (x+1, y+1), decreasing packed index = in-place memmove order
+#pragma unroll
+    for (int x = K - 1; x >= 0; --x) {
+#pragma unroll
+      for (int y = x; y >= 0; --y) Wb(x + 1, y + 1) = fma(-q[x], lr[y], Wb(x, y));
+    }
+    const ix c = i - 1 - K;  // entering column (rows c .. c+K)
+#pragma unroll
+    for (int x = 0; x <= K; ++x) Wb(x, 0) = (c >= 0 && c + x < n) ? gbase[c * cs + x * 32] : T(0);
+  }
+}
+
+template <class T, int K>
+__global__ void k_vchol(VcholP<T> C, Geo G) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* sm = reinterpret_cast<T*>(smraw);
+  const Unit u = unit_of(G);
+  if (!u.live) return;
+  const ix s = ix(u.p) * G.seg, e = s + G.seg < G.n ? s + G.seg : G.n;
+  const ix start = e + G.burn - 1 < G.n - 1 ? e + G.burn - 1 : G.n - 1;
+  vchol_unit<T, K>(C, u.b, G.n, s, e, start, u.p + 1 < G.nseg ? C.side + u.id * ix(K) * (K + 1) : nullptr,
+                   sm + threadIdx.x);
+}
+
+// thread per (unit, row): q_bar rows [e, e+K) from burn-in vs genuine
+template <class T, int K>
+__global__ void k_vchol_check(VcholP<T> C, Geo G) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  const ix id = t / K;
+  const int c = int(t % K);
+  if (id >= G.batch * G.nseg) return;
+  const int p = int(id % G.nseg);
+  if (p + 1 >= G.nseg) return;
+  const ix b = id / G.nseg, i = ix(p + 1) * G.seg + c;
+  if (i >= G.n) return;
+  const T* sd = C.side + (id * K + c) * (K + 1);
+  double sc = 0.0;
+  for (int x = 0; x <= K; ++x)
+    if (i - K + x >= 0) sc = fmax(sc, dabs(C.qb.cell(b, K - x, i - K + x)));
+  const double tol = sizeof(T) == 8 ? kCheckTol : 1e-5;
+  bool bad = false;
+  for (int x = 0; x <= K; ++x)
+    if (i - K + x >= 0)
+      bad |= !(fabs(double(sd[x]) - double(C.qb.cell(b, K - x, i - K + x))) <= tol * (sc + 1e-300));
+  if (bad) C.flag[b] = 1;
+}
+
+template <class T, int K>
+__global__ void k_vchol_repair(VcholP<T> C, Geo G) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* sm = reinterpret_cast<T*>(smraw);
+  const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (b >= G.batch || !C.flag[b]) return;
+  vchol_unit<T, K>(C, b, G.n, 0, G.n, G.n - 1, nullptr, sm + threadIdx.x);
+}
+
+// corner cells (j + r >= n) of an output band are exact zeros
+template <class T>
+__global__ void k_zero_corners(Band<T> o, ix batch) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  const int K = o.lo;
+  ix b, jj;
+  if (!split_bj(t, batch, ix(K) * (K + 1), o.s, b, jj)) return;
+  const ix j = o.n - K + jj / (K + 1);
+  const int r = int(jj % (K + 1));
+  if (j >= 0 && j + r >= o.n) o.cell(b, r, j) = T(0);
+}
+
 // ------------------------------------------------------------------ common
 __global__ void k_init(int64_t* fail, int32_t* flag, ix batch, int64_t v) {
   const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
@@ -495,8 +630,14 @@ bool run_chol(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, c
     timing::Scope t("narrow_chol", s);
     k_chol<T, K><<<unsigned(G.tiles * G.nseg), kThreads, smem, s>>>(C, G);
   }
-  k_chol_check<T, K><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
-  k_chol_repair<T, K><<<blocks_for(G.batch, kThreads), kThreads, smem, s>>>(C, G);
+  {
+    timing::Scope t("narrow_chol_check", s);
+    k_chol_check<T, K><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
+  }
+  {
+    timing::Scope t("narrow_chol_repair", s);
+    k_chol_repair<T, K><<<blocks_for(G.batch, kThreads), kThreads, smem, s>>>(C, G);
+  }
   k_report<<<blocks_for(G.batch, 128), 128, 0, s>>>(C.fail, G.batch, G.n, BGM_ERR_NOT_PD, 0, st, row);
   return true;
 }
@@ -523,8 +664,14 @@ bool run_solve(const bgm_band& l, const bgm_vec& v, const bgm_vec& x, int32_t* s
     timing::Scope t(TR ? "narrow_solve_t" : "narrow_solve", s);
     k_solve<T, K, TR><<<unsigned(G.tiles * G.nseg), kThreads, 0, s>>>(C, G);
   }
-  k_solve_check<T, K, TR><<<blocks_for(units, 128), 128, 0, s>>>(C, G);
-  k_solve_repair<T, K, TR><<<blocks_for(G.batch, kThreads), kThreads, 0, s>>>(C, G);
+  {
+    timing::Scope t("narrow_solve_check", s);
+    k_solve_check<T, K, TR><<<blocks_for(units, 128), 128, 0, s>>>(C, G);
+  }
+  {
+    timing::Scope t("narrow_solve_repair", s);
+    k_solve_repair<T, K, TR><<<blocks_for(G.batch, kThreads), kThreads, 0, s>>>(C, G);
+  }
   k_report<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, G.batch, G.n, BGM_ERR_SINGULAR, TR, st, row);
   return true;
 }
@@ -557,9 +704,53 @@ bool run_subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row
     timing::Scope t("narrow_subset", s);
     k_subset<T, K><<<unsigned(G.tiles * G.nseg), kThreads, smem, s>>>(C, G);
   }
-  k_subset_check<T, K><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
-  k_subset_repair<T, K><<<blocks_for(G.batch, kThreads), kThreads, smem, s>>>(C, G);
+  {
+    timing::Scope t("narrow_subset_check", s);
+    k_subset_check<T, K><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
+  }
+  {
+    timing::Scope t("narrow_subset_repair", s);
+    k_subset_repair<T, K><<<blocks_for(G.batch, kThreads), kThreads, smem, s>>>(C, G);
+  }
   k_report<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, G.batch, G.n, BGM_ERR_SINGULAR, 0, st, row);
+  return true;
+}
+
+template <class T, int K>
+bool run_vchol(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cudaStream_t s) {
+  const size_t smem = sizeof(T) * ((K + 1) * (K + 2) / 2) * kThreads;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_vchol<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_vchol_repair<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = true;
+  }
+  const Geo G = make_geo(k_vchol<T, K>, smem, l.batch, l.n, burn_rows(K));
+  const ix units = G.batch * G.nseg;
+  const size_t side = sizeof(T) * size_t(units) * K * (K + 1);
+  Scratch ws;
+  ws.s = s;
+  if (scratch_alloc(reinterpret_cast<void**>(&ws.p), side + 8 * size_t(G.batch) + 64, s) != cudaSuccess) return false;
+  VcholP<T> C;
+  C.l = view<T>(l);
+  C.lb = view<T>(lb);
+  C.qb = view<T>(qb);
+  C.side = reinterpret_cast<T*>(ws.p);
+  C.flag = reinterpret_cast<int32_t*>(ws.p + (side + 7) / 8 * 8);
+  cudaMemsetAsync(C.flag, 0, sizeof(int32_t) * size_t(G.batch), s);
+  {
+    timing::Scope t("narrow_vjp_chol", s);
+    k_vchol<T, K><<<unsigned(G.tiles * G.nseg), kThreads, smem, s>>>(C, G);
+  }
+  {
+    timing::Scope t("narrow_vjp_chol_check", s);
+    k_vchol_check<T, K><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
+  }
+  {
+    timing::Scope t("narrow_vjp_chol_repair", s);
+    k_vchol_repair<T, K><<<blocks_for(G.batch, kThreads), kThreads, smem, s>>>(C, G);
+  }
+  k_zero_corners<T><<<blocks_for(G.tiles * 32 * K * (K + 1), 128), 128, 0, s>>>(C.qb, G.batch);
   return true;
 }
 
@@ -607,6 +798,20 @@ bool subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cu
   case KK: return f64 ? run_subset<double, KK>(l, sb, st, row, s) : run_subset<float, KK>(l, sb, st, row, s);
     BGM_NARROW_K(U_)
 #undef U_
+    default: return false;
+  }
+}
+
+bool vjp_cholesky(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cudaStream_t s) {
+  if (!shape_ok(l) || lb.tile != 32 || qb.tile != 32 || lb.lower != l.lower || qb.lower != l.lower ||
+      lb.upper != 0 || qb.upper != 0)
+    return false;
+  const bool f64 = l.dtype == BGM_F64;
+  switch (l.lower) {
+#define V_(KK) \
+  case KK: return f64 ? run_vchol<double, KK>(l, lb, qb, s) : run_vchol<float, KK>(l, lb, qb, s);
+    BGM_NARROW_K(V_)
+#undef V_
     default: return false;
   }
 }

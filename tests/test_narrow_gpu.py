@@ -45,6 +45,8 @@ def test_narrow_ops(cuda, oracle, segrows, k, B, n, seg, kind):
         assert cm.max_rel_err(x_g, oracle.solve_vec(l_o, v, tr)[0]) <= 1e-9, f"solve {tr}"
     s_g = gpu.sparse_inverse_subset(l_o)[0]
     assert cm.max_rel_err(s_g, oracle.sparse_inverse_subset(l_o)[0]) <= 1e-9, "subset"
+    lbar = cm.random_band(rng, B, n, k, 0)
+    assert cm.max_rel_err(gpu.vjp_cholesky(l_o, lbar), oracle.vjp_cholesky(l_o, lbar)) <= 1e-9, "vjp_cholesky"
 
 
 def test_narrow_repair_and_errors(cuda, oracle, segrows, monkeypatch):
@@ -80,6 +82,8 @@ def test_narrow_repair_and_errors(cuda, oracle, segrows, monkeypatch):
     assert np.array_equal(st, st_o) and row[7] == 100
     good = np.nonzero(st_o == 0)[0]
     assert cm.max_rel_err(s_g[good], s_o[good]) <= 1e-9
+    lbar = cm.random_band(rng, B, n, k, 0)
+    assert cm.max_rel_err(gpu.vjp_cholesky(l[good], lbar[good]), oracle.vjp_cholesky(l[good], lbar[good])) <= 1e-9
 
 
 def test_narrow_fp32(cuda, oracle, segrows):
