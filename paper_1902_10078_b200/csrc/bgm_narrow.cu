@@ -183,7 +183,8 @@ struct SolveP {
 // reference divides, kernels_serial.cpp:47).  Backward: x window x[a] =
 // x_{i+1+a}; x_i = (v_i - sum_a L(i+1+a, i) x[a]) / L(i,i).
 template <class T, int K, bool TR>
-__device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start, T* side) {
+__device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start, T* side,
+                           const T* carry = nullptr) {
   constexpr int W = K + 1;
   const T* lb = bbase(C.l, b);
   const T* vb = vbase(C.v, b);
@@ -200,9 +201,22 @@ __device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start,
   if (!TR) {
 #pragma unroll
     for (int a = 0; a <= K; ++a) win[a] = (start + a < n) ? vb[(start + a) * 32] : T(0);
+    if (carry) {  // exact carry-in: x_{s-K .. s-1} known; start == s
+#pragma unroll
+      for (int a = 0; a <= K; ++a) {
+        const ix r = start + a;
+        if (r >= n) continue;
+#pragma unroll
+        for (int m = 0; m < K; ++m) {  // column start-K+m, row r: cell r - (start-K+m)
+          const ix c = start - K + m;
+          const int cell = int(r - c);
+          if (c >= 0 && cell <= K) win[a] = fma(-lb[c * cs + cell * 32], carry[m], win[a]);
+        }
+      }
+    }
   } else {
 #pragma unroll
-    for (int a = 0; a <= K; ++a) win[a] = T(0);
+    for (int a = 0; a <= K; ++a) win[a] = (carry && a < K) ? carry[a] : T(0);
   }
   T cn[W], vn;
   load_col(start, cn, vn);
@@ -255,7 +269,7 @@ __global__ void k_solve(SolveP<T> C, Geo G) {
 }
 
 template <class T, int K, bool TR>
-__global__ void k_solve_check(SolveP<T> C, Geo G) {
+__global__ void k_solve_check(SolveP<T> C, Geo G, int32_t* uflag) {
   const ix id = blockIdx.x * ix(blockDim.x) + threadIdx.x;
   if (id >= G.batch * G.nseg) return;
   const int p = int(id % G.nseg);
@@ -269,7 +283,7 @@ __global__ void k_solve_check(SolveP<T> C, Geo G) {
   bool bad = false;
   for (int c = 0; c < K; ++c)
     if (r0 + c < G.n) bad |= !(fabs(double(C.side[id * K + c]) - double(C.x(b, r0 + c))) <= tol * (sc + 1e-300));
-  if (bad) C.flag[b] = 1;
+  uflag[id] = bad ? 1 : 0;
 }
 
 template <class T, int K, bool TR>
@@ -277,6 +291,49 @@ __global__ void k_solve_repair(SolveP<T> C, Geo G) {
   const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
   if (b >= G.batch || !C.flag[b]) return;
   solve_unit<T, K, TR>(C, b, G.n, 0, G.n, TR ? G.n - 1 : 0, nullptr);
+}
+
+// Fix-up of segments whose burn-in did not converge: the neighbour's genuine
+// boundary values (snapshot) give the exact carry-in, and the segment is
+// recomputed from it.  A re-check then confirms the snapshot the next
+// segment used was itself final; anything else goes to the full repair.
+template <class T, int K, bool TR>
+__global__ void k_solve_snap(SolveP<T> C, Geo G, T* snap) {
+  const ix id = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (id >= G.batch * G.nseg) return;
+  const int p = int(id % G.nseg);
+  const ix b = id / G.nseg, s = ix(p) * G.seg, e = s + G.seg < G.n ? s + G.seg : G.n;
+  for (int c = 0; c < K; ++c) {
+    const ix r = TR ? s + c : e - K + c;
+    snap[id * K + c] = (r >= 0 && r < G.n) ? C.x(b, r) : T(0);
+  }
+}
+
+template <class T, int K, bool TR>
+__global__ void k_solve_fix(SolveP<T> C, Geo G, const int32_t* uflag, const T* snap) {
+  const Unit u = unit_of(G);
+  if (!u.live || !uflag[u.id]) return;
+  const ix s = ix(u.p) * G.seg, e = s + G.seg < G.n ? s + G.seg : G.n;
+  const T* carry = snap + (TR ? u.id + 1 : u.id - 1) * K;
+  solve_unit<T, K, TR>(C, u.b, G.n, s, e, TR ? e - 1 : s, nullptr, carry);
+}
+
+template <class T, int K, bool TR>
+__global__ void k_solve_recheck(SolveP<T> C, Geo G, const int32_t* uflag, const T* snap) {
+  const ix id = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (id >= G.batch * G.nseg || !uflag[id]) return;
+  const int p = int(id % G.nseg);
+  if (TR ? p == 0 : p + 1 >= G.nseg) return;  // nobody downstream
+  const ix b = id / G.nseg, s = ix(p) * G.seg, e = s + G.seg < G.n ? s + G.seg : G.n;
+  double sc = 0.0;
+  for (int c = 0; c < K; ++c) sc = fmax(sc, dabs(snap[id * K + c]));
+  const double tol = sizeof(T) == 8 ? kCheckTol : 1e-5;
+  bool bad = false;
+  for (int c = 0; c < K; ++c) {
+    const ix r = TR ? s + c : e - K + c;
+    if (r >= 0 && r < G.n) bad |= !(fabs(double(C.x(b, r)) - double(snap[id * K + c])) <= tol * (sc + 1e-300));
+  }
+  if (bad) C.flag[b] = 1;
 }
 
 template <class T>
@@ -650,14 +707,17 @@ bool run_solve(const bgm_band& l, const bgm_vec& v, const bgm_vec& x, int32_t* s
   const size_t side = sizeof(T) * size_t(units) * K;
   Scratch ws;
   ws.s = s;
-  if (scratch_alloc(reinterpret_cast<void**>(&ws.p), side + 12 * size_t(G.batch) + 64, s) != cudaSuccess) return false;
+  const size_t bytes = 2 * side + sizeof(int32_t) * size_t(units) + 12 * size_t(G.batch) + 128;
+  if (scratch_alloc(reinterpret_cast<void**>(&ws.p), bytes, s) != cudaSuccess) return false;
   SolveP<T> C;
   C.l = view<T>(l);
   C.v = view<T>(v);
   C.x = view<T>(x);
   C.side = reinterpret_cast<T*>(ws.p);
-  int64_t* fail = reinterpret_cast<int64_t*>(ws.p + (side + 7) / 8 * 8);
+  T* snap = reinterpret_cast<T*>(ws.p + side);
+  int64_t* fail = reinterpret_cast<int64_t*>(ws.p + (2 * side + 7) / 8 * 8);
   C.flag = reinterpret_cast<int32_t*>(fail + G.batch);
+  int32_t* uflag = C.flag + G.batch;
   k_init<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, C.flag, G.batch, TR ? 0 : G.n);
   k_singular<T><<<blocks_for(G.tiles * 32 * G.n, 256), 256, 0, s>>>(C.l, G.batch, TR, fail);
   {
@@ -666,7 +726,13 @@ bool run_solve(const bgm_band& l, const bgm_vec& v, const bgm_vec& x, int32_t* s
   }
   {
     timing::Scope t("narrow_solve_check", s);
-    k_solve_check<T, K, TR><<<blocks_for(units, 128), 128, 0, s>>>(C, G);
+    k_solve_check<T, K, TR><<<blocks_for(units, 128), 128, 0, s>>>(C, G, uflag);
+    k_solve_snap<T, K, TR><<<blocks_for(units, 128), 128, 0, s>>>(C, G, snap);
+  }
+  {
+    timing::Scope t("narrow_solve_fix", s);
+    k_solve_fix<T, K, TR><<<unsigned(G.tiles * G.nseg), kThreads, 0, s>>>(C, G, uflag, snap);
+    k_solve_recheck<T, K, TR><<<blocks_for(units, 128), 128, 0, s>>>(C, G, uflag, snap);
   }
   {
     timing::Scope t("narrow_solve_repair", s);
