@@ -55,7 +55,7 @@ bool product(const bgm_band&, int, const bgm_band&, int, const bgm_band&, cudaSt
 bool band_vec(const bgm_band&, const bgm_vec&, int, const bgm_vec&, cudaStream_t) { return false; }
 bool vjp_cholesky(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cudaStream_t s) {
   if (disabled()) return false;
-  return narrow::vjp_cholesky(l, lb, qb, s);
+  return narrow::vjp_cholesky(l, lb, qb, s) || wide::vjp_cholesky(l, lb, qb, s);
 }
 bool vjp_subset(const bgm_band&, const bgm_band&, const bgm_band&, const bgm_band&, int32_t*,
                 int64_t*, cudaStream_t) {

@@ -685,6 +685,190 @@ __global__ void k_logdet_sum(const double* part, const int64_t* fail, ix batch, 
   report(status, row, b, ok ? BGM_OK : BGM_ERR_NONPOS_DIAG, ok ? -1 : fail[b]);
 }
 
+// ------------------------------------------------------------------ vjp_cholesky
+// grad.cpp:11-36 for wide bands, one warp per (matrix, segment).  The l_bar
+// window (rows [i-K, i] x cols [i-K, row]) and the matching window of L live
+// in shared memory as packed lower triangles indexed (x, y) = (row - (i-K),
+// col - (i-K)); per row:
+//   * the row's back-substitution (q_K = 1/2 r_K / L_ii, then right-looking
+//     over x2 = K-1..0: q = r'_x2 / L(j2,j2), r'_y -= q L(j2, j_y)), lanes own
+//     y = lane + 32t, the pivot value travels by shuffle;
+//   * l_bar(j, k) -= q_j L(i, k) fused with the shift (x, y) -> (x+1, y+1) of
+//     both windows, processed in descending 32-entry chunks (each chunk loads
+//     before it stores, so the in-place shift never reads a moved entry);
+//   * column i-1-K of l_bar and L enters at y = 0.
+template <class T>
+struct VcP {
+  Band<T> l, lb, qb;
+  T* side;  // [unit][K][K+1] burn-in copies of q_bar rows [e, e+K)
+  int32_t* flag;
+};
+
+__device__ __forceinline__ int tri_w(int a, int b) { return a * (a + 1) / 2 + b; }
+__device__ __forceinline__ void untri(int idx, int& x, int& y) {
+  int a = int((sqrtf(8.0f * float(idx) + 1.0f) - 1.0f) * 0.5f);
+  if (tri_w(a + 1, 0) <= idx) ++a;
+  if (tri_w(a, 0) > idx) --a;
+  x = a;
+  y = idx - tri_w(a, 0);
+}
+
+template <class T, int K>
+__device__ void vchol_warp(const VcP<T>& C, ix b, ix n, ix s, ix e, ix start, T* side, T* Wb, T* Lw,
+                           T* sq, T* slr, T* sinv) {
+  constexpr int R = (K + 1 + 31) / 32, NP = (K + 1) * (K + 2) / 2, N1 = K * (K + 1) / 2;
+  const int lane = threadIdx.x & 31;
+  for (int idx = lane; idx < NP; idx += 32) {
+    int x, y;
+    untri(idx, x, y);
+    const ix r = start - K + x, c = start - K + y;
+    const bool in = c >= 0 && r < n;
+    Wb[idx] = in ? C.lb.cell(b, x - y, c) : T(0);
+    Lw[idx] = in ? C.l.cell(b, x - y, c) : T(0);
+  }
+  __syncwarp();
+#pragma unroll 1
+  for (ix i = start; i >= s; --i) {
+    T rr[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      const int y = lane + 32 * t;
+      rr[t] = (y <= K) ? Wb[tri_w(K, y)] : T(0);
+      if (y <= K) {
+        slr[y] = Lw[tri_w(K, y)];
+        const T d = Lw[tri_w(y, y)];
+        sinv[y] = (i - K + y >= 0) ? T(1) / d : T(0);
+      }
+    }
+    __syncwarp();
+    const T qK = T(0.5) * Wb[tri_w(K, K)] / Lw[tri_w(K, K)];
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      const int y = lane + 32 * t;
+      if (y < K) rr[t] = fma(T(-2) * qK, slr[y], rr[t]);
+    }
+    if (lane == 0) sq[K] = qK;
+#pragma unroll 1
+    for (int x2 = K - 1; x2 >= 0; --x2) {
+      const int slot = x2 >> 5, owner = x2 & 31;
+      T v = rr[0];
+#pragma unroll
+      for (int t = 1; t < R; ++t)
+        if (slot == t) v = rr[t];
+      v = __shfl_sync(0xffffffffu, v, owner);
+      const T q = v * sinv[x2];
+      if (lane == owner) sq[x2] = q;
+      const T* lrow = Lw + tri_w(x2, 0);  // L(j2, j_y) = Lw(x2, y)
+#pragma unroll
+      for (int t = 0; t < R; ++t) {
+        const int y = lane + 32 * t;
+        if (y < x2) rr[t] = fma(-q, lrow[y], rr[t]);
+      }
+    }
+    __syncwarp();
+    // q_bar row i: q_x at cell (K - x) of column i-K+x
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      const int x = lane + 32 * t;
+      if (x <= K && i - K + x >= 0) {
+        if (i < e) C.qb.cell(b, K - x, i - K + x) = sq[x];
+        else if (side && i < e + K) side[(i - e) * (K + 1) + x] = sq[x];
+      }
+    }
+    // update + shift, descending chunks
+#pragma unroll 1
+    for (int base = (N1 - 1) & ~31; base >= 0; base -= 32) {
+      const int idx = base + lane;
+      T wv = T(0), lv = T(0);
+      int x = 0, y = 0;
+      const bool ok = idx < N1;
+      if (ok) {
+        untri(idx, x, y);
+        wv = fma(-sq[x], slr[y], Wb[idx]);
+        lv = Lw[idx];
+      }
+      __syncwarp();
+      if (ok) {
+        const int d = tri_w(x + 1, y + 1);
+        Wb[d] = wv;
+        Lw[d] = lv;
+      }
+      __syncwarp();
+    }
+    const ix c = i - 1 - K;  // entering column
+    for (int x = lane; x <= K; x += 32) {
+      const bool in = c >= 0 && c + x < n;
+      Wb[tri_w(x, 0)] = in ? C.lb.cell(b, x, c) : T(0);
+      Lw[tri_w(x, 0)] = in ? C.l.cell(b, x, c) : T(0);
+    }
+    __syncwarp();
+  }
+}
+
+template <class T, int K>
+struct VcSmem {
+  static constexpr int NP = (K + 1) * (K + 2) / 2;
+  static constexpr size_t bytes = sizeof(T) * (2 * NP + 3 * (K + 1));
+};
+
+template <class T, int K>
+__global__ void __launch_bounds__(32) k_vchol_w(VcP<T> C, Geo G) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* sm = reinterpret_cast<T*>(smraw);
+  constexpr int NP = VcSmem<T, K>::NP;
+  const ix unit = blockIdx.x;
+  const ix b = unit / G.nseg;
+  const int p = int(unit % G.nseg);
+  if (b >= G.batch) return;
+  const ix s = ix(p) * G.seg, e = s + G.seg < G.n ? s + G.seg : G.n;
+  const ix start = e + G.burn - 1 < G.n - 1 ? e + G.burn - 1 : G.n - 1;
+  vchol_warp<T, K>(C, b, G.n, s, e, start, p + 1 < G.nseg ? C.side + unit * ix(K) * (K + 1) : nullptr, sm,
+                   sm + NP, sm + 2 * NP, sm + 2 * NP + (K + 1), sm + 2 * NP + 2 * (K + 1));
+}
+
+template <class T, int K>
+__global__ void k_vchol_w_check(VcP<T> C, Geo G) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  const ix id = t / K;
+  const int c = int(t % K);
+  if (id >= G.batch * G.nseg) return;
+  const int p = int(id % G.nseg);
+  if (p + 1 >= G.nseg) return;
+  const ix b = id / G.nseg, i = ix(p + 1) * G.seg + c;
+  if (i >= G.n) return;
+  const T* sd = C.side + (id * K + c) * (K + 1);
+  double sc = 0.0;
+  for (int x = 0; x <= K; ++x)
+    if (i - K + x >= 0) sc = fmax(sc, fabs(double(C.qb.cell(b, K - x, i - K + x))));
+  const double tol = sizeof(T) == 8 ? kCheckTol : 1e-5;
+  bool bad = false;
+  for (int x = 0; x <= K; ++x)
+    if (i - K + x >= 0) bad |= !(fabs(double(sd[x]) - double(C.qb.cell(b, K - x, i - K + x))) <= tol * (sc + 1e-300));
+  if (bad) C.flag[b] = 1;
+}
+
+template <class T, int K>
+__global__ void __launch_bounds__(32) k_vchol_w_repair(VcP<T> C, Geo G) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* sm = reinterpret_cast<T*>(smraw);
+  constexpr int NP = VcSmem<T, K>::NP;
+  const ix b = blockIdx.x;
+  if (b >= G.batch || !C.flag[b]) return;
+  vchol_warp<T, K>(C, b, G.n, 0, G.n, G.n - 1, nullptr, sm, sm + NP, sm + 2 * NP, sm + 2 * NP + (K + 1),
+                   sm + 2 * NP + 2 * (K + 1));
+}
+
+template <class T>
+__global__ void k_zero_corners_w(Band<T> o, ix batch) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  const int K = o.lo;
+  ix b, jj;
+  if (!split_bj(t, batch, ix(K) * (K + 1), o.s, b, jj)) return;
+  const ix j = o.n - K + jj / (K + 1);
+  const int r = int(jj % (K + 1));
+  if (j >= 0 && j + r >= o.n) o.cell(b, r, j) = T(0);
+}
+
 int g_segment_rows = 0;
 
 template <class T, int K, int P, int TS>
@@ -857,6 +1041,62 @@ bool run_logdet(const bgm_band& l, void* out, int32_t* st, int64_t* row, cudaStr
   scratch_free(ws, s);
   return true;
 }
+
+template <class T, int K>
+bool run_vchol(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cudaStream_t s) {
+  const size_t smem = VcSmem<T, K>::bytes;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_vchol_w<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_vchol_w_repair<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = true;
+  }
+  Geo G;
+  G.batch = l.batch;
+  G.n = l.n;
+  G.burn = kBurnGen * K;
+  if (const char* bv = std::getenv("BGM_WIDE_BURN"))
+    if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
+  ix seg = g_segment_rows;
+  if (seg <= 0) {
+    int sms = 148, dev = 0, per = 1;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_vchol_w<T, K>, 32, smem);
+    ix nseg = ix(sms) * (per > 0 ? per : 1) / (G.batch > 0 ? G.batch : 1);
+    if (nseg < 1) nseg = 1;
+    seg = (G.n + nseg - 1) / nseg;
+    if (seg < 2 * ix(G.burn)) seg = 2 * ix(G.burn);
+  }
+  G.seg = seg;
+  G.nseg = int((G.n + seg - 1) / seg);
+  const ix units = G.batch * G.nseg;
+  const size_t side = sizeof(T) * size_t(units) * K * (K + 1);
+  char* ws = nullptr;
+  if (scratch_alloc(reinterpret_cast<void**>(&ws), side + 4 * size_t(G.batch) + 64, s) != cudaSuccess) return false;
+  VcP<T> C;
+  C.l = view<T>(l);
+  C.lb = view<T>(lb);
+  C.qb = view<T>(qb);
+  C.side = reinterpret_cast<T*>(ws);
+  C.flag = reinterpret_cast<int32_t*>(ws + (side + 7) / 8 * 8);
+  cudaMemsetAsync(C.flag, 0, sizeof(int32_t) * size_t(G.batch), s);
+  {
+    timing::Scope ts("wide_vjp_chol", s);
+    k_vchol_w<T, K><<<unsigned(units), 32, smem, s>>>(C, G);
+  }
+  {
+    timing::Scope ts("wide_vjp_chol_check", s);
+    k_vchol_w_check<T, K><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
+  }
+  {
+    timing::Scope ts("wide_vjp_chol_repair", s);
+    k_vchol_w_repair<T, K><<<unsigned(G.batch), 32, smem, s>>>(C, G);
+  }
+  const ix zw = ((G.batch + l.tile - 1) / l.tile * l.tile) * K * (K + 1);
+  k_zero_corners_w<T><<<blocks_for(zw, 128), 128, 0, s>>>(C.qb, G.batch);
+  scratch_free(ws, s);
+  return true;
+}
 }  // namespace
 
 bool cholesky(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, cudaStream_t s) {
@@ -903,6 +1143,18 @@ bool solve_vec(const bgm_band& l, const bgm_vec& v, int tr, const bgm_vec& x, in
 bool log_det(const bgm_band& l, void* out, int32_t* st, int64_t* row, cudaStream_t s) {
   if (l.batch == 0 || l.n == 0) return false;
   return l.dtype == BGM_F64 ? run_logdet<double>(l, out, st, row, s) : run_logdet<float>(l, out, st, row, s);
+}
+
+bool vjp_cholesky(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cudaStream_t s) {
+  if (l.upper != 0 || lb.upper != 0 || qb.upper != 0 || lb.lower != l.lower || qb.lower != l.lower ||
+      l.batch == 0 || l.n < 4 * l.lower)
+    return false;
+  const bool f64 = l.dtype == BGM_F64;
+  switch (l.lower) {
+    case 64: return f64 ? run_vchol<double, 64>(l, lb, qb, s) : run_vchol<float, 64>(l, lb, qb, s);
+    case 128: return f64 ? run_vchol<double, 128>(l, lb, qb, s) : run_vchol<float, 128>(l, lb, qb, s);
+    default: return false;
+  }
 }
 
 void set_segment_rows(int rows) { g_segment_rows = rows; }

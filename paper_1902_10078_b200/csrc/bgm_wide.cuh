@@ -15,6 +15,7 @@ bool subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cu
 bool solve_vec(const bgm_band& l, const bgm_vec& v, int tr, const bgm_vec& x, int32_t* st, int64_t* row,
                cudaStream_t s);
 bool log_det(const bgm_band& l, void* out, int32_t* st, int64_t* row, cudaStream_t s);
+bool vjp_cholesky(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cudaStream_t s);
 void set_segment_rows(int rows);
 
 }  // namespace wide

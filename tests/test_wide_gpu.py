@@ -15,10 +15,11 @@ from tests import common as cm
 
 pytestmark = pytest.mark.gpu
 FP32_FLOOR = 1e-5
+FP32_FLOOR_VJP = 1e-4  # adjoints of random-sign cotangents cancel harder
 
 
-def _fp32_ok(g, o):
-    err = cm.max_rel_err(g, o, floor_scale=FP32_FLOOR)
+def _fp32_ok(g, o, floor=FP32_FLOOR):
+    err = cm.max_rel_err(g, o, floor_scale=floor)
     assert err < 1e-4, err
     assert np.linalg.norm(g - o) <= 1e-5 * np.linalg.norm(o)
 
@@ -167,3 +168,32 @@ def test_wide_solve_repair_singular_fp32(cuda, oracle, segrows, monkeypatch, tr)
     l32 = oracle.cholesky(_q(oracle, rng, 2, n, k, "cfg4"))[0].astype(np.float32).astype(np.float64)
     v32 = v[1:].astype(np.float32).astype(np.float64)
     _fp32_ok(GpuOracle(tile=1, dtype=torch.float32).solve_vec(l32, v32, tr)[0], oracle.solve_vec(l32, v32, tr)[0])
+
+
+@pytest.mark.parametrize("k,n", [(64, 700), (128, 1100)])
+@pytest.mark.parametrize("tile", [1, 32])
+@pytest.mark.parametrize("seg", [0, 270])
+@pytest.mark.parametrize("kind", ["cfg4", "dominant"])
+def test_wide_vjp_cholesky(cuda, oracle, segrows, k, n, tile, seg, kind):
+    from tests.gpu_adapter import GpuOracle
+    rng = np.random.default_rng(11 * k + n + seg)
+    l = oracle.cholesky(_q(oracle, rng, 3, n, k, kind))[0]
+    lbar = cm.random_band(rng, 3, n, k, 0)
+    segrows(seg)
+    g = GpuOracle(tile=tile).vjp_cholesky(l, lbar)
+    assert cm.max_rel_err(g, oracle.vjp_cholesky(l, lbar)) <= 1e-9
+
+
+def test_wide_vjp_cholesky_fp32_and_repair(cuda, oracle, segrows, monkeypatch):
+    from tests.gpu_adapter import GpuOracle
+    rng = np.random.default_rng(77)
+    k, n = 64, 900
+    l = oracle.cholesky(_q(oracle, rng, 2, n, k, "cfg4"))[0]
+    lbar = cm.random_band(rng, 2, n, k, 0)
+    segrows(256)
+    l32, lb32 = (a.astype(np.float32).astype(np.float64) for a in (l, lbar))
+    _fp32_ok(GpuOracle(tile=1, dtype=torch.float32).vjp_cholesky(l32, lb32), oracle.vjp_cholesky(l32, lb32),
+             FP32_FLOOR_VJP)
+    monkeypatch.setenv("BGM_WIDE_BURN", "3")
+    segrows(200)
+    assert cm.max_rel_err(GpuOracle(tile=1).vjp_cholesky(l, lbar), oracle.vjp_cholesky(l, lbar)) <= 1e-9
