@@ -57,9 +57,10 @@ bool vjp_cholesky(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cud
   if (disabled()) return false;
   return narrow::vjp_cholesky(l, lb, qb, s) || wide::vjp_cholesky(l, lb, qb, s);
 }
-bool vjp_subset(const bgm_band&, const bgm_band&, const bgm_band&, const bgm_band&, int32_t*,
-                int64_t*, cudaStream_t) {
-  return false;
+bool vjp_subset(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, const bgm_band& lb, int32_t* st,
+                int64_t* row, cudaStream_t s) {
+  if (disabled()) return false;
+  return wide::vjp_subset(l, sm, sb, lb, st, row, s);
 }
 bool vjp_product(const bgm_band&, const bgm_band&, const bgm_band&, const bgm_band&,
                  const bgm_band&, cudaStream_t) {

@@ -869,6 +869,219 @@ __global__ void k_zero_corners_w(Band<T> o, ix batch) {
   if (j >= 0 && j + r >= o.n) o.cell(b, r, j) = T(0);
 }
 
+// ------------------------------------------------------------------ vjp_subset
+// grad.cpp:84-143 for wide bands, one warp per (matrix, segment), forward
+// over columns j.  State in shared memory:
+//   B   -- the symmetric adjoint's lower cells still to be consumed, rows
+//          [j, c+K] of columns c in [j-K, j], packed (y, x) = (c-(j-K), m-j);
+//   bu  -- U-bar rows i in [j-K, j] (circular by i), K entries each.
+// Per column: r_x = B(j, i_x) (the reference's mirror move), a forward
+// substitution cur_x = r_x - sum L(i_x, i_x') scale_x' (scale = cur / L_ii,
+// shuffle-broadcast), bu(i, i+d) -= S(i+d, j) cur_i, the lower cells of
+// column j -= L(m, i) scale_i, then row i = j-K of bu is complete and its
+// L-bar column is written (grad.cpp:130-141).  The sweep runs K columns past
+// the segment so the last owned rows of bu complete from the exact state.
+template <class T>
+struct VsP {
+  Band<T> l, s, sb, lb;
+  T* side;  // [unit][K][K+2]: cur (K+1) + bvec of the K columns before the segment (burn-in)
+  T* tail;  // [unit][K][K+2]: the same for the segment's last K columns (genuine)
+  int32_t* flag;
+};
+
+template <class T, int K>
+struct VsSmem {
+  static constexpr int NP = (K + 1) * (K + 2) / 2;
+  static constexpr int NU = (K + 1) * K;
+  static constexpr size_t count = NP + NU + (2 * K + 1) + 4 * (K + 1);
+  static constexpr size_t bytes = sizeof(T) * count;
+};
+
+template <class T, int K>
+__device__ void vsub_warp(const VsP<T>& C, ix b, ix n, ix s, ix e, ix start, T* side, T* tail, T* sm) {
+  using Sz = VsSmem<T, K>;
+  constexpr int R = (K + 1 + 31) / 32, NP = Sz::NP, NU = Sz::NU, N1 = NP - (K + 1);
+  T* Bw = sm;
+  T* bu = Bw + NP;
+  T* sS = bu + NU;         // S(j + t, j), t in [-K, K] at index t + K
+  T* sinv = sS + 2 * K + 1;  // 1 / L(i_x, i_x)
+  T* ssc = sinv + (K + 1);   // scale_x
+  T* scur = ssc + (K + 1);   // cur_x
+  T* sbv = scur + (K + 1);   // bvec, circular by column mod (K+1)
+  const int lane = threadIdx.x & 31;
+  const Band<T>& L = C.l;
+  const Band<T>& S = C.s;
+  auto lcell = [&](ix r, ix c) -> T { return (c >= 0 && r < n && r - c <= K) ? L.cell(b, int(r - c), c) : T(0); };
+  auto scell = [&](ix r, ix c) -> T {  // symmetric S(r, c), |r - c| <= K
+    if (r < 0 || c < 0 || r >= n || c >= n) return T(0);
+    return r >= c ? S.cell(b, int(r - c), c) : S.cell(b, int(c - r), r);
+  };
+  // B for column `start`: (y, x) -> c = start-K+y, m = start+x, cell m - c = K + x - y
+  for (int idx = lane; idx < NP; idx += 32) {
+    int y, x;
+    untri(idx, y, x);
+    const ix c = start - K + y, m = start + x;
+    Bw[idx] = (c >= 0 && m < n) ? C.sb.cell(b, K + x - y, c) : T(0);
+  }
+  for (int q = lane; q < NU; q += 32) bu[q] = T(0);
+  __syncwarp();
+  const ix jend = e + K < n ? e + K : n;  // K columns past the segment complete its bu rows
+  auto emit = [&](ix c) {  // bu row c complete -> L-bar column c
+    const int slot = int(c % (K + 1));
+    const T lcc = lcell(c, c);
+    const T iv = T(1) / lcc;
+    T dsum = T(0);
+    for (int d = lane + 1; d <= K; d += 32) {
+      const T v = bu[slot * K + d - 1];
+      if (c + d < n) {
+        C.lb.cell(b, d, c) = v * iv;
+        dsum = fma(v, lcell(c + d, c), dsum);
+      } else {
+        C.lb.cell(b, d, c) = T(0);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+    if (lane == 0) C.lb.cell(b, 0, c) = (T(-2) * sbv[slot] * iv - dsum) * (iv * iv);
+  };
+#pragma unroll 1
+  for (ix j = start; j < jend; ++j) {
+    T rr[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      const int x = lane + 32 * t;
+      if (x <= K) {
+        const ix i = j - K + x;
+        rr[t] = Bw[tri_w(x, 0)];
+        sinv[x] = i >= 0 ? T(1) / lcell(i, i) : T(0);
+      } else {
+        rr[t] = T(0);
+      }
+    }
+    for (int t = lane; t <= 2 * K; t += 32) sS[t] = scell(j + t - K, j);
+    __syncwarp();
+    // forward substitution over i_x = j-K+x
+#pragma unroll 1
+    for (int x = 0; x <= K; ++x) {
+      const int slot = x >> 5, owner = x & 31;
+      T v = rr[0];
+#pragma unroll
+      for (int t = 1; t < R; ++t)
+        if (slot == t) v = rr[t];
+      const T cur = __shfl_sync(0xffffffffu, v, owner);
+      const T sc = cur * sinv[x];
+      if (lane == owner) {
+        scur[x] = cur;
+        ssc[x] = sc;
+      }
+      const ix ix_ = j - K + x;
+#pragma unroll
+      for (int t = 0; t < R; ++t) {
+        const int x2 = lane + 32 * t;
+        if (x2 > x && x2 <= K) rr[t] = fma(-lcell(j - K + x2, ix_), sc, rr[t]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) sbv[j % (K + 1)] = scur[K];  // bvec(j): bs(j, j) when i reaches j (grad.cpp:114)
+    __syncwarp();
+    // burn-in / tail copies for the boundary check
+    if (side && j >= s - K && j < s) {
+      T* sd = side + (j - (s - K)) * (K + 2);
+      for (int x = lane; x <= K; x += 32) sd[x] = scur[x];
+      if (lane == 0) sd[K + 1] = sbv[j % (K + 1)];
+    }
+    if (tail && j >= e - K && j < e) {
+      T* td = tail + (j - (e - K)) * (K + 2);
+      for (int x = lane; x <= K; x += 32) td[x] = scur[x];
+      if (lane == 0) td[K + 1] = sbv[j % (K + 1)];
+    }
+    // bu(i_x, i_x + d) -= S(i_x + d, j) cur_x, d = 1..K
+    for (int q = lane; q < NU; q += 32) {
+      const int x = q / K, d = q % K + 1;
+      const ix i = j - K + x;
+      if (i >= 0) bu[int(i % (K + 1)) * K + d - 1] = fma(-sS[x + d], scur[x], bu[int(i % (K + 1)) * K + d - 1]);
+    }
+    // lower cells of column j: B(j+d, j) -= sum_{x >= d} L(j+d, i_x) scale_x
+    for (int d = lane + 1; d <= K; d += 32) {
+      T acc = T(0);
+      for (int x = d; x <= K; ++x) acc = fma(lcell(j + d, j - K + x), ssc[x], acc);
+      Bw[tri_w(K, d)] -= acc;
+    }
+    __syncwarp();
+    // row j - K of bu is complete
+    if (j - K >= s && j - K < e) emit(j - K);
+    __syncwarp();
+    if (j - K >= 0) {
+      const int slot = int((j - K) % (K + 1));
+      for (int d = lane; d < K; d += 32) bu[slot * K + d] = T(0);
+    }
+    // shift B: (y, x) -> (y-1, x-1) for x >= 1, ascending chunks
+#pragma unroll 1
+    for (int base = 0; base < N1 + (K + 1); base += 32) {
+      const int idx = base + lane;
+      int y = 0, x = 0;
+      T v = T(0);
+      const bool ok = idx < NP;
+      if (ok) {
+        untri(idx, y, x);
+        v = Bw[idx];
+      }
+      __syncwarp();
+      if (ok && x >= 1) Bw[tri_w(y - 1, x - 1)] = v;
+      __syncwarp();
+    }
+    // new column j+1 at y = K: S-bar cells (j+1+x, j+1)
+    for (int x = lane; x <= K; x += 32) {
+      const ix c = j + 1, m = c + x;
+      Bw[tri_w(K, x)] = (m < n) ? C.sb.cell(b, x, c) : T(0);
+    }
+    __syncwarp();
+  }
+  // rows completed only by the matrix end
+  for (ix c = (n - K > s ? n - K : s); c < e; ++c)
+    if (c + K >= jend && c + K >= n) emit(c);
+}
+
+template <class T, int K>
+__global__ void __launch_bounds__(32) k_vsub(VsP<T> C, Geo G) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const ix unit = blockIdx.x;
+  const ix b = unit / G.nseg;
+  const int p = int(unit % G.nseg);
+  if (b >= G.batch) return;
+  const ix s = ix(p) * G.seg, e = s + G.seg < G.n ? s + G.seg : G.n;
+  const ix start = s - G.burn > 0 ? s - G.burn : 0;
+  vsub_warp<T, K>(C, b, G.n, s, e, start, p > 0 ? C.side + unit * ix(K) * (K + 2) : nullptr,
+                  p + 1 < G.nseg ? C.tail + unit * ix(K) * (K + 2) : nullptr, reinterpret_cast<T*>(smraw));
+}
+
+template <class T, int K>
+__global__ void k_vsub_check(VsP<T> C, Geo G) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  const ix id = t / K;
+  const int c = int(t % K);
+  if (id >= G.batch * G.nseg) return;
+  const int p = int(id % G.nseg);
+  if (p == 0) return;
+  const ix b = id / G.nseg;
+  const T* a = C.side + (id * K + c) * (K + 2);
+  const T* r = C.tail + ((id - 1) * K + c) * (K + 2);
+  double sc = 0.0;
+  for (int x = 0; x < K + 2; ++x) sc = fmax(sc, fabs(double(r[x])));
+  const double tol = sizeof(T) == 8 ? kCheckTol : 1e-5;
+  bool bad = false;
+  for (int x = 0; x < K + 2; ++x) bad |= !(fabs(double(a[x]) - double(r[x])) <= tol * (sc + 1e-300));
+  if (bad) C.flag[b] = 1;
+}
+
+template <class T, int K>
+__global__ void __launch_bounds__(32) k_vsub_repair(VsP<T> C, Geo G) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const ix b = blockIdx.x;
+  if (b >= G.batch || !C.flag[b]) return;
+  vsub_warp<T, K>(C, b, G.n, 0, G.n, 0, nullptr, nullptr, reinterpret_cast<T*>(smraw));
+}
+
 int g_segment_rows = 0;
 
 template <class T, int K, int P, int TS>
@@ -1097,6 +1310,67 @@ bool run_vchol(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cudaSt
   scratch_free(ws, s);
   return true;
 }
+
+template <class T, int K>
+bool run_vsub(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, const bgm_band& lb, int32_t* st,
+              int64_t* row, cudaStream_t s) {
+  const size_t smem = VsSmem<T, K>::bytes;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_vsub<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_vsub_repair<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = true;
+  }
+  Geo G;
+  G.batch = l.batch;
+  G.n = l.n;
+  G.burn = kBurnGen * K;
+  if (const char* bv = std::getenv("BGM_WIDE_BURN"))
+    if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
+  ix seg = g_segment_rows;
+  if (seg <= 0) {
+    int sms = 148, dev = 0, per = 1;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_vsub<T, K>, 32, smem);
+    ix nseg = ix(sms) * (per > 0 ? per : 1) / (G.batch > 0 ? G.batch : 1);
+    if (nseg < 1) nseg = 1;
+    seg = (G.n + nseg - 1) / nseg;
+    if (seg < 2 * ix(G.burn)) seg = 2 * ix(G.burn);
+  }
+  if (seg < K) seg = K;
+  G.seg = seg;
+  G.nseg = int((G.n + seg - 1) / seg);
+  const ix units = G.batch * G.nseg;
+  const size_t sd = sizeof(T) * size_t(units) * K * (K + 2);
+  char* ws = nullptr;
+  if (scratch_alloc(reinterpret_cast<void**>(&ws), 2 * sd + 12 * size_t(G.batch) + 64, s) != cudaSuccess) return false;
+  VsP<T> C;
+  C.l = view<T>(l);
+  C.s = view<T>(sm);
+  C.sb = view<T>(sb);
+  C.lb = view<T>(lb);
+  C.side = reinterpret_cast<T*>(ws);
+  C.tail = reinterpret_cast<T*>(ws + sd);
+  int64_t* fail = reinterpret_cast<int64_t*>(ws + (2 * sd + 7) / 8 * 8);
+  C.flag = reinterpret_cast<int32_t*>(fail + G.batch);
+  k_init<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, C.flag, G.batch, G.n);
+  k_diag_check<T><<<blocks_for(G.batch * G.n, 256), 256, 0, s>>>(C.l, G.batch, fail);
+  {
+    timing::Scope ts("wide_vjp_subset", s);
+    k_vsub<T, K><<<unsigned(units), 32, smem, s>>>(C, G);
+  }
+  {
+    timing::Scope ts("wide_vjp_subset_check", s);
+    k_vsub_check<T, K><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
+  }
+  {
+    timing::Scope ts("wide_vjp_subset_repair", s);
+    k_vsub_repair<T, K><<<unsigned(G.batch), 32, smem, s>>>(C, G);
+  }
+  k_status_code<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, G.batch, G.n, BGM_ERR_SINGULAR, st, row);
+  scratch_free(ws, s);
+  return true;
+}
 }  // namespace
 
 bool cholesky(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, cudaStream_t s) {
@@ -1153,6 +1427,21 @@ bool vjp_cholesky(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cud
   switch (l.lower) {
     case 64: return f64 ? run_vchol<double, 64>(l, lb, qb, s) : run_vchol<float, 64>(l, lb, qb, s);
     case 128: return f64 ? run_vchol<double, 128>(l, lb, qb, s) : run_vchol<float, 128>(l, lb, qb, s);
+    default: return false;
+  }
+}
+
+bool vjp_subset(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, const bgm_band& lb, int32_t* st,
+                int64_t* row, cudaStream_t s) {
+  if (l.upper != 0 || l.batch == 0 || l.n < 4 * l.lower) return false;
+  const bool f64 = l.dtype == BGM_F64;
+  switch (l.lower) {
+    case 16:
+      return f64 ? run_vsub<double, 16>(l, sm, sb, lb, st, row, s) : run_vsub<float, 16>(l, sm, sb, lb, st, row, s);
+    case 64:
+      return f64 ? run_vsub<double, 64>(l, sm, sb, lb, st, row, s) : run_vsub<float, 64>(l, sm, sb, lb, st, row, s);
+    case 128:
+      return f64 ? run_vsub<double, 128>(l, sm, sb, lb, st, row, s) : run_vsub<float, 128>(l, sm, sb, lb, st, row, s);
     default: return false;
   }
 }

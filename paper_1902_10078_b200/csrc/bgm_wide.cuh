@@ -16,6 +16,8 @@ bool solve_vec(const bgm_band& l, const bgm_vec& v, int tr, const bgm_vec& x, in
                cudaStream_t s);
 bool log_det(const bgm_band& l, void* out, int32_t* st, int64_t* row, cudaStream_t s);
 bool vjp_cholesky(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cudaStream_t s);
+bool vjp_subset(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, const bgm_band& lb, int32_t* st,
+                int64_t* row, cudaStream_t s);
 void set_segment_rows(int rows);
 
 }  // namespace wide

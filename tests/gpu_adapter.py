@@ -106,8 +106,12 @@ class GpuOracle:
     def vjp_sparse_inverse_subset(self, l, s, sbar):
         l = np.asarray(l)
         k = l.shape[2] - 1
-        lb = bgm.vjp_sparse_inverse_subset(self._b(l, k, 0), self._b(s, k, 0), self._b(sbar, k, 0), check=False)
-        return self._np(lb), None, None
+        L, Sd, Sb = self._b(l, k, 0), self._b(s, k, 0), self._b(sbar, k, 0)  # kept alive across the call
+        lb = L.like()
+        st = api.new_status(L.batch)
+        api._call("bgm_vjp_sparse_inverse_subset", L.desc(), Sd.desc(), Sb.desc(), lb.desc(), *st.ptrs(),
+                  api._stream())
+        return (self._np(lb), *self._st(st))
 
     def vjp_product_band_band(self, a, al, au, b, bl, bu, pbar, pl, pu):
         ab, bb = bgm.vjp_product_band_band(self._b(a, al, au), self._b(b, bl, bu), self._b(pbar, pl, pu))

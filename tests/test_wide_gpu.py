@@ -197,3 +197,40 @@ def test_wide_vjp_cholesky_fp32_and_repair(cuda, oracle, segrows, monkeypatch):
     monkeypatch.setenv("BGM_WIDE_BURN", "3")
     segrows(200)
     assert cm.max_rel_err(GpuOracle(tile=1).vjp_cholesky(l, lbar), oracle.vjp_cholesky(l, lbar)) <= 1e-9
+
+
+@pytest.mark.parametrize("k,n", [(64, 700), (128, 1100)])
+@pytest.mark.parametrize("tile", [1, 32])
+@pytest.mark.parametrize("seg", [0, 270])
+@pytest.mark.parametrize("kind", ["cfg4", "dominant"])
+def test_wide_vjp_subset(cuda, oracle, segrows, k, n, tile, seg, kind):
+    from tests.gpu_adapter import GpuOracle
+    rng = np.random.default_rng(13 * k + n + seg)
+    l = oracle.cholesky(_q(oracle, rng, 3, n, k, kind))[0]
+    s = oracle.sparse_inverse_subset(l)[0]
+    sbar = cm.random_band(rng, 3, n, k, 0)
+    segrows(seg)
+    g, st, _ = GpuOracle(tile=tile).vjp_sparse_inverse_subset(l, s, sbar)
+    o, st_o, _ = oracle.vjp_sparse_inverse_subset(l, s, sbar)
+    assert np.array_equal(st, st_o)
+    assert cm.max_rel_err(g, o) <= 1e-9
+
+
+def test_wide_vjp_subset_fp32_repair_singular(cuda, oracle, segrows, monkeypatch):
+    from tests.gpu_adapter import GpuOracle
+    rng = np.random.default_rng(78)
+    k, n = 64, 900
+    l = oracle.cholesky(_q(oracle, rng, 3, n, k, "cfg4"))[0]
+    s = oracle.sparse_inverse_subset(l)[0]
+    sbar = cm.random_band(rng, 3, n, k, 0)
+    segrows(256)
+    a32 = [a[:2].astype(np.float32).astype(np.float64) for a in (l, s, sbar)]
+    _fp32_ok(GpuOracle(tile=1, dtype=torch.float32).vjp_sparse_inverse_subset(*a32)[0],
+             oracle.vjp_sparse_inverse_subset(*a32)[0], FP32_FLOOR_VJP)
+    monkeypatch.setenv("BGM_WIDE_BURN", "3")
+    segrows(200)
+    l[2, 500, 0] = 0.0
+    g, st, row = GpuOracle(tile=1).vjp_sparse_inverse_subset(l, s, sbar)
+    o, st_o, row_o = oracle.vjp_sparse_inverse_subset(l, s, sbar)
+    assert list(st) == list(st_o) and row[2] == row_o[2] == 500
+    assert cm.max_rel_err(g[:2], o[:2]) <= 1e-9
