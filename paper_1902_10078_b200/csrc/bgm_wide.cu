@@ -713,6 +713,22 @@ __device__ __forceinline__ void untri(int idx, int& x, int& y) {
   y = idx - tri_w(a, 0);
 }
 
+// Incremental (row, col) of a packed-triangle index stepping by +-32.
+__device__ __forceinline__ void tri_next32(int& a, int& b) {
+  b += 32;
+  while (b > a) {
+    b -= a + 1;
+    ++a;
+  }
+}
+__device__ __forceinline__ void tri_prev32(int& a, int& b) {
+  b -= 32;
+  while (b < 0) {
+    --a;
+    b += a + 1;
+  }
+}
+
 template <class T, int K>
 __device__ void vchol_warp(const VcP<T>& C, ix b, ix n, ix s, ix e, ix start, T* side, T* Wb, T* Lw,
                            T* sq, T* slr, T* sinv) {
@@ -776,24 +792,27 @@ __device__ void vchol_warp(const VcP<T>& C, ix b, ix n, ix s, ix e, ix start, T*
       }
     }
     // update + shift, descending chunks
+    {
+      int cx, cy;
+      untri(((N1 - 1) & ~31) + lane, cx, cy);
 #pragma unroll 1
-    for (int base = (N1 - 1) & ~31; base >= 0; base -= 32) {
-      const int idx = base + lane;
-      T wv = T(0), lv = T(0);
-      int x = 0, y = 0;
-      const bool ok = idx < N1;
-      if (ok) {
-        untri(idx, x, y);
-        wv = fma(-sq[x], slr[y], Wb[idx]);
-        lv = Lw[idx];
+      for (int base = (N1 - 1) & ~31; base >= 0; base -= 32) {
+        const int idx = base + lane;
+        T wv = T(0), lv = T(0);
+        const bool ok = idx < N1;
+        if (ok) {
+          wv = fma(-sq[cx], slr[cy], Wb[idx]);
+          lv = Lw[idx];
+        }
+        __syncwarp();
+        if (ok) {
+          const int d = idx + cx + 2;  // tri(x+1, y+1)
+          Wb[d] = wv;
+          Lw[d] = lv;
+        }
+        __syncwarp();
+        if (base >= 32) tri_prev32(cx, cy);
       }
-      __syncwarp();
-      if (ok) {
-        const int d = tri_w(x + 1, y + 1);
-        Wb[d] = wv;
-        Lw[d] = lv;
-      }
-      __syncwarp();
     }
     const ix c = i - 1 - K;  // entering column
     for (int x = lane; x <= K; x += 32) {
@@ -911,7 +930,12 @@ __device__ void vsub_warp(const VsP<T>& C, ix b, ix n, ix s, ix e, ix start, T* 
   const int lane = threadIdx.x & 31;
   const Band<T>& L = C.l;
   const Band<T>& S = C.s;
-  auto lcell = [&](ix r, ix c) -> T { return (c >= 0 && r < n && r - c <= K) ? L.cell(b, int(r - c), c) : T(0); };
+  // per-matrix base pointers: cell (r, c) at base[(c * w + r) << s]
+  const int sh = L.s;
+  const T* lbase = L.p + (((b >> sh) * n * L.w) << sh) + (b & ((ix(1) << sh) - 1));
+  auto lcell = [&](ix r, ix c) -> T {
+    return (c >= 0 && r < n && r - c <= K) ? lbase[(c * (K + 1) + (r - c)) << sh] : T(0);
+  };
   auto scell = [&](ix r, ix c) -> T {  // symmetric S(r, c), |r - c| <= K
     if (r < 0 || c < 0 || r >= n || c >= n) return T(0);
     return r >= c ? S.cell(b, int(r - c), c) : S.cell(b, int(c - r), r);
@@ -978,7 +1002,9 @@ __device__ void vsub_warp(const VsP<T>& C, ix b, ix n, ix s, ix e, ix start, T* 
 #pragma unroll
       for (int t = 0; t < R; ++t) {
         const int x2 = lane + 32 * t;
-        if (x2 > x && x2 <= K) rr[t] = fma(-lcell(j - K + x2, ix_), sc, rr[t]);
+        // L(i_x2, i_x) = cell x2 - x of column i_x
+        if (x2 > x && x2 <= K && ix_ >= 0 && j - K + x2 < n)
+          rr[t] = fma(-lbase[(ix_ * (K + 1) + (x2 - x)) << sh], sc, rr[t]);
       }
     }
     __syncwarp();
@@ -995,16 +1021,27 @@ __device__ void vsub_warp(const VsP<T>& C, ix b, ix n, ix s, ix e, ix start, T* 
       for (int x = lane; x <= K; x += 32) td[x] = scur[x];
       if (lane == 0) td[K + 1] = sbv[j % (K + 1)];
     }
-    // bu(i_x, i_x + d) -= S(i_x + d, j) cur_x, d = 1..K
+    // bu(i_x, i_x + d) -= S(i_x + d, j) cur_x, d = 1..K; row slot = i mod (K+1)
+    const int jm = int(((j - K) % (K + 1) + (K + 1)) % (K + 1));
     for (int q = lane; q < NU; q += 32) {
       const int x = q / K, d = q % K + 1;
-      const ix i = j - K + x;
-      if (i >= 0) bu[int(i % (K + 1)) * K + d - 1] = fma(-sS[x + d], scur[x], bu[int(i % (K + 1)) * K + d - 1]);
+      if (j - K + x >= 0) {
+        const int slot = jm + x < K + 1 ? jm + x : jm + x - (K + 1);
+        T* u = bu + slot * K + d - 1;
+        *u = fma(-sS[x + d], scur[x], *u);
+      }
     }
     // lower cells of column j: B(j+d, j) -= sum_{x >= d} L(j+d, i_x) scale_x
     for (int d = lane + 1; d <= K; d += 32) {
       T acc = T(0);
-      for (int x = d; x <= K; ++x) acc = fma(lcell(j + d, j - K + x), ssc[x], acc);
+      if (j + d < n) {
+        // L(j+d, i_x) = cell K + d - x of column i_x = j - K + x
+#pragma unroll 4
+        for (int x = d; x <= K; ++x) {
+          const ix c = j - K + x;
+          if (c >= 0) acc = fma(lbase[(c * (K + 1) + (K + d - x)) << sh], ssc[x], acc);
+        }
+      }
       Bw[tri_w(K, d)] -= acc;
     }
     __syncwarp();
@@ -1016,19 +1053,20 @@ __device__ void vsub_warp(const VsP<T>& C, ix b, ix n, ix s, ix e, ix start, T* 
       for (int d = lane; d < K; d += 32) bu[slot * K + d] = T(0);
     }
     // shift B: (y, x) -> (y-1, x-1) for x >= 1, ascending chunks
+    {
+      int cy, cx;
+      untri(lane, cy, cx);
 #pragma unroll 1
-    for (int base = 0; base < N1 + (K + 1); base += 32) {
-      const int idx = base + lane;
-      int y = 0, x = 0;
-      T v = T(0);
-      const bool ok = idx < NP;
-      if (ok) {
-        untri(idx, y, x);
-        v = Bw[idx];
+      for (int base = 0; base < NP; base += 32) {
+        const int idx = base + lane;
+        const bool ok = idx < NP && cx >= 1;
+        T v = T(0);
+        if (ok) v = Bw[idx];
+        __syncwarp();
+        if (ok) Bw[idx - cy - 1] = v;  // tri(y-1, x-1)
+        __syncwarp();
+        tri_next32(cy, cx);
       }
-      __syncwarp();
-      if (ok && x >= 1) Bw[tri_w(y - 1, x - 1)] = v;
-      __syncwarp();
     }
     // new column j+1 at y = K: S-bar cells (j+1+x, j+1)
     for (int x = lane; x <= K; x += 32) {
