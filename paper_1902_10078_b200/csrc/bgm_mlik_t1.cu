@@ -32,7 +32,7 @@ namespace {
 
 constexpr double kLn2 = 0.69314718055994530942;
 constexpr double kLog2Pi = 1.8378770664093454836;  // inference.cpp:15
-constexpr double kCheckTol = 1e-12;
+constexpr double kCheckTol = 1e-13;  // boundary-state agreement (relative to its scale)
 // One warp per block: shared memory, not threads, bounds residency.  Window
 // entries of one thread are kThreads doubles apart ([entry][thread]).
 constexpr int kThreads = 32;
