@@ -204,6 +204,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--segment-rows", type=int, default=0)
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="time eager launches instead of the captured CUDA graph")
     ap.add_argument("--tile", type=int, choices=[1, 32], default=32,
                     help="device layout: 32 = interleaved (one-thread-per-unit sweeps), 1 = reference layout (team sweeps)")
     args = ap.parse_args()
@@ -248,6 +250,31 @@ def main():
     torch.cuda.synchronize()
     st.raise_first()
 
+    # The step's ~10 launches are captured once into a CUDA graph and
+    # replayed (same kernels, same work; no per-launch host overhead).  The
+    # NCCL all-reduce of the multi-GPU case stays outside the graph.
+    graph = None
+    if args.graph and world == 1:
+        try:
+            g = torch.cuda.CUDAGraph()
+            s0 = torch.cuda.Stream()
+            s0.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s0):
+                step()
+            torch.cuda.current_stream().wait_stream(s0)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g):
+                step()
+            torch.cuda.synchronize()
+            graph = g
+        except Exception as exc:  # capture unsupported: time the eager launches
+            print(f"# graph capture failed ({exc}); timing eager launches", file=sys.stderr)
+            graph = None
+    eager_step = step
+    if graph is not None:
+        def step():
+            graph.replay()
+
     def barrier():
         if world > 1:
             dist.barrier()
@@ -285,7 +312,7 @@ def main():
     # ---------------- per-kernel attribution (CUDA events on the launch stream)
     lib.bgm_timing_enable(1)
     for _ in range(args.steps):
-        step()
+        eager_step()
     torch.cuda.synchronize()
     clk.__exit__(None, None, None)
     kernels = []
@@ -342,6 +369,7 @@ def main():
             "data": "synthetic (seeded on device; BASELINE.md §4 construction)",
             "config": {"workload": args.workload, "desc": wl["desc"], "batch_per_gpu": B, "n": n, "k": k,
                        "tau2": tau2, "parallelism": f"batch-sharded x{world}", "layout_tile": L.tile,
+                       "cuda_graph": graph is not None,
                        "l2": "inputs (%.2f GB/GPU) exceed the 126 MB L2; no flush needed" % (B * n * (k + 1) * 8 / 1e9)},
             "roofline": roofline, "suite_roofline": suite, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(round(launches_per_step * args.steps)),

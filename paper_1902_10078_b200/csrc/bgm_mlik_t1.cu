@@ -840,10 +840,10 @@ int run(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, const bg
 
   const unsigned gf = unsigned(G.tiles * Gf.nseg), gb = unsigned(G.tiles * Gb.nseg);
   const unsigned mb = unsigned((G.batch + kThreads - 1) / kThreads);
+  cudaMemsetAsync(F.uflag, 0, sizeof(int32_t) * size_t(uf + ub), s);
   {
     timing::Scope ts("mlik_init", s);
     k_init<<<blocks_for(G.batch, 128), 128, 0, s>>>(F.fail, flags, G.batch, G.n);
-    cudaMemsetAsync(F.uflag, 0, sizeof(int32_t) * size_t(uf + ub), s);
   }
   {
     timing::Scope ts("mlik_t1_fwd", s);
@@ -856,6 +856,9 @@ int run(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, const bg
   {
     timing::Scope ts("mlik_fix_fwd", s);
     k_fwd_fix<K><<<gf, kThreads, smf, s>>>(F, Gf);
+  }
+  {
+    timing::Scope ts("mlik_recheck_fwd", s);
     k_recheck<Sh::STATEF><<<blocks_for(uf, 128), 128, 0, s>>>(F.uflag, F.exitf, F.exitf2, Gf, 1, flags);
   }
   {
@@ -873,6 +876,9 @@ int run(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, const bg
   {
     timing::Scope ts("mlik_fix_bwd", s);
     k_bwd_fix<K><<<gb, kThreads, smb, s>>>(Bp, Gb);
+  }
+  {
+    timing::Scope ts("mlik_recheck_bwd", s);
     k_recheck<Sh::STATE><<<blocks_for(ub, 128), 128, 0, s>>>(Bp.uflag, Bp.exitb, Bp.exitb2, Gb, 0,
                                                            flags + G.batch);
   }
