@@ -15,7 +15,7 @@ from .api import Bands, Vecs, marginal_likelihood_grad, new_status
 
 
 def marginal_likelihood_grad_host(L_host: torch.Tensor, y_host: torch.Tensor, tau2: float,
-                                  out_host=None, chunk: int = 32, streams: int = 3, device=None,
+                                  out_host=None, chunk: int = 16, streams: int = 4, device=None,
                                   tile: int = 32):
     """Config-3 learning step on host buffers.
 
