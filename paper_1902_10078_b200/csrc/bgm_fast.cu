@@ -49,8 +49,9 @@ bool subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cu
   if (disabled()) return false;
   return narrow::subset(l, sb, st, row, s) || wide::subset(l, sb, st, row, s);
 }
-bool product(const bgm_band&, int, const bgm_band&, int, const bgm_band&, cudaStream_t) {
-  return false;
+bool product(const bgm_band& a, int ta, const bgm_band& b, int tb, const bgm_band& c, cudaStream_t s) {
+  if (disabled()) return false;
+  return prod::product(a, ta, b, tb, c, s);
 }
 bool band_vec(const bgm_band&, const bgm_vec&, int, const bgm_vec&, cudaStream_t) { return false; }
 bool vjp_cholesky(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cudaStream_t s) {

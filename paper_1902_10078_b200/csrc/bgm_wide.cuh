@@ -31,4 +31,9 @@ bool subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cu
 bool vjp_cholesky(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cudaStream_t s);
 void set_segment_rows(int rows);
 }  // namespace narrow
+
+// Band x band products with strided operand walks (bgm_product.cu).
+namespace prod {
+bool product(const bgm_band& a, int ta, const bgm_band& b, int tb, const bgm_band& c, cudaStream_t s);
+}
 }  // namespace bgm
