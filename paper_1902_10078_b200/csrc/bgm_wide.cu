@@ -1120,6 +1120,164 @@ __global__ void __launch_bounds__(32) k_vsub_repair(VsP<T> C, Geo G) {
   vsub_warp<T, K>(C, b, G.n, 0, G.n, 0, nullptr, nullptr, reinterpret_cast<T*>(smraw));
 }
 
+// ------------------------------------------------------------------ cholesky, FP64 DMMA
+// Blocked right-looking banded Cholesky on the FP64 tensor cores
+// (mma.sync m8n8k4 f64, SASS DMMA), k = 64, one warp per (matrix, segment).
+// The band's trailing Schur complement over rows [g, g+K+8) is held as
+// 8x8 tiles (I, J), 0 <= J <= I <= K/8, in the MMA accumulator layout
+// (lane: row lane/4, columns 2(lane%4) + {0,1}) -- 45 tiles, 90 doubles per
+// lane, all in registers.  Per panel of 8 rows:
+//   * panel column tiles (I, 0) go to shared memory, where the warp factors
+//     the diagonal tile and scales the column below it (the unblocked
+//     panel: 8 pivots, lane-parallel updates);
+//   * L columns g..g+7 are written out from there;
+//   * trailing update W_IJ -= L_I0 L_J0^T for 1 <= J <= I: 2 DMMA per tile
+//     (k = 8 = 2 x 4); the A and B fragments of L_I0 / L_J0 are the same
+//     (row lane/4, column 4kc + lane%4) reads of the shared panel;
+//   * the tiles shift by one tile (register moves) and a fresh tile row of
+//     Q enters.  Rows past n are padded with the identity.
+constexpr int kDK = 64, kDT = kDK / 8 + 1, kDTiles = kDT * (kDT + 1) / 2, kDRows = kDK + 8;
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+__host__ __device__ constexpr int dti(int I, int J) { return I * (I + 1) / 2 + J; }
+
+__device__ void chol_dmma_unit(const CholP<double>& C, ix b, ix n, ix s, ix e, ix i0, double* side) {
+  constexpr int K = kDK;
+  const int lane = threadIdx.x & 31, rr = lane >> 2, q = lane & 3, c2 = 2 * q;
+  const Band<double>& Q = C.q;
+  const Band<double>& L = C.l;
+  auto qval = [&](ix r, ix c) -> double {  // symmetric Q(r, c), identity past n
+    if (r < c) {
+      const ix t = r;
+      r = c;
+      c = t;
+    }
+    if (r - c > K || c < 0) return 0.0;
+    if (r >= n) return r == c ? 1.0 : 0.0;
+    return Q.cell(b, int(r - c), c);
+  };
+  auto pick = [](const double* v, int e) -> double { return e ? v[1] : v[0]; };
+  double wt[kDTiles][2];
+#pragma unroll
+  for (int I = 0; I < kDT; ++I)
+#pragma unroll
+    for (int J = 0; J <= I; ++J)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) wt[dti(I, J)][v] = qval(i0 + 8 * I + rr, i0 + 8 * J + c2 + v);
+  ix fail = n;
+#pragma unroll 1
+  for (ix g = i0; g < e; g += 8) {
+    double* D = wt[dti(0, 0)];
+    // (1) Cholesky of the diagonal tile in the fragment layout (shuffles)
+    double rinv[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      const double dpp = __shfl_sync(0xffffffffu, pick(D, p & 1), 4 * p + (p >> 1));
+      if (lane == 0 && g + p >= s && g + p < n && !(dpp > kPivotFloor)) fail = fail < g + p ? fail : g + p;
+      const double piv = sqrt(dpp);
+      rinv[p] = 1.0 / piv;
+      if (q == (p >> 1)) {
+        if (rr > p) D[p & 1] *= rinv[p];
+        else if (rr == p) D[p & 1] = piv;
+      }
+      const double lr = __shfl_sync(0xffffffffu, pick(D, p & 1), 4 * rr + (p >> 1));
+      const double lc0 = __shfl_sync(0xffffffffu, pick(D, p & 1), 4 * c2 + (p >> 1));
+      const double lc1 = __shfl_sync(0xffffffffu, pick(D, p & 1), 4 * (c2 + 1) + (p >> 1));
+      if (c2 > p && rr >= c2) D[0] = fma(-lr, lc0, D[0]);
+      if (c2 + 1 > p && rr >= c2 + 1) D[1] = fma(-lr, lc1, D[1]);
+    }
+    if (c2 > rr) D[0] = 0.0;
+    if (c2 + 1 > rr) D[1] = 0.0;
+    // (2) tiles below: X_I = W_I0 L00^-T, row by row inside each lane quad
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const double l0 = __shfl_sync(0xffffffffu, pick(D, c & 1), 4 * c2 + (c >> 1));        // L00[c2][c]
+      const double l1 = __shfl_sync(0xffffffffu, pick(D, c & 1), 4 * (c2 + 1) + (c >> 1));  // L00[c2+1][c]
+#pragma unroll
+      for (int I = 1; I < kDT; ++I) {
+        double* X = wt[dti(I, 0)];
+        if (q == (c >> 1)) X[c & 1] *= rinv[c];
+        const double x = __shfl_sync(0xffffffffu, pick(X, c & 1), 4 * rr + (c >> 1));
+        if (c2 > c) X[0] = fma(-x, l0, X[0]);
+        if (c2 + 1 > c) X[1] = fma(-x, l1, X[1]);
+      }
+    }
+    // (3) A / B fragments of the panel tiles: column 4kc + q of row rr
+    double pf[kDT][2];
+#pragma unroll
+    for (int I = 1; I < kDT; ++I)
+#pragma unroll
+      for (int kc = 0; kc < 2; ++kc) {
+        const int srcl = 4 * rr + 2 * kc + (q >> 1);
+        const double e0 = __shfl_sync(0xffffffffu, wt[dti(I, 0)][0], srcl);
+        const double e1 = __shfl_sync(0xffffffffu, wt[dti(I, 0)][1], srcl);
+        pf[I][kc] = (q & 1) ? e1 : e0;
+      }
+    // (4) L columns g .. g+7: lane (rr, q) holds rows 8I + rr, columns c2, c2+1
+#pragma unroll
+    for (int I = 0; I < kDT; ++I)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int c = c2 + v;
+        const int cell = 8 * I + rr - c;
+        const ix col = g + c;
+        if (cell >= 0 && cell <= K && col < n) {
+          const double val = (col + cell < n) ? wt[dti(I, 0)][v] : 0.0;
+          if (col >= s) L.cell(b, cell, col) = val;
+          else if (side && col >= s - K) side[(col - (s - K)) * (K + 1) + cell] = val;
+        }
+      }
+    // (5) trailing update W_IJ -= X_I X_J^T on the FP64 tensor cores
+#pragma unroll
+    for (int I = 1; I < kDT; ++I)
+#pragma unroll
+      for (int J = 1; J <= I; ++J) {
+        dmma(wt[dti(I, J)][0], wt[dti(I, J)][1], -pf[I][0], pf[J][0]);
+        dmma(wt[dti(I, J)][0], wt[dti(I, J)][1], -pf[I][1], pf[J][1]);
+      }
+    // (6) shift by one tile; a fresh tile row enters: rows g2+K+rr, cols g2+8J+c2+v
+#pragma unroll
+    for (int I = 1; I < kDT; ++I)
+#pragma unroll
+      for (int J = 1; J <= I; ++J) {
+        wt[dti(I - 1, J - 1)][0] = wt[dti(I, J)][0];
+        wt[dti(I - 1, J - 1)][1] = wt[dti(I, J)][1];
+      }
+    const ix g2 = g + 8;
+#pragma unroll
+    for (int J = 0; J < kDT; ++J)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) wt[dti(kDT - 1, J)][v] = qval(g2 + 8 * (kDT - 1) + rr, g2 + 8 * J + c2 + v);
+  }
+  if (lane == 0 && fail < n)
+    atomicMin(reinterpret_cast<unsigned long long*>(C.fail + b), static_cast<unsigned long long>(fail));
+}
+
+__global__ void __launch_bounds__(32) k_chol_dmma(CholP<double> C, Geo G) {
+  const ix unit = blockIdx.x;
+  const ix b = unit / G.nseg;
+  const int p = int(unit % G.nseg);
+  if (b >= G.batch) return;
+  const ix s = ix(p) * G.seg;
+  const ix e = s + G.seg < G.n ? s + G.seg : G.n;
+  ix i0 = s - G.burn;
+  if (i0 < 0) i0 = 0;
+  i0 -= i0 % 8;
+  chol_dmma_unit(C, b, G.n, s, e, i0, p > 0 ? C.side + unit * ix(kDK) * (kDK + 1) : nullptr);
+}
+
+__global__ void __launch_bounds__(32) k_chol_dmma_repair(CholP<double> C, Geo G) {
+  const ix b = blockIdx.x;
+  if (b >= G.batch || !C.flag[b]) return;
+  if (threadIdx.x == 0) C.fail[b] = G.n;
+  __syncwarp();
+  chol_dmma_unit(C, b, G.n, 0, G.n, 0, nullptr);
+}
+
 int g_segment_rows = 0;
 
 template <class T, int K, int P, int TS>
@@ -1175,6 +1333,57 @@ bool run_chol(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, c
   return true;
 }
 
+
+// config-4 k = 64 fp64 Cholesky on the FP64 tensor cores
+bool run_chol_dmma(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, cudaStream_t s) {
+  constexpr int K = kDK;
+  Geo G;
+  G.batch = q.batch;
+  G.n = q.n;
+  G.burn = kBurnGen * K;
+  if (const char* bv = std::getenv("BGM_WIDE_BURN"))
+    if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
+  int sms = 148, dev = 0, per = 1;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_chol_dmma, 32, 0);
+  if (per < 1) per = 1;
+  ix seg = g_segment_rows;
+  if (seg <= 0) {
+    ix nseg = ix(sms) * per / (G.batch > 0 ? G.batch : 1);
+    if (nseg < 1) nseg = 1;
+    seg = (G.n + nseg - 1) / nseg;
+    if (seg < 2 * ix(G.burn)) seg = 2 * ix(G.burn);
+  }
+  seg = (seg + 7) / 8 * 8;
+  G.seg = seg;
+  G.nseg = int((G.n + seg - 1) / seg);
+  const ix units = G.batch * G.nseg;
+  const size_t sb = sizeof(double) * size_t(units) * K * (K + 1);
+  char* ws = nullptr;
+  if (scratch_alloc(reinterpret_cast<void**>(&ws), sb + 12 * size_t(G.batch) + 64, s) != cudaSuccess) return false;
+  CholP<double> C;
+  C.q = view<double>(q);
+  C.l = view<double>(l);
+  C.side = reinterpret_cast<double*>(ws);
+  C.fail = reinterpret_cast<int64_t*>(ws + sb);
+  C.flag = reinterpret_cast<int32_t*>(C.fail + G.batch);
+  k_init<<<blocks_for(G.batch, 128), 128, 0, s>>>(C.fail, C.flag, G.batch, G.n);
+  {
+    timing::Scope ts("wide_chol_dmma", s);
+    k_chol_dmma<<<unsigned(units), 32, 0, s>>>(C, G);
+  }
+  {
+    timing::Scope ts("wide_chol_check", s);
+    k_chol_check<double, K><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
+  }
+  {
+    timing::Scope ts("wide_chol_repair", s);
+    k_chol_dmma_repair<<<unsigned(G.batch), 32, 0, s>>>(C, G);
+  }
+  k_status<<<blocks_for(G.batch, 128), 128, 0, s>>>(C.fail, G.batch, G.n, st, row);
+  scratch_free(ws, s);
+  return true;
+}
 
 template <class T, int K, int P, int TS>
 bool run_subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cudaStream_t s) {
@@ -1416,7 +1625,14 @@ bool cholesky(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, c
   if (q.n < 4 * q.lower) return false;  // short matrices: the generic sweep is fine
   const bool f64 = q.dtype == BGM_F64;
   switch (q.lower) {
-    case 64: return f64 ? run_chol<double, 64, 8, 9>(q, l, st, row, s) : run_chol<float, 64, 8, 9>(q, l, st, row, s);
+    case 64: {
+      static const bool use_dmma = [] {
+        const char* e = std::getenv("BGM_WIDE_DMMA");
+        return !(e && e[0] == '0');
+      }();
+      if (f64 && use_dmma) return run_chol_dmma(q, l, st, row, s);
+      return f64 ? run_chol<double, 64, 8, 9>(q, l, st, row, s) : run_chol<float, 64, 8, 9>(q, l, st, row, s);
+    }
     case 128:
       return f64 ? run_chol<double, 128, 16, 9>(q, l, st, row, s) : run_chol<float, 128, 16, 9>(q, l, st, row, s);
     default: return false;
