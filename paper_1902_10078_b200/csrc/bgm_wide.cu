@@ -1257,6 +1257,189 @@ __device__ void chol_dmma_unit(const CholP<double>& C, ix b, ix n, ix s, ix e, i
     atomicMin(reinterpret_cast<unsigned long long*>(C.fail + b), static_cast<unsigned long long>(fail));
 }
 
+// Multi-warp variant: the CTA's NW warps split the Schur tiles by DIAGONAL
+// (tile (I, J) has d = I - J); the shift (I, J) -> (I-1, J-1) keeps d, so
+// every warp keeps its tiles across panels and only the panel fragments
+// travel, through shared memory.  Per panel: the owner of d = 0 factors the
+// diagonal tile (shuffles) -- barrier -- the owners of the panel tiles
+// (d, 0) solve them against L00 and publish their MMA fragments --
+// barrier -- every warp applies its DMMA updates and shifts.
+template <int K, int NW>
+struct MW {
+  static constexpr int T = K / 8 + 1;
+  static constexpr int owner(int d) {
+    const int r = d % (2 * NW);
+    return r < NW ? r : 2 * NW - 1 - r;
+  }
+  static constexpr int ntiles(int w) {
+    int c = 0;
+    for (int d = 0; d < T; ++d)
+      if (owner(d) == w) c += T - d;
+    return c;
+  }
+  static constexpr int slot(int w, int d, int J) {
+    int c = 0;
+    for (int dd = 0; dd < d; ++dd)
+      if (owner(dd) == w) c += T - dd;
+    return c + J;
+  }
+};
+
+template <int K, int NW>
+struct MWSmem {
+  double l00[8][9];
+  double rinv[8];
+  double pf[K / 8 + 1][2][32];
+};
+
+template <int K, int NW, int W>
+__device__ void chol_mw_unit(const CholP<double>& C, ix b, ix n, ix s, ix e, ix i0, double* side,
+                             MWSmem<K, NW>& sm) {
+  using M = MW<K, NW>;
+  constexpr int T = M::T;
+  const int lane = threadIdx.x & 31, rr = lane >> 2, q = lane & 3, c2 = 2 * q;
+  const Band<double>& Q = C.q;
+  const Band<double>& L = C.l;
+  auto qval = [&](ix r, ix c) -> double {
+    if (r < c) {
+      const ix t = r;
+      r = c;
+      c = t;
+    }
+    if (r - c > K || c < 0) return 0.0;
+    if (r >= n) return r == c ? 1.0 : 0.0;
+    return Q.cell(b, int(r - c), c);
+  };
+  auto pick = [](const double* v, int e) -> double { return e ? v[1] : v[0]; };
+  auto store_l = [&](ix g, int I, const double* x) {  // rows 8I + rr of columns g + c2 + v
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const int c = c2 + v, cell = 8 * I + rr - c;
+      const ix col = g + c;
+      if (cell >= 0 && cell <= K && col < n) {
+        const double val = (col + cell < n) ? x[v] : 0.0;
+        if (col >= s) L.cell(b, cell, col) = val;
+        else if (side && col >= s - K) side[(col - (s - K)) * (K + 1) + cell] = val;
+      }
+    }
+  };
+  constexpr int NTW = M::ntiles(W) > 0 ? M::ntiles(W) : 1;
+  double wt[NTW][2];
+#pragma unroll
+  for (int d = 0; d < T; ++d)
+    if (M::owner(d) == W)
+#pragma unroll
+      for (int J = 0; J < T - d; ++J)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) wt[M::slot(W, d, J)][v] = qval(i0 + 8 * (J + d) + rr, i0 + 8 * J + c2 + v);
+  ix fail = n;
+#pragma unroll 1
+  for (ix g = i0; g < e; g += 8) {
+    if (M::owner(0) == W) {  // (A) diagonal tile
+      double* D = wt[M::slot(W, 0, 0)];
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        const double dpp = __shfl_sync(0xffffffffu, pick(D, p & 1), 4 * p + (p >> 1));
+        if (lane == 0 && g + p >= s && g + p < n && !(dpp > kPivotFloor)) fail = fail < g + p ? fail : g + p;
+        const double piv = sqrt(dpp), ri = 1.0 / piv;
+        if (lane == 0) sm.rinv[p] = ri;
+        if (q == (p >> 1)) {
+          if (rr > p) D[p & 1] *= ri;
+          else if (rr == p) D[p & 1] = piv;
+        }
+        const double lr = __shfl_sync(0xffffffffu, pick(D, p & 1), 4 * rr + (p >> 1));
+        const double lc0 = __shfl_sync(0xffffffffu, pick(D, p & 1), 4 * c2 + (p >> 1));
+        const double lc1 = __shfl_sync(0xffffffffu, pick(D, p & 1), 4 * (c2 + 1) + (p >> 1));
+        if (c2 > p && rr >= c2) D[0] = fma(-lr, lc0, D[0]);
+        if (c2 + 1 > p && rr >= c2 + 1) D[1] = fma(-lr, lc1, D[1]);
+      }
+      if (c2 > rr) D[0] = 0.0;
+      if (c2 + 1 > rr) D[1] = 0.0;
+      sm.l00[rr][c2] = D[0];
+      sm.l00[rr][c2 + 1] = D[1];
+      store_l(g, 0, D);
+    }
+    __syncthreads();
+    // (B) panel tiles (d, 0), d >= 1: X = W L00^-T; publish MMA fragments
+#pragma unroll
+    for (int d = 1; d < T; ++d)
+      if (M::owner(d) == W) {
+        double* X = wt[M::slot(W, d, 0)];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if (q == (c >> 1)) X[c & 1] *= sm.rinv[c];
+          const double x = __shfl_sync(0xffffffffu, pick(X, c & 1), 4 * rr + (c >> 1));
+          if (c2 > c) X[0] = fma(-x, sm.l00[c2][c], X[0]);
+          if (c2 + 1 > c) X[1] = fma(-x, sm.l00[c2 + 1][c], X[1]);
+        }
+        store_l(g, d, X);
+#pragma unroll
+        for (int kc = 0; kc < 2; ++kc) {
+          const int srcl = 4 * rr + 2 * kc + (q >> 1);
+          const double e0 = __shfl_sync(0xffffffffu, X[0], srcl);
+          const double e1 = __shfl_sync(0xffffffffu, X[1], srcl);
+          sm.pf[d][kc][lane] = (q & 1) ? e1 : e0;
+        }
+      }
+    __syncthreads();
+    // (C) trailing update of this warp's tiles, (D) shift and the fresh row
+    const ix g2 = g + 8;
+#pragma unroll
+    for (int d = 0; d < T; ++d)
+      if (M::owner(d) == W) {
+#pragma unroll
+        for (int J = 1; J < T - d; ++J) {
+          double* t = wt[M::slot(W, d, J)];
+#pragma unroll
+          for (int kc = 0; kc < 2; ++kc) dmma(t[0], t[1], -sm.pf[J + d][kc][lane], sm.pf[J][kc][lane]);
+        }
+#pragma unroll
+        for (int J = 1; J < T - d; ++J) {
+          wt[M::slot(W, d, J - 1)][0] = wt[M::slot(W, d, J)][0];
+          wt[M::slot(W, d, J - 1)][1] = wt[M::slot(W, d, J)][1];
+        }
+#pragma unroll
+        for (int v = 0; v < 2; ++v)
+          wt[M::slot(W, d, T - 1 - d)][v] = qval(g2 + 8 * (T - 1) + rr, g2 + 8 * (T - 1 - d) + c2 + v);
+      }
+  }
+  if (lane == 0 && fail < n)
+    atomicMin(reinterpret_cast<unsigned long long*>(C.fail + b), static_cast<unsigned long long>(fail));
+}
+
+template <int K, int NW, int W>
+__device__ __forceinline__ void chol_mw_dispatch(int w, const CholP<double>& C, ix b, ix n, ix s, ix e, ix i0,
+                                                 double* side, MWSmem<K, NW>& sm) {
+  if (w == W) chol_mw_unit<K, NW, W>(C, b, n, s, e, i0, side, sm);
+  if constexpr (W + 1 < NW) chol_mw_dispatch<K, NW, W + 1>(w, C, b, n, s, e, i0, side, sm);
+}
+
+template <int K, int NW>
+__global__ void __launch_bounds__(32 * NW) k_chol_mw(CholP<double> C, Geo G) {
+  __shared__ MWSmem<K, NW> sm;
+  const ix unit = blockIdx.x;
+  const ix b = unit / G.nseg;
+  const int p = int(unit % G.nseg);
+  if (b >= G.batch) return;
+  const ix s = ix(p) * G.seg;
+  const ix e = s + G.seg < G.n ? s + G.seg : G.n;
+  ix i0 = s - G.burn;
+  if (i0 < 0) i0 = 0;
+  i0 -= i0 % 8;
+  chol_mw_dispatch<K, NW, 0>(threadIdx.x >> 5, C, b, G.n, s, e, i0,
+                             p > 0 ? C.side + unit * ix(K) * (K + 1) : nullptr, sm);
+}
+
+template <int K, int NW>
+__global__ void __launch_bounds__(32 * NW) k_chol_mw_repair(CholP<double> C, Geo G) {
+  __shared__ MWSmem<K, NW> sm;
+  const ix b = blockIdx.x;
+  if (b >= G.batch || !C.flag[b]) return;
+  if (threadIdx.x == 0) C.fail[b] = G.n;
+  __syncthreads();
+  chol_mw_dispatch<K, NW, 0>(threadIdx.x >> 5, C, b, G.n, 0, G.n, 0, nullptr, sm);
+}
+
 __global__ void __launch_bounds__(32) k_chol_dmma(CholP<double> C, Geo G) {
   const ix unit = blockIdx.x;
   const ix b = unit / G.nseg;
@@ -1333,6 +1516,57 @@ bool run_chol(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, c
   return true;
 }
 
+
+// config-4 fp64 Cholesky on the FP64 tensor cores, NW warps per unit
+template <int K, int NW>
+bool run_chol_mw(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, cudaStream_t s) {
+  Geo G;
+  G.batch = q.batch;
+  G.n = q.n;
+  G.burn = kBurnGen * K;
+  if (const char* bv = std::getenv("BGM_WIDE_BURN"))
+    if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
+  int sms = 148, dev = 0, per = 1;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_chol_mw<K, NW>, 32 * NW, 0);
+  if (per < 1) per = 1;
+  ix seg = g_segment_rows;
+  if (seg <= 0) {
+    ix nseg = ix(sms) * per / (G.batch > 0 ? G.batch : 1);
+    if (nseg < 1) nseg = 1;
+    seg = (G.n + nseg - 1) / nseg;
+    if (seg < 2 * ix(G.burn)) seg = 2 * ix(G.burn);
+  }
+  seg = (seg + 7) / 8 * 8;
+  G.seg = seg;
+  G.nseg = int((G.n + seg - 1) / seg);
+  const ix units = G.batch * G.nseg;
+  const size_t sb = sizeof(double) * size_t(units) * K * (K + 1);
+  char* ws = nullptr;
+  if (scratch_alloc(reinterpret_cast<void**>(&ws), sb + 12 * size_t(G.batch) + 64, s) != cudaSuccess) return false;
+  CholP<double> C;
+  C.q = view<double>(q);
+  C.l = view<double>(l);
+  C.side = reinterpret_cast<double*>(ws);
+  C.fail = reinterpret_cast<int64_t*>(ws + sb);
+  C.flag = reinterpret_cast<int32_t*>(C.fail + G.batch);
+  k_init<<<blocks_for(G.batch, 128), 128, 0, s>>>(C.fail, C.flag, G.batch, G.n);
+  {
+    timing::Scope ts("wide_chol_dmma", s);
+    k_chol_mw<K, NW><<<unsigned(units), 32 * NW, 0, s>>>(C, G);
+  }
+  {
+    timing::Scope ts("wide_chol_check", s);
+    k_chol_check<double, K><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
+  }
+  {
+    timing::Scope ts("wide_chol_repair", s);
+    k_chol_mw_repair<K, NW><<<unsigned(G.batch), 32 * NW, 0, s>>>(C, G);
+  }
+  k_status<<<blocks_for(G.batch, 128), 128, 0, s>>>(C.fail, G.batch, G.n, st, row);
+  scratch_free(ws, s);
+  return true;
+}
 
 // config-4 k = 64 fp64 Cholesky on the FP64 tensor cores
 bool run_chol_dmma(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, cudaStream_t s) {
@@ -1630,11 +1864,32 @@ bool cholesky(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, c
         const char* e = std::getenv("BGM_WIDE_DMMA");
         return !(e && e[0] == '0');
       }();
-      if (f64 && use_dmma) return run_chol_dmma(q, l, st, row, s);
+      if (f64 && use_dmma) {
+        static const int nw = [] {
+          const char* e = std::getenv("BGM_WIDE_DMMA_WARPS");
+          return e ? std::atoi(e) : 1;
+        }();
+        if (nw == 2) return run_chol_mw<64, 2>(q, l, st, row, s);
+        return run_chol_dmma(q, l, st, row, s);
+      }
       return f64 ? run_chol<double, 64, 8, 9>(q, l, st, row, s) : run_chol<float, 64, 8, 9>(q, l, st, row, s);
     }
-    case 128:
+    case 128: {
+      static const bool use_dmma = [] {
+        const char* e = std::getenv("BGM_WIDE_DMMA");
+        return !(e && e[0] == '0');
+      }();
+      if (f64 && use_dmma) {
+        static const int nw = [] {
+          const char* e = std::getenv("BGM_WIDE_DMMA_WARPS");
+          return e ? std::atoi(e) : 4;
+        }();
+        if (nw == 8) return run_chol_mw<128, 8>(q, l, st, row, s);
+        if (nw == 2) return run_chol_mw<128, 2>(q, l, st, row, s);
+        return run_chol_mw<128, 4>(q, l, st, row, s);
+      }
       return f64 ? run_chol<double, 128, 16, 9>(q, l, st, row, s) : run_chol<float, 128, 16, 9>(q, l, st, row, s);
+    }
     default: return false;
   }
 }
