@@ -1461,6 +1461,205 @@ __global__ void __launch_bounds__(32) k_chol_dmma_repair(CholP<double> C, Geo G)
   chol_dmma_unit(C, b, G.n, 0, G.n, 0, nullptr);
 }
 
+// ------------------------------------------------------------------ subset, FP64 DMMA
+// Blocked Takahashi recursion on the FP64 tensor cores, one warp per
+// (matrix, segment), panels of 8 columns from the bottom up.  With the panel
+// P = rows [p, p+8) and the trailing window T = the K rows below it,
+// Z L = L^-T gives (block form of the column recursion in bgm_narrow.cu)
+//   Z_TP = -(Z_TT L_TP) L_PP^-1,   Z_PP = (L_PP^-1 - L_TP^T Z_TP)^T L_PP^-1 .
+// Z_TT lives in shared memory as 8x8 tiles, each tile diagonal d = B1 - B2 a
+// ring indexed by block mod (K/8 - d), so the window slides with no copies:
+// the panel's new tiles overwrite the tiles of the block leaving the window.
+// Per panel: L_PP^-1 by shuffles; Y = Z_TT L_TP ((K/8)^2 x 2 DMMA);
+// Z_TP = -Y L_PP^-1; H = L_TP^T Z_TP; Z_PP = (L_PP^-1 - H)^T L_PP^-1 -- all
+// DMMA with operands read from padded (conflict-free) shared tiles.
+template <int K>
+struct TakSmem {
+  static constexpr int NT = K / 8;
+  static constexpr int NZ = NT * (NT + 1) / 2;
+  double z[NZ][8][9];
+  double lp[2][K + 8][9];
+  double y[NT][8][9];
+  double linv[8][9];
+  double h[8][9];
+};
+
+template <int K>
+__device__ __forceinline__ int tak_slot(int d, ix b2) {
+  constexpr int NT = K / 8;
+  return d * NT - d * (d - 1) / 2 + int(b2 % (NT - d));
+}
+
+template <int K>
+__device__ void subset_dmma_unit(const SubP<double>& C, ix b, ix n, ix s, ix e, ix jend, double* side,
+                                 TakSmem<K>& sm) {
+  constexpr int NT = K / 8;
+  const int lane = threadIdx.x & 31, rr = lane >> 2, q = lane & 3, c2 = 2 * q;
+  const Band<double>& L = C.l;
+  const Band<double>& S = C.s;
+  const ix pb_top = (jend - 1) / 8, pb_end = s / 8;
+  const bool exact_top = 8 * (pb_top + 1) >= n;  // window below the top panel is all padding
+  // Z window for the top panel: identity on padded rows, else zero (burn-in)
+  for (int idx = lane; idx < TakSmem<K>::NZ * 64; idx += 32) {
+    const int t = idx >> 6, m = (idx >> 3) & 7, c = idx & 7;
+    double v = 0.0;
+    if (exact_top && t < NT && m == c) {  // diagonal ring d = 0 occupies slots [0, NT)
+      v = 1.0;
+    }
+    sm.z[t][m][c] = v;
+  }
+  auto fill = [&](int buf, ix pb) {  // L rows [8pb, 8pb+K+8) x cols [8pb, 8pb+8), identity past n
+    const ix c0 = 8 * pb;
+    for (int idx = lane; idx < 8 * (K + 8); idx += 32) {
+      const int c = idx / (K + 8), r = idx % (K + 8);
+      double* dst = &sm.lp[buf][r][c];
+      const ix col = c0 + c, row = c0 + r;
+      const int cell = r - c;
+      if (pb >= 0 && cell >= 0 && cell <= K && col < n && row < n) cpa(dst, &L.cell(b, cell, col));
+      else *dst = (cell == 0 && col >= n) ? 1.0 : 0.0;
+    }
+    cpa_commit();
+  };
+  fill(0, pb_top);
+  int buf = 0;
+#pragma unroll 1
+  for (ix pb = pb_top; pb >= pb_end; --pb) {
+    cpa_wait0();
+    __syncwarp();
+    if (pb - 1 >= pb_end) fill(buf ^ 1, pb - 1);
+    double (*lp)[9] = sm.lp[buf];
+    // (1) Linv = L_PP^-1 by forward substitution in the fragment layout
+    {
+      double M0 = rr == c2 ? 1.0 : 0.0, M1 = rr == c2 + 1 ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (rr == k) {
+          const double ri = 1.0 / lp[k][k];
+          M0 *= ri;
+          M1 *= ri;
+        }
+        const double mk0 = __shfl_sync(0xffffffffu, M0, 4 * k + q);
+        const double mk1 = __shfl_sync(0xffffffffu, M1, 4 * k + q);
+        if (rr > k) {
+          const double lrk = lp[rr][k];
+          M0 = fma(-lrk, mk0, M0);
+          M1 = fma(-lrk, mk1, M1);
+        }
+      }
+      sm.linv[rr][c2] = M0;
+      sm.linv[rr][c2 + 1] = M1;
+    }
+    // (2) Y_t = sum_u Z[t][u] L_TP[u]  (window blocks pb+1+t, pb+1+u)
+    double yacc[NT][2];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      yacc[t][0] = yacc[t][1] = 0.0;
+#pragma unroll
+      for (int u = 0; u < NT; ++u) {
+#pragma unroll
+        for (int kc = 0; kc < 2; ++kc) {
+          double a;
+          if (t >= u) a = sm.z[tak_slot<K>(t - u, pb + 1 + u)][rr][4 * kc + q];
+          else a = sm.z[tak_slot<K>(u - t, pb + 1 + t)][4 * kc + q][rr];
+          const double bv = lp[8 + 8 * u + 4 * kc + q][rr];
+          dmma(yacc[t][0], yacc[t][1], a, bv);
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      sm.y[t][rr][c2] = yacc[t][0];
+      sm.y[t][rr][c2 + 1] = yacc[t][1];
+    }
+    __syncwarp();
+    // (3) Z_TP[t] = -Y_t Linv: new tiles (pb+1+t, pb) on diagonal t+1
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      double z0 = 0.0, z1 = 0.0;
+#pragma unroll
+      for (int kc = 0; kc < 2; ++kc) dmma(z0, z1, -sm.y[t][rr][4 * kc + q], sm.linv[4 * kc + q][rr]);
+      yacc[t][0] = z0;
+      yacc[t][1] = z1;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      sm.y[t][rr][c2] = yacc[t][0];
+      sm.y[t][rr][c2 + 1] = yacc[t][1];
+      if (t + 1 < NT) {
+        double (*zt)[9] = sm.z[tak_slot<K>(t + 1, pb)];
+        zt[rr][c2] = yacc[t][0];
+        zt[rr][c2 + 1] = yacc[t][1];
+      }
+    }
+    __syncwarp();
+    // (4) H = L_TP^T Z_TP; h = Linv - H
+    {
+      double h0 = 0.0, h1 = 0.0;
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+#pragma unroll
+        for (int kc = 0; kc < 2; ++kc)
+          dmma(h0, h1, lp[8 + 8 * t + 4 * kc + q][rr], sm.y[t][4 * kc + q][rr]);
+      sm.h[rr][c2] = sm.linv[rr][c2] - h0;
+      sm.h[rr][c2 + 1] = sm.linv[rr][c2 + 1] - h1;
+    }
+    __syncwarp();
+    // (5) Z_PP = h^T Linv -> tile (pb, pb) on diagonal 0
+    double zp0 = 0.0, zp1 = 0.0;
+#pragma unroll
+    for (int kc = 0; kc < 2; ++kc) dmma(zp0, zp1, sm.h[4 * kc + q][rr], sm.linv[4 * kc + q][rr]);
+    {
+      double (*zt)[9] = sm.z[tak_slot<K>(0, pb)];
+      zt[rr][c2] = zp0;
+      zt[rr][c2 + 1] = zp1;
+    }
+    // (6) S columns 8pb + c2 + v: rows from Z_PP and Z_TP
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const ix col = 8 * pb + c2 + v;
+      const bool own = col >= s && col < e && col < n;
+      const bool burn = side && col >= e && col < e + K && col < n;
+      if (own || burn) {
+        auto put = [&](int cell, double val) {
+          if (cell < 0 || cell > K) return;
+          const double w = (col + cell < n) ? val : 0.0;
+          if (own) S.cell(b, cell, col) = w;
+          else side[(col - e) * (K + 1) + cell] = w;
+        };
+        put(rr - c2 - v, v ? zp1 : zp0);
+#pragma unroll
+        for (int t = 0; t < NT; ++t) put(8 + 8 * t + rr - c2 - v, yacc[t][v]);
+      }
+    }
+    __syncwarp();
+    buf ^= 1;
+  }
+  cpa_wait0();
+}
+
+template <int K>
+__global__ void __launch_bounds__(32) k_subset_dmma(SubP<double> C, Geo G) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  TakSmem<K>& sm = *reinterpret_cast<TakSmem<K>*>(smraw);
+  const ix unit = blockIdx.x;
+  const ix b = unit / G.nseg;
+  const int p = int(unit % G.nseg);
+  if (b >= G.batch) return;
+  const ix s = ix(p) * G.seg, e = s + G.seg < G.n ? s + G.seg : G.n;
+  const ix jend = e + G.burn < G.n ? e + G.burn : G.n;  // rows [s, jend) swept, top one first
+  subset_dmma_unit<K>(C, b, G.n, s, e, jend, p + 1 < G.nseg ? C.side + unit * ix(K) * (K + 1) : nullptr, sm);
+}
+
+template <int K>
+__global__ void __launch_bounds__(32) k_subset_dmma_repair(SubP<double> C, Geo G) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  TakSmem<K>& sm = *reinterpret_cast<TakSmem<K>*>(smraw);
+  const ix b = blockIdx.x;
+  if (b >= G.batch || !C.flag[b]) return;
+  subset_dmma_unit<K>(C, b, G.n, 0, G.n, G.n, nullptr, sm);
+}
+
 int g_segment_rows = 0;
 
 template <class T, int K, int P, int TS>
@@ -1615,6 +1814,67 @@ bool run_chol_dmma(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* r
     k_chol_dmma_repair<<<unsigned(G.batch), 32, 0, s>>>(C, G);
   }
   k_status<<<blocks_for(G.batch, 128), 128, 0, s>>>(C.fail, G.batch, G.n, st, row);
+  scratch_free(ws, s);
+  return true;
+}
+
+template <int K>
+bool run_subset_dmma(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cudaStream_t s) {
+  const size_t smem = sizeof(TakSmem<K>);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_subset_dmma<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_subset_dmma_repair<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = true;
+  }
+  Geo G;
+  G.batch = l.batch;
+  G.n = l.n;
+  G.burn = kBurnGen * K;
+  if (const char* bv = std::getenv("BGM_WIDE_BURN"))
+    if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
+  G.burn = (G.burn + 7) / 8 * 8;
+  int sms = 148, dev = 0, per = 1;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_subset_dmma<K>, 32, smem);
+  if (per < 1) per = 1;
+  ix seg = g_segment_rows;
+  if (seg <= 0) {
+    ix nseg = ix(sms) * per / (G.batch > 0 ? G.batch : 1);
+    if (nseg < 1) nseg = 1;
+    seg = (G.n + nseg - 1) / nseg;
+    if (seg < 2 * ix(G.burn)) seg = 2 * ix(G.burn);
+  }
+  seg = (seg + 7) / 8 * 8;
+  if (seg < K) seg = (K + 7) / 8 * 8;
+  G.seg = seg;
+  G.nseg = int((G.n + seg - 1) / seg);
+  const ix units = G.batch * G.nseg;
+  const size_t side_bytes = sizeof(double) * size_t(units) * K * (K + 1);
+  char* ws = nullptr;
+  if (scratch_alloc(reinterpret_cast<void**>(&ws), side_bytes + 12 * size_t(G.batch) + 64, s) != cudaSuccess)
+    return false;
+  SubP<double> C;
+  C.l = view<double>(l);
+  C.s = view<double>(sb);
+  C.side = reinterpret_cast<double*>(ws);
+  int64_t* fail = reinterpret_cast<int64_t*>(ws + side_bytes);
+  C.flag = reinterpret_cast<int32_t*>(fail + G.batch);
+  k_init<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, C.flag, G.batch, G.n);
+  k_diag_check<double><<<blocks_for(G.batch * G.n, 256), 256, 0, s>>>(C.l, G.batch, fail);
+  {
+    timing::Scope ts("wide_subset_dmma", s);
+    k_subset_dmma<K><<<unsigned(units), 32, smem, s>>>(C, G);
+  }
+  {
+    timing::Scope ts("wide_subset_check", s);
+    k_subset_check<double, K><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
+  }
+  {
+    timing::Scope ts("wide_subset_repair", s);
+    k_subset_dmma_repair<K><<<unsigned(G.batch), 32, smem, s>>>(C, G);
+  }
+  k_status_code<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, G.batch, G.n, BGM_ERR_SINGULAR, st, row);
   scratch_free(ws, s);
   return true;
 }
@@ -1898,9 +2158,16 @@ bool subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cu
   if (l.lower != sb.lower || l.upper != 0 || sb.upper != 0 || l.batch == 0 || l.n == 0) return false;
   if (l.n < 4 * l.lower) return false;
   const bool f64 = l.dtype == BGM_F64;
+  static const bool use_dmma = [] {
+    const char* e = std::getenv("BGM_WIDE_DMMA");
+    return !(e && e[0] == '0');
+  }();
   switch (l.lower) {
-    case 64: return f64 ? run_subset<double, 64, 8, 9>(l, sb, st, row, s) : run_subset<float, 64, 8, 9>(l, sb, st, row, s);
+    case 64:
+      if (f64 && use_dmma) return run_subset_dmma<64>(l, sb, st, row, s);
+      return f64 ? run_subset<double, 64, 8, 9>(l, sb, st, row, s) : run_subset<float, 64, 8, 9>(l, sb, st, row, s);
     case 128:
+      if (f64 && use_dmma) return run_subset_dmma<128>(l, sb, st, row, s);
       return f64 ? run_subset<double, 128, 16, 9>(l, sb, st, row, s)
                  : run_subset<float, 128, 16, 9>(l, sb, st, row, s);
     default: return false;
