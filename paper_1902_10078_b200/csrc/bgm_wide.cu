@@ -1660,6 +1660,383 @@ __global__ void __launch_bounds__(32) k_subset_dmma_repair(SubP<double> C, Geo G
   subset_dmma_unit<K>(C, b, G.n, 0, G.n, G.n, nullptr, sm);
 }
 
+// ------------------------------------------------------------------ vjp_subset, FP64 DMMA
+// Reverse of the blocked Takahashi recursion (see k_subset_dmma), panels of
+// 8 columns from the top down, one warp per (matrix, segment).  Per panel P
+// with trailing window T: recompute Linv = L_PP^-1, Y = Z_TT L_TP,
+// Z_TP = -Y Linv, A = Linv - L_TP^T Z_TP from the stored band of Z (= S), then
+//   Zb_TP = 2 W(T,P)  Zb_PP = W(P,P)       (W: adjoint window, symmetric split)
+//   Ab = Linv Zb_PP   Linvb = A Zb_PP + Ab   Hb = -Ab
+//   Ltpb = Z_TP Hb^T  Zb_TP += L_TP Hb   Yb = -Zb_TP Linv^T
+//   Linvb -= Y^T Zb_TP   W(T,T) += (Yb L_TP^T + L_TP Yb^T) / 2   Ltpb += Z_TT Yb
+//   Lppb = -Linv^T Linvb Linv^T (lower part)
+// -- every product an 8x8-tile DMMA with operands read (transposed or not)
+// from padded shared tiles.  Z_TT and W live in diagonal rings as in the
+// forward; the rows entering at the bottom take S (Z) and S-bar (W).
+// Checked against the scalar recursion (grad.cpp:84-143) by the parity tests.
+template <int K>
+struct VtSmem {
+  static constexpr int NT = K / 8;
+  static constexpr int NZ = NT * (NT + 1) / 2;
+  static constexpr int NW = (NT + 1) * (NT + 2) / 2;
+  double z[NZ][8][9];
+  double w[NW][8][9];
+  double lp[2][K + 8][9];
+  double y[NT][8][9];
+  double zt[NT][8][9];
+  double yb[NT][8][9];
+  double lt[NT][8][9];
+  double linv[8][9], am[8][9], ab[8][9], lvb[8][9], hb[8][9];
+};
+
+// acc += sx op(X) op(Y) for 8x8 shared tiles (k = 8: two DMMA), fragment layouts
+template <bool TX, bool TY>
+__device__ __forceinline__ void tmm(double& c0, double& c1, const double (*X)[9], const double (*Y)[9], double sx,
+                                    int rr, int q) {
+#pragma unroll
+  for (int kc = 0; kc < 2; ++kc) {
+    const double a = TX ? X[4 * kc + q][rr] : X[rr][4 * kc + q];
+    const double b = TY ? Y[rr][4 * kc + q] : Y[4 * kc + q][rr];
+    dmma(c0, c1, sx * a, b);
+  }
+}
+
+template <int K>
+__device__ __forceinline__ int wv_slot(int d, ix b2) {  // adjoint window: NT+1 blocks
+  constexpr int NB = K / 8 + 1;
+  return d * NB - d * (d - 1) / 2 + int(b2 % (NB - d));
+}
+
+template <int K>
+__device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix i0, double* side, double* tail,
+                               VtSmem<K>& sm) {
+  constexpr int NT = K / 8, NB = NT + 1;
+  const int lane = threadIdx.x & 31, rr = lane >> 2, q = lane & 3, c2 = 2 * q;
+  const Band<double>& L = C.l;
+  const Band<double>& S = C.s;
+  const Band<double>& SB = C.sb;
+  // Entering tiles are fetched raw with cp.async (lower triangle of a diagonal
+  // tile only) and completed after the wait: mirror, and the symmetric split
+  // (halving) of S-bar's off-diagonal cells.  Rows past n: Z identity, G zero.
+  auto issue = [&](double (*t)[9], const Band<double>& src, bool ident, ix b1, ix b2) {
+    for (int idx = lane; idx < 64; idx += 32) {
+      const int m = idx >> 3, c = idx & 7;
+      if (b1 == b2 && m < c) continue;
+      const ix r = 8 * b1 + m, col = 8 * b2 + c, cell = r - col;
+      if (cell <= K && r < n) cpa(&t[m][c], &src.cell(b, int(cell), col));
+      else t[m][c] = (ident && cell == 0) ? 1.0 : 0.0;
+    }
+  };
+  auto fix = [&](double (*t)[9], bool diag, bool half) {
+    double v[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int idx = lane + 32 * h, m = idx >> 3, c = idx & 7;
+      const double x = (diag && m < c) ? t[c][m] : t[m][c];
+      v[h] = (half && m != c) || (half && !diag) ? 0.5 * x : x;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int idx = lane + 32 * h;
+      t[idx >> 3][idx & 7] = v[h];
+    }
+  };
+  auto issue_row = [&](ix bn) {  // block row bn: W tiles (bn, bn-NT .. bn), Z tiles (bn, bn-NT+1 .. bn)
+    for (int d = 0; d <= NT; ++d) issue(sm.w[wv_slot<K>(d, bn - d)], SB, false, bn, bn - d);
+    for (int d = 0; d < NT; ++d) issue(sm.z[tak_slot<K>(d, bn - d)], S, true, bn, bn - d);
+  };
+  auto fix_row = [&](ix bn) {
+    for (int d = 0; d <= NT; ++d) fix(sm.w[wv_slot<K>(d, bn - d)], d == 0, true);
+    fix(sm.z[tak_slot<K>(0, bn)], true, false);
+  };
+  auto fill = [&](int buf, ix pb) {  // L rows [8pb, 8pb+K+8) x cols [8pb, 8pb+8), identity past n
+    for (int idx = lane; idx < 8 * (K + 8); idx += 32) {
+      const int c = idx / (K + 8), r = idx % (K + 8), cell = r - c;
+      const ix col = 8 * pb + c, row = 8 * pb + r;
+      double* dst = &sm.lp[buf][r][c];
+      if (cell >= 0 && cell <= K && col < n && row < n) cpa(dst, &L.cell(b, cell, col));
+      else *dst = (cell == 0) ? 1.0 : 0.0;
+    }
+  };
+  auto save_w = [&](double* dst, ix pb) {  // window of panel pb: blocks pb .. pb + NT
+    for (int d = 0; d <= NT; ++d)
+      for (int j = 0; j + d <= NT; ++j) {
+        const double (*t)[9] = sm.w[wv_slot<K>(d, pb + j)];
+        double* o = dst + (d * NB - d * (d - 1) / 2 + j) * 64;
+        for (int idx = lane; idx < 64; idx += 32) o[idx] = t[idx >> 3][idx & 7];
+      }
+  };
+  const ix pb0 = i0 / 8, pbe = (e + 7) / 8;
+  // initial window: W blocks pb0 .. pb0+NT, Z blocks pb0+1 .. pb0+NT
+  for (int t1 = 0; t1 <= NT; ++t1)
+    for (int t2 = 0; t2 <= t1; ++t2) {
+      issue(sm.w[wv_slot<K>(t1 - t2, pb0 + t2)], SB, false, pb0 + t1, pb0 + t2);
+      if (t2 >= 1) issue(sm.z[tak_slot<K>(t1 - t2, pb0 + t2)], S, true, pb0 + t1, pb0 + t2);
+    }
+  fill(0, pb0);
+  cpa_commit();
+  cpa_wait0();
+  __syncwarp();
+  for (int t1 = 0; t1 <= NT; ++t1) {
+    for (int t2 = 0; t2 <= t1; ++t2) fix(sm.w[wv_slot<K>(t1 - t2, pb0 + t2)], t1 == t2, true);
+    if (t1 >= 1) fix(sm.z[tak_slot<K>(0, pb0 + t1)], true, false);
+  }
+  __syncwarp();
+  int buf = 0;
+#pragma unroll 1
+  for (ix pb = pb0; pb < pbe; ++pb) {
+    if (pb > pb0) {
+      cpa_wait0();
+      __syncwarp();
+      fix_row(pb + NT);
+      __syncwarp();
+    }
+    if (side && pb == s / 8) save_w(side, pb);  // burn-in state at the segment start
+    if (pb + 1 < pbe) fill(buf ^ 1, pb + 1);
+    cpa_commit();
+    const double (*lp)[9] = sm.lp[buf];
+    // Linv = L_PP^-1 (forward substitution in the fragment layout)
+    {
+      double M0 = rr == c2 ? 1.0 : 0.0, M1 = rr == c2 + 1 ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (rr == k) {
+          const double ri = 1.0 / lp[k][k];
+          M0 *= ri;
+          M1 *= ri;
+        }
+        const double mk0 = __shfl_sync(0xffffffffu, M0, 4 * k + q);
+        const double mk1 = __shfl_sync(0xffffffffu, M1, 4 * k + q);
+        if (rr > k) {
+          const double lrk = lp[rr][k];
+          M0 = fma(-lrk, mk0, M0);
+          M1 = fma(-lrk, mk1, M1);
+        }
+      }
+      sm.linv[rr][c2] = M0;
+      sm.linv[rr][c2 + 1] = M1;
+    }
+    // Z_TT tile (t, u) of the window (blocks pb+1+t, pb+1+u): stored lower, transposed read above
+#define ZTT_MM(acc0, acc1, t, u, Yt)                                              \
+  do {                                                                              \
+    if ((t) >= (u)) tmm<false, false>(acc0, acc1, sm.z[tak_slot<K>((t) - (u), pb + 1 + (u))], Yt, 1.0, rr, q); \
+    else tmm<true, false>(acc0, acc1, sm.z[tak_slot<K>((u) - (t), pb + 1 + (t))], Yt, 1.0, rr, q);             \
+  } while (0)
+    // Y = Z_TT L_TP
+    {
+      double ya[NT][2];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        ya[t][0] = ya[t][1] = 0.0;
+#pragma unroll
+        for (int u = 0; u < NT; ++u) ZTT_MM(ya[t][0], ya[t][1], t, u, lp + 8 + 8 * u);
+      }
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        sm.y[t][rr][c2] = ya[t][0];
+        sm.y[t][rr][c2 + 1] = ya[t][1];
+      }
+    }
+    __syncwarp();
+    // Z_TP = -Y Linv
+    {
+      double za[NT][2];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        za[t][0] = za[t][1] = 0.0;
+        tmm<false, false>(za[t][0], za[t][1], sm.y[t], sm.linv, -1.0, rr, q);
+      }
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        sm.zt[t][rr][c2] = za[t][0];
+        sm.zt[t][rr][c2 + 1] = za[t][1];
+      }
+    }
+    __syncwarp();
+    // A = Linv - L_TP^T Z_TP (four independent accumulators)
+    {
+      double h[4][2] = {};
+#pragma unroll
+      for (int t = 0; t < NT; ++t) tmm<true, false>(h[t & 3][0], h[t & 3][1], lp + 8 + 8 * t, sm.zt[t], 1.0, rr, q);
+      sm.am[rr][c2] = sm.linv[rr][c2] - (h[0][0] + h[1][0]) - (h[2][0] + h[3][0]);
+      sm.am[rr][c2 + 1] = sm.linv[rr][c2 + 1] - (h[0][1] + h[1][1]) - (h[2][1] + h[3][1]);
+    }
+    __syncwarp();
+    // Ab = Linv Zb_PP^T; Linvb = A Zb_PP + Ab; Hb = -Ab
+    {
+      const double (*wpp)[9] = sm.w[wv_slot<K>(0, pb)];
+      double a0 = 0.0, a1 = 0.0, v0 = 0.0, v1 = 0.0;
+      tmm<false, true>(a0, a1, sm.linv, wpp, 1.0, rr, q);
+      tmm<false, false>(v0, v1, sm.am, wpp, 1.0, rr, q);
+      sm.lvb[rr][c2] = v0 + a0;
+      sm.lvb[rr][c2 + 1] = v1 + a1;
+      sm.hb[rr][c2] = -a0;
+      sm.hb[rr][c2 + 1] = -a1;
+    }
+    __syncwarp();
+    // Ltpb = Z_TP Hb^T; Zb_TP = 2 W(T,P) + L_TP Hb
+    {
+      double la[NT][2], za[NT][2];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const double (*wtp)[9] = sm.w[wv_slot<K>(t + 1, pb)];
+        la[t][0] = la[t][1] = 0.0;
+        za[t][0] = 2.0 * wtp[rr][c2];
+        za[t][1] = 2.0 * wtp[rr][c2 + 1];
+        tmm<false, true>(la[t][0], la[t][1], sm.zt[t], sm.hb, 1.0, rr, q);
+        tmm<false, false>(za[t][0], za[t][1], lp + 8 + 8 * t, sm.hb, 1.0, rr, q);
+      }
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        sm.lt[t][rr][c2] = la[t][0];
+        sm.lt[t][rr][c2 + 1] = la[t][1];
+        sm.yb[t][rr][c2] = za[t][0];
+        sm.yb[t][rr][c2 + 1] = za[t][1];
+      }
+    }
+    __syncwarp();
+    // block row pb+NT+1 enters W into the slots of the leaving column pb (free from here on)
+    for (int d = 0; d <= NT; ++d) issue(sm.w[wv_slot<K>(d, pb)], SB, false, pb + NT + 1, pb + NT + 1 - d);
+    cpa_commit();
+    // Linvb -= Y^T Zb_TP; Yb = -Zb_TP Linv^T
+    {
+      double h[4][2] = {};
+#pragma unroll
+      for (int t = 0; t < NT; ++t) tmm<true, false>(h[t & 3][0], h[t & 3][1], sm.y[t], sm.yb[t], 1.0, rr, q);
+      double ya[NT][2];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        ya[t][0] = ya[t][1] = 0.0;
+        tmm<false, true>(ya[t][0], ya[t][1], sm.yb[t], sm.linv, -1.0, rr, q);
+      }
+      __syncwarp();
+      sm.lvb[rr][c2] -= (h[0][0] + h[1][0]) + (h[2][0] + h[3][0]);
+      sm.lvb[rr][c2 + 1] -= (h[0][1] + h[1][1]) + (h[2][1] + h[3][1]);
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        sm.yb[t][rr][c2] = ya[t][0];
+        sm.yb[t][rr][c2 + 1] = ya[t][1];
+      }
+    }
+    __syncwarp();
+    // Ltpb += Z_TT Yb -> L-bar rows 8pb+8+8t+rr, columns 8pb+c2+v (band cells <= K)
+    {
+      double la[NT][2];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        la[t][0] = sm.lt[t][rr][c2];
+        la[t][1] = sm.lt[t][rr][c2 + 1];
+#pragma unroll
+        for (int u = 0; u < NT; ++u) ZTT_MM(la[t][0], la[t][1], t, u, sm.yb[u]);
+      }
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const ix col = 8 * pb + c2 + v;
+          const int cell = 8 + 8 * t + rr - c2 - v;
+          if (col >= s && col < e && cell <= K) C.lb.cell(b, cell, col) = (col + cell < n) ? la[t][v] : 0.0;
+        }
+    }
+#undef ZTT_MM
+    __syncwarp();
+    // block row pb+NT+1 enters Z into the slots of the leaving column pb+1
+    for (int d = 0; d < NT; ++d) issue(sm.z[tak_slot<K>(d, pb + 1)], S, true, pb + NT + 1, pb + NT + 1 - d);
+    cpa_commit();
+    // W(T,T) += (Yb L_TP^T + L_TP Yb^T) / 2: rows t and NT-1-t paired (NT+1 tiles per pass)
+#pragma unroll 1
+    for (int pp = 0; pp < NT / 2; ++pp) {
+      double wa[NT + 1][2];
+#pragma unroll
+      for (int j = 0; j <= NT; ++j) {
+        const int t1 = j <= pp ? pp : NT - 1 - pp, t2 = j <= pp ? j : j - pp - 1;
+        const double (*wt)[9] = sm.w[wv_slot<K>(t1 - t2, pb + 1 + t2)];
+        wa[j][0] = wt[rr][c2];
+        wa[j][1] = wt[rr][c2 + 1];
+        tmm<false, true>(wa[j][0], wa[j][1], sm.yb[t1], lp + 8 + 8 * t2, 0.5, rr, q);
+        tmm<false, true>(wa[j][0], wa[j][1], lp + 8 + 8 * t1, sm.yb[t2], 0.5, rr, q);
+      }
+#pragma unroll
+      for (int j = 0; j <= NT; ++j) {
+        const int t1 = j <= pp ? pp : NT - 1 - pp, t2 = j <= pp ? j : j - pp - 1;
+        double (*wt)[9] = sm.w[wv_slot<K>(t1 - t2, pb + 1 + t2)];
+        wt[rr][c2] = wa[j][0];
+        wt[rr][c2 + 1] = wa[j][1];
+      }
+    }
+    // Lppb = -Linv^T (Linvb Linv^T), lower part
+    {
+      double t0 = 0.0, t1 = 0.0;
+      tmm<false, true>(t0, t1, sm.lvb, sm.linv, 1.0, rr, q);
+      sm.ab[rr][c2] = t0;
+      sm.ab[rr][c2 + 1] = t1;
+      __syncwarp();
+      double p0 = 0.0, p1 = 0.0;
+      tmm<true, false>(p0, p1, sm.linv, sm.ab, -1.0, rr, q);
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const ix col = 8 * pb + c2 + v;
+        const int cell = rr - c2 - v;
+        if (col >= s && col < e && cell >= 0) C.lb.cell(b, cell, col) = (col + cell < n) ? (v ? p1 : p0) : 0.0;
+      }
+    }
+    __syncwarp();
+    buf ^= 1;
+  }
+  cpa_wait0();
+  __syncwarp();
+  fix_row(pbe + NT);
+  __syncwarp();
+  if (tail) save_w(tail, pbe);  // genuine state the next segment's burn-in must reproduce
+}
+
+template <int K>
+__global__ void __launch_bounds__(32) k_vsub_dmma(VsP<double> C, Geo G) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  VtSmem<K>& sm = *reinterpret_cast<VtSmem<K>*>(smraw);
+  constexpr int NB = K / 8 + 1, STATE = NB * (NB + 1) / 2 * 64;
+  const ix unit = blockIdx.x;
+  const ix b = unit / G.nseg;
+  const int p = int(unit % G.nseg);
+  if (b >= G.batch) return;
+  const ix s = ix(p) * G.seg, e = s + G.seg < G.n ? s + G.seg : G.n;
+  ix i0 = s - G.burn;
+  if (i0 < 0) i0 = 0;
+  i0 -= i0 % 8;
+  vsub_dmma_unit<K>(C, b, G.n, s, e, i0, p > 0 ? C.side + unit * ix(STATE) : nullptr,
+                    p + 1 < G.nseg ? C.tail + unit * ix(STATE) : nullptr, sm);
+}
+
+template <int K>
+__global__ void k_vsub_dmma_check(VsP<double> C, Geo G) {
+  constexpr int NB = K / 8 + 1, STATE = NB * (NB + 1) / 2 * 64;
+  const ix id = (blockIdx.x * ix(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (id >= G.batch * G.nseg) return;
+  const int p = int(id % G.nseg);
+  if (p == 0) return;
+  const double* a = C.side + id * ix(STATE);
+  const double* r = C.tail + (id - 1) * ix(STATE);
+  double sc = 0.0;
+  for (int i = lane; i < STATE; i += 32) sc = fmax(sc, fabs(r[i]));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sc = fmax(sc, __shfl_xor_sync(0xffffffffu, sc, o));
+  bool bad = false;
+  for (int i = lane; i < STATE; i += 32) bad |= !(fabs(a[i] - r[i]) <= kCheckTol * (sc + 1e-300));
+  bad = __any_sync(0xffffffffu, bad);
+  if (bad && lane == 0) C.flag[id / G.nseg] = 1;
+}
+
+template <int K>
+__global__ void __launch_bounds__(32) k_vsub_dmma_repair(VsP<double> C, Geo G) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  VtSmem<K>& sm = *reinterpret_cast<VtSmem<K>*>(smraw);
+  const ix b = blockIdx.x;
+  if (b >= G.batch || !C.flag[b]) return;
+  vsub_dmma_unit<K>(C, b, G.n, 0, G.n, 0, nullptr, nullptr, sm);
+}
+
 int g_segment_rows = 0;
 
 template <class T, int K, int P, int TS>
@@ -1814,6 +2191,73 @@ bool run_chol_dmma(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* r
     k_chol_dmma_repair<<<unsigned(G.batch), 32, 0, s>>>(C, G);
   }
   k_status<<<blocks_for(G.batch, 128), 128, 0, s>>>(C.fail, G.batch, G.n, st, row);
+  scratch_free(ws, s);
+  return true;
+}
+
+template <int K>
+bool run_vsub_dmma(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, const bgm_band& lb, int32_t* st,
+                   int64_t* row, cudaStream_t s) {
+  const size_t smem = sizeof(VtSmem<K>);
+  if (smem > 227 * 1024) return false;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_vsub_dmma<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_vsub_dmma_repair<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = true;
+  }
+  constexpr int NB = K / 8 + 1, STATE = NB * (NB + 1) / 2 * 64;
+  Geo G;
+  G.batch = l.batch;
+  G.n = l.n;
+  G.burn = kBurnGen * K;
+  if (const char* bv = std::getenv("BGM_WIDE_BURN"))
+    if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
+  int sms = 148, dev = 0, per = 1;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_vsub_dmma<K>, 32, smem);
+  if (per < 1) per = 1;
+  ix seg = g_segment_rows;
+  if (seg <= 0) {
+    ix nseg = ix(sms) * per / (G.batch > 0 ? G.batch : 1);
+    if (nseg < 1) nseg = 1;
+    seg = (G.n + nseg - 1) / nseg;
+    if (seg < 2 * ix(G.burn)) seg = 2 * ix(G.burn);
+  }
+  seg = (seg + 7) / 8 * 8;
+  G.seg = seg;
+  G.nseg = int((G.n + seg - 1) / seg);
+  const ix units = G.batch * G.nseg;
+  const size_t sb_bytes = sizeof(double) * size_t(units) * STATE;
+  char* ws = nullptr;
+  if (scratch_alloc(reinterpret_cast<void**>(&ws), 2 * sb_bytes + 12 * size_t(G.batch) + 64, s) != cudaSuccess)
+    return false;
+  VsP<double> C;
+  C.l = view<double>(l);
+  C.s = view<double>(sm);
+  C.sb = view<double>(sb);
+  C.lb = view<double>(lb);
+  C.side = reinterpret_cast<double*>(ws);
+  C.tail = reinterpret_cast<double*>(ws + sb_bytes);
+  int64_t* fail = reinterpret_cast<int64_t*>(ws + 2 * sb_bytes);
+  C.flag = reinterpret_cast<int32_t*>(fail + G.batch);
+  k_init<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, C.flag, G.batch, G.n);
+  k_diag_check<double><<<blocks_for(G.batch * G.n, 256), 256, 0, s>>>(C.l, G.batch, fail);
+  {
+    timing::Scope ts("wide_vjp_subset_dmma", s);
+    k_vsub_dmma<K><<<unsigned(units), 32, smem, s>>>(C, G);
+  }
+  {
+    timing::Scope ts("wide_vjp_subset_check", s);
+    k_vsub_dmma_check<K><<<blocks_for(units * 32, 128), 128, 0, s>>>(C, G);
+  }
+  {
+    timing::Scope ts("wide_vjp_subset_repair", s);
+    k_vsub_dmma_repair<K><<<unsigned(G.batch), 32, smem, s>>>(C, G);
+  }
+  const ix zw = ((G.batch + l.tile - 1) / l.tile * l.tile) * K * (K + 1);
+  k_zero_corners_w<double><<<blocks_for(zw, 128), 128, 0, s>>>(C.lb, G.batch);
+  k_status_code<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, G.batch, G.n, BGM_ERR_SINGULAR, st, row);
   scratch_free(ws, s);
   return true;
 }
@@ -2211,12 +2655,18 @@ bool vjp_subset(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, const
                 int64_t* row, cudaStream_t s) {
   if (l.upper != 0 || l.batch == 0 || l.n < 4 * l.lower) return false;
   const bool f64 = l.dtype == BGM_F64;
+  static const bool use_dmma = [] {
+    const char* e = std::getenv("BGM_WIDE_DMMA");
+    return !(e && e[0] == '0');
+  }();
   switch (l.lower) {
     case 16:
       return f64 ? run_vsub<double, 16>(l, sm, sb, lb, st, row, s) : run_vsub<float, 16>(l, sm, sb, lb, st, row, s);
     case 64:
+      if (f64 && use_dmma && run_vsub_dmma<64>(l, sm, sb, lb, st, row, s)) return true;
       return f64 ? run_vsub<double, 64>(l, sm, sb, lb, st, row, s) : run_vsub<float, 64>(l, sm, sb, lb, st, row, s);
     case 128:
+      if (f64 && use_dmma && run_vsub_dmma<128>(l, sm, sb, lb, st, row, s)) return true;
       return f64 ? run_vsub<double, 128>(l, sm, sb, lb, st, row, s) : run_vsub<float, 128>(l, sm, sb, lb, st, row, s);
     default: return false;
   }
