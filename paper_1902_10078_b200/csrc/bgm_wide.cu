@@ -24,6 +24,7 @@
 // single-unit sweep -- the same scheme as the config-3 sweeps.
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 
@@ -1662,340 +1663,311 @@ __global__ void __launch_bounds__(32) k_subset_dmma_repair(SubP<double> C, Geo G
 
 // ------------------------------------------------------------------ vjp_subset, FP64 DMMA
 // Reverse of the blocked Takahashi recursion (see k_subset_dmma), panels of
-// 8 columns from the top down, one warp per (matrix, segment).  Per panel P
-// with trailing window T: recompute Linv = L_PP^-1, Y = Z_TT L_TP,
-// Z_TP = -Y Linv, A = Linv - L_TP^T Z_TP from the stored band of Z (= S), then
-//   Zb_TP = 2 W(T,P)  Zb_PP = W(P,P)       (W: adjoint window, symmetric split)
-//   Ab = Linv Zb_PP   Linvb = A Zb_PP + Ab   Hb = -Ab
-//   Ltpb = Z_TP Hb^T  Zb_TP += L_TP Hb   Yb = -Zb_TP Linv^T
-//   Linvb -= Y^T Zb_TP   W(T,T) += (Yb L_TP^T + L_TP Yb^T) / 2   Ltpb += Z_TT Yb
-//   Lppb = -Linv^T Linvb Linv^T (lower part)
-// -- every product an 8x8-tile DMMA with operands read (transposed or not)
-// from padded shared tiles.  Z_TT and W live in diagonal rings as in the
-// forward; the rows entering at the bottom take S (Z) and S-bar (W).
-// Checked against the scalar recursion (grad.cpp:84-143) by the parity tests.
+// 8 columns from the top down, one CTA of NW warps per (matrix, segment).
+// Per panel P with trailing window T (K rows), from the stored band of Z = S:
+//   Linv = L_PP^-1   Y = Z_TT L_TP   Z_TP = -Y Linv   A = Linv - L_TP^T Z_TP
+// and, with W the adjoint window (symmetric split of S-bar plus what the
+// panels above pushed down):
+//   Zb_TP = 2 W(T,P)  Zb_PP = W(P,P)
+//   Ab = Linv Zb_PP^T   Linvb = A Zb_PP + Ab   Hb = -Ab
+//   Ltpb = Z_TP Hb^T + Z_TT Yb   Zb_TP += L_TP Hb   Yb = -Zb_TP Linv^T
+//   Linvb -= Y^T Zb_TP   W(T,T) += (Yb L_TP^T + L_TP Yb^T) / 2
+//   Lppb = -Linv^T Linvb Linv^T (lower)
+// L-bar(P,P) = Lppb, L-bar(T,P) = Ltpb: each band cell of L belongs to one
+// panel.  Every product is a pair of m8n8k4 DMMA on 8x8 tiles in shared
+// memory, stored row-major with the column XOR-swizzled by bit 1 of the row
+// (conflict-free fragment reads in both orientations and 16-byte fragment
+// stores).  Z and W live in per-diagonal rings of tiles; the block row
+// entering at the bottom is fetched with cp.async a panel ahead.  Warps own
+// the tile rows t = warp (mod NW); the 8x8 panel algebra is done redundantly
+// per warp.  Checked against the scalar recursion (grad.cpp:84-143) by the
+// parity tests.
+__device__ __forceinline__ int sw8(int r, int c) { return r * 8 + (c ^ ((r & 2) << 1)); }
+
 template <int K>
+__device__ __forceinline__ int ring_slot(int d, ix b2) {  // diagonal d holds NT+1-d tiles
+  constexpr int NT = K / 8;
+  return d * (NT + 1) - d * (d - 1) / 2 + int(unsigned(b2) % unsigned(NT + 1 - d));
+}
+
+template <int K, int NW>
 struct VtSmem {
   static constexpr int NT = K / 8;
-  static constexpr int NZ = NT * (NT + 1) / 2;
-  static constexpr int NW = (NT + 1) * (NT + 2) / 2;
-  double z[NZ][8][9];
-  double w[NW][8][9];
-  double lp[2][K + 8][9];
-  double y[NT][8][9];
-  double zt[NT][8][9];
-  double yb[NT][8][9];
-  double lt[NT][8][9];
-  double linv[8][9], am[8][9], ab[8][9], lvb[8][9], hb[8][9];
+  static constexpr int NZ = NT * (NT + 3) / 2;         // Z rings, diagonals 0 .. NT-1
+  static constexpr int NWT = (NT + 1) * (NT + 2) / 2;  // W rings, diagonals 0 .. NT
+  double z[NZ][64];
+  double w[NWT][64];
+  double lp[2][(K + 8) * 8];
+  double y[NT][64], zt[NT][64], yb[NT][64];
+  double lin[NW][64], am[NW][64], ab[NW][64], part[NW][64];
+  short zs[NT * NT];
+  short ws[(NT + 1) * (NT + 1)];
 };
 
-// acc += sx op(X) op(Y) for 8x8 shared tiles (k = 8: two DMMA), fragment layouts
-template <bool TX, bool TY>
-__device__ __forceinline__ void tmm(double& c0, double& c1, const double (*X)[9], const double (*Y)[9], double sx,
-                                    int rr, int q) {
-#pragma unroll
-  for (int kc = 0; kc < 2; ++kc) {
-    const double a = TX ? X[4 * kc + q][rr] : X[rr][4 * kc + q];
-    const double b = TY ? Y[rr][4 * kc + q] : Y[4 * kc + q][rr];
-    dmma(c0, c1, sx * a, b);
-  }
-}
-
-template <int K>
-__device__ __forceinline__ int wv_slot(int d, ix b2) {  // adjoint window: NT+1 blocks
-  constexpr int NB = K / 8 + 1;
-  return d * NB - d * (d - 1) / 2 + int(b2 % (NB - d));
-}
-
-template <int K>
+template <int K, int NW>
 __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix i0, double* side, double* tail,
-                               VtSmem<K>& sm) {
-  constexpr int NT = K / 8, NB = NT + 1;
-  const int lane = threadIdx.x & 31, rr = lane >> 2, q = lane & 3, c2 = 2 * q;
+                               VtSmem<K, NW>& sm) {
+  constexpr int NT = K / 8, NTH = 32 * NW, TPW = NT / NW, NWT = VtSmem<K, NW>::NWT;
+  static_assert(NT % NW == 0 && (NT / 2) % NW == 0, "warps must divide the tile rows");
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, rr = lane >> 2, q = lane & 3, c2 = 2 * q;
+  const int o0[2] = {sw8(rr, q), sw8(rr, 4 + q)}, o1[2] = {sw8(q, rr), sw8(4 + q, rr)};
+  const int oc = sw8(rr, c2);
   const Band<double>& L = C.l;
-  const Band<double>& S = C.s;
-  const Band<double>& SB = C.sb;
-  // Entering tiles are fetched raw with cp.async (lower triangle of a diagonal
-  // tile only) and completed after the wait: mirror, and the symmetric split
-  // (halving) of S-bar's off-diagonal cells.  Rows past n: Z identity, G zero.
-  auto issue = [&](double (*t)[9], const Band<double>& src, bool ident, ix b1, ix b2) {
-    for (int idx = lane; idx < 64; idx += 32) {
-      const int m = idx >> 3, c = idx & 7;
-      if (b1 == b2 && m < c) continue;
-      const ix r = 8 * b1 + m, col = 8 * b2 + c, cell = r - col;
-      if (cell <= K && r < n) cpa(&t[m][c], &src.cell(b, int(cell), col));
-      else t[m][c] = (ident && cell == 0) ? 1.0 : 0.0;
-    }
-  };
-  auto fix = [&](double (*t)[9], bool diag, bool half) {
-    double v[2];
+  auto mm = [&](double* acc, const double* X, bool tx, const double* Y, bool ty) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int idx = lane + 32 * h, m = idx >> 3, c = idx & 7;
-      const double x = (diag && m < c) ? t[c][m] : t[m][c];
-      v[h] = (half && m != c) || (half && !diag) ? 0.5 * x : x;
+    for (int kc = 0; kc < 2; ++kc) dmma(acc[0], acc[1], X[tx ? o1[kc] : o0[kc]], Y[ty ? o0[kc] : o1[kc]]);
+  };
+  auto put = [&](double* T, double v0, double v1) { *reinterpret_cast<double2*>(T + oc) = make_double2(v0, v1); };
+  auto get = [&](const double* T) { return *reinterpret_cast<const double2*>(T + oc); };
+  // element (m, c) of window tile (b1, b2) of the symmetric band X: cp.async of
+  // the lower-stored cell (a diagonal tile's upper half reads the mirror);
+  // rows past n are identity (Z) or zero (S-bar); halve: S-bar's symmetric split
+  auto elem = [&](double* T, const Band<double>& X, bool ident, ix b1, ix b2, int idx, bool fix) {
+    const int m = idx >> 3, c = idx & 7;
+    double* dst = T + sw8(m, c);
+    if (fix) {
+      if (b1 != b2 || m != c) *dst *= 0.5;
+      return;
     }
-    __syncwarp();
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int idx = lane + 32 * h;
-      t[idx >> 3][idx & 7] = v[h];
+    ix r = 8 * b1 + m, cc = 8 * b2 + c;
+    if (r < cc) {
+      const ix t = r;
+      r = cc;
+      cc = t;
+    }
+    const ix cell = r - cc;
+    if (r < n && cell <= K) cpa(dst, &X.cell(b, int(cell), cc));
+    else *dst = (ident && cell == 0) ? 1.0 : 0.0;
+  };
+  // W block row bn (tiles (bn, bn-d), d = 0..NT) / Z block row bn (d < NT)
+  auto w_row = [&](ix bn, bool fix) {
+    for (int x = tid; x < (NT + 1) * 64; x += NTH) {
+      const int d = x >> 6;
+      elem(sm.w[ring_slot<K>(d, bn - d)], C.sb, false, bn, bn - d, x & 63, fix);
     }
   };
-  auto issue_row = [&](ix bn) {  // block row bn: W tiles (bn, bn-NT .. bn), Z tiles (bn, bn-NT+1 .. bn)
-    for (int d = 0; d <= NT; ++d) issue(sm.w[wv_slot<K>(d, bn - d)], SB, false, bn, bn - d);
-    for (int d = 0; d < NT; ++d) issue(sm.z[tak_slot<K>(d, bn - d)], S, true, bn, bn - d);
+  auto z_row = [&](ix bn) {
+    for (int x = tid; x < NT * 64; x += NTH) {
+      const int d = x >> 6;
+      elem(sm.z[ring_slot<K>(d, bn - d)], C.s, true, bn, bn - d, x & 63, false);
+    }
   };
-  auto fix_row = [&](ix bn) {
-    for (int d = 0; d <= NT; ++d) fix(sm.w[wv_slot<K>(d, bn - d)], d == 0, true);
-    fix(sm.z[tak_slot<K>(0, bn)], true, false);
+  auto w_init = [&](ix pb, bool fix) {  // W blocks pb .. pb+NT
+    for (int x = tid; x < NWT * 64; x += NTH) {
+      int j = x >> 6, d = 0;
+      while (j > NT - d) j -= NT + 1 - d++;
+      elem(sm.w[ring_slot<K>(d, pb + j)], C.sb, false, pb + j + d, pb + j, x & 63, fix);
+    }
   };
   auto fill = [&](int buf, ix pb) {  // L rows [8pb, 8pb+K+8) x cols [8pb, 8pb+8), identity past n
-    for (int idx = lane; idx < 8 * (K + 8); idx += 32) {
-      const int c = idx / (K + 8), r = idx % (K + 8), cell = r - c;
+    for (int x = tid; x < 8 * (K + 8); x += NTH) {
+      const int c = x / (K + 8), r = x % (K + 8), cell = r - c;
       const ix col = 8 * pb + c, row = 8 * pb + r;
-      double* dst = &sm.lp[buf][r][c];
+      double* dst = sm.lp[buf] + sw8(r, c);
       if (cell >= 0 && cell <= K && col < n && row < n) cpa(dst, &L.cell(b, cell, col));
       else *dst = (cell == 0) ? 1.0 : 0.0;
     }
   };
-  auto save_w = [&](double* dst, ix pb) {  // window of panel pb: blocks pb .. pb + NT
-    for (int d = 0; d <= NT; ++d)
-      for (int j = 0; j + d <= NT; ++j) {
-        const double (*t)[9] = sm.w[wv_slot<K>(d, pb + j)];
-        double* o = dst + (d * NB - d * (d - 1) / 2 + j) * 64;
-        for (int idx = lane; idx < 64; idx += 32) o[idx] = t[idx >> 3][idx & 7];
-      }
+  auto save_w = [&](double* dst, ix pb) {  // window of panel pb, tiles in (d, j) order
+    for (int x = tid; x < NWT * 64; x += NTH) {
+      int j = x >> 6, d = 0;
+      while (j > NT - d) j -= NT + 1 - d++;
+      dst[x] = sm.w[ring_slot<K>(d, pb + j)][x & 63];
+    }
   };
   const ix pb0 = i0 / 8, pbe = (e + 7) / 8;
-  // initial window: W blocks pb0 .. pb0+NT, Z blocks pb0+1 .. pb0+NT
-  for (int t1 = 0; t1 <= NT; ++t1)
-    for (int t2 = 0; t2 <= t1; ++t2) {
-      issue(sm.w[wv_slot<K>(t1 - t2, pb0 + t2)], SB, false, pb0 + t1, pb0 + t2);
-      if (t2 >= 1) issue(sm.z[tak_slot<K>(t1 - t2, pb0 + t2)], S, true, pb0 + t1, pb0 + t2);
-    }
+  for (int x = tid; x < NT * NT * 64; x += NTH) {  // Z blocks pb0+1 .. pb0+NT (lower tiles)
+    const int t1 = x / (NT * 64), t2 = (x >> 6) % NT;
+    if (t2 <= t1) elem(sm.z[ring_slot<K>(t1 - t2, pb0 + 1 + t2)], C.s, true, pb0 + 1 + t1, pb0 + 1 + t2, x & 63, false);
+  }
+  w_init(pb0, false);
   fill(0, pb0);
   cpa_commit();
-  cpa_wait0();
-  __syncwarp();
-  for (int t1 = 0; t1 <= NT; ++t1) {
-    for (int t2 = 0; t2 <= t1; ++t2) fix(sm.w[wv_slot<K>(t1 - t2, pb0 + t2)], t1 == t2, true);
-    if (t1 >= 1) fix(sm.z[tak_slot<K>(0, pb0 + t1)], true, false);
-  }
-  __syncwarp();
   int buf = 0;
 #pragma unroll 1
   for (ix pb = pb0; pb < pbe; ++pb) {
-    if (pb > pb0) {
-      cpa_wait0();
-      __syncwarp();
-      fix_row(pb + NT);
-      __syncwarp();
+    cpa_wait0();
+    if (pb == pb0) w_init(pb0, true);
+    else w_row(pb + NT, true);
+    for (int x = tid; x < NT * NT; x += NTH) {
+      const int t = x / NT, u = x % NT;
+      sm.zs[x] = short(ring_slot<K>(t > u ? t - u : u - t, pb + 1 + (t < u ? t : u)));
     }
+    for (int x = tid; x < (NT + 1) * (NT + 1); x += NTH) {
+      const int t1 = x / (NT + 1), t2 = x % (NT + 1);
+      if (t1 >= t2) sm.ws[x] = short(ring_slot<K>(t1 - t2, pb + t2));
+    }
+    __syncthreads();
     if (side && pb == s / 8) save_w(side, pb);  // burn-in state at the segment start
+    z_row(pb + NT + 1);  // into the ring slots block pb has left
     if (pb + 1 < pbe) fill(buf ^ 1, pb + 1);
     cpa_commit();
-    const double (*lp)[9] = sm.lp[buf];
-    // Linv = L_PP^-1 (forward substitution in the fragment layout)
+    const double* lp = sm.lp[buf];
+    double* lin = sm.lin[warp];
+    // ---- (1) Linv (per warp), Y and Z_TP for the warp's tile rows
     {
       double M0 = rr == c2 ? 1.0 : 0.0, M1 = rr == c2 + 1 ? 1.0 : 0.0;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         if (rr == k) {
-          const double ri = 1.0 / lp[k][k];
+          const double ri = 1.0 / lp[sw8(k, k)];
           M0 *= ri;
           M1 *= ri;
         }
         const double mk0 = __shfl_sync(0xffffffffu, M0, 4 * k + q);
         const double mk1 = __shfl_sync(0xffffffffu, M1, 4 * k + q);
         if (rr > k) {
-          const double lrk = lp[rr][k];
+          const double lrk = lp[sw8(rr, k)];
           M0 = fma(-lrk, mk0, M0);
           M1 = fma(-lrk, mk1, M1);
         }
       }
-      sm.linv[rr][c2] = M0;
-      sm.linv[rr][c2 + 1] = M1;
+      put(lin, M0, M1);
     }
-    // Z_TT tile (t, u) of the window (blocks pb+1+t, pb+1+u): stored lower, transposed read above
-#define ZTT_MM(acc0, acc1, t, u, Yt)                                              \
-  do {                                                                              \
-    if ((t) >= (u)) tmm<false, false>(acc0, acc1, sm.z[tak_slot<K>((t) - (u), pb + 1 + (u))], Yt, 1.0, rr, q); \
-    else tmm<true, false>(acc0, acc1, sm.z[tak_slot<K>((u) - (t), pb + 1 + (t))], Yt, 1.0, rr, q);             \
-  } while (0)
-    // Y = Z_TT L_TP
     {
-      double ya[NT][2];
+      double ya[TPW][2];
 #pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        ya[t][0] = ya[t][1] = 0.0;
+      for (int i = 0; i < TPW; ++i) {
+        const int t = warp + NW * i;
+        ya[i][0] = ya[i][1] = 0.0;
 #pragma unroll
-        for (int u = 0; u < NT; ++u) ZTT_MM(ya[t][0], ya[t][1], t, u, lp + 8 + 8 * u);
+        for (int u = 0; u < NT; ++u) mm(ya[i], sm.z[sm.zs[t * NT + u]], t < u, lp + (8 + 8 * u) * 8, false);
       }
 #pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        sm.y[t][rr][c2] = ya[t][0];
-        sm.y[t][rr][c2 + 1] = ya[t][1];
+      for (int i = 0; i < TPW; ++i) put(sm.y[warp + NW * i], ya[i][0], ya[i][1]);
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) {
+        ya[i][0] = ya[i][1] = 0.0;
+        mm(ya[i], sm.y[warp + NW * i], false, lin, false);
       }
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) put(sm.zt[warp + NW * i], -ya[i][0], -ya[i][1]);
     }
-    __syncwarp();
-    // Z_TP = -Y Linv
-    {
-      double za[NT][2];
-#pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        za[t][0] = za[t][1] = 0.0;
-        tmm<false, false>(za[t][0], za[t][1], sm.y[t], sm.linv, -1.0, rr, q);
-      }
-#pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        sm.zt[t][rr][c2] = za[t][0];
-        sm.zt[t][rr][c2 + 1] = za[t][1];
-      }
-    }
-    __syncwarp();
-    // A = Linv - L_TP^T Z_TP (four independent accumulators)
+    __syncthreads();
+    // ---- (2) A = Linv - L_TP^T Z_TP; Ab = Linv Zb_PP^T; Linvb0 = A Zb_PP + Ab (per warp)
+    double lvb[2];
     {
       double h[4][2] = {};
 #pragma unroll
-      for (int t = 0; t < NT; ++t) tmm<true, false>(h[t & 3][0], h[t & 3][1], lp + 8 + 8 * t, sm.zt[t], 1.0, rr, q);
-      sm.am[rr][c2] = sm.linv[rr][c2] - (h[0][0] + h[1][0]) - (h[2][0] + h[3][0]);
-      sm.am[rr][c2 + 1] = sm.linv[rr][c2 + 1] - (h[0][1] + h[1][1]) - (h[2][1] + h[3][1]);
+      for (int t = 0; t < NT; ++t) mm(h[t & 3], lp + (8 + 8 * t) * 8, true, sm.zt[t], false);
+      const double2 l2 = get(lin);
+      put(sm.am[warp], l2.x - ((h[0][0] + h[1][0]) + (h[2][0] + h[3][0])),
+          l2.y - ((h[0][1] + h[1][1]) + (h[2][1] + h[3][1])));
+      __syncwarp();
+      const double* wpp = sm.w[sm.ws[0]];
+      double a[2] = {0.0, 0.0}, v[2] = {0.0, 0.0};
+      mm(a, lin, false, wpp, true);
+      mm(v, sm.am[warp], false, wpp, false);
+      lvb[0] = v[0] + a[0];
+      lvb[1] = v[1] + a[1];
+      put(sm.ab[warp], a[0], a[1]);
+      __syncwarp();
     }
-    __syncwarp();
-    // Ab = Linv Zb_PP^T; Linvb = A Zb_PP + Ab; Hb = -Ab
+    // ---- (3) per tile row: G = L_TP Ab - 2 W(T,P) (= -Zb_TP), Z_TP Ab^T (= -Ltpb part),
+    //          Linvb partial sum Y^T G, Yh = G Linv^T / 2 (= Yb / 2)
+    double la[TPW][2];
     {
-      const double (*wpp)[9] = sm.w[wv_slot<K>(0, pb)];
-      double a0 = 0.0, a1 = 0.0, v0 = 0.0, v1 = 0.0;
-      tmm<false, true>(a0, a1, sm.linv, wpp, 1.0, rr, q);
-      tmm<false, false>(v0, v1, sm.am, wpp, 1.0, rr, q);
-      sm.lvb[rr][c2] = v0 + a0;
-      sm.lvb[rr][c2 + 1] = v1 + a1;
-      sm.hb[rr][c2] = -a0;
-      sm.hb[rr][c2 + 1] = -a1;
-    }
-    __syncwarp();
-    // Ltpb = Z_TP Hb^T; Zb_TP = 2 W(T,P) + L_TP Hb
-    {
-      double la[NT][2], za[NT][2];
+      double g[TPW][2], pa[2] = {0.0, 0.0};
 #pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        const double (*wtp)[9] = sm.w[wv_slot<K>(t + 1, pb)];
-        la[t][0] = la[t][1] = 0.0;
-        za[t][0] = 2.0 * wtp[rr][c2];
-        za[t][1] = 2.0 * wtp[rr][c2 + 1];
-        tmm<false, true>(la[t][0], la[t][1], sm.zt[t], sm.hb, 1.0, rr, q);
-        tmm<false, false>(za[t][0], za[t][1], lp + 8 + 8 * t, sm.hb, 1.0, rr, q);
+      for (int i = 0; i < TPW; ++i) {
+        const int t = warp + NW * i;
+        la[i][0] = la[i][1] = 0.0;
+        mm(la[i], sm.zt[t], false, sm.ab[warp], true);
+        const double2 w2 = get(sm.w[sm.ws[(t + 1) * (NT + 1)]]);
+        g[i][0] = -2.0 * w2.x;
+        g[i][1] = -2.0 * w2.y;
+        mm(g[i], lp + (8 + 8 * t) * 8, false, sm.ab[warp], false);
       }
 #pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        sm.lt[t][rr][c2] = la[t][0];
-        sm.lt[t][rr][c2 + 1] = la[t][1];
-        sm.yb[t][rr][c2] = za[t][0];
-        sm.yb[t][rr][c2 + 1] = za[t][1];
-      }
-    }
-    __syncwarp();
-    // block row pb+NT+1 enters W into the slots of the leaving column pb (free from here on)
-    for (int d = 0; d <= NT; ++d) issue(sm.w[wv_slot<K>(d, pb)], SB, false, pb + NT + 1, pb + NT + 1 - d);
-    cpa_commit();
-    // Linvb -= Y^T Zb_TP; Yb = -Zb_TP Linv^T
-    {
-      double h[4][2] = {};
+      for (int i = 0; i < TPW; ++i) put(sm.yb[warp + NW * i], g[i][0], g[i][1]);
+      __syncwarp();
 #pragma unroll
-      for (int t = 0; t < NT; ++t) tmm<true, false>(h[t & 3][0], h[t & 3][1], sm.y[t], sm.yb[t], 1.0, rr, q);
-      double ya[NT][2];
-#pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        ya[t][0] = ya[t][1] = 0.0;
-        tmm<false, true>(ya[t][0], ya[t][1], sm.yb[t], sm.linv, -1.0, rr, q);
+      for (int i = 0; i < TPW; ++i) {
+        const int t = warp + NW * i;
+        mm(pa, sm.y[t], true, sm.yb[t], false);
+        g[i][0] = g[i][1] = 0.0;
+        mm(g[i], sm.yb[t], false, lin, true);
       }
       __syncwarp();
-      sm.lvb[rr][c2] -= (h[0][0] + h[1][0]) + (h[2][0] + h[3][0]);
-      sm.lvb[rr][c2 + 1] -= (h[0][1] + h[1][1]) + (h[2][1] + h[3][1]);
 #pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        sm.yb[t][rr][c2] = ya[t][0];
-        sm.yb[t][rr][c2 + 1] = ya[t][1];
-      }
+      for (int i = 0; i < TPW; ++i) put(sm.yb[warp + NW * i], 0.5 * g[i][0], 0.5 * g[i][1]);
+      put(sm.part[warp], pa[0], pa[1]);
     }
-    __syncwarp();
-    // Ltpb += Z_TT Yb -> L-bar rows 8pb+8+8t+rr, columns 8pb+c2+v (band cells <= K)
-    {
-      double la[NT][2];
-#pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        la[t][0] = sm.lt[t][rr][c2];
-        la[t][1] = sm.lt[t][rr][c2 + 1];
-#pragma unroll
-        for (int u = 0; u < NT; ++u) ZTT_MM(la[t][0], la[t][1], t, u, sm.yb[u]);
-      }
-#pragma unroll
-      for (int t = 0; t < NT; ++t)
-#pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          const ix col = 8 * pb + c2 + v;
-          const int cell = 8 + 8 * t + rr - c2 - v;
-          if (col >= s && col < e && cell <= K) C.lb.cell(b, cell, col) = (col + cell < n) ? la[t][v] : 0.0;
-        }
-    }
-#undef ZTT_MM
-    __syncwarp();
-    // block row pb+NT+1 enters Z into the slots of the leaving column pb+1
-    for (int d = 0; d < NT; ++d) issue(sm.z[tak_slot<K>(d, pb + 1)], S, true, pb + NT + 1, pb + NT + 1 - d);
+    __syncthreads();
+    // ---- (4) W block row pb+NT+1 enters the slots of column pb (read for the last time above)
+    w_row(pb + NT + 1, false);
     cpa_commit();
-    // W(T,T) += (Yb L_TP^T + L_TP Yb^T) / 2: rows t and NT-1-t paired (NT+1 tiles per pass)
+    // Ltpb = -Z_TP Ab^T + 2 Z_TT Yh -> L-bar rows 8pb+8+8t+rr, columns 8pb+c2+v
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) {
+      const int t = warp + NW * i;
+      double acc[2] = {-0.5 * la[i][0], -0.5 * la[i][1]};
+#pragma unroll
+      for (int u = 0; u < NT; ++u) mm(acc, sm.z[sm.zs[t * NT + u]], t < u, sm.yb[u], false);
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const ix col = 8 * pb + c2 + v;
+        const int cell = 8 + 8 * t + rr - c2 - v;
+        if (col >= s && col < e && cell <= K) C.lb.cell(b, cell, col) = (col + cell < n) ? 2.0 * acc[v] : 0.0;
+      }
+    }
+    // W(T,T) += Yh L_TP^T + L_TP Yh^T: tile rows pp and NT-1-pp together (NT+1 tiles)
 #pragma unroll 1
-    for (int pp = 0; pp < NT / 2; ++pp) {
+    for (int pp = warp; pp < NT / 2; pp += NW) {
       double wa[NT + 1][2];
 #pragma unroll
       for (int j = 0; j <= NT; ++j) {
         const int t1 = j <= pp ? pp : NT - 1 - pp, t2 = j <= pp ? j : j - pp - 1;
-        const double (*wt)[9] = sm.w[wv_slot<K>(t1 - t2, pb + 1 + t2)];
-        wa[j][0] = wt[rr][c2];
-        wa[j][1] = wt[rr][c2 + 1];
-        tmm<false, true>(wa[j][0], wa[j][1], sm.yb[t1], lp + 8 + 8 * t2, 0.5, rr, q);
-        tmm<false, true>(wa[j][0], wa[j][1], lp + 8 + 8 * t1, sm.yb[t2], 0.5, rr, q);
+        const double2 w2 = get(sm.w[sm.ws[(t1 + 1) * (NT + 1) + t2 + 1]]);
+        wa[j][0] = w2.x;
+        wa[j][1] = w2.y;
+        mm(wa[j], sm.yb[t1], false, lp + (8 + 8 * t2) * 8, true);
+        mm(wa[j], lp + (8 + 8 * t1) * 8, false, sm.yb[t2], true);
       }
 #pragma unroll
       for (int j = 0; j <= NT; ++j) {
         const int t1 = j <= pp ? pp : NT - 1 - pp, t2 = j <= pp ? j : j - pp - 1;
-        double (*wt)[9] = sm.w[wv_slot<K>(t1 - t2, pb + 1 + t2)];
-        wt[rr][c2] = wa[j][0];
-        wt[rr][c2 + 1] = wa[j][1];
+        put(sm.w[sm.ws[(t1 + 1) * (NT + 1) + t2 + 1]], wa[j][0], wa[j][1]);
       }
     }
-    // Lppb = -Linv^T (Linvb Linv^T), lower part
-    {
-      double t0 = 0.0, t1 = 0.0;
-      tmm<false, true>(t0, t1, sm.lvb, sm.linv, 1.0, rr, q);
-      sm.ab[rr][c2] = t0;
-      sm.ab[rr][c2 + 1] = t1;
+    // Lppb = -Linv^T (Linvb Linv^T), Linvb = Linvb0 + sum of the warps' partials
+    if (warp == NW - 1) {
+#pragma unroll
+      for (int w2 = 0; w2 < NW; ++w2) {
+        const double2 p2 = get(sm.part[w2]);
+        lvb[0] += p2.x;
+        lvb[1] += p2.y;
+      }
+      put(sm.am[warp], lvb[0], lvb[1]);
       __syncwarp();
-      double p0 = 0.0, p1 = 0.0;
-      tmm<true, false>(p0, p1, sm.linv, sm.ab, -1.0, rr, q);
+      double t2[2] = {0.0, 0.0};
+      mm(t2, sm.am[warp], false, lin, true);
+      put(sm.ab[warp], t2[0], t2[1]);
+      __syncwarp();
+      double p2[2] = {0.0, 0.0};
+      mm(p2, lin, true, sm.ab[warp], false);
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const ix col = 8 * pb + c2 + v;
         const int cell = rr - c2 - v;
-        if (col >= s && col < e && cell >= 0) C.lb.cell(b, cell, col) = (col + cell < n) ? (v ? p1 : p0) : 0.0;
+        if (col >= s && col < e && cell >= 0) C.lb.cell(b, cell, col) = (col + cell < n) ? -p2[v] : 0.0;
       }
     }
-    __syncwarp();
+    __syncthreads();
     buf ^= 1;
   }
   cpa_wait0();
-  __syncwarp();
-  fix_row(pbe + NT);
-  __syncwarp();
+  w_row(pbe + NT, true);
+  __syncthreads();
   if (tail) save_w(tail, pbe);  // genuine state the next segment's burn-in must reproduce
 }
 
-template <int K>
-__global__ void __launch_bounds__(32) k_vsub_dmma(VsP<double> C, Geo G) {
+template <int K, int NW>
+__global__ void __launch_bounds__(32 * NW) k_vsub_dmma(VsP<double> C, Geo G) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  VtSmem<K>& sm = *reinterpret_cast<VtSmem<K>*>(smraw);
-  constexpr int NB = K / 8 + 1, STATE = NB * (NB + 1) / 2 * 64;
+  VtSmem<K, NW>& sm = *reinterpret_cast<VtSmem<K, NW>*>(smraw);
+  constexpr int STATE = VtSmem<K, NW>::NWT * 64;
   const ix unit = blockIdx.x;
   const ix b = unit / G.nseg;
   const int p = int(unit % G.nseg);
@@ -2004,13 +1976,13 @@ __global__ void __launch_bounds__(32) k_vsub_dmma(VsP<double> C, Geo G) {
   ix i0 = s - G.burn;
   if (i0 < 0) i0 = 0;
   i0 -= i0 % 8;
-  vsub_dmma_unit<K>(C, b, G.n, s, e, i0, p > 0 ? C.side + unit * ix(STATE) : nullptr,
-                    p + 1 < G.nseg ? C.tail + unit * ix(STATE) : nullptr, sm);
+  vsub_dmma_unit<K, NW>(C, b, G.n, s, e, i0, p > 0 ? C.side + unit * ix(STATE) : nullptr,
+                        p + 1 < G.nseg ? C.tail + unit * ix(STATE) : nullptr, sm);
 }
 
-template <int K>
+template <int K, int NW>
 __global__ void k_vsub_dmma_check(VsP<double> C, Geo G) {
-  constexpr int NB = K / 8 + 1, STATE = NB * (NB + 1) / 2 * 64;
+  constexpr int STATE = VtSmem<K, NW>::NWT * 64;
   const ix id = (blockIdx.x * ix(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (id >= G.batch * G.nseg) return;
@@ -2028,13 +2000,13 @@ __global__ void k_vsub_dmma_check(VsP<double> C, Geo G) {
   if (bad && lane == 0) C.flag[id / G.nseg] = 1;
 }
 
-template <int K>
-__global__ void __launch_bounds__(32) k_vsub_dmma_repair(VsP<double> C, Geo G) {
+template <int K, int NW>
+__global__ void __launch_bounds__(32 * NW) k_vsub_dmma_repair(VsP<double> C, Geo G) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  VtSmem<K>& sm = *reinterpret_cast<VtSmem<K>*>(smraw);
+  VtSmem<K, NW>& sm = *reinterpret_cast<VtSmem<K, NW>*>(smraw);
   const ix b = blockIdx.x;
   if (b >= G.batch || !C.flag[b]) return;
-  vsub_dmma_unit<K>(C, b, G.n, 0, G.n, 0, nullptr, nullptr, sm);
+  vsub_dmma_unit<K, NW>(C, b, G.n, 0, G.n, 0, nullptr, nullptr, sm);
 }
 
 int g_segment_rows = 0;
@@ -2195,18 +2167,38 @@ bool run_chol_dmma(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* r
   return true;
 }
 
+// segments per matrix: fill the resident CTA slots in whole waves, burn-in
+// overhead counted (the k_vsub_dmma grid is one short launch)
+inline int pick_nseg(ix batch, ix n, int slots, int burn, int seg_min) {
+  int best = 1;
+  double best_eff = 0.0;
+  for (int ns = 1; ns <= 256; ++ns) {
+    const ix seg = (n + ns - 1) / ns;
+    if (ns > 1 && seg < seg_min) break;
+    const double units = double(batch) * ns;
+    const double waves = std::ceil(units / slots);
+    const double eff = units / (waves * slots) * double(seg) / double(seg + (ns > 1 ? burn : 0));
+    if (eff > best_eff * 1.0001) {
+      best_eff = eff;
+      best = ns;
+    }
+  }
+  return best;
+}
+
 template <int K>
 bool run_vsub_dmma(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, const bgm_band& lb, int32_t* st,
                    int64_t* row, cudaStream_t s) {
-  const size_t smem = sizeof(VtSmem<K>);
+  constexpr int NW = 4;
+  const size_t smem = sizeof(VtSmem<K, NW>);
   if (smem > 227 * 1024) return false;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_vsub_dmma<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    cudaFuncSetAttribute(k_vsub_dmma_repair<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_vsub_dmma<K, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_vsub_dmma_repair<K, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     attr = true;
   }
-  constexpr int NB = K / 8 + 1, STATE = NB * (NB + 1) / 2 * 64;
+  constexpr int STATE = VtSmem<K, NW>::NWT * 64;
   Geo G;
   G.batch = l.batch;
   G.n = l.n;
@@ -2215,14 +2207,12 @@ bool run_vsub_dmma(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, co
     if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
   int sms = 148, dev = 0, per = 1;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_vsub_dmma<K>, 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_vsub_dmma<K, NW>, 32 * NW, smem);
   if (per < 1) per = 1;
   ix seg = g_segment_rows;
   if (seg <= 0) {
-    ix nseg = ix(sms) * per / (G.batch > 0 ? G.batch : 1);
-    if (nseg < 1) nseg = 1;
-    seg = (G.n + nseg - 1) / nseg;
-    if (seg < 2 * ix(G.burn)) seg = 2 * ix(G.burn);
+    const int ns = pick_nseg(G.batch, G.n, sms * per, G.burn, 2 * G.burn);
+    seg = (G.n + ns - 1) / ns;
   }
   seg = (seg + 7) / 8 * 8;
   G.seg = seg;
@@ -2245,15 +2235,15 @@ bool run_vsub_dmma(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, co
   k_diag_check<double><<<blocks_for(G.batch * G.n, 256), 256, 0, s>>>(C.l, G.batch, fail);
   {
     timing::Scope ts("wide_vjp_subset_dmma", s);
-    k_vsub_dmma<K><<<unsigned(units), 32, smem, s>>>(C, G);
+    k_vsub_dmma<K, NW><<<unsigned(units), 32 * NW, smem, s>>>(C, G);
   }
   {
     timing::Scope ts("wide_vjp_subset_check", s);
-    k_vsub_dmma_check<K><<<blocks_for(units * 32, 128), 128, 0, s>>>(C, G);
+    k_vsub_dmma_check<K, NW><<<blocks_for(units * 32, 128), 128, 0, s>>>(C, G);
   }
   {
     timing::Scope ts("wide_vjp_subset_repair", s);
-    k_vsub_dmma_repair<K><<<unsigned(G.batch), 32, smem, s>>>(C, G);
+    k_vsub_dmma_repair<K, NW><<<unsigned(G.batch), 32 * NW, smem, s>>>(C, G);
   }
   const ix zw = ((G.batch + l.tile - 1) / l.tile * l.tile) * K * (K + 1);
   k_zero_corners_w<double><<<blocks_for(zw, 128), 128, 0, s>>>(C.lb, G.batch);
