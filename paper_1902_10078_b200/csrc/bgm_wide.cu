@@ -2009,6 +2009,267 @@ __global__ void __launch_bounds__(32 * NW) k_vsub_dmma_repair(VsP<double> C, Geo
   vsub_dmma_unit<K, NW>(C, b, G.n, 0, G.n, 0, nullptr, nullptr, sm);
 }
 
+// ------------------------------------------------------------------ vjp_cholesky, FP64 DMMA
+// Blocked reverse of the banded Cholesky (the scalar recursion is
+// grad.cpp:20-36), panels of 8 columns from the bottom up.  With Abar the
+// lower-stored adjoint of Q and G its symmetric split (G = (Abar + Abar^T)/2
+// off the diagonal, Abar_ii on it), the forward panel step
+//   L_PP = chol(A_PP)   L_TP = A_TP L_PP^-T   A_TT -= L_TP L_TP^T
+// reverses to
+//   Lb_TP = Lbar_TP - 2 G_TT L_TP        Abar_TP = Lb_TP L_PP^-1
+//   Lb_PP = tril(Lbar_PP - Abar_TP^T L_TP)
+//   S = L_PP^-T Phi(L_PP^T Lb_PP) L_PP^-1  (Phi: lower part, halved diagonal)
+//   Abar_PP = tril(S + S^T) with diagonal S_ii, i.e. G_PP = (S + S^T) / 2,
+// where G_TT holds only q-bar cells already produced by the panels below.
+// One CTA of NW warps per (matrix, segment); warps own the tile rows
+// t = warp (mod NW), the 8x8 panel algebra runs on the last warp.  G lives
+// in diagonal rings of swizzled 8x8 tiles (see k_vsub_dmma); each panel
+// writes its new tile column into slots no warp reads during the panel.
+template <class T>
+struct VdP {
+  Band<T> l, lb, qb;
+  T* side;  // [unit][NT(NT+1)/2][64] G window entering the segment's first panel (burn-in)
+  T* tail;  // the same after the segment's last panel (genuine)
+  int32_t* flag;
+};
+
+template <int K, int NW>
+struct VdSmem {
+  static constexpr int NT = K / 8;
+  static constexpr int NZ = NT * (NT + 3) / 2;  // rings, diagonal d holds NT+1-d tiles
+  double g[NZ][64];
+  double lp[2][(K + 8) * 8];
+  double lt[NT][64];
+  double lin[NW][64], part[NW][64];
+  double s1[64], s2[64];
+  short zs[NT * NT];
+};
+
+template <int K, int NW>
+__device__ void vchol_dmma_unit(const VdP<double>& C, ix b, ix n, ix s, ix e, ix iend, double* side, double* tail,
+                                VdSmem<K, NW>& sm) {
+  constexpr int NT = K / 8, NTH = 32 * NW, TPW = NT / NW, NST = NT * (NT + 1) / 2;
+  static_assert(NT % NW == 0, "warps must divide the tile rows");
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, rr = lane >> 2, q = lane & 3, c2 = 2 * q;
+  const int o0[2] = {sw8(rr, q), sw8(rr, 4 + q)}, o1[2] = {sw8(q, rr), sw8(4 + q, rr)};
+  const int oc = sw8(rr, c2);
+  const Band<double>& L = C.l;
+  auto mm = [&](double* acc, const double* X, bool tx, const double* Y, bool ty) {
+#pragma unroll
+    for (int kc = 0; kc < 2; ++kc) dmma(acc[0], acc[1], X[tx ? o1[kc] : o0[kc]], Y[ty ? o0[kc] : o1[kc]]);
+  };
+  auto put = [&](double* Tt, double v0, double v1) { *reinterpret_cast<double2*>(Tt + oc) = make_double2(v0, v1); };
+  auto fill = [&](int buf, ix pb) {  // L rows [8pb, 8pb+K+8) x cols [8pb, 8pb+8), identity past n
+    for (int x = tid; x < 8 * (K + 8); x += NTH) {
+      const int c = x / (K + 8), r = x % (K + 8), cell = r - c;
+      const ix col = 8 * pb + c, row = 8 * pb + r;
+      double* dst = sm.lp[buf] + sw8(r, c);
+      if (cell >= 0 && cell <= K && col < n && row < n) cpa(dst, &L.cell(b, cell, col));
+      else *dst = (cell == 0) ? 1.0 : 0.0;
+    }
+  };
+  // l-bar fragments of panel pb: rows 8pb+8+8t+rr (own t) and 8pb+rr, columns 8pb+c2+v
+  auto load_lb = [&](ix pb, double (*ft)[2], double* fp) {
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const ix col = 8 * pb + c2 + v;
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) {
+        const int cell = 8 + 8 * (warp + NW * i) + rr - c2 - v;
+        ft[i][v] = (pb >= 0 && cell <= K && col + cell < n) ? C.lb.cell(b, cell, col) : 0.0;
+      }
+      const int cell = rr - c2 - v;
+      fp[v] = (pb >= 0 && cell >= 0 && col + cell < n) ? C.lb.cell(b, cell, col) : 0.0;
+    }
+  };
+  auto save_g = [&](double* dst, ix b0) {  // window blocks b0 .. b0+NT-1, tiles in (d, j) order
+    for (int x = tid; x < NST * 64; x += NTH) {
+      int j = x >> 6, d = 0;
+      while (j > NT - 1 - d) j -= NT - d++;
+      dst[x] = sm.g[ring_slot<K>(d, b0 + j)][x & 63];
+    }
+  };
+  const ix pb_top = (iend + 7) / 8 - 1, pb_end = s / 8;
+  for (int x = tid; x < VdSmem<K, NW>::NZ * 64; x += NTH) (&sm.g[0][0])[x] = 0.0;
+  fill(0, pb_top);
+  cpa_commit();
+  double lbt[TPW][2], lbp[2];
+  load_lb(pb_top, lbt, lbp);
+  int buf = 0;
+#pragma unroll 1
+  for (ix pb = pb_top; pb >= pb_end; --pb) {
+    cpa_wait0();
+    for (int x = tid; x < NT * NT; x += NTH) {
+      const int t = x / NT, u = x % NT;
+      sm.zs[x] = short(ring_slot<K>(t > u ? t - u : u - t, pb + 1 + (t < u ? t : u)));
+    }
+    __syncthreads();
+    if (side && 8 * (pb + 1) == e) save_g(side, pb + 1);  // burn-in state entering the segment
+    if (pb > pb_end) fill(buf ^ 1, pb - 1);
+    cpa_commit();
+    double nbt[TPW][2], nbp[2];
+    load_lb(pb > pb_end ? pb - 1 : -1, nbt, nbp);
+    const double* lp = sm.lp[buf];
+    double* lin = sm.lin[warp];
+    {  // Linv (per warp)
+      double M0 = rr == c2 ? 1.0 : 0.0, M1 = rr == c2 + 1 ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (rr == k) {
+          const double ri = 1.0 / lp[sw8(k, k)];
+          M0 *= ri;
+          M1 *= ri;
+        }
+        const double mk0 = __shfl_sync(0xffffffffu, M0, 4 * k + q);
+        const double mk1 = __shfl_sync(0xffffffffu, M1, 4 * k + q);
+        if (rr > k) {
+          const double lrk = lp[sw8(rr, k)];
+          M0 = fma(-lrk, mk0, M0);
+          M1 = fma(-lrk, mk1, M1);
+        }
+      }
+      put(lin, M0, M1);
+    }
+    // Lb_TP = Lbar_TP - 2 G_TT L_TP (own tile rows)
+    {
+      double ga[TPW][2];
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) {
+        const int t = warp + NW * i;
+        ga[i][0] = ga[i][1] = 0.0;
+#pragma unroll
+        for (int u = 0; u < NT; ++u) mm(ga[i], sm.g[sm.zs[t * NT + u]], t < u, lp + (8 + 8 * u) * 8, false);
+      }
+#pragma unroll
+      for (int i = 0; i < TPW; ++i)
+        put(sm.lt[warp + NW * i], fma(-2.0, ga[i][0], lbt[i][0]), fma(-2.0, ga[i][1], lbt[i][1]));
+    }
+    __syncwarp();
+    // Abar_TP = Lb_TP Linv -> q-bar cells, G column (halved), and the partial Abar_TP^T L_TP
+    {
+      double aa[TPW][2];
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) {
+        aa[i][0] = aa[i][1] = 0.0;
+        mm(aa[i], sm.lt[warp + NW * i], false, lin, false);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) {
+        const int t = warp + NW * i;
+        put(sm.lt[t], aa[i][0], aa[i][1]);
+        if (t + 1 < NT) put(sm.g[ring_slot<K>(t + 1, pb)], 0.5 * aa[i][0], 0.5 * aa[i][1]);
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const ix col = 8 * pb + c2 + v;
+          const int cell = 8 + 8 * t + rr - c2 - v;
+          if (col >= s && col < e && cell <= K) C.qb.cell(b, cell, col) = (col + cell < n) ? aa[i][v] : 0.0;
+        }
+      }
+      __syncwarp();
+      double pa[2] = {0.0, 0.0};
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) {
+        const int t = warp + NW * i;
+        mm(pa, sm.lt[t], true, lp + (8 + 8 * t) * 8, false);
+      }
+      put(sm.part[warp], pa[0], pa[1]);
+    }
+    __syncthreads();
+    if (warp == NW - 1) {
+      // Lb_PP = tril(Lbar_PP - sum of partials); X = L_PP^T Lb_PP; Phi
+      double x0 = lbp[0], x1 = lbp[1];
+#pragma unroll
+      for (int w2 = 0; w2 < NW; ++w2) {
+        const double2 p2 = *reinterpret_cast<const double2*>(sm.part[w2] + oc);
+        x0 -= p2.x;
+        x1 -= p2.y;
+      }
+      put(sm.s1, c2 <= rr ? x0 : 0.0, c2 + 1 <= rr ? x1 : 0.0);
+      __syncwarp();
+      double xa[2] = {0.0, 0.0};
+      mm(xa, lp, true, sm.s1, false);
+      put(sm.s2, c2 < rr ? xa[0] : (c2 == rr ? 0.5 * xa[0] : 0.0),
+          c2 + 1 < rr ? xa[1] : (c2 + 1 == rr ? 0.5 * xa[1] : 0.0));
+      __syncwarp();
+      double ya[2] = {0.0, 0.0};  // Phi Linv
+      mm(ya, sm.s2, false, lin, false);
+      put(sm.s1, ya[0], ya[1]);
+      __syncwarp();
+      double sa[2] = {0.0, 0.0};  // S = Linv^T (Phi Linv)
+      mm(sa, lin, true, sm.s1, false);
+      put(sm.s2, sa[0], sa[1]);
+      __syncwarp();
+      double gp[2];
+#pragma unroll
+      for (int v = 0; v < 2; ++v) gp[v] = 0.5 * (sa[v] + sm.s2[sw8(c2 + v, rr)]);
+      put(sm.g[ring_slot<K>(0, pb)], gp[0], gp[1]);
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const ix col = 8 * pb + c2 + v;
+        const int cell = rr - c2 - v;
+        if (col >= s && col < e && cell >= 0)
+          C.qb.cell(b, cell, col) = (col + cell < n) ? (cell == 0 ? sa[v] : 2.0 * gp[v]) : 0.0;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) {
+      lbt[i][0] = nbt[i][0];
+      lbt[i][1] = nbt[i][1];
+    }
+    lbp[0] = nbp[0];
+    lbp[1] = nbp[1];
+    buf ^= 1;
+  }
+  cpa_wait0();
+  if (tail) save_g(tail, pb_end);  // genuine state leaving the segment's first column block
+}
+
+template <int K, int NW>
+__global__ void __launch_bounds__(32 * NW) k_vchol_dmma(VdP<double> C, Geo G) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  VdSmem<K, NW>& sm = *reinterpret_cast<VdSmem<K, NW>*>(smraw);
+  constexpr int NT = K / 8, STATE = NT * (NT + 1) / 2 * 64;
+  const ix unit = blockIdx.x;
+  const ix b = unit / G.nseg;
+  const int p = int(unit % G.nseg);
+  if (b >= G.batch) return;
+  const ix s = ix(p) * G.seg, e = s + G.seg < G.n ? s + G.seg : G.n;
+  const ix iend = e + G.burn < G.n ? e + G.burn : G.n;
+  vchol_dmma_unit<K, NW>(C, b, G.n, s, e, iend, p + 1 < G.nseg ? C.side + unit * ix(STATE) : nullptr,
+                         p > 0 ? C.tail + unit * ix(STATE) : nullptr, sm);
+}
+
+template <int K, int NW>
+__global__ void k_vchol_dmma_check(VdP<double> C, Geo G) {
+  constexpr int NT = K / 8, STATE = NT * (NT + 1) / 2 * 64;
+  const ix id = (blockIdx.x * ix(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (id >= G.batch * G.nseg) return;
+  const int p = int(id % G.nseg);
+  if (p + 1 >= G.nseg) return;
+  const double* a = C.side + id * ix(STATE);
+  const double* r = C.tail + (id + 1) * ix(STATE);
+  double sc = 0.0;
+  for (int i = lane; i < STATE; i += 32) sc = fmax(sc, fabs(r[i]));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sc = fmax(sc, __shfl_xor_sync(0xffffffffu, sc, o));
+  bool bad = false;
+  for (int i = lane; i < STATE; i += 32) bad |= !(fabs(a[i] - r[i]) <= kCheckTol * (sc + 1e-300));
+  bad = __any_sync(0xffffffffu, bad);
+  if (bad && lane == 0) C.flag[id / G.nseg] = 1;
+}
+
+template <int K, int NW>
+__global__ void __launch_bounds__(32 * NW) k_vchol_dmma_repair(VdP<double> C, Geo G) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  VdSmem<K, NW>& sm = *reinterpret_cast<VdSmem<K, NW>*>(smraw);
+  const ix b = blockIdx.x;
+  if (b >= G.batch || !C.flag[b]) return;
+  vchol_dmma_unit<K, NW>(C, b, G.n, 0, G.n, G.n, nullptr, nullptr, sm);
+}
+
 int g_segment_rows = 0;
 
 template <class T, int K, int P, int TS>
@@ -2248,6 +2509,65 @@ bool run_vsub_dmma(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, co
   const ix zw = ((G.batch + l.tile - 1) / l.tile * l.tile) * K * (K + 1);
   k_zero_corners_w<double><<<blocks_for(zw, 128), 128, 0, s>>>(C.lb, G.batch);
   k_status_code<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, G.batch, G.n, BGM_ERR_SINGULAR, st, row);
+  scratch_free(ws, s);
+  return true;
+}
+
+template <int K>
+bool run_vchol_dmma(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cudaStream_t s) {
+  constexpr int NW = K >= 128 ? 4 : 2, NT = K / 8, STATE = NT * (NT + 1) / 2 * 64;
+  const size_t smem = sizeof(VdSmem<K, NW>);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_vchol_dmma<K, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_vchol_dmma_repair<K, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = true;
+  }
+  Geo G;
+  G.batch = l.batch;
+  G.n = l.n;
+  G.burn = kBurnGen * K;
+  if (const char* bv = std::getenv("BGM_WIDE_BURN"))
+    if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
+  int sms = 148, dev = 0, per = 1;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_vchol_dmma<K, NW>, 32 * NW, smem);
+  if (per < 1) per = 1;
+  ix seg = g_segment_rows;
+  if (seg <= 0) {
+    const int ns = pick_nseg(G.batch, G.n, sms * per, G.burn, 2 * G.burn);
+    seg = (G.n + ns - 1) / ns;
+  }
+  seg = (seg + 7) / 8 * 8;
+  G.seg = seg;
+  G.nseg = int((G.n + seg - 1) / seg);
+  const ix units = G.batch * G.nseg;
+  const size_t sb_bytes = sizeof(double) * size_t(units) * STATE;
+  char* ws = nullptr;
+  if (scratch_alloc(reinterpret_cast<void**>(&ws), 2 * sb_bytes + 4 * size_t(G.batch) + 64, s) != cudaSuccess)
+    return false;
+  VdP<double> C;
+  C.l = view<double>(l);
+  C.lb = view<double>(lb);
+  C.qb = view<double>(qb);
+  C.side = reinterpret_cast<double*>(ws);
+  C.tail = reinterpret_cast<double*>(ws + sb_bytes);
+  C.flag = reinterpret_cast<int32_t*>(ws + 2 * sb_bytes);
+  cudaMemsetAsync(C.flag, 0, sizeof(int32_t) * size_t(G.batch), s);
+  {
+    timing::Scope ts("wide_vjp_chol_dmma", s);
+    k_vchol_dmma<K, NW><<<unsigned(units), 32 * NW, smem, s>>>(C, G);
+  }
+  {
+    timing::Scope ts("wide_vjp_chol_check", s);
+    k_vchol_dmma_check<K, NW><<<blocks_for(units * 32, 128), 128, 0, s>>>(C, G);
+  }
+  {
+    timing::Scope ts("wide_vjp_chol_repair", s);
+    k_vchol_dmma_repair<K, NW><<<unsigned(G.batch), 32 * NW, smem, s>>>(C, G);
+  }
+  const ix zw = ((G.batch + l.tile - 1) / l.tile * l.tile) * K * (K + 1);
+  k_zero_corners_w<double><<<blocks_for(zw, 128), 128, 0, s>>>(C.qb, G.batch);
   scratch_free(ws, s);
   return true;
 }
@@ -2634,9 +2954,17 @@ bool vjp_cholesky(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cud
       l.batch == 0 || l.n < 4 * l.lower)
     return false;
   const bool f64 = l.dtype == BGM_F64;
+  static const bool use_dmma = [] {
+    const char* e = std::getenv("BGM_WIDE_DMMA");
+    return !(e && e[0] == '0');
+  }();
   switch (l.lower) {
-    case 64: return f64 ? run_vchol<double, 64>(l, lb, qb, s) : run_vchol<float, 64>(l, lb, qb, s);
-    case 128: return f64 ? run_vchol<double, 128>(l, lb, qb, s) : run_vchol<float, 128>(l, lb, qb, s);
+    case 64:
+      if (f64 && use_dmma) return run_vchol_dmma<64>(l, lb, qb, s);
+      return f64 ? run_vchol<double, 64>(l, lb, qb, s) : run_vchol<float, 64>(l, lb, qb, s);
+    case 128:
+      if (f64 && use_dmma) return run_vchol_dmma<128>(l, lb, qb, s);
+      return f64 ? run_vchol<double, 128>(l, lb, qb, s) : run_vchol<float, 128>(l, lb, qb, s);
     default: return false;
   }
 }
