@@ -1684,11 +1684,27 @@ __global__ void __launch_bounds__(32) k_subset_dmma_repair(SubP<double> C, Geo G
 // parity tests.
 __device__ __forceinline__ int sw8(int r, int c) { return r * 8 + (c ^ ((r & 2) << 1)); }
 
-template <int K>
-__device__ __forceinline__ int ring_slot(int d, ix b2) {  // diagonal d holds NT+1-d tiles
-  constexpr int NT = K / 8;
-  return d * (NT + 1) - d * (d - 1) / 2 + int(unsigned(b2) % unsigned(NT + 1 - d));
+// x mod m for m <= 64 by a multiply-high with M = floor((2^32 - 1) / m) + 1
+// (exact for x < 2^26: the error x (M - 2^32/m) / 2^32 stays below 1/m)
+__device__ __forceinline__ unsigned mod_small(unsigned x, unsigned m, unsigned magic) {
+  return x - __umulhi(x, magic) * m;
 }
+
+template <int K>
+__device__ __forceinline__ int ring_slot(int d, ix b2, const unsigned* mg) {  // diagonal d holds NT+1-d tiles
+  constexpr int NT = K / 8;
+  const unsigned m = unsigned(NT + 1 - d);
+  const int base = d * (NT + 1) - d * (d - 1) / 2;
+  return m == 1 ? base : base + int(mod_small(unsigned(b2), m, mg[m]));
+}
+
+// per-matrix base of a band: cell (r, j) at p[(j w + r) << s]
+struct BRow {
+  double* p;
+  int w, s;
+  __device__ __forceinline__ double* at(int r, ix j) const { return p + ((j * w + r) << s); }
+};
+__device__ __forceinline__ BRow brow(const Band<double>& X, ix b) { return BRow{&X.cell(b, 0, 0), X.w, X.s}; }
 
 template <int K, int NW>
 struct VtSmem {
@@ -1700,15 +1716,16 @@ struct VtSmem {
   double lp[2][(K + 8) * 8];
   double y[NT][64], zt[NT][64], yb[NT][64];
   double lin[NW][64], am[NW][64], ab[NW][64], part[NW][64];
-  short zs[NT * NT];
-  short ws[(NT + 1) * (NT + 1)];
+  int zs[NT * NT];               // element offset of Z_TT tile (t, u) in z (lower-stored)
+  int ws[(NT + 1) * (NT + 1)];   // element offset of W tile (t1, t2) in w, window of the panel
+  unsigned mg[NT + 2];           // mod_small multipliers
 };
 
 template <int K, int NW>
 __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix i0, double* side, double* tail,
                                VtSmem<K, NW>& sm) {
   constexpr int NT = K / 8, NTH = 32 * NW, TPW = NT / NW, NWT = VtSmem<K, NW>::NWT;
-  static_assert(NT % NW == 0 && (NT / 2) % NW == 0, "warps must divide the tile rows");
+  static_assert(NT % NW == 0, "warps must divide the tile rows");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, rr = lane >> 2, q = lane & 3, c2 = 2 * q;
   const int o0[2] = {sw8(rr, q), sw8(rr, 4 + q)}, o1[2] = {sw8(q, rr), sw8(4 + q, rr)};
   const int oc = sw8(rr, c2);
@@ -1722,7 +1739,8 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
   // element (m, c) of window tile (b1, b2) of the symmetric band X: cp.async of
   // the lower-stored cell (a diagonal tile's upper half reads the mirror);
   // rows past n are identity (Z) or zero (S-bar); halve: S-bar's symmetric split
-  auto elem = [&](double* T, const Band<double>& X, bool ident, ix b1, ix b2, int idx, bool fix) {
+  const BRow zrow = brow(C.s, b), grow = brow(C.sb, b), lrow = brow(L, b), orow = brow(C.lb, b);
+  auto elem = [&](double* T, const BRow& X, bool ident, ix b1, ix b2, int idx, bool fix) {
     const int m = idx >> 3, c = idx & 7;
     double* dst = T + sw8(m, c);
     if (fix) {
@@ -1735,28 +1753,28 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
       r = cc;
       cc = t;
     }
-    const ix cell = r - cc;
-    if (r < n && cell <= K) cpa(dst, &X.cell(b, int(cell), cc));
+    const int cell = int(r - cc);
+    if (r < n && cell <= K) cpa(dst, X.at(cell, cc));
     else *dst = (ident && cell == 0) ? 1.0 : 0.0;
   };
   // W block row bn (tiles (bn, bn-d), d = 0..NT) / Z block row bn (d < NT)
   auto w_row = [&](ix bn, bool fix) {
     for (int x = tid; x < (NT + 1) * 64; x += NTH) {
       const int d = x >> 6;
-      elem(sm.w[ring_slot<K>(d, bn - d)], C.sb, false, bn, bn - d, x & 63, fix);
+      elem(sm.w[ring_slot<K>(d, bn - d, sm.mg)], grow, false, bn, bn - d, x & 63, fix);
     }
   };
   auto z_row = [&](ix bn) {
     for (int x = tid; x < NT * 64; x += NTH) {
       const int d = x >> 6;
-      elem(sm.z[ring_slot<K>(d, bn - d)], C.s, true, bn, bn - d, x & 63, false);
+      elem(sm.z[ring_slot<K>(d, bn - d, sm.mg)], zrow, true, bn, bn - d, x & 63, false);
     }
   };
   auto w_init = [&](ix pb, bool fix) {  // W blocks pb .. pb+NT
     for (int x = tid; x < NWT * 64; x += NTH) {
       int j = x >> 6, d = 0;
       while (j > NT - d) j -= NT + 1 - d++;
-      elem(sm.w[ring_slot<K>(d, pb + j)], C.sb, false, pb + j + d, pb + j, x & 63, fix);
+      elem(sm.w[ring_slot<K>(d, pb + j, sm.mg)], grow, false, pb + j + d, pb + j, x & 63, fix);
     }
   };
   auto fill = [&](int buf, ix pb) {  // L rows [8pb, 8pb+K+8) x cols [8pb, 8pb+8), identity past n
@@ -1764,7 +1782,7 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
       const int c = x / (K + 8), r = x % (K + 8), cell = r - c;
       const ix col = 8 * pb + c, row = 8 * pb + r;
       double* dst = sm.lp[buf] + sw8(r, c);
-      if (cell >= 0 && cell <= K && col < n && row < n) cpa(dst, &L.cell(b, cell, col));
+      if (cell >= 0 && cell <= K && col < n && row < n) cpa(dst, lrow.at(cell, col));
       else *dst = (cell == 0) ? 1.0 : 0.0;
     }
   };
@@ -1772,13 +1790,15 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
     for (int x = tid; x < NWT * 64; x += NTH) {
       int j = x >> 6, d = 0;
       while (j > NT - d) j -= NT + 1 - d++;
-      dst[x] = sm.w[ring_slot<K>(d, pb + j)][x & 63];
+      dst[x] = sm.w[ring_slot<K>(d, pb + j, sm.mg)][x & 63];
     }
   };
   const ix pb0 = i0 / 8, pbe = (e + 7) / 8;
+  for (int x = tid; x < NT + 2; x += NTH) sm.mg[x] = x ? 0xFFFFFFFFu / unsigned(x) + 1u : 0u;
+  __syncthreads();
   for (int x = tid; x < NT * NT * 64; x += NTH) {  // Z blocks pb0+1 .. pb0+NT (lower tiles)
     const int t1 = x / (NT * 64), t2 = (x >> 6) % NT;
-    if (t2 <= t1) elem(sm.z[ring_slot<K>(t1 - t2, pb0 + 1 + t2)], C.s, true, pb0 + 1 + t1, pb0 + 1 + t2, x & 63, false);
+    if (t2 <= t1) elem(sm.z[ring_slot<K>(t1 - t2, pb0 + 1 + t2, sm.mg)], zrow, true, pb0 + 1 + t1, pb0 + 1 + t2, x & 63, false);
   }
   w_init(pb0, false);
   fill(0, pb0);
@@ -1791,11 +1811,11 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
     else w_row(pb + NT, true);
     for (int x = tid; x < NT * NT; x += NTH) {
       const int t = x / NT, u = x % NT;
-      sm.zs[x] = short(ring_slot<K>(t > u ? t - u : u - t, pb + 1 + (t < u ? t : u)));
+      sm.zs[x] = ring_slot<K>(t > u ? t - u : u - t, pb + 1 + (t < u ? t : u), sm.mg) * 64;
     }
     for (int x = tid; x < (NT + 1) * (NT + 1); x += NTH) {
       const int t1 = x / (NT + 1), t2 = x % (NT + 1);
-      if (t1 >= t2) sm.ws[x] = short(ring_slot<K>(t1 - t2, pb + t2));
+      if (t1 >= t2) sm.ws[x] = ring_slot<K>(t1 - t2, pb + t2, sm.mg) * 64;
     }
     __syncthreads();
     if (side && pb == s / 8) save_w(side, pb);  // burn-in state at the segment start
@@ -1831,7 +1851,7 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
         const int t = warp + NW * i;
         ya[i][0] = ya[i][1] = 0.0;
 #pragma unroll
-        for (int u = 0; u < NT; ++u) mm(ya[i], sm.z[sm.zs[t * NT + u]], t < u, lp + (8 + 8 * u) * 8, false);
+        for (int u = 0; u < NT; ++u) mm(ya[i], &sm.z[0][0] + sm.zs[t * NT + u], t < u, lp + (8 + 8 * u) * 8, false);
       }
 #pragma unroll
       for (int i = 0; i < TPW; ++i) put(sm.y[warp + NW * i], ya[i][0], ya[i][1]);
@@ -1855,7 +1875,7 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
       put(sm.am[warp], l2.x - ((h[0][0] + h[1][0]) + (h[2][0] + h[3][0])),
           l2.y - ((h[0][1] + h[1][1]) + (h[2][1] + h[3][1])));
       __syncwarp();
-      const double* wpp = sm.w[sm.ws[0]];
+      const double* wpp = &sm.w[0][0] + sm.ws[0];
       double a[2] = {0.0, 0.0}, v[2] = {0.0, 0.0};
       mm(a, lin, false, wpp, true);
       mm(v, sm.am[warp], false, wpp, false);
@@ -1874,7 +1894,7 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
         const int t = warp + NW * i;
         la[i][0] = la[i][1] = 0.0;
         mm(la[i], sm.zt[t], false, sm.ab[warp], true);
-        const double2 w2 = get(sm.w[sm.ws[(t + 1) * (NT + 1)]]);
+        const double2 w2 = get(&sm.w[0][0] + sm.ws[(t + 1) * (NT + 1)]);
         g[i][0] = -2.0 * w2.x;
         g[i][1] = -2.0 * w2.y;
         mm(g[i], lp + (8 + 8 * t) * 8, false, sm.ab[warp], false);
@@ -1904,12 +1924,12 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
       const int t = warp + NW * i;
       double acc[2] = {-0.5 * la[i][0], -0.5 * la[i][1]};
 #pragma unroll
-      for (int u = 0; u < NT; ++u) mm(acc, sm.z[sm.zs[t * NT + u]], t < u, sm.yb[u], false);
+      for (int u = 0; u < NT; ++u) mm(acc, &sm.z[0][0] + sm.zs[t * NT + u], t < u, sm.yb[u], false);
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const ix col = 8 * pb + c2 + v;
         const int cell = 8 + 8 * t + rr - c2 - v;
-        if (col >= s && col < e && cell <= K) C.lb.cell(b, cell, col) = (col + cell < n) ? 2.0 * acc[v] : 0.0;
+        if (col >= s && col < e && cell <= K) *orow.at(cell, col) = (col + cell < n) ? 2.0 * acc[v] : 0.0;
       }
     }
     // W(T,T) += Yh L_TP^T + L_TP Yh^T: tile rows pp and NT-1-pp together (NT+1 tiles)
@@ -1919,7 +1939,7 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
 #pragma unroll
       for (int j = 0; j <= NT; ++j) {
         const int t1 = j <= pp ? pp : NT - 1 - pp, t2 = j <= pp ? j : j - pp - 1;
-        const double2 w2 = get(sm.w[sm.ws[(t1 + 1) * (NT + 1) + t2 + 1]]);
+        const double2 w2 = get(&sm.w[0][0] + sm.ws[(t1 + 1) * (NT + 1) + t2 + 1]);
         wa[j][0] = w2.x;
         wa[j][1] = w2.y;
         mm(wa[j], sm.yb[t1], false, lp + (8 + 8 * t2) * 8, true);
@@ -1928,7 +1948,7 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
 #pragma unroll
       for (int j = 0; j <= NT; ++j) {
         const int t1 = j <= pp ? pp : NT - 1 - pp, t2 = j <= pp ? j : j - pp - 1;
-        put(sm.w[sm.ws[(t1 + 1) * (NT + 1) + t2 + 1]], wa[j][0], wa[j][1]);
+        put(&sm.w[0][0] + sm.ws[(t1 + 1) * (NT + 1) + t2 + 1], wa[j][0], wa[j][1]);
       }
     }
     // Lppb = -Linv^T (Linvb Linv^T), Linvb = Linvb0 + sum of the warps' partials
@@ -1951,7 +1971,7 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
       for (int v = 0; v < 2; ++v) {
         const ix col = 8 * pb + c2 + v;
         const int cell = rr - c2 - v;
-        if (col >= s && col < e && cell >= 0) C.lb.cell(b, cell, col) = (col + cell < n) ? -p2[v] : 0.0;
+        if (col >= s && col < e && cell >= 0) *orow.at(cell, col) = (col + cell < n) ? -p2[v] : 0.0;
       }
     }
     __syncthreads();
@@ -2042,7 +2062,8 @@ struct VdSmem {
   double lt[NT][64];
   double lin[NW][64], part[NW][64];
   double s1[64], s2[64];
-  short zs[NT * NT];
+  int zs[NT * NT];  // element offset of G_TT tile (t, u) in g (lower-stored)
+  unsigned mg[NT + 2];
 };
 
 template <int K, int NW>
@@ -2054,6 +2075,7 @@ __device__ void vchol_dmma_unit(const VdP<double>& C, ix b, ix n, ix s, ix e, ix
   const int o0[2] = {sw8(rr, q), sw8(rr, 4 + q)}, o1[2] = {sw8(q, rr), sw8(4 + q, rr)};
   const int oc = sw8(rr, c2);
   const Band<double>& L = C.l;
+  const BRow lrow = brow(L, b), brow_lb = brow(C.lb, b), brow_qb = brow(C.qb, b);
   auto mm = [&](double* acc, const double* X, bool tx, const double* Y, bool ty) {
 #pragma unroll
     for (int kc = 0; kc < 2; ++kc) dmma(acc[0], acc[1], X[tx ? o1[kc] : o0[kc]], Y[ty ? o0[kc] : o1[kc]]);
@@ -2064,7 +2086,7 @@ __device__ void vchol_dmma_unit(const VdP<double>& C, ix b, ix n, ix s, ix e, ix
       const int c = x / (K + 8), r = x % (K + 8), cell = r - c;
       const ix col = 8 * pb + c, row = 8 * pb + r;
       double* dst = sm.lp[buf] + sw8(r, c);
-      if (cell >= 0 && cell <= K && col < n && row < n) cpa(dst, &L.cell(b, cell, col));
+      if (cell >= 0 && cell <= K && col < n && row < n) cpa(dst, lrow.at(cell, col));
       else *dst = (cell == 0) ? 1.0 : 0.0;
     }
   };
@@ -2076,20 +2098,22 @@ __device__ void vchol_dmma_unit(const VdP<double>& C, ix b, ix n, ix s, ix e, ix
 #pragma unroll
       for (int i = 0; i < TPW; ++i) {
         const int cell = 8 + 8 * (warp + NW * i) + rr - c2 - v;
-        ft[i][v] = (pb >= 0 && cell <= K && col + cell < n) ? C.lb.cell(b, cell, col) : 0.0;
+        ft[i][v] = (pb >= 0 && cell <= K && col + cell < n) ? *brow_lb.at(cell, col) : 0.0;
       }
       const int cell = rr - c2 - v;
-      fp[v] = (pb >= 0 && cell >= 0 && col + cell < n) ? C.lb.cell(b, cell, col) : 0.0;
+      fp[v] = (pb >= 0 && cell >= 0 && col + cell < n) ? *brow_lb.at(cell, col) : 0.0;
     }
   };
   auto save_g = [&](double* dst, ix b0) {  // window blocks b0 .. b0+NT-1, tiles in (d, j) order
     for (int x = tid; x < NST * 64; x += NTH) {
       int j = x >> 6, d = 0;
       while (j > NT - 1 - d) j -= NT - d++;
-      dst[x] = sm.g[ring_slot<K>(d, b0 + j)][x & 63];
+      dst[x] = sm.g[ring_slot<K>(d, b0 + j, sm.mg)][x & 63];
     }
   };
   const ix pb_top = (iend + 7) / 8 - 1, pb_end = s / 8;
+  for (int x = tid; x < NT + 2; x += NTH) sm.mg[x] = x ? 0xFFFFFFFFu / unsigned(x) + 1u : 0u;
+  __syncthreads();
   for (int x = tid; x < VdSmem<K, NW>::NZ * 64; x += NTH) (&sm.g[0][0])[x] = 0.0;
   fill(0, pb_top);
   cpa_commit();
@@ -2101,7 +2125,7 @@ __device__ void vchol_dmma_unit(const VdP<double>& C, ix b, ix n, ix s, ix e, ix
     cpa_wait0();
     for (int x = tid; x < NT * NT; x += NTH) {
       const int t = x / NT, u = x % NT;
-      sm.zs[x] = short(ring_slot<K>(t > u ? t - u : u - t, pb + 1 + (t < u ? t : u)));
+      sm.zs[x] = ring_slot<K>(t > u ? t - u : u - t, pb + 1 + (t < u ? t : u), sm.mg) * 64;
     }
     __syncthreads();
     if (side && 8 * (pb + 1) == e) save_g(side, pb + 1);  // burn-in state entering the segment
@@ -2138,7 +2162,7 @@ __device__ void vchol_dmma_unit(const VdP<double>& C, ix b, ix n, ix s, ix e, ix
         const int t = warp + NW * i;
         ga[i][0] = ga[i][1] = 0.0;
 #pragma unroll
-        for (int u = 0; u < NT; ++u) mm(ga[i], sm.g[sm.zs[t * NT + u]], t < u, lp + (8 + 8 * u) * 8, false);
+        for (int u = 0; u < NT; ++u) mm(ga[i], &sm.g[0][0] + sm.zs[t * NT + u], t < u, lp + (8 + 8 * u) * 8, false);
       }
 #pragma unroll
       for (int i = 0; i < TPW; ++i)
@@ -2158,12 +2182,12 @@ __device__ void vchol_dmma_unit(const VdP<double>& C, ix b, ix n, ix s, ix e, ix
       for (int i = 0; i < TPW; ++i) {
         const int t = warp + NW * i;
         put(sm.lt[t], aa[i][0], aa[i][1]);
-        if (t + 1 < NT) put(sm.g[ring_slot<K>(t + 1, pb)], 0.5 * aa[i][0], 0.5 * aa[i][1]);
+        if (t + 1 < NT) put(sm.g[ring_slot<K>(t + 1, pb, sm.mg)], 0.5 * aa[i][0], 0.5 * aa[i][1]);
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
           const ix col = 8 * pb + c2 + v;
           const int cell = 8 + 8 * t + rr - c2 - v;
-          if (col >= s && col < e && cell <= K) C.qb.cell(b, cell, col) = (col + cell < n) ? aa[i][v] : 0.0;
+          if (col >= s && col < e && cell <= K) *brow_qb.at(cell, col) = (col + cell < n) ? aa[i][v] : 0.0;
         }
       }
       __syncwarp();
@@ -2203,13 +2227,13 @@ __device__ void vchol_dmma_unit(const VdP<double>& C, ix b, ix n, ix s, ix e, ix
       double gp[2];
 #pragma unroll
       for (int v = 0; v < 2; ++v) gp[v] = 0.5 * (sa[v] + sm.s2[sw8(c2 + v, rr)]);
-      put(sm.g[ring_slot<K>(0, pb)], gp[0], gp[1]);
+      put(sm.g[ring_slot<K>(0, pb, sm.mg)], gp[0], gp[1]);
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const ix col = 8 * pb + c2 + v;
         const int cell = rr - c2 - v;
         if (col >= s && col < e && cell >= 0)
-          C.qb.cell(b, cell, col) = (col + cell < n) ? (cell == 0 ? sa[v] : 2.0 * gp[v]) : 0.0;
+          *brow_qb.at(cell, col) = (col + cell < n) ? (cell == 0 ? sa[v] : 2.0 * gp[v]) : 0.0;
       }
     }
     __syncthreads();
@@ -2447,10 +2471,9 @@ inline int pick_nseg(ix batch, ix n, int slots, int burn, int seg_min) {
   return best;
 }
 
-template <int K>
+template <int K, int NW>
 bool run_vsub_dmma(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, const bgm_band& lb, int32_t* st,
                    int64_t* row, cudaStream_t s) {
-  constexpr int NW = 4;
   const size_t smem = sizeof(VtSmem<K, NW>);
   if (smem > 227 * 1024) return false;
   static bool attr = false;
@@ -2969,6 +2992,14 @@ bool vjp_cholesky(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cud
   }
 }
 
+static int vsub_warps() {
+  static const int w = [] {
+    const char* e = std::getenv("BGM_VSUB_WARPS");
+    return e ? std::atoi(e) : 0;  // 0: 4 warps for k = 64, 8 for k = 128
+  }();
+  return w;
+}
+
 bool vjp_subset(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, const bgm_band& lb, int32_t* st,
                 int64_t* row, cudaStream_t s) {
   if (l.upper != 0 || l.batch == 0 || l.n < 4 * l.lower) return false;
@@ -2981,10 +3012,14 @@ bool vjp_subset(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, const
     case 16:
       return f64 ? run_vsub<double, 16>(l, sm, sb, lb, st, row, s) : run_vsub<float, 16>(l, sm, sb, lb, st, row, s);
     case 64:
-      if (f64 && use_dmma && run_vsub_dmma<64>(l, sm, sb, lb, st, row, s)) return true;
+      if (f64 && use_dmma && (vsub_warps() == 8 ? run_vsub_dmma<64, 8>(l, sm, sb, lb, st, row, s)
+                                                : run_vsub_dmma<64, 4>(l, sm, sb, lb, st, row, s)))
+        return true;
       return f64 ? run_vsub<double, 64>(l, sm, sb, lb, st, row, s) : run_vsub<float, 64>(l, sm, sb, lb, st, row, s);
     case 128:
-      if (f64 && use_dmma && run_vsub_dmma<128>(l, sm, sb, lb, st, row, s)) return true;
+      if (f64 && use_dmma && (vsub_warps() != 4 ? run_vsub_dmma<128, 8>(l, sm, sb, lb, st, row, s)
+                                                : run_vsub_dmma<128, 4>(l, sm, sb, lb, st, row, s)))
+        return true;
       return f64 ? run_vsub<double, 128>(l, sm, sb, lb, st, row, s) : run_vsub<float, 128>(l, sm, sb, lb, st, row, s);
     default: return false;
   }
