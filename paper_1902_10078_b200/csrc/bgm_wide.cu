@@ -1738,15 +1738,13 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
   auto get = [&](const double* T) { return *reinterpret_cast<const double2*>(T + oc); };
   // element (m, c) of window tile (b1, b2) of the symmetric band X: cp.async of
   // the lower-stored cell (a diagonal tile's upper half reads the mirror);
-  // rows past n are identity (Z) or zero (S-bar); halve: S-bar's symmetric split
+  // rows past n are identity (Z) or zero (S-bar).  W is kept as W2 = 2 W off
+  // the matrix diagonal, so S-bar's cells load raw; its diagonal carries
+  // S-bar_ii + 2 (pushed-down part), corrected where Zb_PP is formed.
   const BRow zrow = brow(C.s, b), grow = brow(C.sb, b), lrow = brow(L, b), orow = brow(C.lb, b);
-  auto elem = [&](double* T, const BRow& X, bool ident, ix b1, ix b2, int idx, bool fix) {
+  auto elem = [&](double* T, const BRow& X, bool ident, ix b1, ix b2, int idx) {
     const int m = idx >> 3, c = idx & 7;
     double* dst = T + sw8(m, c);
-    if (fix) {
-      if (b1 != b2 || m != c) *dst *= 0.5;
-      return;
-    }
     ix r = 8 * b1 + m, cc = 8 * b2 + c;
     if (r < cc) {
       const ix t = r;
@@ -1757,33 +1755,46 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
     if (r < n && cell <= K) cpa(dst, X.at(cell, cc));
     else *dst = (ident && cell == 0) ? 1.0 : 0.0;
   };
-  // W block row bn (tiles (bn, bn-d), d = 0..NT) / Z block row bn (d < NT)
-  auto w_row = [&](ix bn, bool fix) {
-    for (int x = tid; x < (NT + 1) * 64; x += NTH) {
-      const int d = x >> 6;
-      elem(sm.w[ring_slot<K>(d, bn - d, sm.mg)], grow, false, bn, bn - d, x & 63, fix);
+  // block row bn entering a ring (tiles (bn, bn-d), d < ntile) into the slots
+  // tab[d (NT+1)] / 64 of the current panel; each thread owns the element
+  // (em, ec) of tiles et, et + NTH/64, ...  (NTH is a multiple of 64)
+  static_assert(NTH % 64 == 0, "block size");
+  const int em = (tid & 63) >> 3, ec = tid & 7, et = tid >> 6;
+  auto row_issue = [&](double* ring, const BRow& X, bool ident, ix bn, int ntile) {
+    const double* rowp = X.p + ((8 * bn * X.w) << X.s);
+#pragma unroll
+    for (int i = 0; i < (NT + 1 + NTH / 64 - 1) / (NTH / 64); ++i) {
+      const int d = et + (NTH / 64) * i;
+      if (d < ntile) {
+        double* dst = ring + sm.ws[d * (NT + 1)] + sw8(em, ec);
+        const bool mir = d == 0 && em < ec;
+        const int cell = mir ? ec - em : 8 * d + em - ec;
+        const int off = mir ? em * X.w + cell : (ec - 8 * d) * X.w + cell;
+        if (8 * bn + (mir ? ec : em) < n && cell <= K) cpa(dst, rowp + (ix(off) << X.s));
+        else *dst = (ident && cell == 0) ? 1.0 : 0.0;
+      }
     }
   };
-  auto z_row = [&](ix bn) {
-    for (int x = tid; x < NT * 64; x += NTH) {
-      const int d = x >> 6;
-      elem(sm.z[ring_slot<K>(d, bn - d, sm.mg)], zrow, true, bn, bn - d, x & 63, false);
-    }
-  };
-  auto w_init = [&](ix pb, bool fix) {  // W blocks pb .. pb+NT
+  auto w_init = [&](ix pb) {  // W blocks pb .. pb+NT
     for (int x = tid; x < NWT * 64; x += NTH) {
       int j = x >> 6, d = 0;
       while (j > NT - d) j -= NT + 1 - d++;
-      elem(sm.w[ring_slot<K>(d, pb + j, sm.mg)], grow, false, pb + j + d, pb + j, x & 63, fix);
+      elem(sm.w[ring_slot<K>(d, pb + j, sm.mg)], grow, false, pb + j + d, pb + j, x & 63);
     }
   };
-  auto fill = [&](int buf, ix pb) {  // L rows [8pb, 8pb+K+8) x cols [8pb, 8pb+8), identity past n
-    for (int x = tid; x < 8 * (K + 8); x += NTH) {
-      const int c = x / (K + 8), r = x % (K + 8), cell = r - c;
-      const ix col = 8 * pb + c, row = 8 * pb + r;
-      double* dst = sm.lp[buf] + sw8(r, c);
-      if (cell >= 0 && cell <= K && col < n && row < n) cpa(dst, lrow.at(cell, col));
-      else *dst = (cell == 0) ? 1.0 : 0.0;
+  // L rows [8pb, 8pb+K+8) x cols [8pb, 8pb+8), identity past n; thread column fc
+  const int fc = tid & 7, fr = tid >> 3;
+  auto fill = [&](int buf, ix pb) {
+    const ix col = 8 * pb + fc;
+    const double* colp = lrow.at(0, col);
+#pragma unroll
+    for (int i = 0; i < (K + 8 + NTH / 8 - 1) / (NTH / 8); ++i) {
+      const int r = fr + (NTH / 8) * i, cell = r - fc;
+      if (r < K + 8) {
+        double* dst = sm.lp[buf] + sw8(r, fc);
+        if (cell >= 0 && cell <= K && 8 * pb + r < n) cpa(dst, colp + (ix(cell) << lrow.s));
+        else *dst = (cell == 0) ? 1.0 : 0.0;
+      }
     }
   };
   auto save_w = [&](double* dst, ix pb) {  // window of panel pb, tiles in (d, j) order
@@ -1798,17 +1809,15 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
   __syncthreads();
   for (int x = tid; x < NT * NT * 64; x += NTH) {  // Z blocks pb0+1 .. pb0+NT (lower tiles)
     const int t1 = x / (NT * 64), t2 = (x >> 6) % NT;
-    if (t2 <= t1) elem(sm.z[ring_slot<K>(t1 - t2, pb0 + 1 + t2, sm.mg)], zrow, true, pb0 + 1 + t1, pb0 + 1 + t2, x & 63, false);
+    if (t2 <= t1) elem(sm.z[ring_slot<K>(t1 - t2, pb0 + 1 + t2, sm.mg)], zrow, true, pb0 + 1 + t1, pb0 + 1 + t2, x & 63);
   }
-  w_init(pb0, false);
+  w_init(pb0);
   fill(0, pb0);
   cpa_commit();
   int buf = 0;
 #pragma unroll 1
   for (ix pb = pb0; pb < pbe; ++pb) {
     cpa_wait0();
-    if (pb == pb0) w_init(pb0, true);
-    else w_row(pb + NT, true);
     for (int x = tid; x < NT * NT; x += NTH) {
       const int t = x / NT, u = x % NT;
       sm.zs[x] = ring_slot<K>(t > u ? t - u : u - t, pb + 1 + (t < u ? t : u), sm.mg) * 64;
@@ -1819,7 +1828,9 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
     }
     __syncthreads();
     if (side && pb == s / 8) save_w(side, pb);  // burn-in state at the segment start
-    z_row(pb + NT + 1);  // into the ring slots block pb has left
+    row_issue(&sm.z[0][0], zrow, true, pb + NT + 1, NT);  // into the ring slots block pb has left
+    const double dl0 = 8 * pb + c2 < n ? *grow.at(0, 8 * pb + c2) : 0.0;  // S-bar_ii of the panel
+    const double dl1 = 8 * pb + c2 + 1 < n ? *grow.at(0, 8 * pb + c2 + 1) : 0.0;
     if (pb + 1 < pbe) fill(buf ^ 1, pb + 1);
     cpa_commit();
     const double* lp = sm.lp[buf];
@@ -1875,17 +1886,23 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
       put(sm.am[warp], l2.x - ((h[0][0] + h[1][0]) + (h[2][0] + h[3][0])),
           l2.y - ((h[0][1] + h[1][1]) + (h[2][1] + h[3][1])));
       __syncwarp();
+      // Zb_PP = (W2_PP + diag(S-bar_ii)) / 2
       const double* wpp = &sm.w[0][0] + sm.ws[0];
       double a[2] = {0.0, 0.0}, v[2] = {0.0, 0.0};
       mm(a, lin, false, wpp, true);
       mm(v, sm.am[warp], false, wpp, false);
+      const double2 am2 = get(sm.am[warp]);
+      a[0] = 0.5 * fma(l2.x, dl0, a[0]);
+      a[1] = 0.5 * fma(l2.y, dl1, a[1]);
+      v[0] = 0.5 * fma(am2.x, dl0, v[0]);
+      v[1] = 0.5 * fma(am2.y, dl1, v[1]);
       lvb[0] = v[0] + a[0];
       lvb[1] = v[1] + a[1];
       put(sm.ab[warp], a[0], a[1]);
       __syncwarp();
     }
-    // ---- (3) per tile row: G = L_TP Ab - 2 W(T,P) (= -Zb_TP), Z_TP Ab^T (= -Ltpb part),
-    //          Linvb partial sum Y^T G, Yh = G Linv^T / 2 (= Yb / 2)
+    // ---- (3) per tile row: G = L_TP Ab - W2(T,P) (= -Zb_TP), Z_TP Ab^T (= -Ltpb part),
+    //          Linvb partial sum Y^T G, Yb = G Linv^T
     double la[TPW][2];
     {
       double g[TPW][2], pa[2] = {0.0, 0.0};
@@ -1895,8 +1912,8 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
         la[i][0] = la[i][1] = 0.0;
         mm(la[i], sm.zt[t], false, sm.ab[warp], true);
         const double2 w2 = get(&sm.w[0][0] + sm.ws[(t + 1) * (NT + 1)]);
-        g[i][0] = -2.0 * w2.x;
-        g[i][1] = -2.0 * w2.y;
+        g[i][0] = -w2.x;
+        g[i][1] = -w2.y;
         mm(g[i], lp + (8 + 8 * t) * 8, false, sm.ab[warp], false);
       }
 #pragma unroll
@@ -1911,28 +1928,28 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
       }
       __syncwarp();
 #pragma unroll
-      for (int i = 0; i < TPW; ++i) put(sm.yb[warp + NW * i], 0.5 * g[i][0], 0.5 * g[i][1]);
+      for (int i = 0; i < TPW; ++i) put(sm.yb[warp + NW * i], g[i][0], g[i][1]);
       put(sm.part[warp], pa[0], pa[1]);
     }
     __syncthreads();
     // ---- (4) W block row pb+NT+1 enters the slots of column pb (read for the last time above)
-    w_row(pb + NT + 1, false);
+    row_issue(&sm.w[0][0], grow, false, pb + NT + 1, NT + 1);
     cpa_commit();
-    // Ltpb = -Z_TP Ab^T + 2 Z_TT Yh -> L-bar rows 8pb+8+8t+rr, columns 8pb+c2+v
+    // Ltpb = -Z_TP Ab^T + Z_TT Yb -> L-bar rows 8pb+8+8t+rr, columns 8pb+c2+v
 #pragma unroll
     for (int i = 0; i < TPW; ++i) {
       const int t = warp + NW * i;
-      double acc[2] = {-0.5 * la[i][0], -0.5 * la[i][1]};
+      double acc[2] = {-la[i][0], -la[i][1]};
 #pragma unroll
       for (int u = 0; u < NT; ++u) mm(acc, &sm.z[0][0] + sm.zs[t * NT + u], t < u, sm.yb[u], false);
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const ix col = 8 * pb + c2 + v;
         const int cell = 8 + 8 * t + rr - c2 - v;
-        if (col >= s && col < e && cell <= K) *orow.at(cell, col) = (col + cell < n) ? 2.0 * acc[v] : 0.0;
+        if (col >= s && col < e && cell <= K) *orow.at(cell, col) = (col + cell < n) ? acc[v] : 0.0;
       }
     }
-    // W(T,T) += Yh L_TP^T + L_TP Yh^T: tile rows pp and NT-1-pp together (NT+1 tiles)
+    // W2(T,T) += Yb L_TP^T + L_TP Yb^T: tile rows pp and NT-1-pp together (NT+1 tiles)
 #pragma unroll 1
     for (int pp = warp; pp < NT / 2; pp += NW) {
       double wa[NT + 1][2];
@@ -1978,7 +1995,6 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
     buf ^= 1;
   }
   cpa_wait0();
-  w_row(pbe + NT, true);
   __syncthreads();
   if (tail) save_w(tail, pbe);  // genuine state the next segment's burn-in must reproduce
 }
