@@ -1715,7 +1715,7 @@ struct VtSmem {
   double w[NWT][64];
   double lp[2][(K + 8) * 8];
   double y[NT][64], zt[NT][64], yb[NT][64];
-  double lin[NW][64], am[NW][64], ab[NW][64], part[NW][64];
+  double lin[NW][64], am[NW][64], ab[NW][64], part[NW][64], ph[NW][64];
   int zs[NT * NT];               // element offset of Z_TT tile (t, u) in z (lower-stored)
   int ws[(NT + 1) * (NT + 1)];   // element offset of W tile (t1, t2) in w, window of the panel
   unsigned mg[NT + 2];           // mod_small multipliers
@@ -1856,35 +1856,44 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
       put(lin, M0, M1);
     }
     {
-      double ya[TPW][2];
+      double ya[TPW][2][2];
 #pragma unroll
       for (int i = 0; i < TPW; ++i) {
         const int t = warp + NW * i;
-        ya[i][0] = ya[i][1] = 0.0;
+        ya[i][0][0] = ya[i][0][1] = ya[i][1][0] = ya[i][1][1] = 0.0;
 #pragma unroll
-        for (int u = 0; u < NT; ++u) mm(ya[i], &sm.z[0][0] + sm.zs[t * NT + u], t < u, lp + (8 + 8 * u) * 8, false);
+        for (int u = 0; u < NT; ++u)
+          mm(ya[i][u & 1], &sm.z[0][0] + sm.zs[t * NT + u], t < u, lp + (8 + 8 * u) * 8, false);
       }
 #pragma unroll
-      for (int i = 0; i < TPW; ++i) put(sm.y[warp + NW * i], ya[i][0], ya[i][1]);
+      for (int i = 0; i < TPW; ++i) put(sm.y[warp + NW * i], ya[i][0][0] + ya[i][1][0], ya[i][0][1] + ya[i][1][1]);
       __syncwarp();
 #pragma unroll
       for (int i = 0; i < TPW; ++i) {
-        ya[i][0] = ya[i][1] = 0.0;
-        mm(ya[i], sm.y[warp + NW * i], false, lin, false);
+        ya[i][0][0] = ya[i][0][1] = 0.0;
+        mm(ya[i][0], sm.y[warp + NW * i], false, lin, false);
       }
 #pragma unroll
-      for (int i = 0; i < TPW; ++i) put(sm.zt[warp + NW * i], -ya[i][0], -ya[i][1]);
+      for (int i = 0; i < TPW; ++i) put(sm.zt[warp + NW * i], -ya[i][0][0], -ya[i][0][1]);
+      __syncwarp();
+      double h[2] = {0.0, 0.0};  // this warp's share of L_TP^T Z_TP
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) mm(h, lp + (8 + 8 * (warp + NW * i)) * 8, true, sm.zt[warp + NW * i], false);
+      put(sm.ph[warp], h[0], h[1]);
     }
     __syncthreads();
     // ---- (2) A = Linv - L_TP^T Z_TP; Ab = Linv Zb_PP^T; Linvb0 = A Zb_PP + Ab (per warp)
     double lvb[2];
     {
-      double h[4][2] = {};
+      double h0 = 0.0, h1 = 0.0;
 #pragma unroll
-      for (int t = 0; t < NT; ++t) mm(h[t & 3], lp + (8 + 8 * t) * 8, true, sm.zt[t], false);
+      for (int w2 = 0; w2 < NW; ++w2) {
+        const double2 p2 = get(sm.ph[w2]);
+        h0 += p2.x;
+        h1 += p2.y;
+      }
       const double2 l2 = get(lin);
-      put(sm.am[warp], l2.x - ((h[0][0] + h[1][0]) + (h[2][0] + h[3][0])),
-          l2.y - ((h[0][1] + h[1][1]) + (h[2][1] + h[3][1])));
+      put(sm.am[warp], l2.x - h0, l2.y - h1);
       __syncwarp();
       // Zb_PP = (W2_PP + diag(S-bar_ii)) / 2
       const double* wpp = &sm.w[0][0] + sm.ws[0];
@@ -1939,9 +1948,11 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
 #pragma unroll
     for (int i = 0; i < TPW; ++i) {
       const int t = warp + NW * i;
-      double acc[2] = {-la[i][0], -la[i][1]};
+      double acc[2] = {-la[i][0], -la[i][1]}, acc2[2] = {0.0, 0.0};
 #pragma unroll
-      for (int u = 0; u < NT; ++u) mm(acc, &sm.z[0][0] + sm.zs[t * NT + u], t < u, sm.yb[u], false);
+      for (int u = 0; u < NT; ++u) mm(u & 1 ? acc2 : acc, &sm.z[0][0] + sm.zs[t * NT + u], t < u, sm.yb[u], false);
+      acc[0] += acc2[0];
+      acc[1] += acc2[1];
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const ix col = 8 * pb + c2 + v;
