@@ -252,6 +252,57 @@ __global__ void k_outer(Vec<T> m, Vec<T> v, T alpha, Band<T> o, ix batch) {
   o.write_column(b, j, [&](ix i) { return alpha * (m(b, i) * vj); });
 }
 
+// Whole-band writers in storage order: thread x of tile group g writes the
+// x-th element of the group's (n, w, tile) block, so every store is
+// coalesced in both layouts (tile 1 columns are contiguous w-cell runs);
+// f(b, i, j, r) gives the in-band value, corners and batch padding get 0.
+template <class T, class F>
+__global__ void k_band_flat(Band<T> o, ix batch, F f) {
+  const ix g = blockIdx.y;
+  const unsigned tile = 1u << o.s;
+  const unsigned per = unsigned(o.n * o.w) << o.s;
+  for (unsigned x = blockIdx.x * blockDim.x + threadIdx.x; x < per; x += gridDim.x * blockDim.x) {
+    const unsigned cr = x >> o.s;
+    const unsigned j = cr / unsigned(o.w), r = cr - j * unsigned(o.w);
+    const ix b = g * tile + (x & (tile - 1));
+    const ix i = ix(j) - o.up + r;
+    T val = T(0);
+    if (b < batch && i >= 0 && i < o.n) val = f(b, i, ix(j), int(r));
+    o.p[g * ix(per) + x] = val;
+  }
+}
+
+template <class T>
+struct OuterF {  // alpha m_i v_j
+  Vec<T> m, v;
+  T a;
+  __device__ __forceinline__ T operator()(ix b, ix i, ix j, int) const { return a * (m(b, i) * v(b, j)); }
+};
+
+template <class T>
+struct LogDetBarF {  // c / L_jj on the diagonal (grad.cpp:172-176)
+  Band<T> l;
+  const T* c;
+  __device__ __forceinline__ T operator()(ix b, ix, ix j, int r) const { return r == 0 ? c[b] / l.at(b, j, j) : T(0); }
+};
+
+template <class T>
+static bool flat_ok(const Band<T>& o, ix batch) {
+  const ix groups = (batch + (ix(1) << o.s) - 1) >> o.s;
+  return groups > 0 && groups <= 65535 && (o.n * o.w << o.s) < (ix(1) << 32);
+}
+
+template <class T, class F>
+static void launch_flat(const Band<T>& o, ix batch, F f, cudaStream_t s) {
+  const ix groups = (batch + (ix(1) << o.s) - 1) >> o.s;
+  const ix per = o.n * o.w << o.s;
+  ix gx = (per + 255) / 256;
+  const ix cap = (ix(148) * 16 + groups - 1) / groups;  // ~16 blocks per SM in total
+  if (gx > cap) gx = cap;
+  if (gx < 1) gx = 1;
+  k_band_flat<T><<<dim3(unsigned(gx), unsigned(groups)), 256, 0, s>>>(o, batch, f);
+}
+
 // Pivot pre-check shared by solve_mat (kernels.cpp:43-45).
 template <class T>
 __global__ void k_pivot_check(Band<T> l, ix batch, int32_t* status, int64_t* row) {
@@ -425,9 +476,15 @@ template <class T>
 static int run_outer(const bgm_vec& m, const bgm_vec& v, double alpha, const bgm_band& o,
                      cudaStream_t s) {
   const ix work = bj_work(o.batch, o.n, tile_shift(o.tile));
-  if (work)
-    k_outer<T><<<blocks_for(work, kThreads), kThreads, 0, s>>>(view<T>(m), view<T>(v), T(alpha),
-                                                               view<T>(o), o.batch);
+  if (!work) return launched();
+  const Band<T> ob = view<T>(o);
+  if (flat_ok(ob, o.batch)) {
+    const Vec<T> mv = view<T>(m), vv = view<T>(v);
+    const T a = T(alpha);
+    launch_flat(ob, o.batch, OuterF<T>{mv, vv, a}, s);
+  } else {
+    k_outer<T><<<blocks_for(work, kThreads), kThreads, 0, s>>>(view<T>(m), view<T>(v), T(alpha), ob, o.batch);
+  }
   return launched();
 }
 
@@ -743,8 +800,12 @@ int bgm_vjp_log_det(bgm_band l, const void* cbar, bgm_band lbar, bgm_stream stre
   return dispatch(l.dtype, [&](auto z) {
     using T = decltype(z);
     const ix work = bj_work(l.batch, l.n, tile_shift(lbar.tile));
-    k_vjp_log_det<T><<<blocks_for(work, kThreads), kThreads, 0, s>>>(
-        view<T>(l), static_cast<const T*>(cbar), view<T>(lbar), l.batch);
+    const Band<T> lb = view<T>(lbar), lv = view<T>(l);
+    const T* c = static_cast<const T*>(cbar);
+    if (flat_ok(lb, l.batch))
+      launch_flat(lb, l.batch, LogDetBarF<T>{lv, c}, s);
+    else
+      k_vjp_log_det<T><<<blocks_for(work, kThreads), kThreads, 0, s>>>(lv, c, lb, l.batch);
     return launched();
   });
 }

@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <initializer_list>
 #include <cstdio>
 #include <cstdlib>
 
@@ -2918,10 +2919,89 @@ bool run_vsub(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, const b
 }
 }  // namespace
 
+// fp32 bands on the FP64 tensor-core paths: the band is widened into an fp64
+// scratch copy of the same layout, the fp64 kernel runs, the result is
+// narrowed back (conversion traffic is a few MB against a compute-bound op;
+// the arithmetic is then fp64, tighter than the reference's fp32 loop)
+__global__ void k_widen(const float* a, double* b, ix count) {
+  for (ix i = blockIdx.x * ix(blockDim.x) + threadIdx.x; i < count; i += ix(gridDim.x) * blockDim.x) b[i] = a[i];
+}
+__global__ void k_narrow(const double* a, float* b, ix count) {
+  for (ix i = blockIdx.x * ix(blockDim.x) + threadIdx.x; i < count; i += ix(gridDim.x) * blockDim.x)
+    b[i] = float(a[i]);
+}
+
+static ix band_count(const bgm_band& x) {
+  return (x.batch + x.tile - 1) / x.tile * x.tile * x.n * (x.lower + x.upper + 1);
+}
+
+struct Widened {
+  bgm_band d{};
+  bool ok = false;
+  Widened(const bgm_band& x, bool copy, cudaStream_t s) {
+    d = x;
+    d.dtype = BGM_F64;
+    const ix cnt = band_count(x);
+    if (scratch_alloc(&d.data, sizeof(double) * size_t(cnt) + 16, s) != cudaSuccess) return;
+    if (copy) k_widen<<<1184, 256, 0, s>>>(static_cast<const float*>(x.data), static_cast<double*>(d.data), cnt);
+    ok = true;
+  }
+  void narrow_into(const bgm_band& x, cudaStream_t s) const {
+    k_narrow<<<1184, 256, 0, s>>>(static_cast<const double*>(d.data), static_cast<float*>(x.data), band_count(x));
+  }
+  void release(cudaStream_t s) {
+    if (ok) scratch_free(d.data, s);
+    ok = false;
+  }
+};
+
+static bool wide32() {
+  static const bool on = [] {
+    const char* e = std::getenv("BGM_WIDE_F32_DMMA");
+    const char* d = std::getenv("BGM_WIDE_DMMA");
+    return !(e && e[0] == '0') && !(d && d[0] == '0');
+  }();
+  return on;
+}
+
+// run an fp64 entry point on widened copies of fp32 operands
+template <class F>
+bool via_f64(std::initializer_list<const bgm_band*> in, std::initializer_list<const bgm_band*> out, cudaStream_t s,
+             F&& run) {
+  Widened* w[8];
+  int nw = 0;
+  bool ok = true;
+  for (const bgm_band* x : in) {
+    w[nw] = new Widened(*x, true, s);
+    ok = ok && w[nw++]->ok;
+  }
+  for (const bgm_band* x : out) {
+    w[nw] = new Widened(*x, false, s);
+    ok = ok && w[nw++]->ok;
+  }
+  if (ok) {
+    bgm_band d[8];
+    for (int i = 0; i < nw; ++i) d[i] = w[i]->d;
+    ok = run(d);
+    if (ok) {
+      int j = int(in.size());
+      for (const bgm_band* x : out) w[j++]->narrow_into(*x, s);
+    }
+  }
+  for (int i = 0; i < nw; ++i) {
+    w[i]->release(s);
+    delete w[i];
+  }
+  return ok;
+}
+
 bool cholesky(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, cudaStream_t s) {
   if (q.lower != l.lower || q.upper != 0 || l.upper != 0 || q.batch == 0 || q.n == 0) return false;
   if (q.n < 4 * q.lower) return false;  // short matrices: the generic sweep is fine
   const bool f64 = q.dtype == BGM_F64;
+  if (!f64 && (q.lower == 64 || q.lower == 128) && wide32() &&
+      via_f64({&q}, {&l}, s, [&](bgm_band* d) { return cholesky(d[0], d[1], st, row, s); }))
+    return true;
   switch (q.lower) {
     case 64: {
       static const bool use_dmma = [] {
@@ -2962,6 +3042,9 @@ bool subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cu
   if (l.lower != sb.lower || l.upper != 0 || sb.upper != 0 || l.batch == 0 || l.n == 0) return false;
   if (l.n < 4 * l.lower) return false;
   const bool f64 = l.dtype == BGM_F64;
+  if (!f64 && (l.lower == 64 || l.lower == 128) && wide32() &&
+      via_f64({&l}, {&sb}, s, [&](bgm_band* d) { return subset(d[0], d[1], st, row, s); }))
+    return true;
   static const bool use_dmma = [] {
     const char* e = std::getenv("BGM_WIDE_DMMA");
     return !(e && e[0] == '0');
@@ -3004,6 +3087,9 @@ bool vjp_cholesky(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cud
       l.batch == 0 || l.n < 4 * l.lower)
     return false;
   const bool f64 = l.dtype == BGM_F64;
+  if (!f64 && (l.lower == 64 || l.lower == 128) && wide32() &&
+      via_f64({&l, &lb}, {&qb}, s, [&](bgm_band* d) { return vjp_cholesky(d[0], d[1], d[2], s); }))
+    return true;
   static const bool use_dmma = [] {
     const char* e = std::getenv("BGM_WIDE_DMMA");
     return !(e && e[0] == '0');
@@ -3031,6 +3117,9 @@ bool vjp_subset(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, const
                 int64_t* row, cudaStream_t s) {
   if (l.upper != 0 || l.batch == 0 || l.n < 4 * l.lower) return false;
   const bool f64 = l.dtype == BGM_F64;
+  if (!f64 && (l.lower == 64 || l.lower == 128) && wide32() &&
+      via_f64({&l, &sm, &sb}, {&lb}, s, [&](bgm_band* d) { return vjp_subset(d[0], d[1], d[2], d[3], st, row, s); }))
+    return true;
   static const bool use_dmma = [] {
     const char* e = std::getenv("BGM_WIDE_DMMA");
     return !(e && e[0] == '0');

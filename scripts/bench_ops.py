@@ -246,7 +246,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="1,2,4")
     ap.add_argument("--reps", type=int, default=5)
-    ap.add_argument("--wide-vjp", action="store_true", help="also time the wide vjp_cholesky / vjp_subset")
+    ap.add_argument("--no-wide-vjp", dest="wide_vjp", action="store_false",
+                    help="skip the wide vjp_cholesky / vjp_subset")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
