@@ -2322,6 +2322,190 @@ __global__ void __launch_bounds__(32 * NW) k_vchol_dmma_repair(VdP<double> C, Ge
   vchol_dmma_unit<K, NW>(C, b, G.n, 0, G.n, G.n, nullptr, nullptr, sm);
 }
 
+// ------------------------------------------------------------------ subset, FP64 DMMA, multi-warp
+// The blocked Takahashi recursion of k_subset_dmma on a CTA of NW warps with
+// the machinery of k_vsub_dmma (swizzled tiles, rings holding NT+1-d tiles
+// per diagonal, per-panel slot tables).  Warps own the tile rows
+// t = warp (mod NW) of Y = Z_TT L_TP and Z_TP = -Y L_PP^-1 and their share of
+// L_TP^T Z_TP; warp 0 then forms Z_PP while the other warps already start the
+// next panel (its row 0 is the only consumer of Z_PP).  One barrier per
+// panel: the slot tables, the partial sums and the L panel are double
+// buffered, and each panel's new tiles go to slots no warp reads in it.
+template <int K, int NW>
+struct TakMwSmem {
+  static constexpr int NT = K / 8;
+  static constexpr int NZ = NT * (NT + 3) / 2;
+  double z[NZ][64];
+  double lp[2][(K + 8) * 8];
+  double y[NT][64], zt[NT][64];
+  double lin[NW][64], ph[2][NW][64], hm[64];
+  int zs[2][NT * NT];
+  unsigned mg[NT + 2];
+};
+
+template <int K, int NW>
+__device__ void subset_mw_unit(const SubP<double>& C, ix b, ix n, ix s, ix e, ix jend, double* side,
+                               TakMwSmem<K, NW>& sm) {
+  constexpr int NT = K / 8, NTH = 32 * NW, TPW = NT / NW;
+  static_assert(NT % NW == 0, "warps must divide the tile rows");
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, rr = lane >> 2, q = lane & 3, c2 = 2 * q;
+  const int o0[2] = {sw8(rr, q), sw8(rr, 4 + q)}, o1[2] = {sw8(q, rr), sw8(4 + q, rr)};
+  const int oc = sw8(rr, c2);
+  auto mm = [&](double* acc, const double* X, bool tx, const double* Y, bool ty) {
+#pragma unroll
+    for (int kc = 0; kc < 2; ++kc) dmma(acc[0], acc[1], X[tx ? o1[kc] : o0[kc]], Y[ty ? o0[kc] : o1[kc]]);
+  };
+  auto put = [&](double* T, double v0, double v1) { *reinterpret_cast<double2*>(T + oc) = make_double2(v0, v1); };
+  auto get = [&](const double* T) { return *reinterpret_cast<const double2*>(T + oc); };
+  const BRow lrow = brow(C.l, b), srow = brow(C.s, b);
+  const ix pb_top = (jend - 1) / 8, pb_end = s / 8;
+  const bool exact_top = 8 * (pb_top + 1) >= n;  // window below the top panel is all padding
+  for (int x = tid; x < NT + 2; x += NTH) sm.mg[x] = x ? 0xFFFFFFFFu / unsigned(x) + 1u : 0u;
+  for (int x = tid; x < TakMwSmem<K, NW>::NZ * 64; x += NTH) {  // diagonal ring d = 0: slots [0, NT+1)
+    const int t = x >> 6, m = (x >> 3) & 7, c = x & 7;
+    (&sm.z[0][0])[x] = (exact_top && t <= NT && m == c) ? 1.0 : 0.0;
+  }
+  const int fc = tid & 7, fr = tid >> 3;
+  auto fill = [&](int buf, ix pb) {  // L rows [8pb, 8pb+K+8) x cols [8pb, 8pb+8), identity past n
+    const ix col = 8 * pb + fc;
+    const double* colp = lrow.at(0, col);
+#pragma unroll
+    for (int i = 0; i < (K + 8 + NTH / 8 - 1) / (NTH / 8); ++i) {
+      const int r = fr + (NTH / 8) * i, cell = r - fc;
+      if (r < K + 8) {
+        double* dst = sm.lp[buf] + sw8(r, fc);
+        if (cell >= 0 && cell <= K && 8 * pb + r < n) cpa(dst, colp + (ix(cell) << lrow.s));
+        else *dst = (cell == 0) ? 1.0 : 0.0;
+      }
+    }
+  };
+  auto tables = [&](ix pb) {
+    int* zs = sm.zs[pb & 1];
+    for (int x = tid; x < NT * NT; x += NTH) {
+      const int t = x / NT, u = x % NT;
+      zs[x] = ring_slot<K>(t > u ? t - u : u - t, pb + 1 + (t < u ? t : u), sm.mg) * 64;
+    }
+  };
+  // S cell (8pb + rr + rofs, 8pb + c2 + v) of this lane's fragment
+  auto out = [&](ix pb, int rofs, const double* v2) {
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const ix col = 8 * pb + c2 + v;
+      const int cell = rofs + rr - c2 - v;
+      if (cell < 0 || cell > K || col >= n) continue;
+      const double w = (col + cell < n) ? v2[v] : 0.0;
+      if (col >= s && col < e) *srow.at(cell, col) = w;
+      else if (side && col >= e && col < e + K) side[(col - e) * (K + 1) + cell] = w;
+    }
+  };
+  __syncthreads();
+  tables(pb_top);
+  fill(0, pb_top);
+  cpa_commit();
+  cpa_wait0();
+  __syncthreads();
+  int buf = 0;
+#pragma unroll 1
+  for (ix pb = pb_top; pb >= pb_end; --pb) {
+    if (pb > pb_end) fill(buf ^ 1, pb - 1);
+    cpa_commit();
+    const double* lp = sm.lp[buf];
+    const int* zs = sm.zs[pb & 1];
+    double* lin = sm.lin[warp];
+    {  // Linv (per warp)
+      double M0 = rr == c2 ? 1.0 : 0.0, M1 = rr == c2 + 1 ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (rr == k) {
+          const double ri = 1.0 / lp[sw8(k, k)];
+          M0 *= ri;
+          M1 *= ri;
+        }
+        const double mk0 = __shfl_sync(0xffffffffu, M0, 4 * k + q);
+        const double mk1 = __shfl_sync(0xffffffffu, M1, 4 * k + q);
+        if (rr > k) {
+          const double lrk = lp[sw8(rr, k)];
+          M0 = fma(-lrk, mk0, M0);
+          M1 = fma(-lrk, mk1, M1);
+        }
+      }
+      put(lin, M0, M1);
+    }
+    {
+      double ya[TPW][2][2];
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) {
+        const int t = warp + NW * i;
+        ya[i][0][0] = ya[i][0][1] = ya[i][1][0] = ya[i][1][1] = 0.0;
+#pragma unroll
+        for (int u = 0; u < NT; ++u) mm(ya[i][u & 1], &sm.z[0][0] + zs[t * NT + u], t < u, lp + (8 + 8 * u) * 8, false);
+      }
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) put(sm.y[warp + NW * i], ya[i][0][0] + ya[i][1][0], ya[i][0][1] + ya[i][1][1]);
+      __syncwarp();
+      double h[2] = {0.0, 0.0};
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) {
+        const int t = warp + NW * i;
+        double zz[2] = {0.0, 0.0};
+        mm(zz, sm.y[t], false, lin, false);
+        zz[0] = -zz[0];
+        zz[1] = -zz[1];
+        put(sm.zt[t], zz[0], zz[1]);
+        if (t + 1 < NT) put(&sm.z[0][0] + ring_slot<K>(t + 1, pb, sm.mg) * 64, zz[0], zz[1]);
+        out(pb, 8 + 8 * t, zz);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) mm(h, lp + (8 + 8 * (warp + NW * i)) * 8, true, sm.zt[warp + NW * i], false);
+      put(sm.ph[pb & 1][warp], h[0], h[1]);
+    }
+    if (pb > pb_end) tables(pb - 1);
+    cpa_wait0();
+    __syncthreads();
+    if (warp == 0) {  // Z_PP = (Linv - L_TP^T Z_TP)^T Linv -> tile (pb, pb), S cells
+      double h0 = 0.0, h1 = 0.0;
+#pragma unroll
+      for (int w2 = 0; w2 < NW; ++w2) {
+        const double2 p2 = get(sm.ph[pb & 1][w2]);
+        h0 += p2.x;
+        h1 += p2.y;
+      }
+      const double2 l2 = get(lin);
+      put(sm.hm, l2.x - h0, l2.y - h1);
+      __syncwarp();
+      double zp[2] = {0.0, 0.0};
+      mm(zp, sm.hm, true, lin, false);
+      put(&sm.z[0][0] + ring_slot<K>(0, pb, sm.mg) * 64, zp[0], zp[1]);
+      out(pb, 0, zp);
+      __syncwarp();
+    }
+    buf ^= 1;
+  }
+}
+
+template <int K, int NW>
+__global__ void __launch_bounds__(32 * NW) k_subset_mw(SubP<double> C, Geo G) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  TakMwSmem<K, NW>& sm = *reinterpret_cast<TakMwSmem<K, NW>*>(smraw);
+  const ix unit = blockIdx.x;
+  const ix b = unit / G.nseg;
+  const int p = int(unit % G.nseg);
+  if (b >= G.batch) return;
+  const ix s = ix(p) * G.seg, e = s + G.seg < G.n ? s + G.seg : G.n;
+  const ix jend = e + G.burn < G.n ? e + G.burn : G.n;
+  subset_mw_unit<K, NW>(C, b, G.n, s, e, jend, p + 1 < G.nseg ? C.side + unit * ix(K) * (K + 1) : nullptr, sm);
+}
+
+template <int K, int NW>
+__global__ void __launch_bounds__(32 * NW) k_subset_mw_repair(SubP<double> C, Geo G) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  TakMwSmem<K, NW>& sm = *reinterpret_cast<TakMwSmem<K, NW>*>(smraw);
+  const ix b = blockIdx.x;
+  if (b >= G.batch || !C.flag[b]) return;
+  subset_mw_unit<K, NW>(C, b, G.n, 0, G.n, G.n, nullptr, sm);
+}
+
 int g_segment_rows = 0;
 
 template <class T, int K, int P, int TS>
@@ -2619,6 +2803,65 @@ bool run_vchol_dmma(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, c
   }
   const ix zw = ((G.batch + l.tile - 1) / l.tile * l.tile) * K * (K + 1);
   k_zero_corners_w<double><<<blocks_for(zw, 128), 128, 0, s>>>(C.qb, G.batch);
+  scratch_free(ws, s);
+  return true;
+}
+
+template <int K, int NW>
+bool run_subset_mw(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cudaStream_t s) {
+  const size_t smem = sizeof(TakMwSmem<K, NW>);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_subset_mw<K, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_subset_mw_repair<K, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = true;
+  }
+  Geo G;
+  G.batch = l.batch;
+  G.n = l.n;
+  G.burn = kBurnGen * K;
+  if (const char* bv = std::getenv("BGM_WIDE_BURN"))
+    if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
+  G.burn = (G.burn + 7) / 8 * 8;
+  int sms = 148, dev = 0, per = 1;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_subset_mw<K, NW>, 32 * NW, smem);
+  if (per < 1) per = 1;
+  ix seg = g_segment_rows;
+  if (seg <= 0) {
+    const int ns = pick_nseg(G.batch, G.n, sms * per, G.burn, 2 * G.burn);
+    seg = (G.n + ns - 1) / ns;
+  }
+  seg = (seg + 7) / 8 * 8;
+  if (seg < K) seg = (K + 7) / 8 * 8;
+  G.seg = seg;
+  G.nseg = int((G.n + seg - 1) / seg);
+  const ix units = G.batch * G.nseg;
+  const size_t side_bytes = sizeof(double) * size_t(units) * K * (K + 1);
+  char* ws = nullptr;
+  if (scratch_alloc(reinterpret_cast<void**>(&ws), side_bytes + 12 * size_t(G.batch) + 64, s) != cudaSuccess)
+    return false;
+  SubP<double> C;
+  C.l = view<double>(l);
+  C.s = view<double>(sb);
+  C.side = reinterpret_cast<double*>(ws);
+  int64_t* fail = reinterpret_cast<int64_t*>(ws + side_bytes);
+  C.flag = reinterpret_cast<int32_t*>(fail + G.batch);
+  k_init<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, C.flag, G.batch, G.n);
+  k_diag_check<double><<<blocks_for(G.batch * G.n, 256), 256, 0, s>>>(C.l, G.batch, fail);
+  {
+    timing::Scope ts("wide_subset_mw", s);
+    k_subset_mw<K, NW><<<unsigned(units), 32 * NW, smem, s>>>(C, G);
+  }
+  {
+    timing::Scope ts("wide_subset_check", s);
+    k_subset_check<double, K><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
+  }
+  {
+    timing::Scope ts("wide_subset_repair", s);
+    k_subset_mw_repair<K, NW><<<unsigned(G.batch), 32 * NW, smem, s>>>(C, G);
+  }
+  k_status_code<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, G.batch, G.n, BGM_ERR_SINGULAR, st, row);
   scratch_free(ws, s);
   return true;
 }
@@ -3038,6 +3281,14 @@ bool cholesky(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, c
   }
 }
 
+static int subset_warps() {  // BGM_SUBSET_WARPS: 1 = single-warp kernel
+  static const int w = [] {
+    const char* e = std::getenv("BGM_SUBSET_WARPS");
+    return e ? std::atoi(e) : 0;  // 0: 4 warps for k = 64, 8 for k = 128
+  }();
+  return w;
+}
+
 bool subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cudaStream_t s) {
   if (l.lower != sb.lower || l.upper != 0 || sb.upper != 0 || l.batch == 0 || l.n == 0) return false;
   if (l.n < 4 * l.lower) return false;
@@ -3051,10 +3302,18 @@ bool subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cu
   }();
   switch (l.lower) {
     case 64:
-      if (f64 && use_dmma) return run_subset_dmma<64>(l, sb, st, row, s);
+      if (f64 && use_dmma) {
+        const int nw = subset_warps();
+        if (nw == 1) return run_subset_dmma<64>(l, sb, st, row, s);
+        return nw == 2 ? run_subset_mw<64, 2>(l, sb, st, row, s) : run_subset_mw<64, 4>(l, sb, st, row, s);
+      }
       return f64 ? run_subset<double, 64, 8, 9>(l, sb, st, row, s) : run_subset<float, 64, 8, 9>(l, sb, st, row, s);
     case 128:
-      if (f64 && use_dmma) return run_subset_dmma<128>(l, sb, st, row, s);
+      if (f64 && use_dmma) {
+        const int nw = subset_warps();
+        if (nw == 1) return run_subset_dmma<128>(l, sb, st, row, s);
+        return nw == 4 ? run_subset_mw<128, 4>(l, sb, st, row, s) : run_subset_mw<128, 8>(l, sb, st, row, s);
+      }
       return f64 ? run_subset<double, 128, 16, 9>(l, sb, st, row, s)
                  : run_subset<float, 128, 16, 9>(l, sb, st, row, s);
     default: return false;
