@@ -468,81 +468,86 @@ __global__ void k_diag_small(Band<T> l, ix batch, int64_t* fail) {
 }
 
 // ------------------------------------------------------------------ vjp_cholesky
-// grad.cpp:11-36 (Giles' reverse sweep).  Row i of q_bar solves
-//   q_i = 1/2 r_i / L(i,i),   q_j = (r_j - 2 q_i L(i,j) - sum_{j<j'<i} q_j' L(j',j)) / L(j,j)
-// (r = the current l_bar row i; left-looking, so column j of L is read
-// contiguously), then the rows above are updated l_bar(j,k) -= q_j L(i,k)
-// (k <= j; k = j is the reference's diagonal update).  Window: l_bar over
-// rows [i-K, i] x cols [i-K, row], packed [entry][thread], index (x, y) =
-// (row - (i-K), col - (i-K)); each step drops row i and takes column i-K-1
-// of the input.
+// Reverse of the right-looking column Cholesky (the same gradient as Giles'
+// row sweep of grad.cpp:11-36, in the order that reads every input once):
+// the forward's column j sets L(j,j) = sqrt(A(j,j)), L(i,j) = A(i,j)/L(j,j)
+// and updates the trailing K x K window A(i,i') -= L(i,j) L(i',j), so from
+// the bottom up, with Ab the (lower-stored, final) q_bar window of the rows
+// below j,
+//   g_x = l_bar(j+1+x, j) - sum_y (Ab + Ab^T)(x, y) L(j+1+y, j)
+//   q_bar(j+1+x, j) = g_x / L(j,j)
+//   q_bar(j, j) = (l_bar(j,j) - sum_x g_x L(j+1+x, j) / L(j,j)) / (2 L(j,j)).
+// Window: Ab over rows/cols (j, j+K], packed [entry][thread]; one pass reads
+// each entry once (two FMAs) and moves it to (x+1, y+1) in memmove order, the
+// new column enters at y = 0.  Input columns are read once, coalesced across
+// the warp's 32 matrices.
 template <class T>
 struct VcholP {
   Band<T> l, lb, qb;
-  T* side;  // [unit][K][K+1]
+  T* side;  // [unit][K][K+1]: burn-in q_bar columns [e, e+K)
   int32_t* flag;
 };
 
 template <class T, int K>
 __device__ void vchol_unit(const VcholP<T>& C, ix b, ix n, ix s, ix e, ix start, T* side, T* win) {
   constexpr int W = K + 1, ts = kThreads;
-  auto Wb = [&](int x, int y) -> T& { return win[tri(x, y) * ts]; };
+  auto Wa = [&](int x, int y) -> T& { return win[tri(x, y) * ts]; };
   const T* lbase = bbase(C.l, b);
   const T* gbase = bbase(C.lb, b);
   T* qbase = bbase(C.qb, b);
   const ix cs = ix(W) * 32;
-  auto L = [&](ix r, ix c) -> T {  // L(r, c), 0 <= r - c <= K
-    return (c >= 0 && r < n) ? lbase[c * cs + (r - c) * 32] : T(0);
-  };
-  // window for row `start`: input l_bar rows [start-K, start], cols [start-K, row]
-#pragma unroll 1
-  for (int x = 0; x <= K; ++x)
-    for (int y = 0; y <= x; ++y) {
-      const ix r = start - K + x, c = start - K + y;
-      Wb(x, y) = (c >= 0 && r < n) ? gbase[c * cs + (x - y) * 32] : T(0);
-    }
-#pragma unroll 1
-  for (ix i = start; i >= s; --i) {
-    T r[W], lr[W], q[W];
 #pragma unroll
-    for (int y = 0; y <= K; ++y) {
-      r[y] = Wb(K, y);
-      lr[y] = L(i, i - K + y);
+  for (int x = 0; x < K * (K + 1) / 2; ++x) win[x * ts] = T(0);  // burn-in (or rows past n)
+#pragma unroll 1
+  for (ix j = start; j >= s; --j) {
+    const T* lc = lbase + j * cs;
+    const T* gc = gbase + j * cs;
+    T u[K], g[K];
+#pragma unroll
+    for (int x = 0; x < K; ++x) {
+      const bool in = j + 1 + x < n;
+      u[x] = in ? lc[(x + 1) * 32] : T(0);
+      g[x] = in ? gc[(x + 1) * 32] : T(0);
     }
-    q[K] = T(0.5) * r[K] / lr[K];
+    const T d = lc[0];
+    T gd = gc[0];
 #pragma unroll
     for (int x = K - 1; x >= 0; --x) {
-      const ix j = i - K + x;
-      if (j < 0) {
-        q[x] = T(0);
-        continue;
+#pragma unroll
+      for (int y = x; y >= 0; --y) {
+        const T v = Wa(x, y);
+        if (x == y) {
+          g[x] = fma(T(-2) * v, u[x], g[x]);
+        } else {
+          g[x] = fma(-v, u[y], g[x]);
+          g[y] = fma(-v, u[x], g[y]);
+        }
+        if (x < K - 1) Wa(x + 1, y + 1) = v;
       }
-      const T* colj = lbase + j * cs;
-      T acc = fma(T(-2) * q[K], lr[x], r[x]);
-#pragma unroll
-      for (int x2 = x + 1; x2 < K; ++x2) acc = fma(-q[x2], colj[(x2 - x) * 32], acc);
-      q[x] = acc / colj[0];
+      if (x % 4 == 0) asm volatile("" ::: "memory");  // bound the hoisted window loads
     }
-    // q_bar row i (stored at cell (i - j, j)), or the burn-in copy
-    if (i < e) {
+    const T rd = T(1) / d;
+    T a[K];
 #pragma unroll
-      for (int x = 0; x <= K; ++x)
-        if (i - K + x >= 0) qbase[(i - K + x) * cs + (K - x) * 32] = q[x];
-    } else if (side && i < e + K) {
-      T* sd = side + (i - e) * W;
-#pragma unroll
-      for (int x = 0; x <= K; ++x) sd[x] = q[x];
+    for (int x = 0; x < K; ++x) {
+      a[x] = g[x] * rd;
+      gd = fma(-a[x], u[x], gd);
     }
-    // rank-1 update of rows [i-K, i-1] and the shift to row i-1's window:
-    // (x, y) -> (x+1, y+1), decreasing packed index = in-place memmove order
+    const T ad = T(0.5) * gd * rd;
+    Wa(0, 0) = ad;
 #pragma unroll
-    for (int x = K - 1; x >= 0; --x) {
+    for (int x = 0; x + 1 < K; ++x) Wa(x + 1, 0) = a[x];
+    if (j < e) {
+      T* qc = qbase + j * cs;
+      qc[0] = ad;
 #pragma unroll
-      for (int y = x; y >= 0; --y) Wb(x + 1, y + 1) = fma(-q[x], lr[y], Wb(x, y));
+      for (int x = 0; x < K; ++x) qc[(x + 1) * 32] = (j + 1 + x < n) ? a[x] : T(0);
+    } else if (side && j < e + K) {
+      T* sd = side + (j - e) * W;
+      sd[0] = ad;
+#pragma unroll
+      for (int x = 0; x < K; ++x) sd[x + 1] = (j + 1 + x < n) ? a[x] : T(0);
     }
-    const ix c = i - 1 - K;  // entering column (rows c .. c+K)
-#pragma unroll
-    for (int x = 0; x <= K; ++x) Wb(x, 0) = (c >= 0 && c + x < n) ? gbase[c * cs + x * 32] : T(0);
   }
 }
 
@@ -558,7 +563,7 @@ __global__ void k_vchol(VcholP<T> C, Geo G) {
                    sm + threadIdx.x);
 }
 
-// thread per (unit, row): q_bar rows [e, e+K) from burn-in vs genuine
+// thread per (unit, column): q_bar columns [e, e+K) from burn-in vs genuine
 template <class T, int K>
 __global__ void k_vchol_check(VcholP<T> C, Geo G) {
   const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
@@ -567,17 +572,14 @@ __global__ void k_vchol_check(VcholP<T> C, Geo G) {
   if (id >= G.batch * G.nseg) return;
   const int p = int(id % G.nseg);
   if (p + 1 >= G.nseg) return;
-  const ix b = id / G.nseg, i = ix(p + 1) * G.seg + c;
-  if (i >= G.n) return;
+  const ix b = id / G.nseg, j = ix(p + 1) * G.seg + c;
+  if (j >= G.n) return;
   const T* sd = C.side + (id * K + c) * (K + 1);
   double sc = 0.0;
-  for (int x = 0; x <= K; ++x)
-    if (i - K + x >= 0) sc = fmax(sc, dabs(C.qb.cell(b, K - x, i - K + x)));
+  for (int r = 0; r <= K; ++r) sc = fmax(sc, dabs(C.qb.cell(b, r, j)));
   const double tol = sizeof(T) == 8 ? kCheckTol : 1e-5;
   bool bad = false;
-  for (int x = 0; x <= K; ++x)
-    if (i - K + x >= 0)
-      bad |= !(fabs(double(sd[x]) - double(C.qb.cell(b, K - x, i - K + x))) <= tol * (sc + 1e-300));
+  for (int r = 0; r <= K; ++r) bad |= !(fabs(double(sd[r]) - double(C.qb.cell(b, r, j))) <= tol * (sc + 1e-300));
   if (bad) C.flag[b] = 1;
 }
 
