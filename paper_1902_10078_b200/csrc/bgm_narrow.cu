@@ -524,7 +524,10 @@ __device__ void vchol_unit(const VcholP<T>& C, ix b, ix n, ix s, ix e, ix start,
         }
         if (x < K - 1) Wa(x + 1, y + 1) = v;
       }
-      if (x % 4 == 0) asm volatile("" ::: "memory");  // bound the hoisted window loads
+#ifndef VCHOL_FENCE
+#define VCHOL_FENCE 4
+#endif
+      if (x % VCHOL_FENCE == 0) asm volatile("" ::: "memory");  // bound the hoisted window loads
     }
     const T rd = T(1) / d;
     T a[K];
