@@ -64,10 +64,100 @@ __global__ void k_product_stride(Band<T> A, int ta, Band<T> Bm, int tb, Band<T> 
   }
 }
 
+
+// Register-blocked products for the benchmarked band shapes: one thread per
+// (matrix, block of J output columns).  op(A) has bands (AL, AU), op(B)
+// (BL, BU), the output (CL, CU) (full or restricted); all compile-time, so
+// the J x (CL+CU+1) accumulators stay in registers and every op(A) column is
+// loaded once per block instead of once per output cell: for output columns
+// j0 .. j0+J-1 the sweep runs k = j0-BU .. j0+J-1+BL, loads op(A)(:, k) and
+// op(B)(k, j) and scatters the products into the cells they belong to.
+template <class T, int TA, int TB, int AL, int AU, int BL, int BU, int CL, int CU, int J>
+__global__ void __launch_bounds__(128) k_product_blk(Band<T> A, Band<T> Bm, Band<T> C, ix batch) {
+  constexpr int AW = AL + AU + 1, CW = CL + CU + 1, NK = J + BL + BU;
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  const ix n = C.n, nblk = (n + J - 1) / J;
+  const ix lanes = ix(1) << C.s;
+  const ix rest = t >> C.s;
+  const ix b = (rest / nblk) * lanes + (t & (lanes - 1));
+  const ix j0 = (rest % nblk) * J;
+  if (b >= batch) return;
+  const T* a = mbase(A, b);
+  const T* bb = mbase(Bm, b);
+  T acc[J][CW];
+#pragma unroll
+  for (int jj = 0; jj < J; ++jj)
+#pragma unroll
+    for (int r = 0; r < CW; ++r) acc[jj][r] = T(0);
+#pragma unroll
+  for (int kk = 0; kk < NK; ++kk) {
+    const ix k = j0 - BU + kk;
+    if (k < 0 || k >= n) continue;
+    T av[AW];
+#pragma unroll
+    for (int x = 0; x < AW; ++x) {  // op(A)(i, k), i = k - AU + x
+      const ix i = k - AU + x;
+      av[x] = (i >= 0 && i < n) ? (TA ? a[(i * A.w + (k - i + A.up)) << A.s] : a[(k * A.w + (i - k + A.up)) << A.s])
+                                : T(0);
+    }
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj) {
+      const int d = kk - BU - jj;  // k - j, compile-time
+      if (d < -BU || d > BL) continue;
+      const ix j = j0 + jj;
+      if (j >= n) continue;
+      const T bv = TB ? bb[(k * Bm.w + (j - k + Bm.up)) << Bm.s] : bb[(j * Bm.w + (k - j + Bm.up)) << Bm.s];
+#pragma unroll
+      for (int x = 0; x < AW; ++x) {
+        const int r = d - AU + x + CU;  // output cell of row i = k - AU + x in column j
+        if (r >= 0 && r < CW) acc[jj][r] = fma(av[x], bv, acc[jj][r]);
+      }
+    }
+  }
+  T* c = const_cast<T*>(mbase(C, b));
+#pragma unroll
+  for (int jj = 0; jj < J; ++jj) {
+    const ix j = j0 + jj;
+    if (j >= n) break;
+#pragma unroll
+    for (int r = 0; r < CW; ++r) {
+      const ix i = j - CU + r;
+      c[(j * C.w + r) << C.s] = (i >= 0 && i < n) ? acc[jj][r] : T(0);
+    }
+  }
+}
+
+template <class T, int TA, int TB, int AL, int AU, int BL, int BU, int CL, int CU>
+bool try_blk(const bgm_band& a, int ta, const bgm_band& b, int tb, const bgm_band& c, cudaStream_t s) {
+  const int al = ta ? a.upper : a.lower, au = ta ? a.lower : a.upper;
+  const int bl = tb ? b.upper : b.lower, bu = tb ? b.lower : b.upper;
+  if (ta != TA || tb != TB || al != AL || au != AU || bl != BL || bu != BU || c.lower != CL || c.upper != CU)
+    return false;
+  constexpr int J = 4;
+  const ix lanes = c.tile;
+  const ix work = (c.batch + lanes - 1) / lanes * lanes * ((c.n + J - 1) / J);
+  timing::Scope t("product_blk", s);
+  k_product_blk<T, TA, TB, AL, AU, BL, BU, CL, CU, J><<<blocks_for(work, 128), 128, 0, s>>>(
+      view<T>(a), view<T>(b), view<T>(c), c.batch);
+  return true;
+}
+
+template <class T>
+bool product_blk(const bgm_band& a, int ta, const bgm_band& b, int tb, const bgm_band& c, cudaStream_t s) {
+  if (c.n < 64) return false;
+  // the full / lower products of configs 2 and 3 (the restricted VJP halves
+  // keep the strided kernel: there most loaded op(A) cells miss the output band)
+  return try_blk<T, 0, 1, 8, 0, 0, 8, 8, 8>(a, ta, b, tb, c, s) ||
+         try_blk<T, 0, 0, 8, 8, 3, 3, 11, 11>(a, ta, b, tb, c, s) ||
+         try_blk<T, 0, 1, 16, 0, 0, 16, 16, 0>(a, ta, b, tb, c, s);
+}
+
 }  // namespace
 
 bool product(const bgm_band& a, int ta, const bgm_band& b, int tb, const bgm_band& c, cudaStream_t s) {
   if (a.n == 0 || c.batch == 0) return false;
+  if (a.dtype == BGM_F64 ? product_blk<double>(a, ta, b, tb, c, s) : product_blk<float>(a, ta, b, tb, c, s))
+    return true;
   timing::Scope t("product", s);
   const ix lanes = c.tile;
   const ix work = (c.batch + lanes - 1) / lanes * lanes * c.n;

@@ -123,3 +123,43 @@ def test_fp32_factorization_path(cuda, oracle):
     v = cm.random_vec(rng, B, n).astype(np.float32).astype(np.float64)
     assert cm.max_rel_err(g32.solve_vec(l_o, v, True)[0], oracle.solve_vec(l_o, v, True)[0]) < 1e-4
     assert cm.max_rel_err(g32.sparse_inverse_subset(l_o)[0], oracle.sparse_inverse_subset(l_o)[0]) < 1e-4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tile", [1, 32])
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("shape", ["llt8", "ab", "llt16_lower"])
+def test_register_blocked_products(cuda, oracle, tile, dtype, shape):
+    """The register-blocked product kernels (bgm_product.cu) serve these band
+    shapes only: L L^T (8,8), A(8,8) B(3,3), precision_from_factor at k=16
+    (inference.cpp:23-26); n not a multiple of the 4-column block."""
+    import paper_1902_10078_b200 as bgm
+    from tests.gpu_adapter import GpuOracle
+    g = GpuOracle(tile=tile, dtype=dtype)
+    rng = np.random.default_rng(hash(shape) % 1000 + tile)
+    B, n = 5, 203
+    if shape == "ab":
+        a = cm.random_band(rng, B, n, 8, 8)
+        b = cm.random_band(rng, B, n, 3, 3)
+        if dtype == torch.float32:
+            a, b = (x.astype(np.float32).astype(np.float64) for x in (a, b))
+        got = g._np(bgm.product_band_band(g._b(a, 8, 8), g._b(b, 3, 3)))
+        ref = oracle.product_band_band(a, 8, 8, b, 3, 3)[0]
+    else:
+        k = 8 if shape == "llt8" else 16
+        l = cm.random_band(rng, B, n, k, 0)
+        if dtype == torch.float32:
+            l = l.astype(np.float32).astype(np.float64)
+        L = g._b(l, k, 0)
+        lt = cm.transpose_ref(l, k, 0)
+        if shape == "llt8":
+            got = g._np(bgm.product_band_band(L, bgm.T(L)))
+            ref = oracle.product_band_band(l, k, 0, lt, 0, k)[0]
+        else:
+            got = g._np(bgm.product_band_band_restricted(L, bgm.T(L), k, 0))
+            ref = oracle.product_band_band(l, k, 0, lt, 0, k, k, 0)[0]
+    if dtype == torch.float64:
+        assert cm.max_rel_err(got, ref) <= TOL64
+    else:  # fp32 dots of random-sign terms cancel: relative to 1e-5 of the array scale, and normwise
+        assert cm.max_rel_err(got, ref, floor_scale=1e-5) <= 1e-4
+        assert np.linalg.norm(got - ref) <= 1e-5 * np.linalg.norm(ref)
