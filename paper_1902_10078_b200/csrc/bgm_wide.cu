@@ -491,19 +491,29 @@ constexpr int kSolveRing = 8;   // columns in flight per unit
 template <class T, int K, bool TR>
 __device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start, T* side, T* win,
                            T (*ring)[K + 2]) {
-  constexpr int R = (K + 1 + 31) / 32, M = 32 * R, D = kSolveRing;
+  constexpr int R = (K + 1 + 31) / 32, D = kSolveRing;
+  constexpr int M = (K + 2) <= 64 ? 64 : ((K + 2) <= 128 ? 128 : 256);  // window ring, power of two
   const int lane = threadIdx.x & 31;
   const Band<T>& L = C.l;
-  auto pos = [](ix r) -> int { return int(r % M); };
+  const T* lb = &L.cell(b, 0, 0);
+  const T* vb = &C.v(b, 0);
+  const int ls = L.s, vs = C.v.s;
+  const ix cstride = ix(L.w) << ls;
   // ring slot for column j: cells 0..K, then v_j (TR) or v_{j+K+1} (!TR)
   auto issue = [&](ix j, int slot) {
     if (j >= 0 && j < n) {
-      for (int a = lane; a <= K; a += 32)
-        if (j + a < n) cpa(&ring[slot][a], &L.cell(b, a, j));
-        else ring[slot][a] = T(0);
+      const T* col = lb + j * cstride;
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int a = lane + 32 * q;
+        if (a <= K) {
+          if (j + a < n) cpa(&ring[slot][a], col + (ix(a) << ls));
+          else ring[slot][a] = T(0);
+        }
+      }
       if (lane == 0) {
         const ix vr = TR ? j : j + K + 1;
-        if (vr < n) cpa(&ring[slot][K + 1], &C.v(b, vr));
+        if (vr < n) cpa(&ring[slot][K + 1], vb + (vr << vs));
         else ring[slot][K + 1] = T(0);
       }
     }
@@ -511,47 +521,70 @@ __device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start,
   };
   const int dir = TR ? -1 : 1;
   const ix stop = TR ? s - 1 : e;
-  // window init
+  // L2 prefetch of PB columns (and their v entries) PF columns ahead of the sweep
+  constexpr int PF = 96, PB = 16;
+  auto l2pf = [&](ix j0) {
+    ix a = j0 < 0 ? 0 : j0, z = j0 + PB < n ? j0 + PB : n;
+    if (a >= z) return;
+    auto pf = [](const T* lo, const T* hi) {
+      const size_t p0 = reinterpret_cast<size_t>(lo) & ~size_t(15);
+      const size_t p1 = (reinterpret_cast<size_t>(hi) + 15) & ~size_t(15);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0), "r"(unsigned(p1 - p0)) : "memory");
+    };
+    pf(&L.cell(b, 0, a), &L.cell(b, K, z - 1) + 1);
+    const ix va = TR ? a : a + K + 1, vz = TR ? z : (z + K + 1 < n ? z + K + 1 : n);
+    if (va < vz) pf(&C.v(b, va), &C.v(b, vz - 1) + 1);
+  };
+  if (lane == 0)
+    for (int q = 0; q < PF; q += PB) l2pf(TR ? start - q - PB + 1 : start + q);
   for (int p = lane; p < M; p += 32) win[p] = T(0);
   __syncwarp();
   if (!TR) {
     for (int a = lane; a <= K; a += 32)
-      if (start + a < n) win[pos(start + a)] = C.v(b, start + a);
+      if (start + a < n) win[(start + a) & (M - 1)] = C.v(b, start + a);
   }
   for (int d = 0; d < D - 1; ++d) issue(start + dir * d, d);
+  asm volatile("cp.async.wait_group %0;" ::"n"(D - 2) : "memory");
   __syncwarp();
+  // 1 / L(i,i) one row ahead, off the row-to-row dependency chain
+  T rnext = T(1) / ring[0][0];
   int slot = 0;
 #pragma unroll 1
   for (ix i = start; i != stop; i += dir) {
-    issue(i + dir * (D - 1), (slot + D - 1) % D);
-    asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
+    if (lane == 0 && (TR ? start - i : i - start) % PB == 0) l2pf(TR ? i - PF - PB + 1 : i + PF);
+    issue(i + dir * (D - 1), slot == 0 ? D - 1 : slot - 1);
+    asm volatile("cp.async.wait_group %0;" ::"n"(D - 2) : "memory");  // columns i and i + dir landed
     __syncwarp();
     const T* col = ring[slot];
+    const int nslot = slot + 1 == D ? 0 : slot + 1;
+    const T rd = rnext;
     T xi;
     if (!TR) {
-      xi = win[pos(i)] / col[0];
+      xi = win[i & (M - 1)] * rd;
 #pragma unroll
       for (int q = 0; q < R; ++q) {
         const int a = lane + 32 * q + 1;
         if (a <= K && i + a < n) {
-          const int p = pos(i + a);
+          const int p = int((i + a) & (M - 1));
           win[p] = fma(-col[a], xi, win[p]);
         }
       }
+      rnext = T(1) / ring[nslot][0];
       __syncwarp();
-      if (lane == 0) win[pos(i + K + 1)] = col[K + 1];
+      if (lane == 0) win[(i + K + 1) & (M - 1)] = col[K + 1];
     } else {
       T acc = T(0);
 #pragma unroll
       for (int q = 0; q < R; ++q) {
         const int a = lane + 32 * q + 1;
-        if (a <= K && i + a < n) acc = fma(col[a], win[pos(i + a)], acc);
+        if (a <= K && i + a < n) acc = fma(col[a], win[(i + a) & (M - 1)], acc);
       }
+      rnext = T(1) / ring[nslot][0];
 #pragma unroll
       for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      xi = (col[K + 1] - acc) / col[0];
+      xi = (col[K + 1] - acc) * rd;
       __syncwarp();
-      if (lane == 0) win[pos(i)] = xi;
+      if (lane == 0) win[i & (M - 1)] = xi;
     }
     if (lane == 0) {
       if (i >= s && i < e) C.x(b, i) = xi;
@@ -561,14 +594,14 @@ __device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start,
       }
     }
     __syncwarp();
-    slot = slot + 1 == D ? 0 : slot + 1;
+    slot = nslot;
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 template <class T, int K, bool TR>
 __global__ void __launch_bounds__(32 * kSolveWarps) k_solve(SolveP<T> C, Geo G) {
-  __shared__ T win[kSolveWarps][32 * ((K + 1 + 31) / 32)];
+  __shared__ T win[kSolveWarps][(K + 2) <= 64 ? 64 : ((K + 2) <= 128 ? 128 : 256)];
   __shared__ T ring[kSolveWarps][kSolveRing][K + 2];
   const int w = threadIdx.x >> 5;
   const ix unit = blockIdx.x * ix(kSolveWarps) + w;
@@ -612,7 +645,7 @@ __global__ void k_solve_check(SolveP<T> C, Geo G) {
 
 template <class T, int K, bool TR>
 __global__ void __launch_bounds__(32 * kSolveWarps) k_solve_repair(SolveP<T> C, Geo G) {
-  __shared__ T win[kSolveWarps][32 * ((K + 1 + 31) / 32)];
+  __shared__ T win[kSolveWarps][(K + 2) <= 64 ? 64 : ((K + 2) <= 128 ? 128 : 256)];
   __shared__ T ring[kSolveWarps][kSolveRing][K + 2];
   const int w = threadIdx.x >> 5;
   const ix b = blockIdx.x * ix(kSolveWarps) + w;
