@@ -38,8 +38,6 @@ def marginal_likelihood_grad_host(L_host: torch.Tensor, y_host: torch.Tensor, ta
     if tile not in (1, 32):
         raise ValueError("tile must be 1 or 32")
     chunk = max(1, min(chunk, B))
-    if tile == 32:
-        chunk = (chunk + 31) // 32 * 32
     pool = [torch.cuda.Stream(device=dev) for _ in range(max(1, streams))]
     # per-stream device buffers, reused round-robin
     bufs = []

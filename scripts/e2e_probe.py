@@ -38,7 +38,7 @@ torch.cuda.synchronize()
 dt = time.perf_counter() - t0
 print(f"both directions concurrently: {2 * hL.numel() * 8 / dt / 1e9:.1f} GB/s total", flush=True)
 del d
-for chunk, streams in ((32, 3), (16, 3), (16, 4), (8, 4), (64, 3), (32, 2)):
+for chunk, streams in ((32, 4), (16, 4), (8, 4), (8, 6), (4, 6), (16, 6)):
     marginal_likelihood_grad_host(hL, hy, 0.01, out_host=hout, chunk=chunk, streams=streams)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
