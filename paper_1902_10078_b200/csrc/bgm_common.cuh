@@ -19,6 +19,12 @@ using ix = int64_t;
 
 constexpr double kPivotFloor = 1e-300;  // kernels.hpp:20
 
+// Accumulator of the HBM-bound dot products (band x band, band x vector): fp64
+// for both storage types.  fp32 x fp32 products are exact in fp64, so an fp32
+// output is the correctly rounded value of the exact dot up to the fp64 sum's
+// rounding -- no fp32 cancellation -- at no cost on a memory-bound kernel.
+using acc_t = double;
+
 template <class T>
 struct Band {
   T* p;

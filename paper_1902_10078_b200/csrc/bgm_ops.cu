@@ -214,13 +214,13 @@ __global__ void k_product(Band<T> a, int ta, Band<T> bm, int tb, Band<T> c, T al
     ix k1 = i + aup;
     if (j + blo < k1) k1 = j + blo;
     if (n - 1 < k1) k1 = n - 1;
-    T s = 0;
+    acc_t s = 0;
     for (ix k = k0; k <= k1; ++k) {
-      const T av = ta ? a.at(b, k, i) : a.at(b, i, k);
-      const T bv = tb ? bm.at(b, j, k) : bm.at(b, k, j);
+      const acc_t av = ta ? a.at(b, k, i) : a.at(b, i, k);
+      const acc_t bv = tb ? bm.at(b, j, k) : bm.at(b, k, j);
       s += av * bv;
     }
-    return alpha * s;
+    return T(acc_t(alpha) * s);
   });
 }
 
@@ -231,15 +231,15 @@ __global__ void k_band_vec(Band<T> bm, Vec<T> v, int tr, Vec<T> y, ix batch) {
   ix b, i;
   if (bm.n == 0 || !split_bj(t, batch, bm.n, y.s, b, i)) return;
   const ix n = bm.n;
-  T s = 0;
+  acc_t s = 0;
   if (!tr) {
     const ix j0 = i - bm.lo > 0 ? i - bm.lo : 0, j1 = i + bm.up < n - 1 ? i + bm.up : n - 1;
-    for (ix j = j0; j <= j1; ++j) s += bm.at(b, i, j) * v(b, j);
+    for (ix j = j0; j <= j1; ++j) s += acc_t(bm.at(b, i, j)) * acc_t(v(b, j));
   } else {
     const ix j0 = i - bm.up > 0 ? i - bm.up : 0, j1 = i + bm.lo < n - 1 ? i + bm.lo : n - 1;
-    for (ix j = j0; j <= j1; ++j) s += bm.at(b, j, i) * v(b, j);
+    for (ix j = j0; j <= j1; ++j) s += acc_t(bm.at(b, j, i)) * acc_t(v(b, j));
   }
-  y(b, i) = s;
+  y(b, i) = T(s);
 }
 
 // kernels_detail.hpp:48-54

@@ -39,7 +39,7 @@ __global__ void k_product_stride(Band<T> A, int ta, Band<T> Bm, int tb, Band<T> 
 #pragma unroll 1
   for (int r = 0; r < C.w; ++r) {
     const ix i = j - C.up + r;
-    T s = T(0);
+    acc_t s = 0;
     if (i >= 0 && i < n) {
       ix k0 = i - al;
       if (j - bu > k0) k0 = j - bu;
@@ -54,13 +54,13 @@ __global__ void k_product_stride(Band<T> A, int ta, Band<T> Bm, int tb, Band<T> 
         const int cnt = int(k1 - k0) + 1;
 #pragma unroll 4
         for (int q = 0; q < cnt; ++q) {
-          s = fma(*pa, *pb, s);
+          s = fma(acc_t(*pa), acc_t(*pb), s);
           pa += da;
           pb += db;
         }
       }
     }
-    c[ix(r) << C.s] = s;
+    c[ix(r) << C.s] = T(s);
   }
 }
 
@@ -84,16 +84,16 @@ __global__ void __launch_bounds__(128) k_product_blk(Band<T> A, Band<T> Bm, Band
   if (b >= batch) return;
   const T* a = mbase(A, b);
   const T* bb = mbase(Bm, b);
-  T acc[J][CW];
+  acc_t acc[J][CW];
 #pragma unroll
   for (int jj = 0; jj < J; ++jj)
 #pragma unroll
-    for (int r = 0; r < CW; ++r) acc[jj][r] = T(0);
+    for (int r = 0; r < CW; ++r) acc[jj][r] = 0;
 #pragma unroll
   for (int kk = 0; kk < NK; ++kk) {
     const ix k = j0 - BU + kk;
     if (k < 0 || k >= n) continue;
-    T av[AW];
+    acc_t av[AW];
 #pragma unroll
     for (int x = 0; x < AW; ++x) {  // op(A)(i, k), i = k - AU + x
       const ix i = k - AU + x;
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(128) k_product_blk(Band<T> A, Band<T> Bm, Band
       if (d < -BU || d > BL) continue;
       const ix j = j0 + jj;
       if (j >= n) continue;
-      const T bv = TB ? bb[(k * Bm.w + (j - k + Bm.up)) << Bm.s] : bb[(j * Bm.w + (k - j + Bm.up)) << Bm.s];
+      const acc_t bv = TB ? bb[(k * Bm.w + (j - k + Bm.up)) << Bm.s] : bb[(j * Bm.w + (k - j + Bm.up)) << Bm.s];
 #pragma unroll
       for (int x = 0; x < AW; ++x) {
         const int r = d - AU + x + CU;  // output cell of row i = k - AU + x in column j
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(128) k_product_blk(Band<T> A, Band<T> Bm, Band
 #pragma unroll
     for (int r = 0; r < CW; ++r) {
       const ix i = j - CU + r;
-      c[(j * C.w + r) << C.s] = (i >= 0 && i < n) ? acc[jj][r] : T(0);
+      c[(j * C.w + r) << C.s] = (i >= 0 && i < n) ? T(acc[jj][r]) : T(0);
     }
   }
 }
