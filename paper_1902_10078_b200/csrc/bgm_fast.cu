@@ -51,7 +51,7 @@ bool subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cu
 }
 bool product(const bgm_band& a, int ta, const bgm_band& b, int tb, const bgm_band& c, cudaStream_t s) {
   if (disabled()) return false;
-  return prod::product(a, ta, b, tb, c, s);
+  return stream::product(a, ta, b, tb, c, s) || prod::product(a, ta, b, tb, c, s);
 }
 bool band_vec(const bgm_band&, const bgm_vec&, int, const bgm_vec&, cudaStream_t) { return false; }
 bool vjp_cholesky(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cudaStream_t s) {
@@ -63,9 +63,10 @@ bool vjp_subset(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, const
   if (disabled()) return false;
   return wide::vjp_subset(l, sm, sb, lb, st, row, s);
 }
-bool vjp_product(const bgm_band&, const bgm_band&, const bgm_band&, const bgm_band&,
-                 const bgm_band&, cudaStream_t) {
-  return false;
+bool vjp_product(const bgm_band& a, const bgm_band& b, const bgm_band& pb, const bgm_band& ab,
+                 const bgm_band& bb, cudaStream_t s) {
+  if (disabled()) return false;
+  return stream::vjp_product(a, b, pb, ab, bb, s);
 }
 bool vjp_band_vec(const bgm_band&, const bgm_vec&, const bgm_vec&, int, const bgm_band&,
                   const bgm_vec&, cudaStream_t) {

@@ -1,0 +1,484 @@
+// Staged band x band products and the fused product VJP for the 32-matrix
+// interleaved layout (tile 32): kernels_detail.hpp:16-28 (product_column),
+// kernels.cpp:72-90 (product_band_band / _restricted), grad.cpp:145-151
+// (vjp_product_band_band).
+//
+// The band products are HBM streams: every operand column is read from HBM
+// once and reused by the 2k+1 output columns around it.  Here the reuse
+// happens in shared memory instead of L1:
+//
+//  * one persistent CTA per SM walks a contiguous run of output columns of
+//    one tile (32 matrices) -- or of one lane group of LN matrices of it;
+//  * each operand has a ring of RC columns in shared memory, filled by TMA
+//    tensor copies (cp.async.bulk.tensor.2d, box = LN lanes x W storage rows,
+//    i.e. one band column of LN matrices) that complete on an mbarrier;
+//    loads run D steps (D*CJ columns) ahead of the compute;
+//  * the ring keeps a mirror of its first H columns after its end (H = the
+//    operand's column halo), so every thread's window of H+1 columns is
+//    contiguous and every shared-memory read has a compile-time offset;
+//  * thread = (matrix lane, output column): it loads op(Y)(., j) once into
+//    registers, accumulates each output cell over its exact k range with
+//    one LDS + one FMA per term (fp64 accumulation for both storage types),
+//    and stores the column with coalesced 8-byte stores (LN lanes x 8 B);
+//  * the fused VJP stages P-bar, A and B once and produces both A-bar and
+//    B-bar columns from them (grad.cpp:148-149), so P-bar is read from HBM
+//    once instead of twice.
+//
+// Columns outside [0, n) and corner cells are never trusted: steps whose
+// windows touch either matrix end run a predicated variant; interior steps
+// run unpredicated.  Shapes are compile-time (the benchmarked band shapes of
+// configs 2 and 3); anything else returns false and runs bgm_product.cu.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <type_traits>
+
+#include "bgm_common.cuh"
+#include "bgm_timing.cuh"
+#include "bgm_wide.cuh"
+
+namespace bgm {
+namespace stream {
+namespace {
+
+constexpr int cmin(int a, int b) { return a < b ? a : b; }
+constexpr int cmax(int a, int b) { return a > b ? a : b; }
+
+// One product C = op(X) op(Y) restricted to C's band.  X, Y stored bands
+// (XL, XU), (YL, YU); TX / TY = read transposed; output band (CL, CU).
+template <int TX_, int TY_, int XL_, int XU_, int YL_, int YU_, int CL_, int CU_>
+struct PS {
+  static constexpr int TX = TX_, TY = TY_, XL = XL_, XU = XU_, YL = YL_, YU = YU_, CL = CL_, CU = CU_;
+  static constexpr int CW = CL + CU + 1;
+  static constexpr int OXL = TX ? XU : XL, OXU = TX ? XL : XU;
+  static constexpr int OYL = TY ? YU : YL, OYU = TY ? YL : YU;
+  // k - j over all terms of output column j, and i - j of cells with terms
+  static constexpr int EMIN = cmax(-OYU, -CU - OXL), EMAX = cmin(OYL, CL + OXU);
+  static constexpr int DMIN = cmax(-CU, -OYU - OXU), DMAX = cmin(CL, OYL + OXL);
+  // stored-column offsets (relative to j) read from X and from Y
+  static constexpr int XLO = TX ? DMIN : EMIN, XHI = TX ? DMAX : EMAX;
+  static constexpr int YLO = TY ? EMIN : 0, YHI = TY ? EMAX : 0;
+  static constexpr int MARGIN = cmax(cmax(-EMIN, EMAX), cmax(CU, CL));
+};
+
+struct NoP {
+  static constexpr int XLO = 0, XHI = 0, YLO = 0, YHI = 0, MARGIN = 0, CW = 1;
+};
+
+// Up to three staged operands (widths W0..W2) and one or two products
+// reading them (operand indices X1, Y1, X2, Y2).
+template <int NOP_, int W0, int W1, int W2, class P1_, int X1_, int Y1_, class P2_ = NoP, int X2_ = 0, int Y2_ = 0>
+struct Spec {
+  static constexpr int NOP = NOP_;
+  using P1 = P1_;
+  using P2 = P2_;
+  static constexpr int X1 = X1_, Y1 = Y1_, X2 = X2_, Y2 = Y2_;
+  static constexpr bool TWO = !std::is_same<P2_, NoP>::value;
+  static constexpr int W(int o) { return o == 0 ? W0 : o == 1 ? W1 : W2; }
+  static constexpr int lo(int o) {
+    return cmin(cmin(X1 == o ? P1::XLO : 0, Y1 == o ? P1::YLO : 0),
+                cmin(TWO && X2 == o ? P2::XLO : 0, TWO && Y2 == o ? P2::YLO : 0));
+  }
+  static constexpr int hi(int o) {
+    return cmax(cmax(X1 == o ? P1::XHI : 0, Y1 == o ? P1::YHI : 0),
+                cmax(TWO && X2 == o ? P2::XHI : 0, TWO && Y2 == o ? P2::YHI : 0));
+  }
+  static constexpr int H(int o) { return hi(o) - lo(o); }
+  static constexpr int MARGIN = cmax(cmax(P1::MARGIN, P2::MARGIN),
+                                     cmax(cmax(-lo(0), hi(0)), cmax(cmax(-lo(1), hi(1)), cmax(-lo(2), hi(2)))));
+};
+
+// Ring geometry of operand o for lane-group width LN, CJ columns per step
+// and D steps of prefetch.  SS = column slot stride (elements, 128-B
+// multiple for the TMA destination), RC = ring columns, PH = RC + mirror.
+// Consumer threads = LN * CJ * NPART (NPART = 2: the two products of a
+// fused VJP, or the two halves of one product's cells); one producer warp.
+template <class T, int LN, int CJ, int D, int NPART, class S>
+struct Geom {
+  static constexpr int SS(int o) { return ((S::W(o) * LN * int(sizeof(T)) + 127) / 128) * 128 / int(sizeof(T)); }
+  static constexpr int RC(int o) { return (D + 1) * CJ + S::H(o); }
+  static constexpr int PH(int o) { return RC(o) + S::H(o); }
+  static constexpr int OFF(int o) { return o == 0 ? 0 : o == 1 ? PH(0) * SS(0) : PH(0) * SS(0) + PH(1) * SS(1); }
+  static constexpr int ELEMS = OFF(2) + (S::NOP > 2 ? PH(2) * SS(2) : 0);
+  static constexpr size_t SMEM = size_t(ELEMS) * sizeof(T) + 16 * (D + 1);
+  static constexpr int NC = LN * CJ * NPART;
+  static constexpr int THREADS = NC + 32;
+};
+
+struct Maps {
+  CUtensorMap m[3];
+};
+
+struct SGeo {
+  ix n;
+  ix nchunks;  // ceil(n / CJ)
+  ix plane;    // tiles * nchunks: work units of one lane group
+  ix per;      // units per CTA
+  int groups;  // 32 / LN; CTA c serves lane group c % groups
+  int cells[3];  // n * W(o): cells of one tile of operand o
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void bar_init(uint32_t bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_init_n(uint32_t bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void tma_load(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+
+// Output column j of one product from the staged windows.  bx / by point at
+// the thread's lane in the slot of stored column j + LOX / j + LOY; column
+// offset c is c - LO slots further (contiguous thanks to the mirror).
+template <class T, int LN, class P, int SSX, int SSY, int LOX, int LOY, int R0, int R1, bool EDGE>
+__device__ __forceinline__ void prod_col(const T* __restrict__ bx, const T* __restrict__ by, ix j, ix n,
+                                         T* __restrict__ out) {
+  constexpr int NE = P::EMAX - P::EMIN + 1;
+  acc_t yv[NE];
+  bool kv[NE];
+#pragma unroll
+  for (int q = 0; q < NE; ++q) {
+    const int e = P::EMIN + q;
+    const T* p = P::TY ? by + (e - LOY) * SSY + (P::YU - e) * LN : by + (0 - LOY) * SSY + (e + P::YU) * LN;
+    kv[q] = !EDGE || (j + e >= 0 && j + e < n);
+    yv[q] = acc_t(*p);
+  }
+#pragma unroll
+  for (int r = R0; r < R1; ++r) {
+    const int d = r - P::CU;
+    const int elo = cmax(d - P::OXL, P::EMIN), ehi = cmin(d + P::OXU, P::EMAX);
+    acc_t acc = 0;
+#pragma unroll
+    for (int q = 0; q < NE; ++q) {
+      const int e = P::EMIN + q;
+      if (e < elo || e > ehi) continue;
+      const T* p = P::TX ? bx + (d - LOX) * SSX + (e - d + P::XU) * LN : bx + (e - LOX) * SSX + (d - e + P::XU) * LN;
+      if (!EDGE || kv[q]) acc = fma(acc_t(*p), yv[q], acc);
+    }
+    T v = T(acc);
+    if (EDGE && (j + d < 0 || j + d >= n)) v = T(0);
+    out[r * 32] = v;
+  }
+}
+
+// Producer warp: one lane walks the CTA's runs and issues, for every step,
+// the TMA copies of the operand columns new at that step (the whole first
+// window at a run start), after the consumers released the ring slots they
+// overwrite (empty barrier of the step NB earlier; a full drain at run
+// starts, where the column -> slot mapping restarts).  Consumers wait on the
+// step's full barrier, compute their output columns, and release the step.
+template <class T, int LN, int CJ, int D, int NPART, class S>
+__global__ void __launch_bounds__(LN* CJ* NPART + 32) k_stream(const __grid_constant__ Maps maps, T* __restrict__ c1,
+                                                              T* __restrict__ c2, SGeo G) {
+  using Gm = Geom<T, LN, CJ, D, NPART, S>;
+  constexpr int NB = D + 1;
+  constexpr int NC = Gm::NC;
+  static_assert((LN * CJ) % 32 == 0, "a consumer part must be whole warps");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* ring = reinterpret_cast<T*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + size_t(Gm::ELEMS) * sizeof(T));
+  uint64_t* empty = full + NB;
+  const int tid = threadIdx.x;
+  if (tid == NC) {
+    for (int i = 0; i < NB; ++i) {
+      bar_init_n(smem_u32(&full[i]), 1);
+      bar_init_n(smem_u32(&empty[i]), NC / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  const ix n = G.n;
+  const int grp = int(blockIdx.x % unsigned(G.groups));
+  const int lane0 = grp * LN;
+  const ix ubeg = ix(blockIdx.x / unsigned(G.groups)) * G.per;
+  const ix uend = ubeg + G.per < G.plane ? ubeg + G.per : G.plane;
+
+  if (tid >= NC) {  // ---- producer warp
+    if (tid != NC) return;
+    for (int o = 0; o < S::NOP; ++o) asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.m[o]) : "memory");
+    uint32_t g = 0;
+    for (ix u = ubeg; u < uend;) {
+      const ix tile = u / G.nchunks, c0 = u % G.nchunks;
+      const int steps = int((c0 + (uend - u) < G.nchunks ? c0 + (uend - u) : G.nchunks) - c0);
+      u += steps;
+      const ix jf = c0 * CJ;
+      // drain: every step of the previous run released
+      for (uint32_t q = g >= uint32_t(NB) ? g - NB : 0; q < g; ++q) bar_wait(smem_u32(&empty[q % NB]), (q / NB) & 1);
+      for (int l = 0; l < steps; ++l) {
+        const uint32_t m = g + l;
+        if (l >= NB) bar_wait(smem_u32(&empty[m % NB]), ((m - NB) / NB) & 1);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t bar = smem_u32(&full[m % NB]);
+        uint32_t bytes = 0;
+#pragma unroll
+        for (int pass = 0; pass < 2; ++pass) {
+#pragma unroll
+          for (int o = 0; o < S::NOP; ++o) {
+            const int lo = S::lo(o), hi = S::hi(o), Ho = S::H(o), RCo = Gm::RC(o);
+            // run-relative columns: c = jf + rel, rel in [rf, rt]; slot = (rel - lo) % RC
+            const int rf = l == 0 ? lo : l * CJ + hi;
+            const int rt = (l + 1) * CJ - 1 + hi;
+            const uint32_t box = uint32_t(S::W(o) * LN * sizeof(T));
+            int slot = (rf - lo) % RCo;
+            const int ybase = int(tile * G.cells[o] + jf * S::W(o));
+            T* base = ring + Gm::OFF(o);
+            for (int rel = rf; rel <= rt; ++rel) {
+              if (pass == 0) {
+                bytes += (slot < Ho ? 2u : 1u) * box;
+              } else {
+                const int y = ybase + rel * S::W(o);
+                tma_load(smem_u32(base + slot * Gm::SS(o)), &maps.m[o], lane0, y, bar);
+                if (slot < Ho) tma_load(smem_u32(base + (slot + RCo) * Gm::SS(o)), &maps.m[o], lane0, y, bar);
+              }
+              if (++slot == RCo) slot = 0;
+            }
+          }
+          if (pass == 0) bar_expect(bar, bytes);
+        }
+      }
+      g += steps;
+    }
+    return;
+  }
+
+  // ---- consumers
+  constexpr int PT = LN * CJ;
+  const int part = tid / PT;
+  const int lane = tid % LN, cj = (tid % PT) / LN;
+  uint32_t g = 0;
+  for (ix u = ubeg; u < uend;) {
+    const ix tile = u / G.nchunks, c0 = u % G.nchunks;
+    const int steps = int((c0 + (uend - u) < G.nchunks ? c0 + (uend - u) : G.nchunks) - c0);
+    u += steps;
+    const ix jf = c0 * CJ;
+    for (int l = 0; l < steps; ++l) {
+      const uint32_t m = g + l;
+      bar_wait(smem_u32(&full[m % NB]), (m / NB) & 1);
+      const ix jt = jf + ix(l) * CJ;
+      const ix j = jt + cj;
+      if (j < n) {
+        const int rel = l * CJ + cj;  // column j relative to the run start
+        const T* b[3];
+#pragma unroll
+        for (int o = 0; o < 3; ++o)
+          b[o] = o < S::NOP ? ring + Gm::OFF(o) + (rel % Gm::RC(o)) * Gm::SS(o) + lane : ring;
+        const bool interior = jt >= S::MARGIN && jt + CJ - 1 + S::MARGIN <= n - 1;
+        using P1 = typename S::P1;
+        constexpr int SX1 = Gm::SS(S::X1), SY1 = Gm::SS(S::Y1), LX1 = S::lo(S::X1), LY1 = S::lo(S::Y1);
+        T* o1 = c1 + ((tile * n + j) * P1::CW) * 32 + lane0 + lane;
+        if constexpr (S::TWO) {
+          using P2 = typename S::P2;
+          constexpr int SX2 = Gm::SS(S::X2), SY2 = Gm::SS(S::Y2), LX2 = S::lo(S::X2), LY2 = S::lo(S::Y2);
+          T* o2 = c2 + ((tile * n + j) * P2::CW) * 32 + lane0 + lane;
+          if (NPART == 1 || part == 0) {
+            if (interior)
+              prod_col<T, LN, P1, SX1, SY1, LX1, LY1, 0, P1::CW, false>(b[S::X1], b[S::Y1], j, n, o1);
+            else
+              prod_col<T, LN, P1, SX1, SY1, LX1, LY1, 0, P1::CW, true>(b[S::X1], b[S::Y1], j, n, o1);
+          }
+          if (NPART == 1 || part == 1) {
+            if (interior)
+              prod_col<T, LN, P2, SX2, SY2, LX2, LY2, 0, P2::CW, false>(b[S::X2], b[S::Y2], j, n, o2);
+            else
+              prod_col<T, LN, P2, SX2, SY2, LX2, LY2, 0, P2::CW, true>(b[S::X2], b[S::Y2], j, n, o2);
+          }
+        } else {
+          constexpr int HALF = NPART == 2 ? (P1::CW + 1) / 2 : P1::CW;
+          if (part == 0) {
+            if (interior)
+              prod_col<T, LN, P1, SX1, SY1, LX1, LY1, 0, HALF, false>(b[S::X1], b[S::Y1], j, n, o1);
+            else
+              prod_col<T, LN, P1, SX1, SY1, LX1, LY1, 0, HALF, true>(b[S::X1], b[S::Y1], j, n, o1);
+          } else {
+            if (interior)
+              prod_col<T, LN, P1, SX1, SY1, LX1, LY1, HALF, P1::CW, false>(b[S::X1], b[S::Y1], j, n, o1);
+            else
+              prod_col<T, LN, P1, SX1, SY1, LX1, LY1, HALF, P1::CW, true>(b[S::X1], b[S::Y1], j, n, o1);
+          }
+        }
+      }
+      __syncwarp();
+      if ((tid & 31) == 0) bar_arrive(smem_u32(&empty[m % NB]));
+    }
+    g += steps;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// Whole band array as a 2-D tensor: 32 lanes (contiguous) x tiles*n*w cells.
+template <class T>
+bool make_map(CUtensorMap* m, const bgm_band& d, int LN) {
+  auto enc = encoder();
+  if (!enc) return false;
+  const int w = d.lower + d.upper + 1;
+  const ix tiles = (d.batch + 31) / 32;
+  cuuint64_t dims[2] = {32, cuuint64_t(tiles * d.n * w)};
+  cuuint64_t strides[1] = {32 * sizeof(T)};
+  cuuint32_t box[2] = {cuuint32_t(LN), cuuint32_t(w)};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, d.data, dims,
+             strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             // promote to the box row only: a wider promotion fetches the other lane
+             // groups' halves, which their own CTAs re-read later
+             LN * sizeof(T) >= 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+             : LN * sizeof(T) >= 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                     : CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool usable(const bgm_band& d) {
+  const ix tiles = (d.batch + 31) / 32;
+  const ix cells = tiles * d.n * (d.lower + d.upper + 1);
+  return d.tile == 32 && (reinterpret_cast<uintptr_t>(d.data) & 15) == 0 && cells < (ix(1) << 31);
+}
+
+template <class T, int LN, int CJ, int D, int NPART, class S>
+bool run(const bgm_band* ops, const bgm_band& c1, const bgm_band* c2, const char* name, cudaStream_t s) {
+  using Gm = Geom<T, LN, CJ, D, NPART, S>;
+  static_assert(Gm::SMEM <= 227 * 1024, "ring does not fit in shared memory");
+  auto kern = k_stream<T, LN, CJ, D, NPART, S>;
+  const ix n = c1.n;
+  if (n < 4 * (S::MARGIN + CJ)) return false;
+  for (int o = 0; o < S::NOP; ++o)
+    if (!usable(ops[o]) || ops[o].lower + ops[o].upper + 1 != S::W(o)) return false;
+  if (!usable(c1) || (c2 && !usable(*c2))) return false;
+  Maps maps;
+  for (int o = 0; o < S::NOP; ++o)
+    if (!make_map<T>(&maps.m[o], ops[o], LN)) return false;
+  static int occ = -1;
+  if (occ < 0) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Gm::SMEM));
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, Gm::THREADS, Gm::SMEM);
+    occ = per;
+  }
+  if (occ < 1) return false;
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  SGeo G;
+  G.n = n;
+  G.nchunks = (n + CJ - 1) / CJ;
+  G.groups = 32 / LN;
+  G.plane = (c1.batch + 31) / 32 * G.nchunks;
+  ix per_plane = ix(sms) * occ / G.groups;
+  if (per_plane < 1) per_plane = 1;
+  G.per = (G.plane + per_plane - 1) / per_plane;
+  per_plane = (G.plane + G.per - 1) / G.per;
+  for (int o = 0; o < 3; ++o) G.cells[o] = o < S::NOP ? int(n * S::W(o)) : 0;
+  timing::Scope t(name, s);
+  kern<<<unsigned(per_plane * G.groups), Gm::THREADS, Gm::SMEM, s>>>(
+      maps, static_cast<T*>(c1.data), c2 ? static_cast<T*>(c2->data) : nullptr, G);
+  return cudaPeekAtLastError() == cudaSuccess;
+}
+
+// Configurations are given for fp64 (lane-group width LN, CJ columns per
+// step).  fp32 rows are half as wide: twice the lanes and half the columns
+// per step when LN < 32 (same thread count, same TMA row bytes).
+template <class T, int LN, int CJ, int D, int NPART, class S>
+bool run_cfg(const bgm_band* ops, const bgm_band& c1, const bgm_band* c2, const char* name, cudaStream_t s) {
+  constexpr bool widen = sizeof(T) == 4 && LN < 32 && CJ % 2 == 0;
+  return run<T, widen ? 2 * LN : LN, widen ? CJ / 2 : CJ, D, NPART, S>(ops, c1, c2, name, s);
+}
+
+bool same(const bgm_band& a, const bgm_band& b) {
+  return a.data == b.data && a.lower == b.lower && a.upper == b.upper && a.n == b.n && a.tile == b.tile;
+}
+
+// ---- the benchmarked shapes ----
+// L L^T full (8,8) from one staged L (8,0)           [config 2]
+using S_llt8 = Spec<1, 9, 1, 1, PS<0, 1, 8, 0, 8, 0, 8, 8>, 0, 0>;
+// band(L L^T) lower (16,0) = precision_from_factor  [config 3, inference.cpp:23-26]
+using S_llt16 = Spec<1, 17, 1, 1, PS<0, 1, 16, 0, 16, 0, 16, 0>, 0, 0>;
+// A(8,8) B(3,3) -> (11,11)                          [config 2]
+using S_ab = Spec<2, 17, 7, 1, PS<0, 0, 8, 8, 3, 3, 11, 11>, 0, 1>;
+// fused VJP, operands 0 = P-bar, 1 = A, 2 = B:
+//   A-bar = P-bar op(B)^T on band(A), B-bar = op(A)^T P-bar on band(B)
+template <int AL, int AU, int BL, int BU, int PL, int PU>
+using S_vjp = Spec<3, PL + PU + 1, AL + AU + 1, BL + BU + 1, PS<0, 1, PL, PU, BL, BU, AL, AU>, 0, 2,
+                   PS<1, 0, AL, AU, PL, PU, BL, BU>, 1, 0>;
+using S_vab = S_vjp<8, 8, 3, 3, 11, 11>;   // config 2: A(8,8), B(3,3), P-bar (11,11)
+using S_vllt = S_vjp<8, 0, 0, 8, 8, 8>;    // config 2: L, L^T, P-bar (8,8)
+using S_vdl = S_vjp<16, 0, 0, 16, 16, 0>;  // config 3 dL: L, L^T, G (16,0)
+
+template <class T>
+bool product_t(const bgm_band& a, int ta, const bgm_band& b, int tb, const bgm_band& c, cudaStream_t s) {
+  if (!ta && tb && same(a, b) && a.lower == 8 && a.upper == 0 && c.lower == 8 && c.upper == 8)
+    return run_cfg<T, 32, 8, 3, 2, S_llt8>(&a, c, nullptr, "stream_llt8", s);
+  if (!ta && tb && same(a, b) && a.lower == 16 && a.upper == 0 && c.lower == 16 && c.upper == 0)
+    return run_cfg<T, 16, 8, 3, 2, S_llt16>(&a, c, nullptr, "stream_llt16", s);
+  if (!ta && !tb && a.lower == 8 && a.upper == 8 && b.lower == 3 && b.upper == 3 && c.lower == 11 && c.upper == 11) {
+    const bgm_band ops[2] = {a, b};
+    return run_cfg<T, 16, 16, 2, 2, S_ab>(ops, c, nullptr, "stream_ab", s);
+  }
+  return false;
+}
+
+template <class T>
+bool vjp_t(const bgm_band& a, const bgm_band& b, const bgm_band& pb, const bgm_band& ab, const bgm_band& bb,
+           cudaStream_t s) {
+  const bgm_band ops[3] = {pb, a, b};
+  auto is = [](const bgm_band& x, int l, int u) { return x.lower == l && x.upper == u; };
+  if (is(a, 8, 8) && is(b, 3, 3) && is(pb, 11, 11))
+    return run_cfg<T, 16, 8, 2, 2, S_vab>(ops, ab, &bb, "stream_vjp_ab", s);
+  if (is(a, 8, 0) && is(b, 0, 8) && is(pb, 8, 8))
+    return run_cfg<T, 16, 8, 2, 2, S_vllt>(ops, ab, &bb, "stream_vjp_llt", s);
+  if (is(a, 16, 0) && is(b, 0, 16) && is(pb, 16, 0))
+    return run_cfg<T, 8, 16, 1, 2, S_vdl>(ops, ab, &bb, "stream_vjp_dl", s);
+  return false;
+}
+
+}  // namespace
+
+bool product(const bgm_band& a, int ta, const bgm_band& b, int tb, const bgm_band& c, cudaStream_t s) {
+  if (c.tile != 32 || c.n == 0 || c.batch == 0) return false;
+  return a.dtype == BGM_F64 ? product_t<double>(a, ta, b, tb, c, s) : product_t<float>(a, ta, b, tb, c, s);
+}
+
+bool vjp_product(const bgm_band& a, const bgm_band& b, const bgm_band& pb, const bgm_band& ab, const bgm_band& bb,
+                 cudaStream_t s) {
+  if (a.tile != 32 || a.n == 0 || a.batch == 0) return false;
+  return a.dtype == BGM_F64 ? vjp_t<double>(a, b, pb, ab, bb, s) : vjp_t<float>(a, b, pb, ab, bb, s);
+}
+
+}  // namespace stream
+}  // namespace bgm

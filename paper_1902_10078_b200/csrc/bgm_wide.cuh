@@ -36,4 +36,11 @@ void set_segment_rows(int rows);
 namespace prod {
 bool product(const bgm_band& a, int ta, const bgm_band& b, int tb, const bgm_band& c, cudaStream_t s);
 }
+
+// Staged (TMA ring) products and fused product VJP, tile 32 (bgm_stream.cu).
+namespace stream {
+bool product(const bgm_band& a, int ta, const bgm_band& b, int tb, const bgm_band& c, cudaStream_t s);
+bool vjp_product(const bgm_band& a, const bgm_band& b, const bgm_band& pb, const bgm_band& ab,
+                 const bgm_band& bb, cudaStream_t s);
+}  // namespace stream
 }  // namespace bgm

@@ -163,3 +163,69 @@ def test_register_blocked_products(cuda, oracle, tile, dtype, shape):
     else:  # fp32 storage, fp64 accumulation (acc_t): each cell is the rounded exact dot
         assert cm.max_rel_err(got, ref) <= 1e-4
         assert np.linalg.norm(got - ref) <= 1e-6 * np.linalg.norm(ref)
+
+
+STAGED_VJP = {"vjp_ab": (8, 8, 3, 3, 11, 11), "vjp_llt": (8, 0, 0, 8, 8, 8), "vjp_dl": (16, 0, 0, 16, 16, 0)}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("shape", sorted(STAGED_VJP))
+@pytest.mark.parametrize("B,n", [(5, 203), (70, 1031)])
+def test_staged_vjp_products(cuda, oracle, dtype, shape, B, n):
+    """The fused product VJP of bgm_stream.cu (grad.cpp:145-151: A-bar = P-bar
+    B^T on band(A), B-bar = A^T P-bar on band(B), P-bar staged once) for the
+    config-2 / config-3 band shapes, tile 32; B = 70 spans three tiles (a
+    partial one) and n = 1031 gives each CTA runs that start mid-matrix."""
+    from tests.gpu_adapter import GpuOracle
+    al, au, bl, bu, pl, pu = STAGED_VJP[shape]
+    g = GpuOracle(tile=32, dtype=dtype)
+    rng = np.random.default_rng(100 + len(shape) + n)
+    a = cm.random_band(rng, B, n, al, au)
+    b = cm.random_band(rng, B, n, bl, bu)
+    p = cm.random_band(rng, B, n, pl, pu)
+    if dtype == torch.float32:
+        a, b, p = (x.astype(np.float32).astype(np.float64) for x in (a, b, p))
+    ga, gb = g.vjp_product_band_band(a, al, au, b, bl, bu, p, pl, pu)
+    ra, rb = oracle.vjp_product_band_band(a, al, au, b, bl, bu, p, pl, pu)[:2]
+    tol = TOL64 if dtype == torch.float64 else 1e-4
+    assert cm.max_rel_err(ga, ra) <= tol
+    assert cm.max_rel_err(gb, rb) <= tol
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", ["llt8", "ab", "llt16_lower"])
+def test_staged_products_multi_tile(cuda, oracle, shape):
+    """Staged products over several tiles, with corner cells of the inputs
+    poisoned (NaN): they must never be read (kernels_detail.hpp:16-28)."""
+    import paper_1902_10078_b200 as bgm
+    from tests.gpu_adapter import GpuOracle
+    g = GpuOracle(tile=32, dtype=torch.float64)
+    rng = np.random.default_rng({"llt8": 21, "ab": 22, "llt16_lower": 23}[shape])
+    B, n = 70, 1031
+
+    def poisoned(x, lo, up):
+        y = x.copy()
+        for r in range(lo + up + 1):  # storage row r of column j holds i = j - up + r
+            i = np.arange(n) - up + r
+            y[:, (i < 0) | (i >= n), r] = np.nan
+        return y
+
+    if shape == "ab":
+        a = cm.random_band(rng, B, n, 8, 8)
+        b = cm.random_band(rng, B, n, 3, 3)
+        got = g._np(bgm.product_band_band(g._b(poisoned(a, 8, 8), 8, 8), g._b(poisoned(b, 3, 3), 3, 3)))
+        ref = oracle.product_band_band(a, 8, 8, b, 3, 3)[0]
+    else:
+        k = 8 if shape == "llt8" else 16
+        l = cm.random_band(rng, B, n, k, 0)
+        L = g._b(poisoned(l, k, 0), k, 0)
+        lt = cm.transpose_ref(l, k, 0)
+        if shape == "llt8":
+            got = g._np(bgm.product_band_band(L, bgm.T(L)))
+            ref = oracle.product_band_band(l, k, 0, lt, 0, k)[0]
+        else:
+            got = g._np(bgm.product_band_band_restricted(L, bgm.T(L), k, 0))
+            ref = oracle.product_band_band(l, k, 0, lt, 0, k, k, 0)[0]
+    assert np.all(np.isfinite(got))
+    assert cm.max_rel_err(got, ref) <= TOL64
