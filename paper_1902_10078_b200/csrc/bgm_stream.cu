@@ -63,7 +63,7 @@ struct PS {
 };
 
 struct NoP {
-  static constexpr int XLO = 0, XHI = 0, YLO = 0, YHI = 0, MARGIN = 0, CW = 1;
+  static constexpr int XLO = 0, XHI = 0, YLO = 0, YHI = 0, MARGIN = 0;
 };
 
 // Up to three staged operands (widths W0..W2) and one or two products
@@ -90,15 +90,24 @@ struct Spec {
 };
 
 // Ring geometry of operand o for lane-group width LN, CJ columns per step
-// and D steps of prefetch.  SS = column slot stride (elements, 128-B
-// multiple for the TMA destination), RC = ring columns, PH = RC + mirror.
+// and D steps of prefetch.  A ring slot holds one band column of LN
+// matrices: WP >= W cells (the TMA box pads the column with out-of-bounds
+// zero cells so every slot starts on a 128-byte boundary), SS = WP * LN
+// elements.  RC = ring columns (a multiple of CJ: step loads land on
+// CJ-aligned slots as one box); PH = RC + mirror of the first H slots.
 // Consumer threads = LN * CJ * NPART (NPART = 2: the two products of a
 // fused VJP, or the two halves of one product's cells); one producer warp.
 template <class T, int LN, int CJ, int D, int NPART, class S>
 struct Geom {
-  static constexpr int SS(int o) { return ((S::W(o) * LN * int(sizeof(T)) + 127) / 128) * 128 / int(sizeof(T)); }
-  static constexpr int RC(int o) { return (D + 1) * CJ + S::H(o); }
-  static constexpr int PH(int o) { return RC(o) + S::H(o); }
+  static constexpr int WP(int o) {
+    return (S::W(o) * LN * int(sizeof(T))) % 128 == 0 ? S::W(o)
+           : (S::W(o) + 1) * LN * int(sizeof(T)) % 128 == 0 ? S::W(o) + 1
+           : (S::W(o) + 2) * LN * int(sizeof(T)) % 128 == 0 ? S::W(o) + 2
+                                                             : S::W(o) + 3;
+  }
+  static constexpr int SS(int o) { return WP(o) * LN; }
+  static constexpr int RC(int o) { return ((D + 1) * CJ + S::H(o) + CJ - 1) / CJ * CJ; }
+  static constexpr int PH(int o) { return RC(o) + (S::H(o) + CJ - 1) / CJ * CJ; }
   static constexpr int OFF(int o) { return o == 0 ? 0 : o == 1 ? PH(0) * SS(0) : PH(0) * SS(0) + PH(1) * SS(1); }
   static constexpr int ELEMS = OFF(2) + (S::NOP > 2 ? PH(2) * SS(2) : 0);
   static constexpr size_t SMEM = size_t(ELEMS) * sizeof(T) + 16 * (D + 1);
@@ -106,8 +115,10 @@ struct Geom {
   static constexpr int THREADS = NC + 32;
 };
 
+// per operand: box of CJ columns (step loads) and of one column (run starts)
 struct Maps {
-  CUtensorMap m[3];
+  CUtensorMap step[3];
+  CUtensorMap col[3];
 };
 
 struct SGeo {
@@ -116,16 +127,12 @@ struct SGeo {
   ix plane;    // tiles * nchunks: work units of one lane group
   ix per;      // units per CTA
   int groups;  // 32 / LN; CTA c serves lane group c % groups
-  int cells[3];  // n * W(o): cells of one tile of operand o
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__device__ __forceinline__ void bar_init(uint32_t bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
-}
 __device__ __forceinline__ void bar_expect(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
@@ -145,10 +152,12 @@ __device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
   } while (!ok);
 }
-__device__ __forceinline__ void tma_load(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
+// box at (lane x, cell 0, column z) of the (lanes, cells, columns) tensor
+__device__ __forceinline__ void tma_load(uint32_t dst, const CUtensorMap* map, int x, int z, uint32_t bar) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(0), "r"(z), "r"(bar)
       : "memory");
 }
 
@@ -199,6 +208,7 @@ __global__ void __launch_bounds__(LN* CJ* NPART + 32) k_stream(const __grid_cons
   constexpr int NB = D + 1;
   constexpr int NC = Gm::NC;
   static_assert((LN * CJ) % 32 == 0, "a consumer part must be whole warps");
+  static_assert(CJ <= 256 && LN * sizeof(T) % 16 == 0, "TMA box limits");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* ring = reinterpret_cast<T*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + size_t(Gm::ELEMS) * sizeof(T));
@@ -221,13 +231,16 @@ __global__ void __launch_bounds__(LN* CJ* NPART + 32) k_stream(const __grid_cons
 
   if (tid >= NC) {  // ---- producer warp
     if (tid != NC) return;
-    for (int o = 0; o < S::NOP; ++o) asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.m[o]) : "memory");
+    for (int o = 0; o < S::NOP; ++o) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.step[o]) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.col[o]) : "memory");
+    }
     uint32_t g = 0;
     for (ix u = ubeg; u < uend;) {
       const ix tile = u / G.nchunks, c0 = u % G.nchunks;
       const int steps = int((c0 + (uend - u) < G.nchunks ? c0 + (uend - u) : G.nchunks) - c0);
       u += steps;
-      const ix jf = c0 * CJ;
+      const int zf = int(tile * n + c0 * CJ);  // global column index of the run start
       // drain: every step of the previous run released
       for (uint32_t q = g >= uint32_t(NB) ? g - NB : 0; q < g; ++q) bar_wait(smem_u32(&empty[q % NB]), (q / NB) & 1);
       for (int l = 0; l < steps; ++l) {
@@ -235,31 +248,32 @@ __global__ void __launch_bounds__(LN* CJ* NPART + 32) k_stream(const __grid_cons
         if (l >= NB) bar_wait(smem_u32(&empty[m % NB]), ((m - NB) / NB) & 1);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         const uint32_t bar = smem_u32(&full[m % NB]);
+        // run-relative column rel sits in slot (rel - hi) mod RC: step l's new
+        // columns [l CJ + hi, (l+1) CJ + hi) are the CJ-aligned slots from l CJ mod RC
         uint32_t bytes = 0;
 #pragma unroll
-        for (int pass = 0; pass < 2; ++pass) {
+        for (int o = 0; o < S::NOP; ++o) {
+          const uint32_t colb = uint32_t(Gm::SS(o) * sizeof(T));
+          const int slot = (l * CJ) % Gm::RC(o);
+          bytes += colb * CJ * (slot < S::H(o) ? 2u : 1u);
+          if (l == 0) bytes += colb * S::H(o) * (Gm::RC(o) - S::H(o) < S::H(o) ? 2u : 1u);
+        }
+        bar_expect(bar, bytes);
 #pragma unroll
-          for (int o = 0; o < S::NOP; ++o) {
-            const int lo = S::lo(o), hi = S::hi(o), Ho = S::H(o), RCo = Gm::RC(o);
-            // run-relative columns: c = jf + rel, rel in [rf, rt]; slot = (rel - lo) % RC
-            const int rf = l == 0 ? lo : l * CJ + hi;
-            const int rt = (l + 1) * CJ - 1 + hi;
-            const uint32_t box = uint32_t(S::W(o) * LN * sizeof(T));
-            int slot = (rf - lo) % RCo;
-            const int ybase = int(tile * G.cells[o] + jf * S::W(o));
-            T* base = ring + Gm::OFF(o);
-            for (int rel = rf; rel <= rt; ++rel) {
-              if (pass == 0) {
-                bytes += (slot < Ho ? 2u : 1u) * box;
-              } else {
-                const int y = ybase + rel * S::W(o);
-                tma_load(smem_u32(base + slot * Gm::SS(o)), &maps.m[o], lane0, y, bar);
-                if (slot < Ho) tma_load(smem_u32(base + (slot + RCo) * Gm::SS(o)), &maps.m[o], lane0, y, bar);
-              }
-              if (++slot == RCo) slot = 0;
+        for (int o = 0; o < S::NOP; ++o) {
+          const int lo = S::lo(o), hi = S::hi(o), Ho = S::H(o), RCo = Gm::RC(o);
+          T* base = ring + Gm::OFF(o);
+          if (l == 0) {  // the halo [lo, hi) before the first step's columns
+            for (int rel = lo; rel < hi; ++rel) {
+              const int slot = rel - hi + RCo;
+              tma_load(smem_u32(base + slot * Gm::SS(o)), &maps.col[o], lane0, zf + rel, bar);
+              if (slot < Ho) tma_load(smem_u32(base + (slot + RCo) * Gm::SS(o)), &maps.col[o], lane0, zf + rel, bar);
             }
           }
-          if (pass == 0) bar_expect(bar, bytes);
+          const int slot = (l * CJ) % RCo;
+          const int z = zf + l * CJ + hi;
+          tma_load(smem_u32(base + slot * Gm::SS(o)), &maps.step[o], lane0, z, bar);
+          if (slot < Ho) tma_load(smem_u32(base + (slot + RCo) * Gm::SS(o)), &maps.step[o], lane0, z, bar);
         }
       }
       g += steps;
@@ -283,11 +297,11 @@ __global__ void __launch_bounds__(LN* CJ* NPART + 32) k_stream(const __grid_cons
       const ix jt = jf + ix(l) * CJ;
       const ix j = jt + cj;
       if (j < n) {
-        const int rel = l * CJ + cj;  // column j relative to the run start
+        const int rel = l * CJ + cj;  // column j relative to the run start; window starts at rel + lo
         const T* b[3];
 #pragma unroll
         for (int o = 0; o < 3; ++o)
-          b[o] = o < S::NOP ? ring + Gm::OFF(o) + (rel % Gm::RC(o)) * Gm::SS(o) + lane : ring;
+          b[o] = o < S::NOP ? ring + Gm::OFF(o) + ((rel + Gm::RC(o) - S::H(o)) % Gm::RC(o)) * Gm::SS(o) + lane : ring;
         const bool interior = jt >= S::MARGIN && jt + CJ - 1 + S::MARGIN <= n - 1;
         using P1 = typename S::P1;
         constexpr int SX1 = Gm::SS(S::X1), SY1 = Gm::SS(S::Y1), LX1 = S::lo(S::X1), LY1 = S::lo(S::Y1);
@@ -345,18 +359,20 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   return fn;
 }
 
-// Whole band array as a 2-D tensor: 32 lanes (contiguous) x tiles*n*w cells.
+// Whole band array as a 3-D tensor (32 lanes, w cells, tiles * n columns);
+// box = (LN lanes, WP cells, ncol columns), cells w.. WP-1 out of bounds
+// (zero-filled) so that each column fills a 128-byte-aligned slot.
 template <class T>
-bool make_map(CUtensorMap* m, const bgm_band& d, int LN) {
+bool make_map(CUtensorMap* m, const bgm_band& d, int LN, int WP, int ncol) {
   auto enc = encoder();
   if (!enc) return false;
   const int w = d.lower + d.upper + 1;
   const ix tiles = (d.batch + 31) / 32;
-  cuuint64_t dims[2] = {32, cuuint64_t(tiles * d.n * w)};
-  cuuint64_t strides[1] = {32 * sizeof(T)};
-  cuuint32_t box[2] = {cuuint32_t(LN), cuuint32_t(w)};
-  cuuint32_t es[2] = {1, 1};
-  return enc(m, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, d.data, dims,
+  cuuint64_t dims[3] = {32, cuuint64_t(w), cuuint64_t(tiles * d.n)};
+  cuuint64_t strides[2] = {32 * sizeof(T), cuuint64_t(w) * 32 * sizeof(T)};
+  cuuint32_t box[3] = {cuuint32_t(LN), cuuint32_t(WP), cuuint32_t(ncol)};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, d.data, dims,
              strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
              // promote to the box row only: a wider promotion fetches the other lane
              // groups' halves, which their own CTAs re-read later
@@ -368,8 +384,7 @@ bool make_map(CUtensorMap* m, const bgm_band& d, int LN) {
 
 bool usable(const bgm_band& d) {
   const ix tiles = (d.batch + 31) / 32;
-  const ix cells = tiles * d.n * (d.lower + d.upper + 1);
-  return d.tile == 32 && (reinterpret_cast<uintptr_t>(d.data) & 15) == 0 && cells < (ix(1) << 31);
+  return d.tile == 32 && (reinterpret_cast<uintptr_t>(d.data) & 15) == 0 && tiles * d.n < (ix(1) << 31);
 }
 
 template <class T, int LN, int CJ, int D, int NPART, class S>
@@ -384,7 +399,8 @@ bool run(const bgm_band* ops, const bgm_band& c1, const bgm_band* c2, const char
   if (!usable(c1) || (c2 && !usable(*c2))) return false;
   Maps maps;
   for (int o = 0; o < S::NOP; ++o)
-    if (!make_map<T>(&maps.m[o], ops[o], LN)) return false;
+    if (!make_map<T>(&maps.step[o], ops[o], LN, Gm::WP(o), CJ) || !make_map<T>(&maps.col[o], ops[o], LN, Gm::WP(o), 1))
+      return false;
   static int occ = -1;
   if (occ < 0) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Gm::SMEM));
@@ -404,7 +420,6 @@ bool run(const bgm_band* ops, const bgm_band& c1, const bgm_band* c2, const char
   if (per_plane < 1) per_plane = 1;
   G.per = (G.plane + per_plane - 1) / per_plane;
   per_plane = (G.plane + G.per - 1) / G.per;
-  for (int o = 0; o < 3; ++o) G.cells[o] = o < S::NOP ? int(n * S::W(o)) : 0;
   timing::Scope t(name, s);
   kern<<<unsigned(per_plane * G.groups), Gm::THREADS, Gm::SMEM, s>>>(
       maps, static_cast<T*>(c1.data), c2 ? static_cast<T*>(c2->data) : nullptr, G);
@@ -459,7 +474,7 @@ bool vjp_t(const bgm_band& a, const bgm_band& b, const bgm_band& pb, const bgm_b
   const bgm_band ops[3] = {pb, a, b};
   auto is = [](const bgm_band& x, int l, int u) { return x.lower == l && x.upper == u; };
   if (is(a, 8, 8) && is(b, 3, 3) && is(pb, 11, 11))
-    return run_cfg<T, 16, 8, 2, 2, S_vab>(ops, ab, &bb, "stream_vjp_ab", s);
+    return run_cfg<T, 16, 4, 3, 2, S_vab>(ops, ab, &bb, "stream_vjp_ab", s);
   if (is(a, 8, 0) && is(b, 0, 8) && is(pb, 8, 8))
     return run_cfg<T, 16, 8, 2, 2, S_vllt>(ops, ab, &bb, "stream_vjp_llt", s);
   if (is(a, 16, 0) && is(b, 0, 16) && is(pb, 16, 0))
