@@ -53,7 +53,10 @@ bool product(const bgm_band& a, int ta, const bgm_band& b, int tb, const bgm_ban
   if (disabled()) return false;
   return stream::product(a, ta, b, tb, c, s) || prod::product(a, ta, b, tb, c, s);
 }
-bool band_vec(const bgm_band&, const bgm_vec&, int, const bgm_vec&, cudaStream_t) { return false; }
+bool band_vec(const bgm_band& b, const bgm_vec& v, int tr, const bgm_vec& y, cudaStream_t s) {
+  if (disabled()) return false;
+  return prod::band_vec(b, v, tr, y, s);
+}
 bool vjp_cholesky(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cudaStream_t s) {
   if (disabled()) return false;
   return narrow::vjp_cholesky(l, lb, qb, s) || wide::vjp_cholesky(l, lb, qb, s);
@@ -68,9 +71,10 @@ bool vjp_product(const bgm_band& a, const bgm_band& b, const bgm_band& pb, const
   if (disabled()) return false;
   return stream::vjp_product(a, b, pb, ab, bb, s);
 }
-bool vjp_band_vec(const bgm_band&, const bgm_vec&, const bgm_vec&, int, const bgm_band&,
-                  const bgm_vec&, cudaStream_t) {
-  return false;
+bool vjp_band_vec(const bgm_band& b, const bgm_vec& v, const bgm_vec& pb, int tr, const bgm_band& bb,
+                  const bgm_vec& vb, cudaStream_t s) {
+  if (disabled()) return false;
+  return prod::vjp_band_vec(b, v, pb, tr, bb, vb, s);
 }
 
 }  // namespace fast

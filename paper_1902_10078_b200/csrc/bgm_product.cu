@@ -152,6 +152,73 @@ bool product_blk(const bgm_band& a, int ta, const bgm_band& b, int tb, const bgm
          try_blk<T, 0, 1, 16, 0, 0, 16, 16, 0>(a, ta, b, tb, c, s);
 }
 
+
+// Band x vector for tile 32 (kernels_detail.hpp:31-45): thread = (matrix
+// lane, output index i), y_i = sum_j op(B)(i, j) v_j with pointer walks:
+// untransposed, B(i, j) for consecutive j lies (w - 1) cells apart (the
+// storage diagonal); transposed, B(j, i) is column i of the storage.
+// Every load is one 256-byte warp transaction; fp64 accumulation.
+template <class T>
+__global__ void k_band_vec32(Band<T> B, Vec<T> v, int tr, Vec<T> y, ix tiles) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  const int lane = int(t & 31);
+  const ix rest = t >> 5, n = B.n;
+  if (rest >= tiles * n) return;
+  const ix tile = rest / n, i = rest - tile * n;
+  const int lo = tr ? B.up : B.lo, up = tr ? B.lo : B.up;  // bands of op(B)
+  const ix j0 = i - lo > 0 ? i - lo : 0, j1 = i + up < n - 1 ? i + up : n - 1;
+  const T* pb = B.p + tile * n * B.w * 32 + lane +
+                (tr ? (i * B.w + (j0 - i + B.up)) : (j0 * B.w + (i - j0 + B.up))) * 32;
+  const ix db = tr ? 32 : ix(B.w - 1) * 32;
+  const T* pv = v.p + (tile * n + j0) * 32 + lane;
+  acc_t s = 0;
+#pragma unroll 4
+  for (ix j = j0; j <= j1; ++j) {
+    s = fma(acc_t(*pb), acc_t(*pv), s);
+    pb += db;
+    pv += 32;
+  }
+  y.p[(tile * n + i) * 32 + lane] = T(s);
+}
+
+// Fused vjp_product_band_vec column pass (grad.cpp:153-162), tile 32:
+// thread = (matrix lane, column j of B).  B-bar's column j is p-bar_i v_j
+// (untransposed) or v_i p-bar_j (transposed), i over the column's band
+// rows; untransposed, v-bar_j = sum_i B(i, j) p-bar_i comes from the same
+// column read.  B is read once, B-bar written once, corners zero.
+template <class T, bool TR>
+__global__ void k_vjp_band_vec32(Band<T> B, Vec<T> v, Vec<T> pb, Band<T> bb, Vec<T> vb, ix tiles) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  const int lane = int(t & 31);
+  const ix rest = t >> 5, n = B.n;
+  if (rest >= tiles * n) return;
+  const ix tile = rest / n, j = rest - tile * n;
+  const ix col = ((tile * n + j) * B.w) * 32 + lane;
+  const T* pc = B.p + col;
+  T* oc = bb.p + col;
+  const T* vt = v.p + tile * n * 32 + lane;
+  const T* pt = pb.p + tile * n * 32 + lane;
+  const acc_t cj = acc_t(TR ? pt[j * 32] : vt[j * 32]);
+  acc_t s = 0;
+  for (int r = 0; r < B.w; ++r) {
+    const ix i = j - B.up + r;
+    T o = T(0);
+    if (i >= 0 && i < n) {
+      const acc_t ri = acc_t(TR ? vt[i * 32] : pt[i * 32]);
+      o = T(ri * cj);
+      if (!TR) s = fma(acc_t(pc[r * 32]), ri, s);
+    }
+    oc[r * 32] = o;
+  }
+  if (!TR) vb.p[(tile * n + j) * 32 + lane] = T(s);
+}
+
+template <class T>
+void launch_band_vec32(const bgm_band& b, const bgm_vec& v, int tr, const bgm_vec& y, cudaStream_t s) {
+  const ix tiles = (b.batch + 31) / 32;
+  k_band_vec32<T><<<blocks_for(tiles * b.n * 32, 256), 256, 0, s>>>(view<T>(b), view<T>(v), tr, view<T>(y), tiles);
+}
+
 }  // namespace
 
 bool product(const bgm_band& a, int ta, const bgm_band& b, int tb, const bgm_band& c, cudaStream_t s) {
@@ -167,6 +234,41 @@ bool product(const bgm_band& a, int ta, const bgm_band& b, int tb, const bgm_ban
   else
     k_product_stride<float><<<blocks_for(work, 128), 128, 0, s>>>(view<float>(a), ta, view<float>(b), tb,
                                                                   view<float>(c), c.batch);
+  return true;
+}
+
+bool band_vec(const bgm_band& b, const bgm_vec& v, int tr, const bgm_vec& y, cudaStream_t s) {
+  if (b.tile != 32 || v.tile != 32 || y.tile != 32 || b.n == 0 || b.batch == 0) return false;
+  timing::Scope t("band_vec32", s);
+  if (b.dtype == BGM_F64)
+    launch_band_vec32<double>(b, v, tr, y, s);
+  else
+    launch_band_vec32<float>(b, v, tr, y, s);
+  return true;
+}
+
+bool vjp_band_vec(const bgm_band& b, const bgm_vec& v, const bgm_vec& pb, int tr, const bgm_band& bb,
+                  const bgm_vec& vb, cudaStream_t s) {
+  if (b.tile != 32 || v.tile != 32 || pb.tile != 32 || bb.tile != 32 || vb.tile != 32 || b.n == 0 || b.batch == 0)
+    return false;
+  timing::Scope t("vjp_band_vec32", s);
+  const ix tiles = (b.batch + 31) / 32;
+  const unsigned blocks = blocks_for(tiles * b.n * 32, 256);
+  auto go = [&](auto z) {
+    using T = decltype(z);
+    if (tr) {  // v-bar = B p-bar (row sums), B-bar = outer(v, p-bar)
+      launch_band_vec32<T>(b, pb, 0, vb, s);
+      k_vjp_band_vec32<T, true><<<blocks, 256, 0, s>>>(view<T>(b), view<T>(v), view<T>(pb), view<T>(bb), view<T>(vb),
+                                                       tiles);
+    } else {
+      k_vjp_band_vec32<T, false><<<blocks, 256, 0, s>>>(view<T>(b), view<T>(v), view<T>(pb), view<T>(bb),
+                                                        view<T>(vb), tiles);
+    }
+  };
+  if (b.dtype == BGM_F64)
+    go(double(0));
+  else
+    go(float(0));
   return true;
 }
 

@@ -35,6 +35,9 @@ void set_segment_rows(int rows);
 // Band x band products with strided operand walks (bgm_product.cu).
 namespace prod {
 bool product(const bgm_band& a, int ta, const bgm_band& b, int tb, const bgm_band& c, cudaStream_t s);
+bool band_vec(const bgm_band& b, const bgm_vec& v, int tr, const bgm_vec& y, cudaStream_t s);
+bool vjp_band_vec(const bgm_band& b, const bgm_vec& v, const bgm_vec& pb, int tr, const bgm_band& bb,
+                  const bgm_vec& vb, cudaStream_t s);
 }
 
 // Staged (TMA ring) products and fused product VJP, tile 32 (bgm_stream.cu).

@@ -229,3 +229,33 @@ def test_staged_products_multi_tile(cuda, oracle, shape):
             ref = oracle.product_band_band(l, k, 0, lt, 0, k, k, 0)[0]
     assert np.all(np.isfinite(got))
     assert cm.max_rel_err(got, ref) <= TOL64
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("transpose", [False, True])
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_band_vec_tile32_multi_tile(cuda, oracle, transpose, dtype):
+    """Tile-32 band x vector and its fused VJP (kernels_detail.hpp:31-45,
+    grad.cpp:153-162) over three tiles (one partial), band (8,8) as config 2
+    and a ragged (2,5) band; corner cells poisoned with NaN."""
+    from tests.gpu_adapter import GpuOracle
+    g = GpuOracle(tile=32, dtype=dtype)
+    rng = np.random.default_rng(31 + int(transpose))
+    B, n = 70, 517
+    tol = TOL64 if dtype == torch.float64 else 1e-4
+    for lo, up in ((8, 8), (2, 5)):
+        b = cm.random_band(rng, B, n, lo, up)
+        v, p = cm.random_vec(rng, B, n), cm.random_vec(rng, B, n)
+        if dtype == torch.float32:
+            b, v, p = (x.astype(np.float32).astype(np.float64) for x in (b, v, p))
+        bp = b.copy()
+        for r in range(lo + up + 1):
+            i = np.arange(n) - up + r
+            bp[:, (i < 0) | (i >= n), r] = np.nan
+        y = g.product_band_vec(bp, lo, up, v, transpose)
+        assert cm.max_rel_err(y, oracle.product_band_vec(b, lo, up, v, transpose)) <= tol
+        gb, gv = g.vjp_product_band_vec(bp, lo, up, v, p, transpose)
+        rb, rv = oracle.vjp_product_band_vec(b, lo, up, v, p, transpose)[:2]
+        assert np.all(np.isfinite(gb)) and np.all(np.isfinite(gv))
+        assert cm.max_rel_err(gb, rb) <= tol
+        assert cm.max_rel_err(gv, rv) <= tol
