@@ -13,9 +13,9 @@
 //    tensor copies (cp.async.bulk.tensor.2d, box = LN lanes x W storage rows,
 //    i.e. one band column of LN matrices) that complete on an mbarrier;
 //    loads run D steps (D*CJ columns) ahead of the compute;
-//  * the ring keeps a mirror of its first H columns after its end (H = the
-//    operand's column halo), so every thread's window of H+1 columns is
-//    contiguous and every shared-memory read has a compile-time offset;
+//  * a thread's window of H+1 columns (H = the operand's column halo) wraps
+//    at most once around the ring: one compare-select per column, and every
+//    shared-memory read within a column has a compile-time offset;
 //  * thread = (matrix lane, output column): it loads op(Y)(., j) once into
 //    registers, accumulates each output cell over its exact k range with
 //    one LDS + one FMA per term (fp64 accumulation for both storage types),
@@ -94,10 +94,12 @@ struct Spec {
 // matrices: WP >= W cells (the TMA box pads the column with out-of-bounds
 // zero cells so every slot starts on a 128-byte boundary), SS = WP * LN
 // elements.  RC = ring columns (a multiple of CJ: step loads land on
-// CJ-aligned slots as one box); PH = RC + mirror of the first H slots.
+// CJ-aligned slots as one box).  MIR: the ring keeps a copy of its first H
+// slots after its end (PH = physical slots), so windows never wrap (no
+// per-column select) at the cost of H more slots.
 // Consumer threads = LN * CJ * NPART (NPART = 2: the two products of a
 // fused VJP, or the two halves of one product's cells); one producer warp.
-template <class T, int LN, int CJ, int D, int NPART, class S>
+template <class T, int LN, int CJ, int D, int NPART, class S, bool MIR>
 struct Geom {
   static constexpr int WP(int o) {
     return (S::W(o) * LN * int(sizeof(T))) % 128 == 0 ? S::W(o)
@@ -107,7 +109,9 @@ struct Geom {
   }
   static constexpr int SS(int o) { return WP(o) * LN; }
   static constexpr int RC(int o) { return ((D + 1) * CJ + S::H(o) + CJ - 1) / CJ * CJ; }
-  static constexpr int PH(int o) { return RC(o) + (S::H(o) + CJ - 1) / CJ * CJ; }
+  static constexpr int PH(int o) { return RC(o) + (MIR ? (S::H(o) + CJ - 1) / CJ * CJ : 0); }
+  // ring size seen by a window: with the mirror a window never wraps
+  static constexpr int WRC(int o) { return MIR ? (1 << 30) : RC(o); }
   static constexpr int OFF(int o) { return o == 0 ? 0 : o == 1 ? PH(0) * SS(0) : PH(0) * SS(0) + PH(1) * SS(1); }
   static constexpr int ELEMS = OFF(2) + (S::NOP > 2 ? PH(2) * SS(2) : 0);
   static constexpr size_t SMEM = size_t(ELEMS) * sizeof(T) + 16 * (D + 1);
@@ -161,19 +165,30 @@ __device__ __forceinline__ void tma_load(uint32_t dst, const CUtensorMap* map, i
       : "memory");
 }
 
-// Output column j of one product from the staged windows.  bx / by point at
-// the thread's lane in the slot of stored column j + LOX / j + LOY; column
-// offset c is c - LO slots further (contiguous thanks to the mirror).
-template <class T, int LN, class P, int SSX, int SSY, int LOX, int LOY, int R0, int R1, bool EDGE>
-__device__ __forceinline__ void prod_col(const T* __restrict__ bx, const T* __restrict__ by, ix j, ix n,
-                                         T* __restrict__ out) {
+// Output column j of one product from the staged windows.  A window points
+// at the thread's lane in the slot s of stored column j + LO; stored column
+// j + LO + q sits q slots further, wrapping once at RC (one compare-select
+// per column; the row offsets within a column are immediates).
+template <int SS, int RC>
+struct Win {
+  const void* b;
+  int s;
+  template <class T>
+  __device__ __forceinline__ const T* col(int q) const {
+    const T* p = static_cast<const T*>(b);
+    return s + q >= RC ? p + (q - RC) * SS : p + q * SS;
+  }
+};
+
+template <class T, int LN, class P, class WX, class WY, int LOX, int LOY, int R0, int R1, bool EDGE>
+__device__ __forceinline__ void prod_col(WX wx, WY wy, ix j, ix n, T* __restrict__ out) {
   constexpr int NE = P::EMAX - P::EMIN + 1;
   acc_t yv[NE];
   bool kv[NE];
 #pragma unroll
   for (int q = 0; q < NE; ++q) {
     const int e = P::EMIN + q;
-    const T* p = P::TY ? by + (e - LOY) * SSY + (P::YU - e) * LN : by + (0 - LOY) * SSY + (e + P::YU) * LN;
+    const T* p = P::TY ? wy.template col<T>(e - LOY) + (P::YU - e) * LN : wy.template col<T>(0 - LOY) + (e + P::YU) * LN;
     kv[q] = !EDGE || (j + e >= 0 && j + e < n);
     yv[q] = acc_t(*p);
   }
@@ -186,7 +201,8 @@ __device__ __forceinline__ void prod_col(const T* __restrict__ bx, const T* __re
     for (int q = 0; q < NE; ++q) {
       const int e = P::EMIN + q;
       if (e < elo || e > ehi) continue;
-      const T* p = P::TX ? bx + (d - LOX) * SSX + (e - d + P::XU) * LN : bx + (e - LOX) * SSX + (d - e + P::XU) * LN;
+      const T* p = P::TX ? wx.template col<T>(d - LOX) + (e - d + P::XU) * LN
+                         : wx.template col<T>(e - LOX) + (d - e + P::XU) * LN;
       if (!EDGE || kv[q]) acc = fma(acc_t(*p), yv[q], acc);
     }
     T v = T(acc);
@@ -195,19 +211,41 @@ __device__ __forceinline__ void prod_col(const T* __restrict__ bx, const T* __re
   }
 }
 
+// Consumer part PART of NPART (warp-uniform): the product it serves (the
+// two products of a fused VJP split the parts) and its share of that
+// product's output cells.
+template <class T, int LN, class Gm, class S, int NPART, int PART>
+__device__ __forceinline__ void do_part(const T* const* b, const int* sl, ix j, ix n, bool interior, T* o1, T* o2) {
+  constexpr int NSUB = S::TWO ? NPART / 2 : NPART;
+  constexpr int PI = S::TWO ? PART / NSUB : 0;
+  constexpr int SUB = PART % NSUB;
+  using P = std::conditional_t<PI == 0, typename S::P1, typename S::P2>;
+  constexpr int X = PI == 0 ? S::X1 : S::X2, Y = PI == 0 ? S::Y1 : S::Y2;
+  constexpr int R0 = P::CW * SUB / NSUB, R1 = P::CW * (SUB + 1) / NSUB;
+  using WX = Win<Gm::SS(X), Gm::WRC(X)>;
+  using WY = Win<Gm::SS(Y), Gm::WRC(Y)>;
+  T* o = PI == 0 ? o1 : o2;
+  if (interior)
+    prod_col<T, LN, P, WX, WY, S::lo(X), S::lo(Y), R0, R1, false>(WX{b[X], sl[X]}, WY{b[Y], sl[Y]}, j, n, o);
+  else
+    prod_col<T, LN, P, WX, WY, S::lo(X), S::lo(Y), R0, R1, true>(WX{b[X], sl[X]}, WY{b[Y], sl[Y]}, j, n, o);
+}
+
 // Producer warp: one lane walks the CTA's runs and issues, for every step,
 // the TMA copies of the operand columns new at that step (the whole first
 // window at a run start), after the consumers released the ring slots they
 // overwrite (empty barrier of the step NB earlier; a full drain at run
 // starts, where the column -> slot mapping restarts).  Consumers wait on the
 // step's full barrier, compute their output columns, and release the step.
-template <class T, int LN, int CJ, int D, int NPART, class S>
+template <class T, int LN, int CJ, int D, int NPART, class S, bool MIR>
 __global__ void __launch_bounds__(LN* CJ* NPART + 32) k_stream(const __grid_constant__ Maps maps, T* __restrict__ c1,
                                                               T* __restrict__ c2, SGeo G) {
-  using Gm = Geom<T, LN, CJ, D, NPART, S>;
+  using Gm = Geom<T, LN, CJ, D, NPART, S, MIR>;
   constexpr int NB = D + 1;
   constexpr int NC = Gm::NC;
   static_assert((LN * CJ) % 32 == 0, "a consumer part must be whole warps");
+  static_assert(NPART == 1 || NPART == 2 || NPART == 4, "parts");
+  static_assert(!S::TWO || NPART >= 2, "a fused VJP needs a part per product");
   static_assert(CJ <= 256 && LN * sizeof(T) % 16 == 0, "TMA box limits");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* ring = reinterpret_cast<T*>(smem_raw);
@@ -254,26 +292,26 @@ __global__ void __launch_bounds__(LN* CJ* NPART + 32) k_stream(const __grid_cons
 #pragma unroll
         for (int o = 0; o < S::NOP; ++o) {
           const uint32_t colb = uint32_t(Gm::SS(o) * sizeof(T));
-          const int slot = (l * CJ) % Gm::RC(o);
-          bytes += colb * CJ * (slot < S::H(o) ? 2u : 1u);
-          if (l == 0) bytes += colb * S::H(o) * (Gm::RC(o) - S::H(o) < S::H(o) ? 2u : 1u);
+          bytes += colb * CJ * (MIR && (l * CJ) % Gm::RC(o) < S::H(o) ? 2u : 1u);
+          if (l == 0) bytes += colb * S::H(o) * (MIR && Gm::RC(o) - S::H(o) < S::H(o) ? 2u : 1u);
         }
         bar_expect(bar, bytes);
 #pragma unroll
         for (int o = 0; o < S::NOP; ++o) {
-          const int lo = S::lo(o), hi = S::hi(o), Ho = S::H(o), RCo = Gm::RC(o);
+          const int lo = S::lo(o), hi = S::hi(o), RCo = Gm::RC(o);
           T* base = ring + Gm::OFF(o);
           if (l == 0) {  // the halo [lo, hi) before the first step's columns
             for (int rel = lo; rel < hi; ++rel) {
               const int slot = rel - hi + RCo;
               tma_load(smem_u32(base + slot * Gm::SS(o)), &maps.col[o], lane0, zf + rel, bar);
-              if (slot < Ho) tma_load(smem_u32(base + (slot + RCo) * Gm::SS(o)), &maps.col[o], lane0, zf + rel, bar);
+              if (MIR && slot < S::H(o))
+                tma_load(smem_u32(base + (slot + RCo) * Gm::SS(o)), &maps.col[o], lane0, zf + rel, bar);
             }
           }
           const int slot = (l * CJ) % RCo;
           const int z = zf + l * CJ + hi;
           tma_load(smem_u32(base + slot * Gm::SS(o)), &maps.step[o], lane0, z, bar);
-          if (slot < Ho) tma_load(smem_u32(base + (slot + RCo) * Gm::SS(o)), &maps.step[o], lane0, z, bar);
+          if (MIR && slot < S::H(o)) tma_load(smem_u32(base + (slot + RCo) * Gm::SS(o)), &maps.step[o], lane0, z, bar);
         }
       }
       g += steps;
@@ -298,43 +336,30 @@ __global__ void __launch_bounds__(LN* CJ* NPART + 32) k_stream(const __grid_cons
       const ix j = jt + cj;
       if (j < n) {
         const int rel = l * CJ + cj;  // column j relative to the run start; window starts at rel + lo
+        int sl[3];
         const T* b[3];
 #pragma unroll
-        for (int o = 0; o < 3; ++o)
-          b[o] = o < S::NOP ? ring + Gm::OFF(o) + ((rel + Gm::RC(o) - S::H(o)) % Gm::RC(o)) * Gm::SS(o) + lane : ring;
+        for (int o = 0; o < 3; ++o) {
+          sl[o] = o < S::NOP ? (rel + Gm::RC(o) - S::H(o)) % Gm::RC(o) : 0;
+          b[o] = o < S::NOP ? ring + Gm::OFF(o) + sl[o] * Gm::SS(o) + lane : ring;
+        }
         const bool interior = jt >= S::MARGIN && jt + CJ - 1 + S::MARGIN <= n - 1;
-        using P1 = typename S::P1;
-        constexpr int SX1 = Gm::SS(S::X1), SY1 = Gm::SS(S::Y1), LX1 = S::lo(S::X1), LY1 = S::lo(S::Y1);
-        T* o1 = c1 + ((tile * n + j) * P1::CW) * 32 + lane0 + lane;
-        if constexpr (S::TWO) {
-          using P2 = typename S::P2;
-          constexpr int SX2 = Gm::SS(S::X2), SY2 = Gm::SS(S::Y2), LX2 = S::lo(S::X2), LY2 = S::lo(S::Y2);
-          T* o2 = c2 + ((tile * n + j) * P2::CW) * 32 + lane0 + lane;
-          if (NPART == 1 || part == 0) {
-            if (interior)
-              prod_col<T, LN, P1, SX1, SY1, LX1, LY1, 0, P1::CW, false>(b[S::X1], b[S::Y1], j, n, o1);
-            else
-              prod_col<T, LN, P1, SX1, SY1, LX1, LY1, 0, P1::CW, true>(b[S::X1], b[S::Y1], j, n, o1);
-          }
-          if (NPART == 1 || part == 1) {
-            if (interior)
-              prod_col<T, LN, P2, SX2, SY2, LX2, LY2, 0, P2::CW, false>(b[S::X2], b[S::Y2], j, n, o2);
-            else
-              prod_col<T, LN, P2, SX2, SY2, LX2, LY2, 0, P2::CW, true>(b[S::X2], b[S::Y2], j, n, o2);
-          }
-        } else {
-          constexpr int HALF = NPART == 2 ? (P1::CW + 1) / 2 : P1::CW;
-          if (part == 0) {
-            if (interior)
-              prod_col<T, LN, P1, SX1, SY1, LX1, LY1, 0, HALF, false>(b[S::X1], b[S::Y1], j, n, o1);
-            else
-              prod_col<T, LN, P1, SX1, SY1, LX1, LY1, 0, HALF, true>(b[S::X1], b[S::Y1], j, n, o1);
-          } else {
-            if (interior)
-              prod_col<T, LN, P1, SX1, SY1, LX1, LY1, HALF, P1::CW, false>(b[S::X1], b[S::Y1], j, n, o1);
-            else
-              prod_col<T, LN, P1, SX1, SY1, LX1, LY1, HALF, P1::CW, true>(b[S::X1], b[S::Y1], j, n, o1);
-          }
+        T* o1 = c1 + ((tile * n + j) * S::P1::CW) * 32 + lane0 + lane;
+        T* o2 = nullptr;
+        if constexpr (S::TWO) o2 = c2 + ((tile * n + j) * S::P2::CW) * 32 + lane0 + lane;
+        switch (part) {
+          case 0:
+            do_part<T, LN, Gm, S, NPART, 0>(b, sl, j, n, interior, o1, o2);
+            break;
+          case 1:
+            if constexpr (NPART > 1) do_part<T, LN, Gm, S, NPART, 1>(b, sl, j, n, interior, o1, o2);
+            break;
+          case 2:
+            if constexpr (NPART > 2) do_part<T, LN, Gm, S, NPART, 2>(b, sl, j, n, interior, o1, o2);
+            break;
+          default:
+            if constexpr (NPART > 3) do_part<T, LN, Gm, S, NPART, 3>(b, sl, j, n, interior, o1, o2);
+            break;
         }
       }
       __syncwarp();
@@ -387,11 +412,12 @@ bool usable(const bgm_band& d) {
   return d.tile == 32 && (reinterpret_cast<uintptr_t>(d.data) & 15) == 0 && tiles * d.n < (ix(1) << 31);
 }
 
-template <class T, int LN, int CJ, int D, int NPART, class S>
+template <class T, int LN, int CJ, int D, int NPART, class S, bool MIR>
 bool run(const bgm_band* ops, const bgm_band& c1, const bgm_band* c2, const char* name, cudaStream_t s) {
-  using Gm = Geom<T, LN, CJ, D, NPART, S>;
+  using Gm = Geom<T, LN, CJ, D, NPART, S, MIR>;
   static_assert(Gm::SMEM <= 227 * 1024, "ring does not fit in shared memory");
-  auto kern = k_stream<T, LN, CJ, D, NPART, S>;
+  static_assert(Gm::THREADS <= 1024, "block too large");
+  auto kern = k_stream<T, LN, CJ, D, NPART, S, MIR>;
   const ix n = c1.n;
   if (n < 4 * (S::MARGIN + CJ)) return false;
   for (int o = 0; o < S::NOP; ++o)
@@ -429,10 +455,10 @@ bool run(const bgm_band* ops, const bgm_band& c1, const bgm_band* c2, const char
 // Configurations are given for fp64 (lane-group width LN, CJ columns per
 // step).  fp32 rows are half as wide: twice the lanes and half the columns
 // per step when LN < 32 (same thread count, same TMA row bytes).
-template <class T, int LN, int CJ, int D, int NPART, class S>
+template <class T, int LN, int CJ, int D, int NPART, class S, bool MIR>
 bool run_cfg(const bgm_band* ops, const bgm_band& c1, const bgm_band* c2, const char* name, cudaStream_t s) {
   constexpr bool widen = sizeof(T) == 4 && LN < 32 && CJ % 2 == 0;
-  return run<T, widen ? 2 * LN : LN, widen ? CJ / 2 : CJ, D, NPART, S>(ops, c1, c2, name, s);
+  return run<T, widen ? 2 * LN : LN, widen ? CJ / 2 : CJ, D, NPART, S, MIR>(ops, c1, c2, name, s);
 }
 
 bool same(const bgm_band& a, const bgm_band& b) {
@@ -458,12 +484,12 @@ using S_vdl = S_vjp<16, 0, 0, 16, 16, 0>;  // config 3 dL: L, L^T, G (16,0)
 template <class T>
 bool product_t(const bgm_band& a, int ta, const bgm_band& b, int tb, const bgm_band& c, cudaStream_t s) {
   if (!ta && tb && same(a, b) && a.lower == 8 && a.upper == 0 && c.lower == 8 && c.upper == 8)
-    return run_cfg<T, 32, 8, 3, 2, S_llt8>(&a, c, nullptr, "stream_llt8", s);
+    return run_cfg<T, 32, 8, 3, 2, S_llt8, true>(&a, c, nullptr, "stream_llt8", s);
   if (!ta && tb && same(a, b) && a.lower == 16 && a.upper == 0 && c.lower == 16 && c.upper == 0)
-    return run_cfg<T, 16, 8, 3, 2, S_llt16>(&a, c, nullptr, "stream_llt16", s);
+    return run_cfg<T, 16, 8, 3, 2, S_llt16, false>(&a, c, nullptr, "stream_llt16", s);
   if (!ta && !tb && a.lower == 8 && a.upper == 8 && b.lower == 3 && b.upper == 3 && c.lower == 11 && c.upper == 11) {
     const bgm_band ops[2] = {a, b};
-    return run_cfg<T, 16, 16, 2, 2, S_ab>(ops, c, nullptr, "stream_ab", s);
+    return run_cfg<T, 16, 16, 2, 2, S_ab, true>(ops, c, nullptr, "stream_ab", s);
   }
   return false;
 }
@@ -474,11 +500,11 @@ bool vjp_t(const bgm_band& a, const bgm_band& b, const bgm_band& pb, const bgm_b
   const bgm_band ops[3] = {pb, a, b};
   auto is = [](const bgm_band& x, int l, int u) { return x.lower == l && x.upper == u; };
   if (is(a, 8, 8) && is(b, 3, 3) && is(pb, 11, 11))
-    return run_cfg<T, 16, 4, 3, 2, S_vab>(ops, ab, &bb, "stream_vjp_ab", s);
+    return run_cfg<T, 16, 4, 3, 4, S_vab, true>(ops, ab, &bb, "stream_vjp_ab", s);
   if (is(a, 8, 0) && is(b, 0, 8) && is(pb, 8, 8))
-    return run_cfg<T, 16, 8, 2, 2, S_vllt>(ops, ab, &bb, "stream_vjp_llt", s);
+    return run_cfg<T, 16, 8, 2, 2, S_vllt, true>(ops, ab, &bb, "stream_vjp_llt", s);
   if (is(a, 16, 0) && is(b, 0, 16) && is(pb, 16, 0))
-    return run_cfg<T, 8, 16, 1, 2, S_vdl>(ops, ab, &bb, "stream_vjp_dl", s);
+    return run_cfg<T, 16, 8, 1, 2, S_vdl, false>(ops, ab, &bb, "stream_vjp_dl", s);
   return false;
 }
 
