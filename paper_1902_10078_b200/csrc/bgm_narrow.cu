@@ -33,6 +33,7 @@ __host__ __device__ constexpr int tri(int a, int b) { return a * (a + 1) / 2 + b
 struct Geo {
   ix batch, n, seg, tiles;
   int nseg, burn;
+  int l2a;  // solves: L2 bulk-prefetch distance in rows (0 = off)
 };
 
 struct Unit {
@@ -183,7 +184,7 @@ struct SolveP {
 // reference divides, kernels_serial.cpp:47).  Backward: x window x[a] =
 // x_{i+1+a}; x_i = (v_i - sum_a L(i+1+a, i) x[a]) / L(i,i).
 template <class T, int K, bool TR>
-__device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start, T* side,
+__device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start, T* side, int l2a,
                            const T* carry = nullptr) {
   constexpr int W = K + 1;
   const T* lb = bbase(C.l, b);
@@ -218,16 +219,26 @@ __device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start,
 #pragma unroll
     for (int a = 0; a <= K; ++a) win[a] = (carry && a < K) ? carry[a] : T(0);
   }
-  T cn[W], vn;
-  load_col(start, cn, vn);
+  // rows stream through a ring of PF prefetched columns (static register
+  // indices: the row loop is unrolled by PF); the tile's columns further
+  // ahead are pulled into L2 by one bulk prefetch per PF rows (a column of
+  // the 32 interleaved matrices is w * 256 contiguous bytes).
+  constexpr int PF = K * sizeof(T) >= 128 ? 2 : 4;
   const int dir = TR ? -1 : 1;
   const ix stop = TR ? s - 1 : e;
-#pragma unroll 1
-  for (ix i = start; i != stop; i += dir) {
-    T col[W], vv = vn;
+  const ix rows = TR ? start - stop : stop - start;
+  T cb[PF][W], vb_[PF];
 #pragma unroll
-    for (int a = 0; a <= K; ++a) col[a] = cn[a];
-    load_col(i + dir, cn, vn);
+  for (int q = 0; q < PF; ++q) load_col(start + q * dir, cb[q], vb_[q]);
+  auto l2_ahead = [&](ix i) {
+    const ix lo = TR ? i - l2a - PF + 1 : i + l2a, hi = lo + PF - 1;
+    if (l2a > 0 && lo >= 0 && hi < n)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lb - (b & 31) + lo * cs),
+                   "r"(unsigned(PF * cs * sizeof(T)))
+                   : "memory");
+  };
+  int same = 0;
+  auto row = [&](ix i, const T* col, T vv) {
     T xi;
     if (!TR) {
       xi = win[0] / col[0];
@@ -243,11 +254,37 @@ __device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start,
       for (int a = K - 1; a >= 1; --a) win[a] = win[a - 1];
       win[0] = xi;
     }
-    if (i >= s && i < e) xb[i * 32] = xi;
-    else if (side) {
+    if (i >= s && i < e) {
+      if (carry) {  // fix-up: K consecutive rows equal to pass 1 => same state => pass 1 is exact onwards
+        const T old = xb[i * 32];
+        same = (__double_as_longlong(double(old)) == __double_as_longlong(double(xi))) ? same + 1 : 0;
+      }
+      xb[i * 32] = xi;
+    } else if (side) {
       const ix o = TR ? i - e : i - (s - K);
       if (o >= 0 && o < K) side[o] = xi;
     }
+  };
+  ix i = start;
+#pragma unroll 1
+  for (ix blk = 0; blk + PF <= rows; blk += PF) {
+    if ((threadIdx.x & 31) == 0) l2_ahead(i);
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      T col[W], vv = vb_[q];
+#pragma unroll
+      for (int a = 0; a <= K; ++a) col[a] = cb[q][a];
+      load_col(i + PF * dir, cb[q], vb_[q]);
+      row(i, col, vv);
+      i += dir;
+    }
+    if (carry && same >= K) return;
+  }
+#pragma unroll
+  for (int q = 0; q < PF; ++q) {  // tail (rows % PF), ring order continues at slot 0
+    if (i == stop) break;
+    row(i, cb[q], vb_[q]);
+    i += dir;
   }
 }
 
@@ -265,7 +302,7 @@ __global__ void k_solve(SolveP<T> C, Geo G) {
     start = e + G.burn - 1 < G.n - 1 ? e + G.burn - 1 : G.n - 1;
     if (u.p + 1 < G.nseg) side = C.side + u.id * K;
   }
-  solve_unit<T, K, TR>(C, u.b, G.n, s, e, start, side);
+  solve_unit<T, K, TR>(C, u.b, G.n, s, e, start, side, G.l2a);
 }
 
 template <class T, int K, bool TR>
@@ -276,13 +313,11 @@ __global__ void k_solve_check(SolveP<T> C, Geo G, int32_t* uflag) {
   if (TR ? p + 1 >= G.nseg : p == 0) return;
   const ix b = id / G.nseg;
   const ix r0 = TR ? ix(p + 1) * G.seg : ix(p) * G.seg - K;
-  double sc = 0.0;
-  for (int c = 0; c < K; ++c)
-    if (r0 + c < G.n) sc = fmax(sc, dabs(C.x(b, r0 + c)));
-  const double tol = sizeof(T) == 8 ? kCheckTol : 1e-5;
+  // bitwise: the fix-up of a flagged segment stops as soon as it rejoins pass 1,
+  // so an exact check costs only the rows the burn-in had not yet converged
   bool bad = false;
   for (int c = 0; c < K; ++c)
-    if (r0 + c < G.n) bad |= !(fabs(double(C.side[id * K + c]) - double(C.x(b, r0 + c))) <= tol * (sc + 1e-300));
+    if (r0 + c < G.n) bad |= C.side[id * K + c] != C.x(b, r0 + c);
   uflag[id] = bad ? 1 : 0;
 }
 
@@ -290,7 +325,7 @@ template <class T, int K, bool TR>
 __global__ void k_solve_repair(SolveP<T> C, Geo G) {
   const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
   if (b >= G.batch || !C.flag[b]) return;
-  solve_unit<T, K, TR>(C, b, G.n, 0, G.n, TR ? G.n - 1 : 0, nullptr);
+  solve_unit<T, K, TR>(C, b, G.n, 0, G.n, TR ? G.n - 1 : 0, nullptr, G.l2a);
 }
 
 // Fix-up of segments whose burn-in did not converge: the neighbour's genuine
@@ -315,7 +350,7 @@ __global__ void k_solve_fix(SolveP<T> C, Geo G, const int32_t* uflag, const T* s
   if (!u.live || !uflag[u.id]) return;
   const ix s = ix(u.p) * G.seg, e = s + G.seg < G.n ? s + G.seg : G.n;
   const T* carry = snap + (TR ? u.id + 1 : u.id - 1) * K;
-  solve_unit<T, K, TR>(C, u.b, G.n, s, e, TR ? e - 1 : s, nullptr, carry);
+  solve_unit<T, K, TR>(C, u.b, G.n, s, e, TR ? e - 1 : s, nullptr, G.l2a, carry);
 }
 
 template <class T, int K, bool TR>
@@ -626,6 +661,17 @@ __global__ void k_report(const int64_t* fail, ix batch, ix n, int code, int back
 
 int g_segment_rows = 0;
 
+// Solves forget their carry-in more slowly than the Cholesky Schur window
+// (the error of a zero start decays with L^-1, ~0.9 per row for config-0
+// factors at k = 16, and the slowest of a warp's 32 matrices sets the pace):
+// a longer burn-in, and flagged segments rejoin pass 1 bitwise (early exit).
+int solve_burn_rows(int K) {
+  int burn = 24 * K > kBurnMin ? 24 * K : kBurnMin;
+  if (const char* bv = std::getenv("BGM_NARROW_BURN"))
+    if (std::atoi(bv) >= 1) burn = std::atoi(bv);
+  return burn;
+}
+
 int burn_rows(int K) {
   int burn = kBurnGen * K > kBurnMin ? kBurnGen * K : kBurnMin;
   if (const char* bv = std::getenv("BGM_NARROW_BURN"))
@@ -634,12 +680,14 @@ int burn_rows(int K) {
 }
 
 template <class KernelT>
-Geo make_geo(KernelT kern, size_t smem, ix batch, ix n, int burn) {
+Geo make_geo(KernelT kern, size_t smem, ix batch, ix n, int burn, int segf_default = 4) {
   Geo G;
   G.batch = batch;
   G.n = n;
   G.tiles = (batch + 31) / 32;
   G.burn = burn;
+  G.l2a = 8;
+  if (const char* v = std::getenv("BGM_NARROW_L2AHEAD")) G.l2a = std::atoi(v);
   int sms = 148, dev = 0, per = 1;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, smem);
@@ -649,7 +697,9 @@ Geo make_geo(KernelT kern, size_t smem, ix batch, ix n, int burn) {
     ix nseg = ix(sms) * per / G.tiles;
     if (nseg < 1) nseg = 1;
     seg = (n + nseg - 1) / nseg;
-    if (seg < 4 * ix(burn)) seg = 4 * ix(burn);
+    const char* sv = std::getenv("BGM_NARROW_SEGF");
+    const int segf = sv ? std::atoi(sv) : segf_default;
+    if (seg < segf * ix(burn)) seg = segf * ix(burn);
   }
   if (seg < 1) seg = 1;
   G.seg = seg;
@@ -706,8 +756,8 @@ bool run_chol(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, c
 
 template <class T, int K, bool TR>
 bool run_solve(const bgm_band& l, const bgm_vec& v, const bgm_vec& x, int32_t* st, int64_t* row, cudaStream_t s) {
-  const int burn = burn_rows(K);
-  const Geo G = make_geo(k_solve<T, K, TR>, 0, l.batch, l.n, burn);
+  const int burn = solve_burn_rows(K);
+  const Geo G = make_geo(k_solve<T, K, TR>, 0, l.batch, l.n, burn, 2);
   const ix units = G.batch * G.nseg;
   const size_t side = sizeof(T) * size_t(units) * K;
   Scratch ws;
