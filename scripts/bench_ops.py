@@ -69,21 +69,30 @@ def counts(op, k, wa=None, wb=None, w=None):
 
 
 def timeit(fn, reps):
+    """Median per-call time.  Ops shorter than 2 ms are timed as `inner`
+    back-to-back API calls between two events (the host enqueues call i+1
+    while call i runs, as a caller looping over batches would), so the
+    figure is the op's device throughput rather than Python launch latency;
+    a host-bound op still shows as host-bound."""
     fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    fn()
+    e1.record()
+    torch.cuda.synchronize()
+    t_first = e0.elapsed_time(e1)
+    if t_first > 2000:  # very slow op: one timed rep is enough
+        return t_first
+    inner = 1 if t_first > 2.0 else max(2, min(20, int(4.0 / max(t_first, 1e-3))))
     out = []
-    t_first = None
-    for r in range(reps):
+    for _ in range(reps):
         e0.record()
-        fn()
+        for _ in range(inner):
+            fn()
         e1.record()
         torch.cuda.synchronize()
-        out.append(e0.elapsed_time(e1))
-        if r == 0:
-            t_first = out[0]
-            if t_first > 2000:  # very slow op: one timed rep is enough
-                break
+        out.append(e0.elapsed_time(e1) / inner)
     return statistics.median(out)
 
 
