@@ -594,6 +594,7 @@ __global__ void k_diag_small(Band<T> l, ix batch, int64_t* fail) {
 template <class T>
 struct VcholP {
   Band<T> l, lb, qb;
+  int l2a;
   T* side;  // [unit][K][K+1]: burn-in q_bar columns [e, e+K)
   int32_t* flag;
 };
@@ -650,8 +651,16 @@ __device__ void vchol_unit(const VcholP<T>& C, ix b, ix n, ix s, ix e, ix start,
   // (x, y) feeds row j's g at (x, y) and row j-1's at (x+1, y+1), and moves
   // two places down the diagonal; row j's new column (the window's column 0
   // after row j) is folded into row j-1 after the pass.
+  const int L2A = C.l2a;  // L2 bulk prefetch distance (columns) of L and L-bar, per tile (0 = off)
+  const T* ltile = lbase - (b & 31);
+  const T* gtile = gbase - (b & 31);
 #pragma unroll 1
   for (; j - 1 >= s; j -= 2) {
+    if (L2A > 0 && (threadIdx.x & 31) == 0 && j - 1 - L2A >= 0) {
+      const unsigned bytes = unsigned(2 * cs * sizeof(T));
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ltile + (j - 1 - L2A) * cs), "r"(bytes) : "memory");
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gtile + (j - 1 - L2A) * cs), "r"(bytes) : "memory");
+    }
     T u[K], g[K], u2[K], g2[K], d, gd, d2, gd2;
     load(j, u, g, d, gd);
     load(j - 1, u2, g2, d2, gd2);
@@ -991,6 +1000,8 @@ bool run_vchol(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cudaSt
   C.l = view<T>(l);
   C.lb = view<T>(lb);
   C.qb = view<T>(qb);
+  C.l2a = 4;  // measured best of 0 / 4 / 16 at k = 8, 16
+  if (const char* v = std::getenv("BGM_VCHOL_L2A")) C.l2a = std::atoi(v);
   C.side = reinterpret_cast<T*>(ws.p);
   C.flag = reinterpret_cast<int32_t*>(ws.p + (side + 7) / 8 * 8);
   cudaMemsetAsync(C.flag, 0, sizeof(int32_t) * size_t(G.batch), s);
