@@ -10,6 +10,8 @@
 // the path for everything else.  There is no CPU fallback anywhere.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
@@ -261,14 +263,37 @@ __global__ void k_band_flat(Band<T> o, ix batch, F f) {
   const ix g = blockIdx.y;
   const unsigned tile = 1u << o.s;
   const unsigned per = unsigned(o.n * o.w) << o.s;
-  for (unsigned x = blockIdx.x * blockDim.x + threadIdx.x; x < per; x += gridDim.x * blockDim.x) {
-    const unsigned cr = x >> o.s;
-    const unsigned j = cr / unsigned(o.w), r = cr - j * unsigned(o.w);
-    const ix b = g * tile + (x & (tile - 1));
-    const ix i = ix(j) - o.up + r;
-    T val = T(0);
-    if (b < batch && i >= 0 && i < o.n) val = f(b, i, ix(j), int(r));
-    o.p[g * ix(per) + x] = val;
+  T* base = o.p + g * ix(per);
+  // two consecutive elements per thread, one 2-wide store (per is even for
+  // tile 32 and for tile 1 when n * w is even)
+  using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
+  if (per & 1) {  // odd block (tile 1, n * w odd): blocks of odd groups are not 2-element aligned
+    for (unsigned x = blockIdx.x * blockDim.x + threadIdx.x; x < per; x += gridDim.x * blockDim.x) {
+      const unsigned cr = x >> o.s;
+      const unsigned j = cr / unsigned(o.w), r = cr - j * unsigned(o.w);
+      const ix b = g * tile + (x & (tile - 1));
+      const ix i = ix(j) - o.up + r;
+      base[x] = (b < batch && i >= 0 && i < o.n) ? f(b, i, ix(j), int(r)) : T(0);
+    }
+    return;
+  }
+  const unsigned pairs = per >> 1;
+  for (unsigned x2 = blockIdx.x * blockDim.x + threadIdx.x; x2 < pairs; x2 += gridDim.x * blockDim.x) {
+    const unsigned x = x2 << 1;
+    T val[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const unsigned xe = x + h;
+      const unsigned cr = xe >> o.s;
+      const unsigned j = cr / unsigned(o.w), r = cr - j * unsigned(o.w);
+      const ix b = g * tile + (xe & (tile - 1));
+      const ix i = ix(j) - o.up + r;
+      val[h] = (b < batch && i >= 0 && i < o.n) ? f(b, i, ix(j), int(r)) : T(0);
+    }
+    V2 v;
+    v.x = val[0];
+    v.y = val[1];
+    *reinterpret_cast<V2*>(base + x) = v;
   }
 }
 
