@@ -43,4 +43,6 @@ from .api import (  # noqa: F401
     vjp_sparse_inverse_subset,
 )
 
+from . import autograd  # noqa: E402,F401  (torch.autograd.Function wrappers)
+
 __all__ = [n for n in dir() if not n.startswith("_")]
