@@ -178,6 +178,31 @@ int bgm_marginal_likelihood_grad(bgm_band l, bgm_vec y, double tau2, double* los
                                  bgm_band l_bar, double* tau2_bar, int32_t* status, int64_t* row,
                                  bgm_stream stream);
 
+/* ------------------------------------------------- VI objective */
+/* Tape::trace_product_sym (tape.cpp:274-302): per matrix
+ * sum_j a(j,j) b(j,j) + 2 sum_{0 < i-j <= min(bw_a, bw_b)} a(i,j) b(i,j)
+ * of two symmetric lower stores.  out: B device doubles.  fp64. */
+int bgm_trace_product_sym(bgm_band a, bgm_band b, double* out, bgm_stream stream);
+
+/* Reverse of trace_product_sym (tape.cpp:285-301): a_bar = c_bar * seed(b)
+ * on band(a), b_bar = c_bar * seed(a) on band(b), seed(x) = x on the
+ * diagonal and 2x below it (stored-cell convention).  c_bar: B device
+ * doubles; either output may have data == NULL (not wanted).  fp64. */
+int bgm_vjp_trace_product_sym(bgm_band a, bgm_band b, const double* c_bar, bgm_band a_bar,
+                              bgm_band b_bar, bgm_stream stream);
+
+/* infer::kl_divergence (inference.cpp:247-268) and its gradient:
+ * KL(N(m_q, (L_q L_q^T)^-1) || N(m_p, (L_p L_p^T)^-1)) per matrix,
+ *   = 1/2 [ tr(Q_p S_q) + 2 (log|L_q| - log|L_p|) + |L_p^T (m_p - m_q)|^2 - n ]
+ * with S_q the inverse subset of L_q and Q_p = band(L_p L_p^T).  Outputs kl
+ * (B device doubles), m_q_bar and l_q_bar (stored cells).  L_q's band must
+ * cover L_p's (BGM_ERR_DIM otherwise, as the reference).  Errors, first of
+ * log|L_p| (NONPOS_DIAG), the subset of L_q (SINGULAR), log|L_q|
+ * (NONPOS_DIAG).  fp64. */
+int bgm_kl_divergence_grad(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p, double* kl,
+                           bgm_vec m_q_bar, bgm_band l_q_bar, int32_t* status, int64_t* row,
+                           bgm_stream stream);
+
 /* ------------------------------------------------- instrumentation */
 /* Per-kernel CUDA-event timing on the launching stream (off by default).
  * bgm_timing_enable(1) clears and starts recording; bgm_timing_read(i, ...)

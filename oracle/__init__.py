@@ -244,6 +244,21 @@ class Oracle:
                                              st.ctypes.data_as(_i32p), row.ctypes.data_as(_i64p))
         return loss, lbar, tbar, st, row
 
+    def kl_divergence_grad(self, mq, lq, mp, lp):
+        """infer::kl_divergence (inference.cpp:247-268) and its gradient in
+        (m_q, L_q); reference (verbatim tape) only."""
+        if self.which != "reference":
+            raise RuntimeError("kl_divergence lives in the compiled reference tape only")
+        mq, lq, mp, lp = _f64(mq), _f64(lq), _f64(mp), _f64(lp)
+        B, n, wq = lq.shape
+        wp = lp.shape[2]
+        kl, mb, lb = np.zeros(B), np.zeros((B, n)), np.zeros_like(lq)
+        st, row = self._status(B)
+        self._fn("kl_divergence_grad")(_i64(B), _i64(n), _i64(wq - 1), _i64(wp - 1), _ptr(mq), _ptr(lq), _ptr(mp),
+                                       _ptr(lp), _ptr(kl), _ptr(mb), _ptr(lb), st.ctypes.data_as(_i32p),
+                                       row.ctypes.data_as(_i64p))
+        return kl, mb, lb, st, row
+
     # ---------------------------------------------------------- reference only
     def run_grad_suite(self, seed: int, instances: int):
         if self.which != "reference":

@@ -326,6 +326,47 @@ int ref_marginal_likelihood_grad(ix batch, ix n, ix bw, const double* L, const d
   return 0;
 }
 
+// VI objective term: infer::kl_divergence (inference.cpp:247-268) restated
+// over the compiled reference Tape node for node -- trace_product_sym of the
+// inverse subset with the prior precision (tape.cpp:274-302), the log-det
+// difference, the whitened mean difference -- with precision_from_factor
+// (inference.cpp:23-26) as the restricted product.  Gradients in m_q and L_q
+// (stored cells) come from Tape::backward.
+int ref_kl_divergence_grad(ix batch, ix n, ix bq, ix bp, const double* mq, const double* lq,
+                           const double* mp, const double* lp, double* kl, double* mq_bar,
+                           double* lq_bar, std::int32_t* status, ix* row) {
+  over_batch(batch, [&](ix b) {
+    status[b] = guarded(
+        [&] {
+          const BandedMatrix l_q = load(n, bq, 0, lq + b * n * (bq + 1));
+          const BandedMatrix l_p = load(n, bp, 0, lp + b * n * (bp + 1));
+          const Eigen::VectorXd m_q = load_vec(n, mq + b * n);
+          const Eigen::VectorXd m_p = load_vec(n, mp + b * n);
+          const SymmetricBandedMatrix qp = SymmetricBandedMatrix::from_lower(
+              ops::product_band_band_restricted(l_p, transpose(l_p), bp, 0));
+          const double logdet_p = ops::log_det_from_cholesky(l_p);
+          tape::Tape t;
+          const tape::NodeRef mn = t.leaf("m", m_q);
+          const tape::NodeRef ln = t.leaf("l", l_q);
+          const tape::NodeRef trace = t.trace_product_sym(t.sparse_inverse_subset(ln), t.constant(qp));
+          const tape::NodeRef logdets =
+              t.mul(t.constant(2.0), t.sub(t.log_det_from_cholesky(ln), t.constant(logdet_p)));
+          const tape::NodeRef diff = t.sub_vec(t.constant(m_p), mn);
+          const tape::NodeRef white = t.product_band_vec(t.constant(l_p), diff, true);
+          tape::NodeRef inner = t.add(trace, logdets);
+          inner = t.add(inner, t.dot(white, white));
+          inner = t.add(inner, t.constant(-static_cast<double>(n)));
+          const tape::NodeRef obj = t.mul(t.constant(0.5), inner);
+          kl[b] = t.scalar(obj);
+          auto grads = t.backward(obj);
+          store_vec(std::get<Eigen::VectorXd>(grads.at("m")), mq_bar + b * n);
+          store(std::get<BandedMatrix>(grads.at("l")), lq_bar + b * n * (bq + 1));
+        },
+        &row[b]);
+  });
+  return 0;
+}
+
 // Reference gradient suite (gradcheck.cpp:288-304), used to pin the oracle
 // build against the reference's own FD tests (test_grad.cpp:32-40,
 // acceptance.cpp:142-147).  Writes one max-rel-err per op in op_names() order.

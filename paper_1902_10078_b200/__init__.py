@@ -22,6 +22,7 @@ from .api import (  # noqa: F401
     T,
     cholesky,
     library,
+    kl_divergence_grad,
     library_path,
     log_det_from_cholesky,
     marginal_likelihood_grad,
@@ -33,6 +34,7 @@ from .api import (  # noqa: F401
     solve_mat,
     solve_vec,
     sparse_inverse_subset,
+    trace_product_sym,
     vjp_cholesky,
     vjp_log_det_from_cholesky,
     vjp_outer_band,
@@ -41,6 +43,7 @@ from .api import (  # noqa: F401
     vjp_solve_mat,
     vjp_solve_vec,
     vjp_sparse_inverse_subset,
+    vjp_trace_product_sym,
 )
 
 from . import autograd  # noqa: E402,F401  (torch.autograd.Function wrappers)

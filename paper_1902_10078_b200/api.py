@@ -515,6 +515,44 @@ def vjp_log_det_from_cholesky(l: Bands, c_bar) -> Bands:
     return l_bar
 
 
+# --------------------------------------------------------------------- VI objective
+def trace_product_sym(a: Bands, b: Bands) -> torch.Tensor:
+    """Tape::trace_product_sym (tape.cpp:274-284) of two symmetric lower
+    stores: (B,) tensor of tr(A B) over their common band.  fp64."""
+    _same(a, b)
+    out = torch.empty(a.batch, dtype=torch.float64, device=a.data.device)
+    _call("bgm_trace_product_sym", a.desc(), b.desc(), C.c_void_p(out.data_ptr()), _stream())
+    return out
+
+
+def vjp_trace_product_sym(a: Bands, b: Bands, c_bar):
+    """Reverse of trace_product_sym (tape.cpp:285-301) -> (a_bar, b_bar),
+    stored-cell convention; c_bar scalar or (B,)."""
+    cb = torch.as_tensor(c_bar, dtype=torch.float64, device=a.data.device).expand(a.batch).contiguous()
+    a_bar, b_bar = a.like(), b.like()
+    _call("bgm_vjp_trace_product_sym", a.desc(), b.desc(), C.c_void_p(cb.data_ptr()), a_bar.desc(), b_bar.desc(),
+          _stream())
+    return a_bar, b_bar
+
+
+def kl_divergence_grad(m_q: Vecs, l_q: Bands, m_p: Vecs, l_p: Bands, check: bool = True):
+    """infer::kl_divergence (inference.cpp:247-268): KL(q || p) for
+    q = N(m_q, (L_q L_q^T)^-1), p = N(m_p, (L_p L_p^T)^-1), per matrix, with
+    its gradient in the variational parameters.  Returns (kl[B], m_q_bar,
+    l_q_bar).  L_q's band must cover L_p's (DimensionMismatch otherwise)."""
+    if l_q.lower < l_p.lower:
+        raise DimensionMismatch("kl: variational band must cover the prior band")
+    _same(l_q, m_q)
+    _same(l_q, l_p)
+    kl = torch.empty(l_q.batch, dtype=torch.float64, device=l_q.data.device)
+    m_bar, l_bar = m_q.like(), l_q.like()
+    st = _Status(l_q.batch, l_q.data.device)
+    _call("bgm_kl_divergence_grad", m_q.desc(), l_q.desc(), m_p.desc(), l_p.desc(), C.c_void_p(kl.data_ptr()),
+          m_bar.desc(), l_bar.desc(), *st.ptrs(), _stream())
+    _check(st, check)
+    return kl, m_bar, l_bar
+
+
 # --------------------------------------------------------------------- config 3
 def marginal_likelihood_grad(L: Bands, y: Vecs, tau2: float, check: bool = True, out=None):
     """Config-3 learning step: per matrix, the log marginal

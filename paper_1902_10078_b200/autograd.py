@@ -263,3 +263,33 @@ def marginal_likelihood(L: Bands, y: Vecs, tau2) -> torch.Tensor:
     a 0-d tensor).  One fused forward+reverse pass; y is not differentiated."""
     t = tau2 if isinstance(tau2, torch.Tensor) else torch.tensor(float(tau2), dtype=torch.float64)
     return _MarginalLikelihood.apply(L.data, y.data, t, _meta(L), (y.batch, y.n, y.tile))
+
+
+class _KL(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, mqd, lqd, mpd, lpd, vmeta, qmeta, pmeta):
+        kl, mb, lb = api.kl_divergence_grad(_vecs(mqd, vmeta), _bands(lqd, qmeta), _vecs(mpd, vmeta),
+                                            _bands(lpd, pmeta))
+        ctx.vmeta, ctx.qmeta = vmeta, qmeta
+        ctx.save_for_backward(mb.data, lb.data)
+        return kl
+
+    @staticmethod
+    def backward(ctx, gkl):
+        mbd, lbd = ctx.saved_tensors
+        b, tile = ctx.qmeta[0], ctx.qmeta[4]
+        g = gkl.to(lbd.dtype)
+        if tile == 32:
+            gp = torch.zeros(lbd.shape[0] * 32, dtype=lbd.dtype, device=lbd.device)
+            gp[:b] = g
+            gl, gm = lbd * gp.view(lbd.shape[0], 1, 1, 32), mbd * gp.view(mbd.shape[0], 1, 32)
+        else:
+            gl, gm = lbd * g.view(b, 1, 1), mbd * g.view(b, 1)
+        return _clean(gm, b, tile), _clean(gl, b, tile), None, None, None, None, None
+
+
+def kl_divergence(m_q: Vecs, l_q: Bands, m_p: Vecs, l_p: Bands) -> torch.Tensor:
+    """infer::kl_divergence (inference.cpp:247-268) as a (B,) tensor,
+    differentiable in the variational parameters m_q and L_q (stored cells);
+    the prior (m_p, L_p) is constant, as in the reference's VI objective."""
+    return _KL.apply(m_q.data, l_q.data, m_p.data, l_p.data, (m_q.batch, m_q.n, m_q.tile), _meta(l_q), _meta(l_p))
