@@ -203,6 +203,16 @@ int bgm_kl_divergence_grad(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p,
                            bgm_vec m_q_bar, bgm_band l_q_bar, int32_t* status, int64_t* row,
                            bgm_stream stream);
 
+/* infer::elbo (inference.cpp:276-287) for a Gaussian likelihood observing
+ * every latent (selection = identity): E_q[log N(y | F, tau2 I)] - KL(q || p),
+ * the expected log-likelihood in closed form (inference.cpp:52-63) with the
+ * marginal variances diag(S_q).  Outputs elbo and kl (B device doubles each),
+ * the ELBO's gradient in m_q and L_q, and optionally (tau2_bar != NULL) its
+ * tau2 partial.  Errors as bgm_kl_divergence_grad; tau2 <= 0: BGM_ERR_ARG.  fp64. */
+int bgm_elbo_gaussian_grad(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p, bgm_vec y, double tau2,
+                           double* elbo, double* kl, bgm_vec m_q_bar, bgm_band l_q_bar, double* tau2_bar,
+                           int32_t* status, int64_t* row, bgm_stream stream);
+
 /* ------------------------------------------------- instrumentation */
 /* Per-kernel CUDA-event timing on the launching stream (off by default).
  * bgm_timing_enable(1) clears and starts recording; bgm_timing_read(i, ...)

@@ -259,6 +259,21 @@ class Oracle:
                                        row.ctypes.data_as(_i64p))
         return kl, mb, lb, st, row
 
+    def elbo_gaussian_grad(self, mq, lq, mp, lp, y, tau2):
+        """infer::elbo (inference.cpp:276-287), GaussianLik, full observation;
+        reference (verbatim tape) only.  -> elbo, m_bar, l_bar, tau2_bar, st, row."""
+        if self.which != "reference":
+            raise RuntimeError("elbo lives in the compiled reference tape only")
+        mq, lq, mp, lp, y = _f64(mq), _f64(lq), _f64(mp), _f64(lp), _f64(y)
+        B, n, wq = lq.shape
+        wp = lp.shape[2]
+        el, mb, lb, tb = np.zeros(B), np.zeros((B, n)), np.zeros_like(lq), np.zeros(B)
+        st, row = self._status(B)
+        self._fn("elbo_gaussian_grad")(_i64(B), _i64(n), _i64(wq - 1), _i64(wp - 1), _ptr(mq), _ptr(lq), _ptr(mp),
+                                       _ptr(lp), _ptr(y), C.c_double(tau2), _ptr(el), _ptr(mb), _ptr(lb), _ptr(tb),
+                                       st.ctypes.data_as(_i32p), row.ctypes.data_as(_i64p))
+        return el, mb, lb, tb, st, row
+
     # ---------------------------------------------------------- reference only
     def run_grad_suite(self, seed: int, instances: int):
         if self.which != "reference":

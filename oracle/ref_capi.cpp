@@ -367,6 +367,65 @@ int ref_kl_divergence_grad(ix batch, ix n, ix bq, ix bp, const double* mq, const
   return 0;
 }
 
+// infer::elbo (inference.cpp:276-287) for a GaussianLik observing every
+// latent: the Gaussian branch of expected_loglik (inference.cpp:52-63,
+// anonymous in the reference, restated) joins the compiled reference Tape as
+// a linearized scalar over (m_q, diag_sym(subset(L_q))), minus the KL built
+// node for node as in ref_kl_divergence_grad.
+int ref_elbo_gaussian_grad(ix batch, ix n, ix bq, ix bp, const double* mq, const double* lq,
+                           const double* mp, const double* lp, const double* y, double tau2,
+                           double* elbo, double* mq_bar, double* lq_bar, double* tau2_bar,
+                           std::int32_t* status, ix* row) {
+  over_batch(batch, [&](ix b) {
+    status[b] = guarded(
+        [&] {
+          const BandedMatrix l_q = load(n, bq, 0, lq + b * n * (bq + 1));
+          const BandedMatrix l_p = load(n, bp, 0, lp + b * n * (bp + 1));
+          const Eigen::VectorXd m_q = load_vec(n, mq + b * n);
+          const Eigen::VectorXd m_p = load_vec(n, mp + b * n);
+          const Eigen::VectorXd yv = load_vec(n, y + b * n);
+          const SymmetricBandedMatrix qp = SymmetricBandedMatrix::from_lower(
+              ops::product_band_band_restricted(l_p, transpose(l_p), bp, 0));
+          const double logdet_p = ops::log_det_from_cholesky(l_p);
+          tape::Tape t;
+          const tape::NodeRef mn = t.leaf("m", m_q);
+          const tape::NodeRef ln = t.leaf("l", l_q);
+          // expected log-likelihood (inference.cpp:278-285)
+          const tape::NodeRef marg_var = t.diag_sym(t.sparse_inverse_subset(ln));
+          const Eigen::VectorXd& mean = t.vector(mn);
+          const Eigen::VectorXd& var = t.vector(marg_var);
+          const double kLog2Pi = 1.8378770664093454836;
+          double value = 0.0, d_tau2 = 0.0;
+          Eigen::VectorXd d_mean = Eigen::VectorXd::Zero(n), d_var = Eigen::VectorXd::Zero(n);
+          for (ix i = 0; i < n; ++i) {
+            const double r = yv(i) - mean(i);
+            value += -0.5 * (std::log(tau2) + kLog2Pi) - (r * r + var(i)) / (2.0 * tau2);
+            d_mean(i) = r / tau2;
+            d_var(i) = -0.5 / tau2;
+            d_tau2 += (r * r + var(i)) / (2.0 * tau2 * tau2) - 0.5 / tau2;
+          }
+          const tape::NodeRef ve = t.linearized_scalar(value, {{mn, d_mean}, {marg_var, d_var}});
+          // kl_divergence (inference.cpp:255-267)
+          const tape::NodeRef trace = t.trace_product_sym(t.sparse_inverse_subset(ln), t.constant(qp));
+          const tape::NodeRef logdets =
+              t.mul(t.constant(2.0), t.sub(t.log_det_from_cholesky(ln), t.constant(logdet_p)));
+          const tape::NodeRef diff = t.sub_vec(t.constant(m_p), mn);
+          const tape::NodeRef white = t.product_band_vec(t.constant(l_p), diff, true);
+          tape::NodeRef inner = t.add(trace, logdets);
+          inner = t.add(inner, t.dot(white, white));
+          inner = t.add(inner, t.constant(-static_cast<double>(n)));
+          const tape::NodeRef obj = t.sub(ve, t.mul(t.constant(0.5), inner));
+          elbo[b] = t.scalar(obj);
+          tau2_bar[b] = d_tau2;
+          auto grads = t.backward(obj);
+          store_vec(std::get<Eigen::VectorXd>(grads.at("m")), mq_bar + b * n);
+          store(std::get<BandedMatrix>(grads.at("l")), lq_bar + b * n * (bq + 1));
+        },
+        &row[b]);
+  });
+  return 0;
+}
+
 // Reference gradient suite (gradcheck.cpp:288-304), used to pin the oracle
 // build against the reference's own FD tests (test_grad.cpp:32-40,
 // acceptance.cpp:142-147).  Writes one max-rel-err per op in op_names() order.

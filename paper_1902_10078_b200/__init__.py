@@ -22,6 +22,7 @@ from .api import (  # noqa: F401
     T,
     cholesky,
     library,
+    elbo_gaussian_grad,
     kl_divergence_grad,
     library_path,
     log_det_from_cholesky,

@@ -553,6 +553,29 @@ def kl_divergence_grad(m_q: Vecs, l_q: Bands, m_p: Vecs, l_p: Bands, check: bool
     return kl, m_bar, l_bar
 
 
+def elbo_gaussian_grad(m_q: Vecs, l_q: Bands, m_p: Vecs, l_p: Bands, y: Vecs, tau2: float, check: bool = True):
+    """infer::elbo (inference.cpp:276-287) for a Gaussian likelihood that
+    observes every latent: E_q log N(y | F, tau2 I) - KL(q || p) per matrix.
+    Returns (elbo[B], kl[B], m_q_bar, l_q_bar, tau2_bar[B]) -- the ELBO's
+    gradient in the variational parameters and its tau2 partial."""
+    if l_q.lower < l_p.lower:
+        raise DimensionMismatch("kl: variational band must cover the prior band")
+    if not tau2 > 0:
+        raise BandgmError("parameter 'tau2' must be strictly positive")
+    _same(l_q, m_q)
+    _same(l_q, l_p)
+    _same(l_q, y)
+    dev = l_q.data.device
+    elbo, kl, tb = (torch.empty(l_q.batch, dtype=torch.float64, device=dev) for _ in range(3))
+    m_bar, l_bar = m_q.like(), l_q.like()
+    st = _Status(l_q.batch, dev)
+    _call("bgm_elbo_gaussian_grad", m_q.desc(), l_q.desc(), m_p.desc(), l_p.desc(), y.desc(), C.c_double(tau2),
+          C.c_void_p(elbo.data_ptr()), C.c_void_p(kl.data_ptr()), m_bar.desc(), l_bar.desc(),
+          C.c_void_p(tb.data_ptr()), *st.ptrs(), _stream())
+    _check(st, check)
+    return elbo, kl, m_bar, l_bar, tb
+
+
 # --------------------------------------------------------------------- config 3
 def marginal_likelihood_grad(L: Bands, y: Vecs, tau2: float, check: bool = True, out=None):
     """Config-3 learning step: per matrix, the log marginal

@@ -80,14 +80,6 @@ __global__ void k_sub(Vec<double> a, Vec<double> b, Vec<double> out, ix batch) {
   out(mb, i) = a(mb, i) - b(mb, i);
 }
 
-// L_q-bar(j, j) += 1 / L_q(j, j): the log|L_q| term (grad.cpp:172-176 with c_bar = 1)
-__global__ void k_add_logdet_bar(Band<double> lb, Band<double> l, ix batch) {
-  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
-  ix mb, j;
-  if (l.n == 0 || !split_bj(t, batch, l.n, l.s, mb, j)) return;
-  lb.cell(mb, 0, j) += 1.0 / l.cell(mb, 0, j);
-}
-
 // inference.cpp:262-267: 0.5 * (trace + 2 (logdet_q - logdet_p) + quad - n)
 __global__ void k_kl_final(const double* tr, const double* ldq, const double* ldp, const double* quad, ix n,
                            ix batch, double* kl) {
@@ -187,30 +179,100 @@ int bgm_vjp_trace_product_sym(bgm_band a, bgm_band b, const double* c_bar, bgm_b
   return e == cudaSuccess ? BGM_OK : set_error(e);
 }
 
-int bgm_kl_divergence_grad(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p, double* kl, bgm_vec m_q_bar,
-                           bgm_band l_q_bar, int32_t* status, int64_t* row, bgm_stream stream) {
+}  // extern "C"
+
+namespace bgm {
+namespace vi {
+namespace {
+
+constexpr double kLog2Pi = 1.8378770664093454836;  // inference.cpp:15
+
+// Gaussian expected log-likelihood, full observation (inference.cpp:52-63):
+// per matrix sum_i -1/2 (log tau2 + log 2 pi) - ((y_i - m_i)^2 + v_i) / (2 tau2)
+// with v_i = S(i, i); d_mean_i = r_i / tau2 goes to dm, the tau2 partial to part2.
+__global__ void k_gauss_part(Vec<double> y, Vec<double> m, Band<double> S, double t2, ix batch, double* part,
+                             double* part2, Vec<double> dm) {
+  const ix nch = chunks(y.n);
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (t >= batch * nch) return;
+  const ix mb = t % batch, c = t / batch;
+  const ix j1 = (c + 1) * kChunk < y.n ? (c + 1) * kChunk : y.n;
+  const double lt = -0.5 * (log(t2) + kLog2Pi);
+  double v = 0.0, dt = 0.0;
+  for (ix i = c * kChunk; i < j1; ++i) {
+    const double r = y(mb, i) - m(mb, i), var = S.cell(mb, 0, i);
+    v += lt - (r * r + var) / (2.0 * t2);
+    dt += (r * r + var) / (2.0 * t2 * t2) - 0.5 / t2;
+    dm(mb, i) = r / t2;
+  }
+  part[mb * nch + c] = v;
+  part2[mb * nch + c] = dt;
+}
+
+// out = a - out (the ELBO's m-bar: expected-loglik minus KL parts)
+__global__ void k_rsub(Vec<double> a, Vec<double> out, ix batch) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  ix mb, i;
+  if (a.n == 0 || !split_bj(t, batch, a.n, a.s, mb, i)) return;
+  out(mb, i) = a(mb, i) - out(mb, i);
+}
+
+// S-bar(i, i) += d_var_i (Tape::diag_sym reverse, tape.cpp:304-312)
+__global__ void k_add_diag(Band<double> sb, double v, ix batch) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  ix mb, j;
+  if (sb.n == 0 || !split_bj(t, batch, sb.n, sb.s, mb, j)) return;
+  sb.cell(mb, 0, j) += v;
+}
+
+__global__ void k_scale_logdet_bar(Band<double> lb, Band<double> l, double c, ix batch) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  ix mb, j;
+  if (l.n == 0 || !split_bj(t, batch, l.n, l.s, mb, j)) return;
+  lb.cell(mb, 0, j) += c / l.cell(mb, 0, j);
+}
+
+__global__ void k_elbo_final(const double* ve, const double* kl, ix batch, double* elbo) {
+  const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (b < batch) elbo[b] = ve[b] - kl[b];
+}
+
+struct GaussTerm {
+  bgm_vec y;
+  double tau2;
+  double* elbo;
+  double* tau2_bar;  // may be null
+};
+
+// KL(q || p) (inference.cpp:247-268) and, with `g`, the Gaussian ELBO
+// (inference.cpp:276-287): expected log-likelihood minus KL.  Gradients in
+// (m_q, L_q) of the objective computed (KL, or the ELBO).
+int vi_core(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p, double* kl, bgm_vec m_q_bar, bgm_band l_q_bar,
+            int32_t* status, int64_t* row, bgm_stream stream, const GaussTerm* g) {
   if (!ok_band(l_q) || !ok_band(l_p) || !ok_band(l_q_bar) || !ok_vec(m_q) || !ok_vec(m_p) || !ok_vec(m_q_bar))
     return BGM_ERR_ARG;
+  if (g && (!ok_vec(g->y) || !(g->tau2 > 0.0))) return BGM_ERR_ARG;  // NonPositiveParam("tau2")
   const ix B = l_q.batch, n = l_q.n;
-  if (B > 0 && !kl) return BGM_ERR_ARG;
+  if (B > 0 && (!kl || (g && !g->elbo))) return BGM_ERR_ARG;
   const bool same = l_p.batch == B && m_q.batch == B && m_p.batch == B && m_q_bar.batch == B && l_q_bar.batch == B &&
-                    l_p.n == n && m_q.n == n && m_p.n == n && m_q_bar.n == n && l_q_bar.n == n;
+                    l_p.n == n && m_q.n == n && m_p.n == n && m_q_bar.n == n && l_q_bar.n == n &&
+                    (!g || (g->y.batch == B && g->y.n == n));
   const int tile = l_q.tile;
   const bool tiles = l_p.tile == tile && m_q.tile == tile && m_p.tile == tile && m_q_bar.tile == tile &&
-                     l_q_bar.tile == tile;
+                     l_q_bar.tile == tile && (!g || g->y.tile == tile);
   if (!same || !tiles || l_q.upper != 0 || l_p.upper != 0 || l_q_bar.lower != l_q.lower || l_q_bar.upper != 0 ||
       l_q.lower < l_p.lower)  // inference.cpp:252-253
     return BGM_ERR_DIM;
   if (B == 0 || n == 0) return BGM_OK;
   auto s = static_cast<cudaStream_t>(stream);
-  timing::Scope t("kl_divergence_grad", s);
+  timing::Scope t(g ? "elbo_grad" : "kl_divergence_grad", s);
   const ix nch = chunks(n);
   bgm_band S = l_q, Sb = l_q, Qp = l_p;
-  bgm_vec d = m_q, wv = m_q;
+  bgm_vec d = m_q, wv = m_q, dm = m_q;
   const size_t scal = sizeof(double) * size_t(B);
-  const size_t total = 2 * band_bytes(l_q) + band_bytes(l_p) + 2 * vec_bytes(m_q) + 5 * scal +
-                       sizeof(double) * size_t(B * nch) + 4 * (sizeof(int32_t) + sizeof(int64_t)) * size_t(B) +
-                       16 * 256;
+  const size_t total = 2 * band_bytes(l_q) + band_bytes(l_p) + 3 * vec_bytes(m_q) + 7 * scal +
+                       2 * sizeof(double) * size_t(B * nch) + 4 * (sizeof(int32_t) + sizeof(int64_t)) * size_t(B) +
+                       24 * 256;
   Arena ar;
   ar.s = s;
   if (scratch_alloc(reinterpret_cast<void**>(&ar.base), total, s) != cudaSuccess) return BGM_ERR_CUDA;
@@ -219,12 +281,15 @@ int bgm_kl_divergence_grad(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p,
   Qp.data = ar.take(band_bytes(l_p));
   d.data = ar.take(vec_bytes(m_q));
   wv.data = ar.take(vec_bytes(m_q));
+  dm.data = ar.take(vec_bytes(m_q));
   double* tr = static_cast<double*>(ar.take(scal));
   double* ldq = static_cast<double*>(ar.take(scal));
   double* ldp = static_cast<double*>(ar.take(scal));
   double* quad = static_cast<double*>(ar.take(scal));
-  double* half = static_cast<double*>(ar.take(scal));
+  double* cb = static_cast<double*>(ar.take(scal));
+  double* ve = static_cast<double*>(ar.take(scal));
   double* part = static_cast<double*>(ar.take(sizeof(double) * size_t(B * nch)));
+  double* part2 = static_cast<double*>(ar.take(sizeof(double) * size_t(B * nch)));
   int32_t* st[4];
   int64_t* rw[4];
   for (int q = 0; q < 4; ++q) {
@@ -245,20 +310,51 @@ int bgm_kl_divergence_grad(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p,
   k_dot_part<<<blocks_for(B * nch, kThreads), kThreads, 0, s>>>(view<double>(wv), B, part);
   k_sum_parts<<<blocks_for(B, kThreads), kThreads, 0, s>>>(part, nch, B, quad);
   k_kl_final<<<blocks_for(B, kThreads), kThreads, 0, s>>>(tr, ldq, ldp, quad, n, B, kl);
-  // reverse: m_q-bar = -L_p white = L_p white'
+  // reverse of KL: m_q-bar = -L_p white = L_p white'; S-bar = 1/2 seed(Q_p)
+  // (trace node, tape.cpp:285-301); L-bar += diag(1 / L_q(j,j)) (log|L_q|).
+  // The ELBO negates the KL parts and adds the expected log-likelihood's
+  // d_mean (to m-bar) and d_var (to S-bar's diagonal, diag_sym).
+  const double sgn = g ? -1.0 : 1.0;
   if ((rc = bgm_product_band_vec(l_p, wv, 0, m_q_bar, stream))) return rc;
-  // S-bar = 1/2 seed(Q_p) on band(S) (the trace node's c_bar = 1/2, tape.cpp:285-301)
-  k_fill<<<blocks_for(B, kThreads), kThreads, 0, s>>>(half, B, 0.5);
+  k_fill<<<blocks_for(B, kThreads), kThreads, 0, s>>>(cb, B, 0.5 * sgn);
   bgm_band none = Sb;
   none.data = nullptr;
-  if ((rc = bgm_vjp_trace_product_sym(S, Qp, half, Sb, none, stream))) return rc;
-  // L_q-bar = vjp_sparse_inverse_subset(L_q, S, S-bar) + diag(1 / L_q(j,j))
-  if ((rc = bgm_vjp_sparse_inverse_subset(l_q, S, Sb, l_q_bar, st[3], rw[3], stream))) return rc;
+  if ((rc = bgm_vjp_trace_product_sym(S, Qp, cb, Sb, none, stream))) return rc;
   const ix bwork = (B + tile - 1) / tile * tile * n;
-  k_add_logdet_bar<<<blocks_for(bwork, kThreads), kThreads, 0, s>>>(view<double>(l_q_bar), view<double>(l_q), B);
+  if (g) {
+    k_gauss_part<<<blocks_for(B * nch, kThreads), kThreads, 0, s>>>(view<double>(g->y), view<double>(m_q),
+                                                                     view<double>(S), g->tau2, B, part, part2,
+                                                                     view<double>(dm));
+    k_sum_parts<<<blocks_for(B, kThreads), kThreads, 0, s>>>(part, nch, B, ve);
+    if (g->tau2_bar) k_sum_parts<<<blocks_for(B, kThreads), kThreads, 0, s>>>(part2, nch, B, g->tau2_bar);
+    k_elbo_final<<<blocks_for(B, kThreads), kThreads, 0, s>>>(ve, kl, B, g->elbo);
+    k_rsub<<<blocks_for(vwork, kThreads), kThreads, 0, s>>>(view<double>(dm), view<double>(m_q_bar), B);
+    k_add_diag<<<blocks_for(bwork, kThreads), kThreads, 0, s>>>(view<double>(Sb), -0.5 / g->tau2, B);
+  }
+  if ((rc = bgm_vjp_sparse_inverse_subset(l_q, S, Sb, l_q_bar, st[3], rw[3], stream))) return rc;
+  k_scale_logdet_bar<<<blocks_for(bwork, kThreads), kThreads, 0, s>>>(view<double>(l_q_bar), view<double>(l_q), sgn,
+                                                                       B);
   k_status3<<<blocks_for(B, kThreads), kThreads, 0, s>>>(st[0], rw[0], st[1], rw[1], st[2], rw[2], B, status, row);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? BGM_OK : set_error(e);
+}
+
+}  // namespace
+}  // namespace vi
+}  // namespace bgm
+
+extern "C" {
+
+int bgm_kl_divergence_grad(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p, double* kl, bgm_vec m_q_bar,
+                           bgm_band l_q_bar, int32_t* status, int64_t* row, bgm_stream stream) {
+  return vi::vi_core(m_q, l_q, m_p, l_p, kl, m_q_bar, l_q_bar, status, row, stream, nullptr);
+}
+
+int bgm_elbo_gaussian_grad(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p, bgm_vec y, double tau2,
+                           double* elbo, double* kl, bgm_vec m_q_bar, bgm_band l_q_bar, double* tau2_bar,
+                           int32_t* status, int64_t* row, bgm_stream stream) {
+  const vi::GaussTerm g{y, tau2, elbo, tau2_bar};
+  return vi::vi_core(m_q, l_q, m_p, l_p, kl, m_q_bar, l_q_bar, status, row, stream, &g);
 }
 
 }  // extern "C"

@@ -103,3 +103,24 @@ def test_kl_autograd(cuda):
 
     assert torch.autograd.gradcheck(f, (Mq.data.clone().requires_grad_(True), Lq.data.clone().requires_grad_(True)),
                                     eps=1e-6, atol=1e-7, rtol=1e-6)
+
+
+@pytest.mark.parametrize("tile", [1, 32])
+@pytest.mark.parametrize("kq,kp", [(4, 2), (16, 8)])
+def test_elbo_gaussian_vs_reference_tape(cuda, ref, tile, kq, kp):
+    import paper_1902_10078_b200 as bgm
+    rng = np.random.default_rng(7 * kq + kp + tile)
+    B, n, tau2 = 37, 401, 0.3
+    mq, lq, mp, lp = _kl_inputs(rng, B, n, kq, kp)
+    y = rng.normal(0, 1, (B, n))
+    V = lambda a: bgm.Vecs.from_reference(a, tile=tile)  # noqa: E731
+    el, kl, mb, lb, tb = bgm.elbo_gaussian_grad(V(mq), bgm.Bands.from_reference(lq, kq, 0, tile=tile), V(mp),
+                                                bgm.Bands.from_reference(lp, kp, 0, tile=tile), V(y), tau2)
+    rel, rmb, rlb, rtb, st, _ = ref.elbo_gaussian_grad(mq, lq, mp, lp, y, tau2)
+    assert np.all(st == 0)
+    rkl = ref.kl_divergence_grad(mq, lq, mp, lp)[0]
+    assert cm.max_rel_err(el.cpu().numpy(), rel) <= TOL
+    assert cm.max_rel_err(kl.cpu().numpy(), rkl) <= TOL
+    assert cm.max_rel_err(mb.numpy(), rmb) <= TOL
+    assert cm.max_rel_err(lb.numpy(), rlb) <= TOL
+    assert cm.max_rel_err(tb.cpu().numpy(), rtb) <= TOL
