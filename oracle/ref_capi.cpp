@@ -12,6 +12,7 @@
 // Exceptions (errors.hpp:27-50) become per-matrix status codes + rows.
 #include <cstdint>
 #include <cstring>
+#include <sstream>
 #include <functional>
 #include <random>
 #include <string>
@@ -424,6 +425,18 @@ int ref_elbo_gaussian_grad(ix batch, ix n, ix bq, ix bp, const double* mq, const
         &row[b]);
   });
   return 0;
+}
+
+// write_band_text (banded.cpp:192-202), verbatim, into a caller buffer: the
+// byte-level pin of the Python band text writer.  Returns the length, or -1
+// when the buffer is too small.
+long long ref_write_band_text(ix n, ix lo, ix up, const double* a, char* buf, long long cap) {
+  std::ostringstream os;
+  write_band_text(os, load(n, lo, up, a));
+  const std::string s = os.str();
+  if (static_cast<long long>(s.size()) + 1 > cap) return -1;
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+  return static_cast<long long>(s.size());
 }
 
 // Reference gradient suite (gradcheck.cpp:288-304), used to pin the oracle
