@@ -213,6 +213,20 @@ int bgm_elbo_gaussian_grad(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p,
                            double* elbo, double* kl, bgm_vec m_q_bar, bgm_band l_q_bar, double* tau2_bar,
                            int32_t* status, int64_t* row, bgm_stream stream);
 
+/* infer::elbo (inference.cpp:276-287) for a Poisson likelihood with
+ * per-observation exposure weights observing every latent: the expected
+ * log-likelihood by quad_points-node Gauss-Hermite quadrature
+ * (inference.cpp:65-100, 120-137) minus KL(q || p), with the ELBO's gradient
+ * in m_q and L_q.  A non-positive weight reports BGM_ERR_ARG at that
+ * observation (the reference's NonPositiveParam).  quad_points in [1, 64].  fp64. */
+int bgm_elbo_poisson_grad(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p, bgm_vec y, bgm_vec weight,
+                          int quad_points, double* elbo, double* kl, bgm_vec m_q_bar, bgm_band l_q_bar,
+                          int32_t* status, int64_t* row, bgm_stream stream);
+
+/* infer::gauss_hermite (inference.cpp:120-137): quad_points ascending nodes x
+ * and weights w (host arrays), by the Golub-Welsch eigen-decomposition. */
+int bgm_gauss_hermite(int quad_points, double* x, double* w);
+
 /* ------------------------------------------------- instrumentation */
 /* Per-kernel CUDA-event timing on the launching stream (off by default).
  * bgm_timing_enable(1) clears and starts recording; bgm_timing_read(i, ...)

@@ -274,6 +274,23 @@ class Oracle:
                                        st.ctypes.data_as(_i32p), row.ctypes.data_as(_i64p))
         return el, mb, lb, tb, st, row
 
+    def elbo_poisson_grad(self, mq, lq, mp, lp, y, weight, quad_points=20):
+        """infer::elbo (inference.cpp:276-287), PoissonLik, full observation,
+        Gauss-Hermite nodes from numpy's hermgauss; reference tape only."""
+        if self.which != "reference":
+            raise RuntimeError("elbo lives in the compiled reference tape only")
+        gx, gw = np.polynomial.hermite.hermgauss(quad_points)
+        mq, lq, mp, lp, y, weight = (_f64(a) for a in (mq, lq, mp, lp, y, weight))
+        B, n, wq = lq.shape
+        wp = lp.shape[2]
+        el, mb, lb = np.zeros(B), np.zeros((B, n)), np.zeros_like(lq)
+        st, row = self._status(B)
+        self._fn("elbo_poisson_grad")(_i64(B), _i64(n), _i64(wq - 1), _i64(wp - 1), _ptr(mq), _ptr(lq), _ptr(mp),
+                                      _ptr(lp), _ptr(y), _ptr(weight), _i64(quad_points), _ptr(_f64(gx)),
+                                      _ptr(_f64(gw)), _ptr(el), _ptr(mb), _ptr(lb), st.ctypes.data_as(_i32p),
+                                      row.ctypes.data_as(_i64p))
+        return el, mb, lb, st, row
+
     # ---------------------------------------------------------- reference only
     def run_grad_suite(self, seed: int, instances: int):
         if self.which != "reference":

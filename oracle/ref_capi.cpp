@@ -10,7 +10,9 @@
 // matrix is the reference's own storage block (BandedMatrix::storage(),
 // banded.hpp:77-79): column-major (lower+upper+1) x n, batch-major.
 // Exceptions (errors.hpp:27-50) become per-matrix status codes + rows.
+#include <cmath>
 #include <cstdint>
+#include <stdexcept>
 #include <cstring>
 #include <sstream>
 #include <functional>
@@ -418,6 +420,80 @@ int ref_elbo_gaussian_grad(ix batch, ix n, ix bq, ix bp, const double* mq, const
           const tape::NodeRef obj = t.sub(ve, t.mul(t.constant(0.5), inner));
           elbo[b] = t.scalar(obj);
           tau2_bar[b] = d_tau2;
+          auto grads = t.backward(obj);
+          store_vec(std::get<Eigen::VectorXd>(grads.at("m")), mq_bar + b * n);
+          store(std::get<BandedMatrix>(grads.at("l")), lq_bar + b * n * (bq + 1));
+        },
+        &row[b]);
+  });
+  return 0;
+}
+
+// infer::elbo (inference.cpp:276-287) for a PoissonLik observing every
+// latent: the Poisson branch of expected_loglik (inference.cpp:65-100,
+// restated) with the Gauss-Hermite rule passed in by the caller (the tests
+// use numpy's hermgauss, independent of the library's own Golub-Welsch),
+// joined to the compiled reference Tape as in ref_elbo_gaussian_grad.
+int ref_elbo_poisson_grad(ix batch, ix n, ix bq, ix bp, const double* mq, const double* lq,
+                          const double* mp, const double* lp, const double* y, const double* wt,
+                          ix nq, const double* ghx, const double* ghw, double* elbo, double* mq_bar,
+                          double* lq_bar, std::int32_t* status, ix* row) {
+  over_batch(batch, [&](ix b) {
+    status[b] = guarded(
+        [&] {
+          const BandedMatrix l_q = load(n, bq, 0, lq + b * n * (bq + 1));
+          const BandedMatrix l_p = load(n, bp, 0, lp + b * n * (bp + 1));
+          const Eigen::VectorXd m_q = load_vec(n, mq + b * n);
+          const Eigen::VectorXd m_p = load_vec(n, mp + b * n);
+          const Eigen::VectorXd yv = load_vec(n, y + b * n);
+          const Eigen::VectorXd wv = load_vec(n, wt + b * n);
+          const SymmetricBandedMatrix qp = SymmetricBandedMatrix::from_lower(
+              ops::product_band_band_restricted(l_p, transpose(l_p), bp, 0));
+          tape::Tape t;
+          const tape::NodeRef mn = t.leaf("m", m_q);
+          const tape::NodeRef ln = t.leaf("l", l_q);
+          const tape::NodeRef marg_var = t.diag_sym(t.sparse_inverse_subset(ln));
+          const Eigen::VectorXd& mean = t.vector(mn);
+          const Eigen::VectorXd& var = t.vector(marg_var);
+          const double norm = 1.0 / std::sqrt(M_PI);
+          double value = 0.0;
+          Eigen::VectorXd d_mean = Eigen::VectorXd::Zero(n), d_var = Eigen::VectorXd::Zero(n);
+          for (ix i = 0; i < n; ++i) {
+            const double w = wv(i);
+            if (w <= 0.0) throw std::invalid_argument("weight");
+            const double m = mean(i), v = var(i);
+            const double base = yv(i) * std::log(w) - std::lgamma(yv(i) + 1.0);
+            if (v <= 0.0) {
+              value += yv(i) * m + base - w * std::exp(m);
+              d_mean(i) = yv(i) - w * std::exp(m);
+              continue;
+            }
+            const double spread = std::sqrt(2.0 * v);
+            double ev = 0.0, dm = 0.0, dv = 0.0;
+            for (ix k = 0; k < nq; ++k) {
+              const double f = m + spread * ghx[k];
+              const double rate = w * std::exp(f);
+              ev += ghw[k] * (yv(i) * f - rate);
+              const double gprime = yv(i) - rate;
+              dm += ghw[k] * gprime;
+              dv += ghw[k] * gprime * ghx[k] / spread;
+            }
+            value += norm * ev + base;
+            d_mean(i) = norm * dm;
+            d_var(i) = norm * dv;
+          }
+          const tape::NodeRef ve = t.linearized_scalar(value, {{mn, d_mean}, {marg_var, d_var}});
+          const double logdet_p = ops::log_det_from_cholesky(l_p);
+          const tape::NodeRef trace = t.trace_product_sym(t.sparse_inverse_subset(ln), t.constant(qp));
+          const tape::NodeRef logdets =
+              t.mul(t.constant(2.0), t.sub(t.log_det_from_cholesky(ln), t.constant(logdet_p)));
+          const tape::NodeRef diff = t.sub_vec(t.constant(m_p), mn);
+          const tape::NodeRef white = t.product_band_vec(t.constant(l_p), diff, true);
+          tape::NodeRef inner = t.add(trace, logdets);
+          inner = t.add(inner, t.dot(white, white));
+          inner = t.add(inner, t.constant(-static_cast<double>(n)));
+          const tape::NodeRef obj = t.sub(ve, t.mul(t.constant(0.5), inner));
+          elbo[b] = t.scalar(obj);
           auto grads = t.backward(obj);
           store_vec(std::get<Eigen::VectorXd>(grads.at("m")), mq_bar + b * n);
           store(std::get<BandedMatrix>(grads.at("l")), lq_bar + b * n * (bq + 1));

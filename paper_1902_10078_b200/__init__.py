@@ -23,6 +23,8 @@ from .api import (  # noqa: F401
     cholesky,
     library,
     elbo_gaussian_grad,
+    elbo_poisson_grad,
+    gauss_hermite,
     kl_divergence_grad,
     library_path,
     log_det_from_cholesky,

@@ -576,6 +576,46 @@ def elbo_gaussian_grad(m_q: Vecs, l_q: Bands, m_p: Vecs, l_p: Bands, y: Vecs, ta
     return elbo, kl, m_bar, l_bar, tb
 
 
+def elbo_poisson_grad(m_q: Vecs, l_q: Bands, m_p: Vecs, l_p: Bands, y: Vecs, weight: Vecs, quad_points: int = 20,
+                      check: bool = True):
+    """infer::elbo (inference.cpp:276-287) for a Poisson likelihood with
+    exposure weights observing every latent; the expectation by
+    ``quad_points``-node Gauss-Hermite quadrature (inference.cpp:65-100).
+    Returns (elbo[B], kl[B], m_q_bar, l_q_bar).  A non-positive weight raises
+    (the reference's NonPositiveParam) with its observation index."""
+    if l_q.lower < l_p.lower:
+        raise DimensionMismatch("kl: variational band must cover the prior band")
+    if not 1 <= quad_points <= 64:
+        raise BandgmError("parameter 'quad_points' must be in [1, 64]")
+    for x in (m_q, l_p, y, weight):
+        _same(l_q, x)
+    dev = l_q.data.device
+    elbo, kl = (torch.empty(l_q.batch, dtype=torch.float64, device=dev) for _ in range(2))
+    m_bar, l_bar = m_q.like(), l_q.like()
+    st = _Status(l_q.batch, dev)
+    _call("bgm_elbo_poisson_grad", m_q.desc(), l_q.desc(), m_p.desc(), l_p.desc(), y.desc(), weight.desc(),
+          C.c_int(quad_points), C.c_void_p(elbo.data_ptr()), C.c_void_p(kl.data_ptr()), m_bar.desc(), l_bar.desc(),
+          *st.ptrs(), _stream())
+    if check:
+        stn = st.st.cpu().numpy()
+        bad = np.nonzero(stn == BGM_ERR_ARG)[0]
+        if bad.size:
+            b = int(bad[0])
+            raise BandgmError(f"parameter 'weight' must be strictly positive (observation {int(st.row[b])}, "
+                              f"batch matrix {b})")
+    _check(st, check)
+    return elbo, kl, m_bar, l_bar
+
+
+def gauss_hermite(quad_points: int):
+    """infer::gauss_hermite (inference.cpp:120-137): (nodes, weights), ascending."""
+    x = (C.c_double * quad_points)()
+    w = (C.c_double * quad_points)()
+    if library().bgm_gauss_hermite(C.c_int(quad_points), x, w) != BGM_OK:
+        raise BandgmError("parameter 'quad_points' must be in [1, 64]")
+    return np.array(x[:]), np.array(w[:])
+
+
 # --------------------------------------------------------------------- config 3
 def marginal_likelihood_grad(L: Bands, y: Vecs, tau2: float, check: bool = True, out=None):
     """Config-3 learning step: per matrix, the log marginal

@@ -237,29 +237,184 @@ __global__ void k_elbo_final(const double* ve, const double* kl, ix batch, doubl
   if (b < batch) elbo[b] = ve[b] - kl[b];
 }
 
-struct GaussTerm {
-  bgm_vec y;
-  double tau2;
-  double* elbo;
-  double* tau2_bar;  // may be null
+constexpr int kMaxQuad = 64;
+struct GH {  // Gauss-Hermite rule, ascending nodes (inference.cpp:120-137)
+  int k;
+  double x[kMaxQuad], w[kMaxQuad];
 };
+
+struct LikTerm {
+  int kind;  // 0 Gaussian (tau2), 1 Poisson (weight, Gauss-Hermite)
+  bgm_vec y, weight;
+  double tau2;
+  GH gh;
+  double* elbo;
+  double* tau2_bar;  // Gaussian only; may be null
+};
+
+// Poisson expected log-likelihood, full observation (inference.cpp:65-100):
+// per observation the Gauss-Hermite expectation of y f - w e^f plus
+// y log w - lgamma(y + 1), its mean / variance partials to dm / dv; the first
+// non-positive weight per matrix is recorded in bad (NonPositiveParam).
+__global__ void k_poisson_part(Vec<double> y, Vec<double> wt, Vec<double> m, Band<double> S, const GH gh, ix batch,
+                               double* part, Vec<double> dm, Vec<double> dv, unsigned long long* bad) {
+  const ix nch = chunks(y.n);
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (t >= batch * nch) return;
+  const ix mb = t % batch, c = t / batch;
+  const ix j1 = (c + 1) * kChunk < y.n ? (c + 1) * kChunk : y.n;
+  const double norm = 1.0 / sqrt(3.14159265358979323846);
+  double val = 0.0;
+  for (ix i = c * kChunk; i < j1; ++i) {
+    const double w = wt(mb, i), yi = y(mb, i), mi = m(mb, i), v = S.cell(mb, 0, i);
+    if (!(w > 0.0)) {
+      atomicMin(bad + mb, static_cast<unsigned long long>(i));
+      dm(mb, i) = 0.0;
+      dv(mb, i) = 0.0;
+      continue;
+    }
+    const double base = yi * log(w) - lgamma(yi + 1.0);
+    if (v <= 0.0) {
+      val += yi * mi + base - w * exp(mi);
+      dm(mb, i) = yi - w * exp(mi);
+      dv(mb, i) = 0.0;
+      continue;
+    }
+    const double spread = sqrt(2.0 * v);
+    double ev = 0.0, sm = 0.0, sv = 0.0;
+    for (int q = 0; q < gh.k; ++q) {
+      const double f = mi + spread * gh.x[q];
+      const double rate = w * exp(f);
+      ev += gh.w[q] * (yi * f - rate);
+      const double gp = yi - rate;
+      sm += gh.w[q] * gp;
+      sv += gh.w[q] * gp * gh.x[q] / spread;
+    }
+    val += norm * ev + base;
+    dm(mb, i) = norm * sm;
+    dv(mb, i) = norm * sv;
+  }
+  part[mb * nch + c] = val;
+}
+
+// S-bar(i, i) += dv_i (Tape::diag_sym reverse with a per-entry adjoint)
+__global__ void k_add_diag_vec(Band<double> sb, Vec<double> dv, ix batch) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  ix mb, j;
+  if (sb.n == 0 || !split_bj(t, batch, sb.n, sb.s, mb, j)) return;
+  sb.cell(mb, 0, j) += dv(mb, j);
+}
+
+__global__ void k_bad_init(unsigned long long* bad, ix batch, ix n) {
+  const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (b < batch) bad[b] = static_cast<unsigned long long>(n);
+}
+
+// ELBO error order (inference.cpp:278-286): subset of L_q, likelihood
+// parameters (Poisson weights), then the KL's log|L_p| and log|L_q|
+__global__ void k_status_elbo(const int32_t* s_sub, const int64_t* r_sub, const unsigned long long* bad, ix n,
+                              const int32_t* s_p, const int64_t* r_p, const int32_t* s_q, const int64_t* r_q,
+                              ix batch, int32_t* st, int64_t* row) {
+  const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  if (b >= batch) return;
+  if (s_sub[b] != BGM_OK) return report(st, row, b, s_sub[b], r_sub[b]);
+  if (bad && bad[b] < static_cast<unsigned long long>(n)) return report(st, row, b, BGM_ERR_ARG, ix(bad[b]));
+  if (s_p[b] != BGM_OK) return report(st, row, b, s_p[b], r_p[b]);
+  report(st, row, b, s_q[b], r_q[b]);
+}
+
+// Golub-Welsch: nodes = eigenvalues of the Jacobi matrix (off-diagonal
+// sqrt(k/2)), weights = sqrt(pi) v_0^2, by implicit-shift QL iterations on
+// the symmetric tridiagonal matrix carrying the first eigenvector components.
+bool gauss_hermite(int k, GH& gh) {
+  if (k < 1 || k > kMaxQuad) return false;
+  gh.k = k;
+  if (k == 1) {
+    gh.x[0] = 0.0;
+    gh.w[0] = sqrt(3.14159265358979323846);
+    return true;
+  }
+  double d[kMaxQuad], e[kMaxQuad], z[kMaxQuad];  // diagonal, sub-diagonal, first row of the eigenvectors
+  for (int i = 0; i < k; ++i) {
+    d[i] = 0.0;
+    e[i] = i + 1 < k ? sqrt(0.5 * (i + 1)) : 0.0;
+    z[i] = i == 0 ? 1.0 : 0.0;
+  }
+  for (int l = 0; l < k; ++l) {
+    for (int iter = 0; iter < 200; ++iter) {
+      int m = l;
+      for (; m + 1 < k; ++m) {
+        const double dd = fabs(d[m]) + fabs(d[m + 1]);
+        if (fabs(e[m]) <= 1e-300 + 2.2e-16 * dd) break;
+      }
+      if (m == l) break;
+      double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+      double r = hypot(g, 1.0);
+      g = d[m] - d[l] + e[l] / (g + (g >= 0 ? r : -r));
+      double sn = 1.0, cs = 1.0, p = 0.0;
+      int i = m - 1;
+      for (; i >= l; --i) {
+        double f = sn * e[i], b = cs * e[i];
+        r = hypot(f, g);
+        e[i + 1] = r;
+        if (r == 0.0) {
+          d[i + 1] -= p;
+          e[m] = 0.0;
+          break;
+        }
+        sn = f / r;
+        cs = g / r;
+        g = d[i + 1] - p;
+        r = (d[i] - g) * sn + 2.0 * cs * b;
+        p = sn * r;
+        d[i + 1] = g + p;
+        g = cs * r - b;
+        f = z[i + 1];
+        z[i + 1] = sn * z[i] + cs * f;
+        z[i] = cs * z[i] - sn * f;
+      }
+      if (r == 0.0 && i >= l) continue;
+      d[l] -= p;
+      e[l] = g;
+      e[m] = 0.0;
+    }
+  }
+  // ascending nodes, as Eigen's SelfAdjointEigenSolver returns them
+  int idx[kMaxQuad];
+  for (int i = 0; i < k; ++i) idx[i] = i;
+  for (int i = 1; i < k; ++i)
+    for (int j = i; j > 0 && d[idx[j]] < d[idx[j - 1]]; --j) {
+      const int t = idx[j];
+      idx[j] = idx[j - 1];
+      idx[j - 1] = t;
+    }
+  for (int i = 0; i < k; ++i) {
+    gh.x[i] = d[idx[i]];
+    gh.w[i] = sqrt(3.14159265358979323846) * z[idx[i]] * z[idx[i]];
+  }
+  return true;
+}
 
 // KL(q || p) (inference.cpp:247-268) and, with `g`, the Gaussian ELBO
 // (inference.cpp:276-287): expected log-likelihood minus KL.  Gradients in
 // (m_q, L_q) of the objective computed (KL, or the ELBO).
 int vi_core(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p, double* kl, bgm_vec m_q_bar, bgm_band l_q_bar,
-            int32_t* status, int64_t* row, bgm_stream stream, const GaussTerm* g) {
+            int32_t* status, int64_t* row, bgm_stream stream, const LikTerm* g) {
   if (!ok_band(l_q) || !ok_band(l_p) || !ok_band(l_q_bar) || !ok_vec(m_q) || !ok_vec(m_p) || !ok_vec(m_q_bar))
     return BGM_ERR_ARG;
-  if (g && (!ok_vec(g->y) || !(g->tau2 > 0.0))) return BGM_ERR_ARG;  // NonPositiveParam("tau2")
+  if (g && !ok_vec(g->y)) return BGM_ERR_ARG;
+  if (g && g->kind == 0 && !(g->tau2 > 0.0)) return BGM_ERR_ARG;  // NonPositiveParam("tau2")
+  if (g && g->kind == 1 && !ok_vec(g->weight)) return BGM_ERR_ARG;
   const ix B = l_q.batch, n = l_q.n;
   if (B > 0 && (!kl || (g && !g->elbo))) return BGM_ERR_ARG;
   const bool same = l_p.batch == B && m_q.batch == B && m_p.batch == B && m_q_bar.batch == B && l_q_bar.batch == B &&
                     l_p.n == n && m_q.n == n && m_p.n == n && m_q_bar.n == n && l_q_bar.n == n &&
-                    (!g || (g->y.batch == B && g->y.n == n));
+                    (!g || (g->y.batch == B && g->y.n == n)) &&
+                    (!g || g->kind != 1 || (g->weight.batch == B && g->weight.n == n));
   const int tile = l_q.tile;
   const bool tiles = l_p.tile == tile && m_q.tile == tile && m_p.tile == tile && m_q_bar.tile == tile &&
-                     l_q_bar.tile == tile && (!g || g->y.tile == tile);
+                     l_q_bar.tile == tile && (!g || g->y.tile == tile) &&
+                     (!g || g->kind != 1 || g->weight.tile == tile);
   if (!same || !tiles || l_q.upper != 0 || l_p.upper != 0 || l_q_bar.lower != l_q.lower || l_q_bar.upper != 0 ||
       l_q.lower < l_p.lower)  // inference.cpp:252-253
     return BGM_ERR_DIM;
@@ -268,9 +423,9 @@ int vi_core(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p, double* kl, bg
   timing::Scope t(g ? "elbo_grad" : "kl_divergence_grad", s);
   const ix nch = chunks(n);
   bgm_band S = l_q, Sb = l_q, Qp = l_p;
-  bgm_vec d = m_q, wv = m_q, dm = m_q;
+  bgm_vec d = m_q, wv = m_q, dm = m_q, dvv = m_q;
   const size_t scal = sizeof(double) * size_t(B);
-  const size_t total = 2 * band_bytes(l_q) + band_bytes(l_p) + 3 * vec_bytes(m_q) + 7 * scal +
+  const size_t total = 2 * band_bytes(l_q) + band_bytes(l_p) + 4 * vec_bytes(m_q) + 8 * scal +
                        2 * sizeof(double) * size_t(B * nch) + 4 * (sizeof(int32_t) + sizeof(int64_t)) * size_t(B) +
                        24 * 256;
   Arena ar;
@@ -282,6 +437,8 @@ int vi_core(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p, double* kl, bg
   d.data = ar.take(vec_bytes(m_q));
   wv.data = ar.take(vec_bytes(m_q));
   dm.data = ar.take(vec_bytes(m_q));
+  dvv.data = ar.take(vec_bytes(m_q));
+  unsigned long long* bad = static_cast<unsigned long long*>(ar.take(scal));
   double* tr = static_cast<double*>(ar.take(scal));
   double* ldq = static_cast<double*>(ar.take(scal));
   double* ldp = static_cast<double*>(ar.take(scal));
@@ -322,19 +479,31 @@ int vi_core(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p, double* kl, bg
   if ((rc = bgm_vjp_trace_product_sym(S, Qp, cb, Sb, none, stream))) return rc;
   const ix bwork = (B + tile - 1) / tile * tile * n;
   if (g) {
-    k_gauss_part<<<blocks_for(B * nch, kThreads), kThreads, 0, s>>>(view<double>(g->y), view<double>(m_q),
-                                                                     view<double>(S), g->tau2, B, part, part2,
-                                                                     view<double>(dm));
+    if (g->kind == 0) {
+      k_gauss_part<<<blocks_for(B * nch, kThreads), kThreads, 0, s>>>(view<double>(g->y), view<double>(m_q),
+                                                                       view<double>(S), g->tau2, B, part, part2,
+                                                                       view<double>(dm));
+      if (g->tau2_bar) k_sum_parts<<<blocks_for(B, kThreads), kThreads, 0, s>>>(part2, nch, B, g->tau2_bar);
+      k_add_diag<<<blocks_for(bwork, kThreads), kThreads, 0, s>>>(view<double>(Sb), -0.5 / g->tau2, B);
+    } else {
+      k_bad_init<<<blocks_for(B, kThreads), kThreads, 0, s>>>(bad, B, n);
+      k_poisson_part<<<blocks_for(B * nch, kThreads), kThreads, 0, s>>>(
+          view<double>(g->y), view<double>(g->weight), view<double>(m_q), view<double>(S), g->gh, B, part,
+          view<double>(dm), view<double>(dvv), bad);
+      k_add_diag_vec<<<blocks_for(bwork, kThreads), kThreads, 0, s>>>(view<double>(Sb), view<double>(dvv), B);
+    }
     k_sum_parts<<<blocks_for(B, kThreads), kThreads, 0, s>>>(part, nch, B, ve);
-    if (g->tau2_bar) k_sum_parts<<<blocks_for(B, kThreads), kThreads, 0, s>>>(part2, nch, B, g->tau2_bar);
     k_elbo_final<<<blocks_for(B, kThreads), kThreads, 0, s>>>(ve, kl, B, g->elbo);
     k_rsub<<<blocks_for(vwork, kThreads), kThreads, 0, s>>>(view<double>(dm), view<double>(m_q_bar), B);
-    k_add_diag<<<blocks_for(bwork, kThreads), kThreads, 0, s>>>(view<double>(Sb), -0.5 / g->tau2, B);
   }
   if ((rc = bgm_vjp_sparse_inverse_subset(l_q, S, Sb, l_q_bar, st[3], rw[3], stream))) return rc;
   k_scale_logdet_bar<<<blocks_for(bwork, kThreads), kThreads, 0, s>>>(view<double>(l_q_bar), view<double>(l_q), sgn,
                                                                        B);
-  k_status3<<<blocks_for(B, kThreads), kThreads, 0, s>>>(st[0], rw[0], st[1], rw[1], st[2], rw[2], B, status, row);
+  if (g)
+    k_status_elbo<<<blocks_for(B, kThreads), kThreads, 0, s>>>(st[1], rw[1], g->kind == 1 ? bad : nullptr, n, st[0],
+                                                                rw[0], st[2], rw[2], B, status, row);
+  else
+    k_status3<<<blocks_for(B, kThreads), kThreads, 0, s>>>(st[0], rw[0], st[1], rw[1], st[2], rw[2], B, status, row);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? BGM_OK : set_error(e);
 }
@@ -353,8 +522,35 @@ int bgm_kl_divergence_grad(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p,
 int bgm_elbo_gaussian_grad(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p, bgm_vec y, double tau2,
                            double* elbo, double* kl, bgm_vec m_q_bar, bgm_band l_q_bar, double* tau2_bar,
                            int32_t* status, int64_t* row, bgm_stream stream) {
-  const vi::GaussTerm g{y, tau2, elbo, tau2_bar};
+  vi::LikTerm g{};
+  g.kind = 0;
+  g.y = y;
+  g.tau2 = tau2;
+  g.elbo = elbo;
+  g.tau2_bar = tau2_bar;
   return vi::vi_core(m_q, l_q, m_p, l_p, kl, m_q_bar, l_q_bar, status, row, stream, &g);
+}
+
+int bgm_elbo_poisson_grad(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p, bgm_vec y, bgm_vec weight,
+                          int quad_points, double* elbo, double* kl, bgm_vec m_q_bar, bgm_band l_q_bar,
+                          int32_t* status, int64_t* row, bgm_stream stream) {
+  vi::LikTerm g{};
+  g.kind = 1;
+  g.y = y;
+  g.weight = weight;
+  if (!vi::gauss_hermite(quad_points, g.gh)) return BGM_ERR_ARG;  // NonPositiveParam("quad_points")
+  g.elbo = elbo;
+  return vi::vi_core(m_q, l_q, m_p, l_p, kl, m_q_bar, l_q_bar, status, row, stream, &g);
+}
+
+int bgm_gauss_hermite(int quad_points, double* x, double* w) {
+  vi::GH gh;
+  if (!x || !w || !vi::gauss_hermite(quad_points, gh)) return BGM_ERR_ARG;
+  for (int i = 0; i < gh.k; ++i) {
+    x[i] = gh.x[i];
+    w[i] = gh.w[i];
+  }
+  return BGM_OK;
 }
 
 }  // extern "C"

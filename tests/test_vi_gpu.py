@@ -124,3 +124,27 @@ def test_elbo_gaussian_vs_reference_tape(cuda, ref, tile, kq, kp):
     assert cm.max_rel_err(mb.numpy(), rmb) <= TOL
     assert cm.max_rel_err(lb.numpy(), rlb) <= TOL
     assert cm.max_rel_err(tb.cpu().numpy(), rtb) <= TOL
+
+
+@pytest.mark.parametrize("tile", [1, 32])
+@pytest.mark.parametrize("quad", [1, 20])
+def test_elbo_poisson_vs_reference_tape(cuda, ref, tile, quad):
+    import paper_1902_10078_b200 as bgm
+    rng = np.random.default_rng(31 + tile + quad)
+    B, n, kq, kp = 37, 257, 4, 2
+    mq, lq, mp, lp = _kl_inputs(rng, B, n, kq, kp)
+    mq *= 0.3
+    y = rng.poisson(1.5, (B, n)).astype(np.float64)
+    wt = rng.uniform(0.5, 2.0, (B, n))
+    V = lambda a: bgm.Vecs.from_reference(a, tile=tile)  # noqa: E731
+    el, kl, mb, lb = bgm.elbo_poisson_grad(V(mq), bgm.Bands.from_reference(lq, kq, 0, tile=tile), V(mp),
+                                           bgm.Bands.from_reference(lp, kp, 0, tile=tile), V(y), V(wt), quad)
+    rel, rmb, rlb, st, _ = ref.elbo_poisson_grad(mq, lq, mp, lp, y, wt, quad)
+    assert np.all(st == 0)
+    assert cm.max_rel_err(el.cpu().numpy(), rel) <= TOL
+    assert cm.max_rel_err(mb.numpy(), rmb) <= TOL
+    assert cm.max_rel_err(lb.numpy(), rlb) <= TOL
+    wt[3, 10] = 0.0
+    with pytest.raises(bgm.BandgmError, match="weight"):
+        bgm.elbo_poisson_grad(V(mq), bgm.Bands.from_reference(lq, kq, 0, tile=tile), V(mp),
+                              bgm.Bands.from_reference(lp, kp, 0, tile=tile), V(y), V(wt), quad)
