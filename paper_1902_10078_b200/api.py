@@ -324,6 +324,29 @@ class _Status:
             raise _ROW_ERRORS.get(code, BandgmError)(row, b)
 
 
+_SCRATCH_STATUS = {}
+
+
+class _ScratchStatus(_Status):
+    """Uninitialized status arrays reused by unchecked calls (nobody reads
+    them), so a check=False call allocates and fills nothing on the device."""
+
+    def __init__(self, st, row):
+        self.st, self.row = st, row
+
+
+def _status_for(batch: int, device, check: bool) -> _Status:
+    if check:
+        return _Status(batch, device)
+    key = (str(device), max(batch, 1))
+    s = _SCRATCH_STATUS.get(key)
+    if s is None:
+        s = _ScratchStatus(torch.empty(max(batch, 1), dtype=torch.int32, device=device),
+                           torch.empty(max(batch, 1), dtype=torch.int64, device=device))
+        _SCRATCH_STATUS[key] = s
+    return s
+
+
 def _check(status: _Status, check: bool):
     if check:
         status.raise_first()
@@ -343,7 +366,7 @@ def cholesky(q: Bands, check: bool = True) -> Bands:
     if q.upper != 0:
         raise DimensionMismatch("cholesky expects a symmetric lower store")
     l = q.like()
-    s = _Status(q.batch, q.data.device)
+    s = _status_for(q.batch, q.data.device, check)
     _call("bgm_cholesky", q.desc(), l.desc(), *s.ptrs(), _stream())
     _check(s, check)
     return l
@@ -355,7 +378,7 @@ def solve_vec(l: Bands, v: Vecs, transpose_l: bool = False, check: bool = True) 
         raise DimensionMismatch("solve_vec: factor must be lower triangular")
     _same(l, v)
     x = Vecs.empty(v.batch, v.n, v.tile, v.dtype, v.data.device)
-    s = _Status(l.batch, l.data.device)
+    s = _status_for(l.batch, l.data.device, check)
     _call("bgm_solve_vec", l.desc(), v.desc(), C.c_int(int(transpose_l)), x.desc(), *s.ptrs(), _stream())
     _check(s, check)
     return x
@@ -369,7 +392,7 @@ def solve_mat(l: Bands, r: Bands, out_lower: int, out_upper: int, transpose_l: b
     _same(l, r)
     n = l.n
     out = Bands.empty(l.batch, n, min(out_lower, n - 1), min(out_upper, n - 1), l.tile, l.dtype, l.data.device)
-    s = _Status(l.batch, l.data.device)
+    s = _status_for(l.batch, l.data.device, check)
     _call("bgm_solve_mat", l.desc(), r.desc(), C.c_int(int(transpose_l)), out.desc(), *s.ptrs(), _stream())
     _check(s, check)
     return out
@@ -380,7 +403,7 @@ def sparse_inverse_subset(l: Bands, check: bool = True) -> Bands:
     if l.upper != 0:
         raise DimensionMismatch("sparse_inverse_subset: factor must be lower triangular")
     out = l.like()
-    s = _Status(l.batch, l.data.device)
+    s = _status_for(l.batch, l.data.device, check)
     _call("bgm_sparse_inverse_subset", l.desc(), out.desc(), *s.ptrs(), _stream())
     _check(s, check)
     return out
@@ -428,7 +451,7 @@ def outer_band(m: Vecs, v: Vecs, lower: int, upper: int) -> Bands:
 def log_det_from_cholesky(l: Bands, check: bool = True) -> torch.Tensor:
     """ops::log_det_from_cholesky (kernels.hpp:72): one value per matrix."""
     out = torch.empty(l.batch, dtype=l.dtype, device=l.data.device)
-    s = _Status(l.batch, l.data.device)
+    s = _status_for(l.batch, l.data.device, check)
     _call("bgm_log_det", l.desc(), C.c_void_p(out.data_ptr()), *s.ptrs(), _stream())
     _check(s, check)
     return out
@@ -450,7 +473,7 @@ def vjp_solve_vec(l: Bands, s: Vecs, s_bar: Vecs, transpose_l: bool, check: bool
     """grad::vjp_solve_vec (grad.hpp:31-32) -> (l_bar, v_bar)."""
     l_bar = l.like()
     v_bar = s.like()
-    st = _Status(l.batch, l.data.device)
+    st = _status_for(l.batch, l.data.device, check)
     _call("bgm_vjp_solve_vec", l.desc(), s.desc(), s_bar.desc(), C.c_int(int(transpose_l)), l_bar.desc(),
           v_bar.desc(), *st.ptrs(), _stream())
     _check(st, check)
@@ -464,7 +487,7 @@ def vjp_solve_mat(l: Bands, s: Bands, s_bar: Bands, r_band_lower: int, r_band_up
     l_bar = l.like()
     r_bar = Bands.empty(l.batch, n, min(r_band_lower, n - 1), min(r_band_upper, n - 1), l.tile, l.dtype,
                         l.data.device)
-    st = _Status(l.batch, l.data.device)
+    st = _status_for(l.batch, l.data.device, check)
     _call("bgm_vjp_solve_mat", l.desc(), s.desc(), s_bar.desc(), C.c_int(int(transpose_l)), l_bar.desc(),
           r_bar.desc(), *st.ptrs(), _stream())
     _check(st, check)
@@ -476,7 +499,7 @@ def vjp_sparse_inverse_subset(l: Bands, s: Bands, s_bar: Bands, check: bool = Tr
     if s.lower != l.lower or s_bar.lower != l.lower or s.n != l.n or s_bar.n != l.n:
         raise DimensionMismatch("vjp_sparse_inverse_subset: shape mismatch")
     l_bar = l.like()
-    st = _Status(l.batch, l.data.device)
+    st = _status_for(l.batch, l.data.device, check)
     _call("bgm_vjp_sparse_inverse_subset", l.desc(), s.desc(), s_bar.desc(), l_bar.desc(), *st.ptrs(),
           _stream())
     _check(st, check)
@@ -546,7 +569,7 @@ def kl_divergence_grad(m_q: Vecs, l_q: Bands, m_p: Vecs, l_p: Bands, check: bool
     _same(l_q, l_p)
     kl = torch.empty(l_q.batch, dtype=torch.float64, device=l_q.data.device)
     m_bar, l_bar = m_q.like(), l_q.like()
-    st = _Status(l_q.batch, l_q.data.device)
+    st = _status_for(l_q.batch, l_q.data.device, check)
     _call("bgm_kl_divergence_grad", m_q.desc(), l_q.desc(), m_p.desc(), l_p.desc(), C.c_void_p(kl.data_ptr()),
           m_bar.desc(), l_bar.desc(), *st.ptrs(), _stream())
     _check(st, check)
@@ -568,7 +591,7 @@ def elbo_gaussian_grad(m_q: Vecs, l_q: Bands, m_p: Vecs, l_p: Bands, y: Vecs, ta
     dev = l_q.data.device
     elbo, kl, tb = (torch.empty(l_q.batch, dtype=torch.float64, device=dev) for _ in range(3))
     m_bar, l_bar = m_q.like(), l_q.like()
-    st = _Status(l_q.batch, dev)
+    st = _status_for(l_q.batch, dev, check)
     _call("bgm_elbo_gaussian_grad", m_q.desc(), l_q.desc(), m_p.desc(), l_p.desc(), y.desc(), C.c_double(tau2),
           C.c_void_p(elbo.data_ptr()), C.c_void_p(kl.data_ptr()), m_bar.desc(), l_bar.desc(),
           C.c_void_p(tb.data_ptr()), *st.ptrs(), _stream())
@@ -592,7 +615,7 @@ def elbo_poisson_grad(m_q: Vecs, l_q: Bands, m_p: Vecs, l_p: Bands, y: Vecs, wei
     dev = l_q.data.device
     elbo, kl = (torch.empty(l_q.batch, dtype=torch.float64, device=dev) for _ in range(2))
     m_bar, l_bar = m_q.like(), l_q.like()
-    st = _Status(l_q.batch, dev)
+    st = _status_for(l_q.batch, dev, check)
     _call("bgm_elbo_poisson_grad", m_q.desc(), l_q.desc(), m_p.desc(), l_p.desc(), y.desc(), weight.desc(),
           C.c_int(quad_points), C.c_void_p(elbo.data_ptr()), C.c_void_p(kl.data_ptr()), m_bar.desc(), l_bar.desc(),
           *st.ptrs(), _stream())
