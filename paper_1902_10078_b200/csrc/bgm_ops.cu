@@ -220,7 +220,7 @@ __global__ void k_product(Band<T> a, int ta, Band<T> bm, int tb, Band<T> c, T al
     for (ix k = k0; k <= k1; ++k) {
       const acc_t av = ta ? a.at(b, k, i) : a.at(b, i, k);
       const acc_t bv = tb ? bm.at(b, j, k) : bm.at(b, k, j);
-      s += av * bv;
+      s = __dadd_rn(s, __dmul_rn(av, bv));  // kernels_detail.hpp:24, uncontracted
     }
     return T(acc_t(alpha) * s);
   });
@@ -236,10 +236,10 @@ __global__ void k_band_vec(Band<T> bm, Vec<T> v, int tr, Vec<T> y, ix batch) {
   acc_t s = 0;
   if (!tr) {
     const ix j0 = i - bm.lo > 0 ? i - bm.lo : 0, j1 = i + bm.up < n - 1 ? i + bm.up : n - 1;
-    for (ix j = j0; j <= j1; ++j) s += acc_t(bm.at(b, i, j)) * acc_t(v(b, j));
+    for (ix j = j0; j <= j1; ++j) s = __dadd_rn(s, __dmul_rn(acc_t(bm.at(b, i, j)), acc_t(v(b, j))));
   } else {
     const ix j0 = i - bm.up > 0 ? i - bm.up : 0, j1 = i + bm.lo < n - 1 ? i + bm.lo : n - 1;
-    for (ix j = j0; j <= j1; ++j) s += acc_t(bm.at(b, j, i)) * acc_t(v(b, j));
+    for (ix j = j0; j <= j1; ++j) s = __dadd_rn(s, __dmul_rn(acc_t(bm.at(b, j, i)), acc_t(v(b, j))));
   }
   y(b, i) = T(s);
 }

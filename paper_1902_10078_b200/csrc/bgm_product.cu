@@ -1,3 +1,8 @@
+// Every dot product here is accumulated in the reference's order with a
+// separate multiply and add (no FMA contraction), as kernels_detail.hpp:16-45
+// computes it: fp64 products and band x vector results are bitwise the
+// reference's.
+//
 // Band x band products (kernels_detail.hpp:16-28), streamlined: one thread
 // per (matrix, output column j) as the generic kernel, but every operand
 // walk is a pointer increment.  In the band storage both op(A)(i, k) and
@@ -54,7 +59,7 @@ __global__ void k_product_stride(Band<T> A, int ta, Band<T> Bm, int tb, Band<T> 
         const int cnt = int(k1 - k0) + 1;
 #pragma unroll 4
         for (int q = 0; q < cnt; ++q) {
-          s = fma(acc_t(*pa), acc_t(*pb), s);
+          s = __dadd_rn(s, __dmul_rn(acc_t(*pa), acc_t(*pb)));
           pa += da;
           pb += db;
         }
@@ -110,7 +115,7 @@ __global__ void __launch_bounds__(128) k_product_blk(Band<T> A, Band<T> Bm, Band
 #pragma unroll
       for (int x = 0; x < AW; ++x) {
         const int r = d - AU + x + CU;  // output cell of row i = k - AU + x in column j
-        if (r >= 0 && r < CW) acc[jj][r] = fma(av[x], bv, acc[jj][r]);
+        if (r >= 0 && r < CW) acc[jj][r] = __dadd_rn(acc[jj][r], __dmul_rn(av[x], bv));
       }
     }
   }
@@ -174,7 +179,7 @@ __global__ void k_band_vec32(Band<T> B, Vec<T> v, int tr, Vec<T> y, ix tiles) {
   acc_t s = 0;
 #pragma unroll 4
   for (ix j = j0; j <= j1; ++j) {
-    s = fma(acc_t(*pb), acc_t(*pv), s);
+    s = __dadd_rn(s, __dmul_rn(acc_t(*pb), acc_t(*pv)));
     pb += db;
     pv += 32;
   }
@@ -206,7 +211,7 @@ __global__ void k_vjp_band_vec32(Band<T> B, Vec<T> v, Vec<T> pb, Band<T> bb, Vec
     if (i >= 0 && i < n) {
       const acc_t ri = acc_t(TR ? vt[i * 32] : pt[i * 32]);
       o = T(ri * cj);
-      if (!TR) s = fma(acc_t(pc[r * 32]), ri, s);
+      if (!TR) s = __dadd_rn(s, __dmul_rn(acc_t(pc[r * 32]), ri));
     }
     oc[r * 32] = o;
   }

@@ -18,7 +18,9 @@
 //    shared-memory read within a column has a compile-time offset;
 //  * thread = (matrix lane, output column): it loads op(Y)(., j) once into
 //    registers, accumulates each output cell over its exact k range with
-//    one LDS + one FMA per term (fp64 accumulation for both storage types),
+//    one LDS + a multiply and an add per term, in the reference's k order
+//    without FMA contraction (kernels_detail.hpp:22-24: s += a(i,k) b(k,j)),
+//    so fp64 results are bitwise the reference's; fp64 accumulation for fp32,
 //    and stores the column with coalesced 8-byte stores (LN lanes x 8 B);
 //  * the fused VJP stages P-bar, A and B once and produces both A-bar and
 //    B-bar columns from them (grad.cpp:148-149), so P-bar is read from HBM
@@ -203,7 +205,7 @@ __device__ __forceinline__ void prod_col(WX wx, WY wy, ix j, ix n, T* __restrict
       if (e < elo || e > ehi) continue;
       const T* p = P::TX ? wx.template col<T>(d - LOX) + (e - d + P::XU) * LN
                          : wx.template col<T>(e - LOX) + (d - e + P::XU) * LN;
-      if (!EDGE || kv[q]) acc = fma(acc_t(*p), yv[q], acc);
+      if (!EDGE || kv[q]) acc = __dadd_rn(acc, __dmul_rn(acc_t(*p), yv[q]));  // no contraction: the reference's s += a * b
     }
     T v = T(acc);
     if (EDGE && (j + d < 0 || j + d >= n)) v = T(0);

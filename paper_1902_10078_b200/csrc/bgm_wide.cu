@@ -477,6 +477,8 @@ ix pick_seg(KernelT kern, int threads, const Geo& G, ix min_seg) {
 // the lanes apply res_{i+a} -= L(i+a, i) x_i (right-looking, column i read
 // contiguously).  Backward row i: the lanes dot column i with the window,
 // a butterfly sum, x_i = (v_i - s) / L(i,i) (kernels_serial.cpp:34-60).
+// The window and the arithmetic are fp64 for both storage types (acc_t):
+// an fp32 solve then rounds only its inputs and outputs, not n recurrences.
 template <class T>
 struct SolveP {
   Band<T> l;
@@ -489,7 +491,7 @@ constexpr int kSolveWarps = 4;  // units per CTA
 constexpr int kSolveRing = 8;   // columns in flight per unit
 
 template <class T, int K, bool TR>
-__device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start, T* side, T* win,
+__device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start, T* side, acc_t* win,
                            T (*ring)[K + 2]) {
   constexpr int R = (K + 1 + 31) / 32, D = kSolveRing;
   constexpr int M = (K + 2) <= 64 ? 64 : ((K + 2) <= 128 ? 128 : 256);  // window ring, power of two
@@ -537,7 +539,7 @@ __device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start,
   };
   if (lane == 0)
     for (int q = 0; q < PF; q += PB) l2pf(TR ? start - q - PB + 1 : start + q);
-  for (int p = lane; p < M; p += 32) win[p] = T(0);
+  for (int p = lane; p < M; p += 32) win[p] = 0.0;
   __syncwarp();
   if (!TR) {
     for (int a = lane; a <= K; a += 32)
@@ -547,7 +549,7 @@ __device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start,
   asm volatile("cp.async.wait_group %0;" ::"n"(D - 2) : "memory");
   __syncwarp();
   // 1 / L(i,i) one row ahead, off the row-to-row dependency chain
-  T rnext = T(1) / ring[0][0];
+  acc_t rnext = 1.0 / acc_t(ring[0][0]);
   int slot = 0;
 #pragma unroll 1
   for (ix i = start; i != stop; i += dir) {
@@ -557,8 +559,8 @@ __device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start,
     __syncwarp();
     const T* col = ring[slot];
     const int nslot = slot + 1 == D ? 0 : slot + 1;
-    const T rd = rnext;
-    T xi;
+    const acc_t rd = rnext;
+    acc_t xi;
     if (!TR) {
       xi = win[i & (M - 1)] * rd;
 #pragma unroll
@@ -566,31 +568,31 @@ __device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start,
         const int a = lane + 32 * q + 1;
         if (a <= K && i + a < n) {
           const int p = int((i + a) & (M - 1));
-          win[p] = fma(-col[a], xi, win[p]);
+          win[p] = fma(-acc_t(col[a]), xi, win[p]);
         }
       }
-      rnext = T(1) / ring[nslot][0];
+      rnext = 1.0 / acc_t(ring[nslot][0]);
       __syncwarp();
       if (lane == 0) win[(i + K + 1) & (M - 1)] = col[K + 1];
     } else {
-      T acc = T(0);
+      acc_t acc = 0.0;
 #pragma unroll
       for (int q = 0; q < R; ++q) {
         const int a = lane + 32 * q + 1;
-        if (a <= K && i + a < n) acc = fma(col[a], win[(i + a) & (M - 1)], acc);
+        if (a <= K && i + a < n) acc = fma(acc_t(col[a]), win[(i + a) & (M - 1)], acc);
       }
-      rnext = T(1) / ring[nslot][0];
+      rnext = 1.0 / acc_t(ring[nslot][0]);
 #pragma unroll
       for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      xi = (col[K + 1] - acc) * rd;
+      xi = (acc_t(col[K + 1]) - acc) * rd;
       __syncwarp();
       if (lane == 0) win[i & (M - 1)] = xi;
     }
     if (lane == 0) {
-      if (i >= s && i < e) C.x(b, i) = xi;
+      if (i >= s && i < e) C.x(b, i) = T(xi);
       else if (side) {
         const ix o = TR ? i - e : i - (s - K);
-        if (o >= 0 && o < K) side[o] = xi;
+        if (o >= 0 && o < K) side[o] = T(xi);
       }
     }
     __syncwarp();
@@ -601,7 +603,7 @@ __device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start,
 
 template <class T, int K, bool TR>
 __global__ void __launch_bounds__(32 * kSolveWarps) k_solve(SolveP<T> C, Geo G) {
-  __shared__ T win[kSolveWarps][(K + 2) <= 64 ? 64 : ((K + 2) <= 128 ? 128 : 256)];
+  __shared__ acc_t win[kSolveWarps][(K + 2) <= 64 ? 64 : ((K + 2) <= 128 ? 128 : 256)];
   __shared__ T ring[kSolveWarps][kSolveRing][K + 2];
   const int w = threadIdx.x >> 5;
   const ix unit = blockIdx.x * ix(kSolveWarps) + w;
@@ -645,7 +647,7 @@ __global__ void k_solve_check(SolveP<T> C, Geo G) {
 
 template <class T, int K, bool TR>
 __global__ void __launch_bounds__(32 * kSolveWarps) k_solve_repair(SolveP<T> C, Geo G) {
-  __shared__ T win[kSolveWarps][(K + 2) <= 64 ? 64 : ((K + 2) <= 128 ? 128 : 256)];
+  __shared__ acc_t win[kSolveWarps][(K + 2) <= 64 ? 64 : ((K + 2) <= 128 ? 128 : 256)];
   __shared__ T ring[kSolveWarps][kSolveRing][K + 2];
   const int w = threadIdx.x >> 5;
   const ix b = blockIdx.x * ix(kSolveWarps) + w;
