@@ -504,9 +504,9 @@ bool vjp_t(const bgm_band& a, const bgm_band& b, const bgm_band& pb, const bgm_b
   if (is(a, 8, 8) && is(b, 3, 3) && is(pb, 11, 11))
     return run_cfg<T, 16, 4, 3, 4, S_vab, true>(ops, ab, &bb, "stream_vjp_ab", s);
   if (is(a, 8, 0) && is(b, 0, 8) && is(pb, 8, 8))
-    return run_cfg<T, 16, 8, 2, 2, S_vllt, true>(ops, ab, &bb, "stream_vjp_llt", s);
+    return run_cfg<T, 16, 8, 2, 4, S_vllt, true>(ops, ab, &bb, "stream_vjp_llt", s);
   if (is(a, 16, 0) && is(b, 0, 16) && is(pb, 16, 0))
-    return run_cfg<T, 16, 8, 1, 2, S_vdl, false>(ops, ab, &bb, "stream_vjp_dl", s);
+    return run_cfg<T, 16, 8, 1, 4, S_vdl, false>(ops, ab, &bb, "stream_vjp_dl", s);
   return false;
 }
 
