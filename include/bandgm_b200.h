@@ -227,6 +227,19 @@ int bgm_elbo_poisson_grad(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p, 
  * and weights w (host arrays), by the Golub-Welsch eigen-decomposition. */
 int bgm_gauss_hermite(int quad_points, double* x, double* w);
 
+/* ------------------------------------------------- model assembly */
+/* models::prior_natural_params (models.cpp:165-189) for B state-space models
+ * with d-dimensional states (1 <= d <= 8) and `steps` transitions, device
+ * arrays, row-major blocks: a, q [B][steps][d][d], b [B][steps][d],
+ * mu0 [B][d], sigma0 [B][d][d].  Writes the joint prior precision Lambda as a
+ * symmetric lower store (n = (steps+1) d, lower = 2d-1, upper = 0) and
+ * eta = Lambda m (m the propagated prior mean).  A block that is not SPD
+ * (the reference's SingularBlock(t)) reports BGM_ERR_NOT_PD with row = t
+ * (Q_{t-1} -> t, Sigma0 -> 0), in the reference's order.  fp64. */
+int bgm_prior_natural_params(int64_t batch, int d, int64_t steps, const double* a, const double* b,
+                             const double* q, const double* mu0, const double* sigma0, bgm_band lambda,
+                             bgm_vec eta, int32_t* status, int64_t* row, bgm_stream stream);
+
 /* ------------------------------------------------- instrumentation */
 /* Per-kernel CUDA-event timing on the launching stream (off by default).
  * bgm_timing_enable(1) clears and starts recording; bgm_timing_read(i, ...)

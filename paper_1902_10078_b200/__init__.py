@@ -18,6 +18,7 @@ from .api import (  # noqa: F401
     DimensionMismatch,
     NotPositiveDefinite,
     NonPositiveDiagonal,
+    SingularBlock,
     SingularDiagonal,
     T,
     cholesky,
@@ -32,6 +33,7 @@ from .api import (  # noqa: F401
     outer_band,
     product_band_band,
     product_band_band_restricted,
+    prior_natural_params,
     product_band_vec,
     set_segment_rows,
     solve_mat,

@@ -639,6 +639,43 @@ def gauss_hermite(quad_points: int):
     return np.array(x[:]), np.array(w[:])
 
 
+# --------------------------------------------------------------------- model assembly
+class SingularBlock(_RowError):
+    """errors.hpp (models.cpp:27): a state-space block is not SPD; .row = block."""
+    what = "state-space block is not positive definite"
+
+
+def prior_natural_params(a, b, q, mu0, sigma0, tile: int = 32, check: bool = True):
+    """models::prior_natural_params (models.cpp:165-189), batched: B models
+    with d-dim states and T transitions, given as tensors a, q (B, T, d, d),
+    b (B, T, d), mu0 (B, d), sigma0 (B, d, d).  Returns (Lambda, eta): the
+    joint prior precision as a symmetric lower store (Bands, n = (T+1) d,
+    band 2d-1) and eta = Lambda m (Vecs)."""
+    dev = _device()
+    t = [torch.as_tensor(x, dtype=torch.float64).to(dev).contiguous() for x in (a, b, q, mu0, sigma0)]
+    a, b, q, mu0, sigma0 = t
+    B, T, d, _ = a.shape
+    if b.shape != (B, T, d) or q.shape != (B, T, d, d) or mu0.shape != (B, d) or sigma0.shape != (B, d, d):
+        raise DimensionMismatch("prior_natural_params: block shapes do not agree")
+    if T < 1 or d < 1:
+        raise BandgmError("state-space model is empty")
+    if d > 8:
+        raise BandgmError("prior_natural_params: state dimension above 8 is not supported")
+    n = (T + 1) * d
+    lam = Bands.empty(B, n, 2 * d - 1, 0, tile, torch.float64, dev)
+    eta = Vecs.empty(B, n, tile, torch.float64, dev)
+    st = _status_for(B, dev, check)
+    _call("bgm_prior_natural_params", C.c_int64(B), C.c_int(d), C.c_int64(T), *(C.c_void_p(x.data_ptr()) for x in t),
+          lam.desc(), eta.desc(), *st.ptrs(), _stream())
+    if check:
+        stn = st.st.cpu().numpy()
+        bad = np.nonzero(stn)[0]
+        if bad.size:
+            m = int(bad[0])
+            raise SingularBlock(int(st.row[m]), m)
+    return lam, eta
+
+
 # --------------------------------------------------------------------- config 3
 def marginal_likelihood_grad(L: Bands, y: Vecs, tau2: float, check: bool = True, out=None):
     """Config-3 learning step: per matrix, the log marginal
