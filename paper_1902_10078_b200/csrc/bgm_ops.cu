@@ -305,6 +305,14 @@ struct OuterF {  // alpha m_i v_j
 };
 
 template <class T>
+__global__ void k_logdet_diag(Band<T> l, const T* c, Band<T> lb, ix batch) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  ix b, j;
+  if (l.n == 0 || !split_bj(t, batch, l.n, lb.s, b, j)) return;
+  lb.cell(b, 0, j) = c[b] / l.cell(b, 0, j);
+}
+
+template <class T>
 struct LogDetBarF {  // c / L_jj on the diagonal (grad.cpp:172-176)
   Band<T> l;
   const T* c;
@@ -827,10 +835,13 @@ int bgm_vjp_log_det(bgm_band l, const void* cbar, bgm_band lbar, bgm_stream stre
     const ix work = bj_work(l.batch, l.n, tile_shift(lbar.tile));
     const Band<T> lb = view<T>(lbar), lv = view<T>(l);
     const T* c = static_cast<const T*>(cbar);
-    if (flat_ok(lb, l.batch))
-      launch_flat(lb, l.batch, LogDetBarF<T>{lv, c}, s);
-    else
-      k_vjp_log_det<T><<<blocks_for(work, kThreads), kThreads, 0, s>>>(lv, c, lb, l.batch);
+    // the band is zero but for its diagonal: a memset at copy-engine speed,
+    // then c / L_jj on the diagonal (grad.cpp:172-176)
+    const size_t bytes = size_t((l.batch + lbar.tile - 1) / lbar.tile * lbar.tile) * size_t(l.n) *
+                         size_t(lbar.lower + 1) * sizeof(T);
+    const cudaError_t e = cudaMemsetAsync(lbar.data, 0, bytes, s);
+    if (e != cudaSuccess) return set_error(e);
+    k_logdet_diag<T><<<blocks_for(work, kThreads), kThreads, 0, s>>>(lv, c, lb, l.batch);
     return launched();
   });
 }
