@@ -254,6 +254,62 @@ __global__ void k_outer(Vec<T> m, Vec<T> v, T alpha, Band<T> o, ix batch) {
   o.write_column(b, j, [&](ix i) { return alpha * (m(b, i) * vj); });
 }
 
+// Outer-product band writers (kernels_detail.hpp:48-54: out(i, j) = m_i v_j),
+// alpha in {1, -1} exact.  Tile 32: thread = (matrix lane, column j) walks
+// the column's w cells (every load / store a 256-byte warp transaction).
+template <class T>
+__global__ void k_outer_t32(Vec<T> m, Vec<T> v, T alpha, Band<T> o, ix batch) {
+  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
+  const int lane = int(t & 31);
+  const ix rest = t >> 5, n = o.n;
+  const ix tiles = (batch + 31) / 32;
+  if (rest >= tiles * n) return;
+  const ix tile = rest / n, j = rest - tile * n;
+  const T vj = v.p[(tile * n + j) * 32 + lane];
+  const T* mp = m.p + (tile * n + j - o.up) * 32 + lane;
+  T* op = o.p + (tile * n + j) * ix(o.w) * 32 + lane;
+  const bool live = tile * 32 + lane < batch;
+  for (int r = 0; r < o.w; ++r) {
+    const ix i = j - o.up + r;
+    op[r * 32] = (live && i >= 0 && i < n) ? alpha * (mp[r * 32] * vj) : T(0);
+  }
+}
+
+// Tile 1: warp = (matrix, 32 consecutive columns), whose storage is one
+// contiguous run of 32 w cells; lane l writes cells l, l+32, ... of the run
+// (coalesced), stepping (column, row) incrementally; v of the 32 columns is
+// loaded once and shuffled.
+template <class T>
+__global__ void k_outer_t1(Vec<T> m, Vec<T> v, T alpha, Band<T> o, ix batch) {
+  const ix gw = (blockIdx.x * ix(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const ix n = o.n, nblk = (n + 31) / 32;
+  if (gw >= batch * nblk) return;  // whole warps
+  const ix b = gw / nblk, j0 = (gw - b * nblk) * 32;
+  const int w = o.w;
+  const int cols = int(n - j0 < 32 ? n - j0 : 32);
+  const T vl = lane < cols ? v.p[b * n + j0 + lane] : T(0);
+  T* run = o.p + (b * n + j0) * ix(w);
+  const T* mb = m.p + b * n;
+  const int total = cols * w;
+  const int dj = 32 / w, dr = 32 % w;  // (column, row) step of 32 cells
+  int jj = lane / w, r = lane % w;
+  const int iters = (total + 31) / 32;  // warp-uniform (the shuffle needs every lane)
+  for (int it = 0, e = lane; it < iters; ++it, e += 32) {
+    const T vj = __shfl_sync(0xffffffffu, vl, jj & 31);
+    if (e < total) {
+      const ix i = j0 + jj - o.up + r;
+      run[e] = (i >= 0 && i < n) ? alpha * (mb[i] * vj) : T(0);
+    }
+    jj += dj;
+    r += dr;
+    if (r >= w) {
+      r -= w;
+      ++jj;
+    }
+  }
+}
+
 // Whole-band writers in storage order: thread x of tile group g writes the
 // x-th element of the group's (n, w, tile) block, so every store is
 // coalesced in both layouts (tile 1 columns are contiguous w-cell runs);
@@ -277,23 +333,35 @@ __global__ void k_band_flat(Band<T> o, ix batch, F f) {
     }
     return;
   }
+  // U pairs per thread and iteration: every value (the functor's loads) is
+  // computed before any of the U stores, so U x 2 loads are in flight at once
+  constexpr int U = 4;
   const unsigned pairs = per >> 1;
-  for (unsigned x2 = blockIdx.x * blockDim.x + threadIdx.x; x2 < pairs; x2 += gridDim.x * blockDim.x) {
-    const unsigned x = x2 << 1;
-    T val[2];
+  const unsigned stride = gridDim.x * blockDim.x;
+  for (unsigned x0 = blockIdx.x * blockDim.x + threadIdx.x; x0 < pairs; x0 += U * stride) {
+    T val[U][2];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const unsigned xe = x + h;
-      const unsigned cr = xe >> o.s;
-      const unsigned j = cr / unsigned(o.w), r = cr - j * unsigned(o.w);
-      const ix b = g * tile + (xe & (tile - 1));
-      const ix i = ix(j) - o.up + r;
-      val[h] = (b < batch && i >= 0 && i < o.n) ? f(b, i, ix(j), int(r)) : T(0);
+    for (int u = 0; u < U; ++u) {
+      const unsigned x2 = x0 + u * stride;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const unsigned xe = (x2 << 1) + h;
+        const unsigned cr = xe >> o.s;
+        const unsigned j = cr / unsigned(o.w), r = cr - j * unsigned(o.w);
+        const ix b = g * tile + (xe & (tile - 1));
+        const ix i = ix(j) - o.up + r;
+        val[u][h] = (x2 < pairs && b < batch && i >= 0 && i < o.n) ? f(b, i, ix(j), int(r)) : T(0);
+      }
     }
-    V2 v;
-    v.x = val[0];
-    v.y = val[1];
-    *reinterpret_cast<V2*>(base + x) = v;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const unsigned x2 = x0 + u * stride;
+      if (x2 >= pairs) break;
+      V2 v;
+      v.x = val[u][0];
+      v.y = val[u][1];
+      *reinterpret_cast<V2*>(base + (x2 << 1)) = v;
+    }
   }
 }
 
@@ -511,6 +579,15 @@ static int run_outer(const bgm_vec& m, const bgm_vec& v, double alpha, const bgm
   const ix work = bj_work(o.batch, o.n, tile_shift(o.tile));
   if (!work) return launched();
   const Band<T> ob = view<T>(o);
+  if (o.tile == 32) {  // thread per (matrix lane, column): a pointer walk down the column
+    k_outer_t32<T><<<blocks_for(work, kThreads), kThreads, 0, s>>>(view<T>(m), view<T>(v), T(alpha), ob, o.batch);
+    return launched();
+  }
+  if (o.n >= 32 && ob.w <= 4096) {  // warp per (matrix, 32 columns): contiguous stores, no per-cell division
+    const ix blocks = ix(o.batch) * ((o.n + 31) / 32);
+    k_outer_t1<T><<<blocks_for(blocks * 32, 256), 256, 0, s>>>(view<T>(m), view<T>(v), T(alpha), ob, o.batch);
+    return launched();
+  }
   if (flat_ok(ob, o.batch)) {
     const Vec<T> mv = view<T>(m), vv = view<T>(v);
     const T a = T(alpha);
