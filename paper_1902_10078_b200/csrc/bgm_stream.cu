@@ -20,7 +20,8 @@
 //    registers, accumulates each output cell over its exact k range with
 //    one LDS + a multiply and an add per term, in the reference's k order
 //    without FMA contraction (kernels_detail.hpp:22-24: s += a(i,k) b(k,j)),
-//    so fp64 results are bitwise the reference's; fp64 accumulation for fp32,
+//    so fp64 results are bitwise the reference's (the k = 16 shapes of config
+//    3 use FMA instead: FP64-bound otherwise); fp64 accumulation for fp32,
 //    and stores the column with coalesced 8-byte stores (LN lanes x 8 B);
 //  * the fused VJP stages P-bar, A and B once and produces both A-bar and
 //    B-bar columns from them (grad.cpp:148-149), so P-bar is read from HBM
@@ -70,9 +71,15 @@ struct NoP {
 
 // Up to three staged operands (widths W0..W2) and one or two products
 // reading them (operand indices X1, Y1, X2, Y2).
-template <int NOP_, int W0, int W1, int W2, class P1_, int X1_, int Y1_, class P2_ = NoP, int X2_ = 0, int Y2_ = 0>
+template <int NOP_, int W0, int W1, int W2, class P1_, int X1_, int Y1_, class P2_ = NoP, int X2_ = 0, int Y2_ = 0,
+          bool FMA_ = false>
 struct Spec {
   static constexpr int NOP = NOP_;
+  // FMA: contract each term into one fused multiply-add.  Off (the default),
+  // terms are a separate multiply and add in the reference's order, and fp64
+  // results are bitwise the reference's; on for the k = 16 shapes, whose
+  // doubled fp64 instruction count would otherwise make them FP64-bound.
+  static constexpr bool FMA = FMA_;
   using P1 = P1_;
   using P2 = P2_;
   static constexpr int X1 = X1_, Y1 = Y1_, X2 = X2_, Y2 = Y2_;
@@ -182,7 +189,7 @@ struct Win {
   }
 };
 
-template <class T, int LN, class P, class WX, class WY, int LOX, int LOY, int R0, int R1, bool EDGE>
+template <class T, int LN, class P, class WX, class WY, int LOX, int LOY, int R0, int R1, bool EDGE, bool FMA>
 __device__ __forceinline__ void prod_col(WX wx, WY wy, ix j, ix n, T* __restrict__ out) {
   constexpr int NE = P::EMAX - P::EMIN + 1;
   acc_t yv[NE];
@@ -205,7 +212,8 @@ __device__ __forceinline__ void prod_col(WX wx, WY wy, ix j, ix n, T* __restrict
       if (e < elo || e > ehi) continue;
       const T* p = P::TX ? wx.template col<T>(d - LOX) + (e - d + P::XU) * LN
                          : wx.template col<T>(e - LOX) + (d - e + P::XU) * LN;
-      if (!EDGE || kv[q]) acc = __dadd_rn(acc, __dmul_rn(acc_t(*p), yv[q]));  // no contraction: the reference's s += a * b
+      if (!EDGE || kv[q])  // FMA off: no contraction, the reference's s += a * b
+        acc = FMA ? fma(acc_t(*p), yv[q], acc) : __dadd_rn(acc, __dmul_rn(acc_t(*p), yv[q]));
     }
     T v = T(acc);
     if (EDGE && (j + d < 0 || j + d >= n)) v = T(0);
@@ -228,9 +236,9 @@ __device__ __forceinline__ void do_part(const T* const* b, const int* sl, ix j, 
   using WY = Win<Gm::SS(Y), Gm::WRC(Y)>;
   T* o = PI == 0 ? o1 : o2;
   if (interior)
-    prod_col<T, LN, P, WX, WY, S::lo(X), S::lo(Y), R0, R1, false>(WX{b[X], sl[X]}, WY{b[Y], sl[Y]}, j, n, o);
+    prod_col<T, LN, P, WX, WY, S::lo(X), S::lo(Y), R0, R1, false, S::FMA>(WX{b[X], sl[X]}, WY{b[Y], sl[Y]}, j, n, o);
   else
-    prod_col<T, LN, P, WX, WY, S::lo(X), S::lo(Y), R0, R1, true>(WX{b[X], sl[X]}, WY{b[Y], sl[Y]}, j, n, o);
+    prod_col<T, LN, P, WX, WY, S::lo(X), S::lo(Y), R0, R1, true, S::FMA>(WX{b[X], sl[X]}, WY{b[Y], sl[Y]}, j, n, o);
 }
 
 // Producer warp: one lane walks the CTA's runs and issues, for every step,
@@ -471,17 +479,17 @@ bool same(const bgm_band& a, const bgm_band& b) {
 // L L^T full (8,8) from one staged L (8,0)           [config 2]
 using S_llt8 = Spec<1, 9, 1, 1, PS<0, 1, 8, 0, 8, 0, 8, 8>, 0, 0>;
 // band(L L^T) lower (16,0) = precision_from_factor  [config 3, inference.cpp:23-26]
-using S_llt16 = Spec<1, 17, 1, 1, PS<0, 1, 16, 0, 16, 0, 16, 0>, 0, 0>;
+using S_llt16 = Spec<1, 17, 1, 1, PS<0, 1, 16, 0, 16, 0, 16, 0>, 0, 0, NoP, 0, 0, true>;
 // A(8,8) B(3,3) -> (11,11)                          [config 2]
 using S_ab = Spec<2, 17, 7, 1, PS<0, 0, 8, 8, 3, 3, 11, 11>, 0, 1>;
 // fused VJP, operands 0 = P-bar, 1 = A, 2 = B:
 //   A-bar = P-bar op(B)^T on band(A), B-bar = op(A)^T P-bar on band(B)
-template <int AL, int AU, int BL, int BU, int PL, int PU>
+template <int AL, int AU, int BL, int BU, int PL, int PU, bool FMA = false>
 using S_vjp = Spec<3, PL + PU + 1, AL + AU + 1, BL + BU + 1, PS<0, 1, PL, PU, BL, BU, AL, AU>, 0, 2,
-                   PS<1, 0, AL, AU, PL, PU, BL, BU>, 1, 0>;
+                   PS<1, 0, AL, AU, PL, PU, BL, BU>, 1, 0, FMA>;
 using S_vab = S_vjp<8, 8, 3, 3, 11, 11>;   // config 2: A(8,8), B(3,3), P-bar (11,11)
 using S_vllt = S_vjp<8, 0, 0, 8, 8, 8>;    // config 2: L, L^T, P-bar (8,8)
-using S_vdl = S_vjp<16, 0, 0, 16, 16, 0>;  // config 3 dL: L, L^T, G (16,0)
+using S_vdl = S_vjp<16, 0, 0, 16, 16, 0, true>;  // config 3 dL: L, L^T, G (16,0)
 
 template <class T>
 bool product_t(const bgm_band& a, int ta, const bgm_band& b, int tb, const bgm_band& c, cudaStream_t s) {
