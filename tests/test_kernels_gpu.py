@@ -259,3 +259,27 @@ def test_band_vec_tile32_multi_tile(cuda, oracle, transpose, dtype):
         assert np.all(np.isfinite(gb)) and np.all(np.isfinite(gv))
         assert cm.max_rel_err(gb, rb) <= tol
         assert cm.max_rel_err(gv, rv) <= tol
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tile", [1, 32])
+@pytest.mark.parametrize("B,n", [(1, 1), (1, 2), (33, 31), (3, 33), (2, 97)])
+@pytest.mark.parametrize("lo,up", [(0, 0), (2, 1), (1, 3)])
+def test_vector_kernels_edge_shapes(cuda, oracle, tile, B, n, lo, up):
+    """band x vector, outer band and their VJPs on degenerate and ragged
+    shapes (n = 1, bands clipped to n - 1, partial tiles, n not a multiple of
+    the 32-column runs) in both layouts, bitwise against the oracle
+    (kernels_detail.hpp:31-54 evaluated in the same order, uncontracted)."""
+    from tests.gpu_adapter import GpuOracle
+    g = GpuOracle(tile=tile)
+    rng = np.random.default_rng(B * 100 + n + lo + 7 * up)
+    lo, up = min(lo, n - 1), min(up, n - 1)
+    b = cm.random_band(rng, B, n, lo, up)
+    v, p = cm.random_vec(rng, B, n), cm.random_vec(rng, B, n)
+    for tr in (False, True):
+        np.testing.assert_array_equal(g.product_band_vec(b, lo, up, v, tr), oracle.product_band_vec(b, lo, up, v, tr))
+        gb, gv = g.vjp_product_band_vec(b, lo, up, v, p, tr)
+        rb, rv = oracle.vjp_product_band_vec(b, lo, up, v, p, tr)[:2]
+        np.testing.assert_array_equal(gb, rb)
+        np.testing.assert_array_equal(gv, rv)
+    np.testing.assert_array_equal(g.outer_band(v, p, lo, up), oracle.outer_band(v, p, lo, up))
