@@ -499,7 +499,7 @@ bool product_t(const bgm_band& a, int ta, const bgm_band& b, int tb, const bgm_b
     return run_cfg<T, 16, 8, 3, 2, S_llt16, false>(&a, c, nullptr, "stream_llt16", s);
   if (!ta && !tb && a.lower == 8 && a.upper == 8 && b.lower == 3 && b.upper == 3 && c.lower == 11 && c.upper == 11) {
     const bgm_band ops[2] = {a, b};
-    return run_cfg<T, 16, 16, 2, 2, S_ab, true>(ops, c, nullptr, "stream_ab", s);
+    return run_cfg<T, 16, 8, 3, 4, S_ab, true>(ops, c, nullptr, "stream_ab", s);
   }
   return false;
 }
