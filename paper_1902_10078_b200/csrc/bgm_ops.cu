@@ -380,12 +380,6 @@ __global__ void k_logdet_diag(Band<T> l, const T* c, Band<T> lb, ix batch) {
   lb.cell(b, 0, j) = c[b] / l.cell(b, 0, j);
 }
 
-template <class T>
-struct LogDetBarF {  // c / L_jj on the diagonal (grad.cpp:172-176)
-  Band<T> l;
-  const T* c;
-  __device__ __forceinline__ T operator()(ix b, ix, ix j, int r) const { return r == 0 ? c[b] / l.at(b, j, j) : T(0); }
-};
 
 template <class T>
 static bool flat_ok(const Band<T>& o, ix batch) {
@@ -522,15 +516,6 @@ __global__ void k_vjp_subset(Band<T> l, Band<T> s, Band<T> sb, Band<T> lb, Band<
 }
 
 // grad.cpp:172-176
-template <class T>
-__global__ void k_vjp_log_det(Band<T> l, const T* cbar, Band<T> lb, ix batch) {
-  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
-  ix b, j;
-  if (l.n == 0 || !split_bj(t, batch, l.n, lb.s, b, j)) return;
-  const T c = cbar[b];
-  const T d = l.at(b, j, j);
-  for (int r = 0; r < lb.w; ++r) lb.cell(b, r, j) = r == 0 ? c / d : T(0);
-}
 
 // ------------------------------------------------------ typed launchers
 
