@@ -602,6 +602,9 @@ struct VcholP {
 #ifndef VCHOL_FENCE
 #define VCHOL_FENCE 4
 #endif
+#ifndef VCHOL_SLOT
+#define VCHOL_SLOT 1  // vjp_cholesky pairs: the next pair's columns by cp.async into a slot
+#endif
 template <class T, int K>
 __device__ void vchol_unit(const VcholP<T>& C, ix b, ix n, ix s, ix e, ix start, T* side, T* win) {
   constexpr int W = K + 1, ts = kThreads;
@@ -652,6 +655,21 @@ __device__ void vchol_unit(const VcholP<T>& C, ix b, ix n, ix s, ix e, ix start,
   // two places down the diagonal; row j's new column (the window's column 0
   // after row j) is folded into row j-1 after the pass.
   const int L2A = C.l2a;  // L2 bulk prefetch distance (columns) of L and L-bar, per tile (0 = off)
+#if VCHOL_SLOT
+  // cp.async slot after the window: [4 columns: L j, L-bar j, L j-1, L-bar j-1][W][thread]
+  T* vslot = win + (K * (K + 1) / 2) * ts;
+  bool slot_ready = false;
+  auto fetch4 = [&](ix jj) {  // columns jj, jj-1 of L and L-bar (all in [0, n))
+#pragma unroll
+    for (int r = 0; r < W; ++r) {
+      cpa(vslot + (0 * W + r) * ts, lbase + jj * cs + r * 32);
+      cpa(vslot + (1 * W + r) * ts, gbase + jj * cs + r * 32);
+      cpa(vslot + (2 * W + r) * ts, lbase + (jj - 1) * cs + r * 32);
+      cpa(vslot + (3 * W + r) * ts, gbase + (jj - 1) * cs + r * 32);
+    }
+    cpa_commit();
+  };
+#endif
   const T* ltile = lbase - (b & 31);
   const T* gtile = gbase - (b & 31);
 #pragma unroll 1
@@ -662,8 +680,30 @@ __device__ void vchol_unit(const VcholP<T>& C, ix b, ix n, ix s, ix e, ix start,
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gtile + (j - 1 - L2A) * cs), "r"(bytes) : "memory");
     }
     T u[K], g[K], u2[K], g2[K], d, gd, d2, gd2;
+#if VCHOL_SLOT
+    // the pair's four columns arrived by cp.async during the previous pair
+    if (!slot_ready) fetch4(j);
+    cpa_wait();
+    auto take = [&](int c, ix jj, T* uu, T* gg, T& dd_, T& gdd) {
+      const T* su = vslot + (2 * c) * W * ts;
+      const T* sg = vslot + (2 * c + 1) * W * ts;
+#pragma unroll
+      for (int x = 0; x < K; ++x) {
+        const bool in = jj + 1 + x < n;
+        uu[x] = in ? su[(x + 1) * ts] : T(0);
+        gg[x] = in ? sg[(x + 1) * ts] : T(0);
+      }
+      dd_ = su[0];
+      gdd = sg[0];
+    };
+    take(0, j, u, g, d, gd);
+    take(1, j - 1, u2, g2, d2, gd2);
+    slot_ready = j - 3 >= s;
+    if (slot_ready) fetch4(j - 2);
+#else
     load(j, u, g, d, gd);
     load(j - 1, u2, g2, d2, gd2);
+#endif
 #pragma unroll
     for (int x = K - 1; x >= 0; --x) {
 #pragma unroll
@@ -703,6 +743,9 @@ __device__ void vchol_unit(const VcholP<T>& C, ix b, ix n, ix s, ix e, ix start,
     emit(j, ad, a);
     emit(j - 1, ad2, a2);
   }
+#if VCHOL_SLOT
+  cpa_wait();
+#endif
 #pragma unroll 1
   for (; j >= s; --j) {
     T u[K], g[K], d, gd;
@@ -983,7 +1026,7 @@ bool run_subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row
 
 template <class T, int K>
 bool run_vchol(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cudaStream_t s) {
-  const size_t smem = sizeof(T) * ((K + 1) * (K + 2) / 2) * kThreads;
+  const size_t smem = sizeof(T) * ((K + 1) * (K + 2) / 2 + (VCHOL_SLOT ? 4 * (K + 1) : 0)) * kThreads;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_vchol<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
