@@ -24,6 +24,12 @@ namespace narrow {
 namespace {
 
 constexpr int kThreads = 32;     // one warp per CTA: shared memory bounds residency
+// narrow solves: rows in flight per thread (shared-memory ring); measured at
+// configs 1 / 3: k = 16 gains from depth (1.26 -> 1.03 ms), k = 4 does not
+template <int K>
+constexpr int solve_pf() {
+  return K >= 16 ? 10 : 3;
+}
 constexpr int kBurnMin = 64;     // burn-in rows: max(kBurnMin, kBurnGen * K)
 constexpr int kBurnGen = 16;
 constexpr double kCheckTol = 1e-12;
@@ -259,7 +265,7 @@ struct SolveP {
 // reference divides, kernels_serial.cpp:47).  Backward: x window x[a] =
 // x_{i+1+a}; x_i = (v_i - sum_a L(i+1+a, i) x[a]) / L(i,i).
 template <class T, int K, bool TR>
-__device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start, T* side, int l2a,
+__device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start, T* side, int l2a, T* ring,
                            const T* carry = nullptr) {
   constexpr int W = K + 1;
   const T* lb = bbase(C.l, b);
@@ -298,13 +304,33 @@ __device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start,
   // indices: the row loop is unrolled by PF); the tile's columns further
   // ahead are pulled into L2 by one bulk prefetch per PF rows (a column of
   // the 32 interleaved matrices is w * 256 contiguous bytes).
-  constexpr int PF = K * sizeof(T) >= 128 ? 2 : 4;
+  constexpr int PF = solve_pf<K>();
   const int dir = TR ? -1 : 1;
   const ix stop = TR ? s - 1 : e;
   const ix rows = TR ? start - stop : stop - start;
-  T cb[PF][W], vb_[PF];
+  // rows stream through a per-thread shared-memory ring of PF slots
+  // ([slot][cell][thread]) filled by cp.async PF rows ahead; the tile's
+  // columns further ahead are pulled into L2 by one bulk prefetch per PF rows
+  constexpr int ts = kThreads;
+  auto issue = [&](ix j, int q) {
+    if (j >= 0 && j < n) {
+      T* d = ring + q * (W + 1) * ts;
 #pragma unroll
-  for (int q = 0; q < PF; ++q) load_col(start + q * dir, cb[q], vb_[q]);
+      for (int a = 0; a <= K; ++a)
+        if (j + a < n) cpa(d + a * ts, lb + j * cs + a * 32);
+      const ix vr = TR ? j : j + K + 1;
+      if (vr >= 0 && vr < n) cpa(d + W * ts, vb + vr * 32);
+    }
+    cpa_commit();
+  };
+  auto take = [&](ix j, int q, T* col, T& vv) {
+    const T* d = ring + q * (W + 1) * ts;
+    const bool in = j >= 0 && j < n;
+#pragma unroll
+    for (int a = 0; a <= K; ++a) col[a] = (in && j + a < n) ? d[a * ts] : T(0);
+    const ix vr = TR ? j : j + K + 1;
+    vv = (in && vr >= 0 && vr < n) ? d[W * ts] : T(0);
+  };
   auto l2_ahead = [&](ix i) {
     const ix lo = TR ? i - l2a - PF + 1 : i + l2a, hi = lo + PF - 1;
     if (l2a > 0 && lo >= 0 && hi < n)
@@ -340,27 +366,25 @@ __device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start,
       if (o >= 0 && o < K) side[o] = xi;
     }
   };
+#pragma unroll
+  for (int q = 0; q < PF; ++q) issue(start + q * dir, q);
   ix i = start;
 #pragma unroll 1
-  for (ix blk = 0; blk + PF <= rows; blk += PF) {
+  for (ix blk = 0; blk < rows; blk += PF) {
     if ((threadIdx.x & 31) == 0) l2_ahead(i);
 #pragma unroll
     for (int q = 0; q < PF; ++q) {
-      T col[W], vv = vb_[q];
-#pragma unroll
-      for (int a = 0; a <= K; ++a) col[a] = cb[q][a];
-      load_col(i + PF * dir, cb[q], vb_[q]);
+      if (i == stop) break;
+      T col[W], vv;
+      asm volatile("cp.async.wait_group %0;" ::"n"(PF - 1) : "memory");  // row i's group has landed
+      take(i, q, col, vv);
+      issue(i + PF * dir, q);  // refill the slot PF rows ahead
       row(i, col, vv);
       i += dir;
     }
-    if (carry && same >= K) return;
+    if (carry && same >= K) break;
   }
-#pragma unroll
-  for (int q = 0; q < PF; ++q) {  // tail (rows % PF), ring order continues at slot 0
-    if (i == stop) break;
-    row(i, cb[q], vb_[q]);
-    i += dir;
-  }
+  cpa_wait();
 }
 
 template <class T, int K, bool TR>
@@ -377,7 +401,8 @@ __global__ void k_solve(SolveP<T> C, Geo G) {
     start = e + G.burn - 1 < G.n - 1 ? e + G.burn - 1 : G.n - 1;
     if (u.p + 1 < G.nseg) side = C.side + u.id * K;
   }
-  solve_unit<T, K, TR>(C, u.b, G.n, s, e, start, side, G.l2a);
+  extern __shared__ __align__(16) unsigned char smraw[];
+  solve_unit<T, K, TR>(C, u.b, G.n, s, e, start, side, G.l2a, reinterpret_cast<T*>(smraw) + threadIdx.x);
 }
 
 template <class T, int K, bool TR>
@@ -400,7 +425,8 @@ template <class T, int K, bool TR>
 __global__ void k_solve_repair(SolveP<T> C, Geo G) {
   const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
   if (b >= G.batch || !C.flag[b]) return;
-  solve_unit<T, K, TR>(C, b, G.n, 0, G.n, TR ? G.n - 1 : 0, nullptr, G.l2a);
+  extern __shared__ __align__(16) unsigned char smraw[];
+  solve_unit<T, K, TR>(C, b, G.n, 0, G.n, TR ? G.n - 1 : 0, nullptr, G.l2a, reinterpret_cast<T*>(smraw) + threadIdx.x);
 }
 
 // Fix-up of segments whose burn-in did not converge: the neighbour's genuine
@@ -425,7 +451,9 @@ __global__ void k_solve_fix(SolveP<T> C, Geo G, const int32_t* uflag, const T* s
   if (!u.live || !uflag[u.id]) return;
   const ix s = ix(u.p) * G.seg, e = s + G.seg < G.n ? s + G.seg : G.n;
   const T* carry = snap + (TR ? u.id + 1 : u.id - 1) * K;
-  solve_unit<T, K, TR>(C, u.b, G.n, s, e, TR ? e - 1 : s, nullptr, G.l2a, carry);
+  extern __shared__ __align__(16) unsigned char smraw[];
+  solve_unit<T, K, TR>(C, u.b, G.n, s, e, TR ? e - 1 : s, nullptr, G.l2a, reinterpret_cast<T*>(smraw) + threadIdx.x,
+                       carry);
 }
 
 template <class T, int K, bool TR>
@@ -602,6 +630,7 @@ struct VcholP {
 #ifndef VCHOL_FENCE
 #define VCHOL_FENCE 4
 #endif
+
 #ifndef VCHOL_SLOT
 #define VCHOL_SLOT 1  // vjp_cholesky pairs: the next pair's columns by cp.async into a slot
 #endif
@@ -944,7 +973,8 @@ bool run_chol(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, c
 template <class T, int K, bool TR>
 bool run_solve(const bgm_band& l, const bgm_vec& v, const bgm_vec& x, int32_t* st, int64_t* row, cudaStream_t s) {
   const int burn = solve_burn_rows(K);
-  const Geo G = make_geo(k_solve<T, K, TR>, 0, l.batch, l.n, burn, 2);
+  const size_t smem = sizeof(T) * solve_pf<K>() * (K + 2) * kThreads;  // the per-thread row ring
+  const Geo G = make_geo(k_solve<T, K, TR>, smem, l.batch, l.n, burn, 2);
   const ix units = G.batch * G.nseg;
   const size_t side = sizeof(T) * size_t(units) * K;
   Scratch ws;
@@ -964,7 +994,7 @@ bool run_solve(const bgm_band& l, const bgm_vec& v, const bgm_vec& x, int32_t* s
   k_singular<T><<<blocks_for(G.tiles * 32 * G.n, 256), 256, 0, s>>>(C.l, G.batch, TR, fail);
   {
     timing::Scope t(TR ? "narrow_solve_t" : "narrow_solve", s);
-    k_solve<T, K, TR><<<unsigned(G.tiles * G.nseg), kThreads, 0, s>>>(C, G);
+    k_solve<T, K, TR><<<unsigned(G.tiles * G.nseg), kThreads, smem, s>>>(C, G);
   }
   {
     timing::Scope t("narrow_solve_check", s);
@@ -973,12 +1003,12 @@ bool run_solve(const bgm_band& l, const bgm_vec& v, const bgm_vec& x, int32_t* s
   }
   {
     timing::Scope t("narrow_solve_fix", s);
-    k_solve_fix<T, K, TR><<<unsigned(G.tiles * G.nseg), kThreads, 0, s>>>(C, G, uflag, snap);
+    k_solve_fix<T, K, TR><<<unsigned(G.tiles * G.nseg), kThreads, smem, s>>>(C, G, uflag, snap);
     k_solve_recheck<T, K, TR><<<blocks_for(units, 128), 128, 0, s>>>(C, G, uflag, snap);
   }
   {
     timing::Scope t("narrow_solve_repair", s);
-    k_solve_repair<T, K, TR><<<blocks_for(G.batch, kThreads), kThreads, 0, s>>>(C, G);
+    k_solve_repair<T, K, TR><<<blocks_for(G.batch, kThreads), kThreads, smem, s>>>(C, G);
   }
   k_report<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, G.batch, G.n, BGM_ERR_SINGULAR, TR, st, row);
   return true;
