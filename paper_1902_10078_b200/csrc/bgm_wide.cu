@@ -488,12 +488,19 @@ struct SolveP {
 };
 
 constexpr int kSolveWarps = 4;  // units per CTA
-constexpr int kSolveRing = 8;   // columns in flight per unit
+#ifndef WSOLVE_RING64
+#define WSOLVE_RING64 12
+#endif
+// columns in flight per unit (static shared memory: 4 units x ring x (K+2) cells)
+template <int K>
+constexpr int solve_ring() {
+  return K <= 64 ? WSOLVE_RING64 : 8;
+}
 
 template <class T, int K, bool TR>
 __device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start, T* side, acc_t* win,
                            T (*ring)[K + 2]) {
-  constexpr int R = (K + 1 + 31) / 32, D = kSolveRing;
+  constexpr int R = (K + 1 + 31) / 32, D = solve_ring<K>();
   constexpr int M = (K + 2) <= 64 ? 64 : ((K + 2) <= 128 ? 128 : 256);  // window ring, power of two
   const int lane = threadIdx.x & 31;
   const Band<T>& L = C.l;
@@ -604,7 +611,7 @@ __device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start,
 template <class T, int K, bool TR>
 __global__ void __launch_bounds__(32 * kSolveWarps) k_solve(SolveP<T> C, Geo G) {
   __shared__ acc_t win[kSolveWarps][(K + 2) <= 64 ? 64 : ((K + 2) <= 128 ? 128 : 256)];
-  __shared__ T ring[kSolveWarps][kSolveRing][K + 2];
+  __shared__ T ring[kSolveWarps][solve_ring<K>()][K + 2];
   const int w = threadIdx.x >> 5;
   const ix unit = blockIdx.x * ix(kSolveWarps) + w;
   if (unit >= G.batch * G.nseg) return;  // whole warps
@@ -648,7 +655,7 @@ __global__ void k_solve_check(SolveP<T> C, Geo G) {
 template <class T, int K, bool TR>
 __global__ void __launch_bounds__(32 * kSolveWarps) k_solve_repair(SolveP<T> C, Geo G) {
   __shared__ acc_t win[kSolveWarps][(K + 2) <= 64 ? 64 : ((K + 2) <= 128 ? 128 : 256)];
-  __shared__ T ring[kSolveWarps][kSolveRing][K + 2];
+  __shared__ T ring[kSolveWarps][solve_ring<K>()][K + 2];
   const int w = threadIdx.x >> 5;
   const ix b = blockIdx.x * ix(kSolveWarps) + w;
   if (b >= G.batch || !C.flag[b]) return;  // whole warps
