@@ -259,6 +259,7 @@ struct SolveP {
   Vec<T> v, x;
   T* side;  // [unit][K]
   int32_t* flag;
+  int64_t* fail;  // singular pivots (first row forward, last row + 1 backward)
 };
 
 // Forward: res[a] = residual of row i+a; x_i = res[0] / L(i,i) (the
@@ -339,6 +340,7 @@ __device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start,
                    : "memory");
   };
   int same = 0;
+  ix sing = -1;  // pass 1 vets the pivots of its own rows (kernels.cpp:43-45)
   auto row = [&](ix i, const T* col, T vv) {
     T xi;
     if (!TR) {
@@ -356,6 +358,7 @@ __device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start,
       win[0] = xi;
     }
     if (i >= s && i < e) {
+      if (!carry && sing < 0 && dabs(col[0]) < kPivotFloor) sing = i;  // first met: lowest forward, highest backward
       if (carry) {  // fix-up: K consecutive rows equal to pass 1 => same state => pass 1 is exact onwards
         const T old = xb[i * 32];
         same = (__double_as_longlong(double(old)) == __double_as_longlong(double(xi))) ? same + 1 : 0;
@@ -385,6 +388,10 @@ __device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start,
     if (carry && same >= K) break;
   }
   cpa_wait();
+  if (sing >= 0) {
+    if (!TR) atomicMin(reinterpret_cast<unsigned long long*>(C.fail + b), static_cast<unsigned long long>(sing));
+    else atomicMax(reinterpret_cast<unsigned long long*>(C.fail + b), static_cast<unsigned long long>(sing + 1));
+  }
 }
 
 template <class T, int K, bool TR>
@@ -474,16 +481,6 @@ __global__ void k_solve_recheck(SolveP<T> C, Geo G, const int32_t* uflag, const 
   if (bad) C.flag[b] = 1;
 }
 
-template <class T>
-__global__ void k_singular(Band<T> l, ix batch, int tr, int64_t* fail) {
-  const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
-  ix b, i;
-  if (!split_bj(t, batch, l.n, l.s, b, i)) return;
-  if (dabs(l.cell(b, 0, i)) < kPivotFloor) {
-    if (!tr) atomicMin(reinterpret_cast<unsigned long long*>(fail + b), static_cast<unsigned long long>(i));
-    else atomicMax(reinterpret_cast<unsigned long long*>(fail + b), static_cast<unsigned long long>(i + 1));
-  }
-}
 
 // ------------------------------------------------------------------ subset
 // Column-form Takahashi (see bgm_wide.cu): window S over rows j+1 .. j+K,
@@ -989,9 +986,9 @@ bool run_solve(const bgm_band& l, const bgm_vec& v, const bgm_vec& x, int32_t* s
   T* snap = reinterpret_cast<T*>(ws.p + side);
   int64_t* fail = reinterpret_cast<int64_t*>(ws.p + (2 * side + 7) / 8 * 8);
   C.flag = reinterpret_cast<int32_t*>(fail + G.batch);
+  C.fail = fail;
   int32_t* uflag = C.flag + G.batch;
   k_init<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, C.flag, G.batch, TR ? 0 : G.n);
-  k_singular<T><<<blocks_for(G.tiles * 32 * G.n, 256), 256, 0, s>>>(C.l, G.batch, TR, fail);
   {
     timing::Scope t(TR ? "narrow_solve_t" : "narrow_solve", s);
     k_solve<T, K, TR><<<unsigned(G.tiles * G.nseg), kThreads, smem, s>>>(C, G);

@@ -702,12 +702,35 @@ __global__ void k_logdet_part(Band<T> l, ix batch, ix chunks, double* part, int6
   if (!split_bj(t, batch, chunks, l.s, b, c)) return;
   const ix i0 = c * kLogChunk;
   const ix i1 = i0 + kLogChunk < l.n ? i0 + kLogChunk : l.n;
-  double acc = 0.0;
+  // sum of logs as one log of a product: each pivot splits into 2^e * m with
+  // m in [1/sqrt2, sqrt2) (bit fields), the m multiply (|log prod| <= 23 for
+  // 64 rows), so one libdevice log per chunk instead of one per row; zero,
+  // negative, subnormal, inf and NaN pivots take the per-row loop
+  double prod = 1.0;
+  int esum = 0;
   ix bad = -1;
+  bool slow = false;
+#pragma unroll 8
   for (ix i = i0; i < i1; ++i) {
     const double d = double(l.cell(b, 0, i));
-    if (!(d > 0.0) && bad < 0) bad = i;
-    acc += log(d);
+    const int hi = __double2hiint(d);
+    const int ex = (hi >> 20) & 0x7ff;
+    slow |= (hi < 0) | (ex == 0) | (ex == 0x7ff);
+    // mantissa with exponent 0 (in [1, 2)); halve it above sqrt 2
+    const int top = hi & 0x000fffff;
+    const bool up = top >= 0x6a09e;  // 1.4142... = 0x3ff6a09e...
+    const double m = __hiloint2double(top | (up ? 0x3fe00000 : 0x3ff00000), __double2loint(d));
+    esum += ex - 1023 + (up ? 1 : 0);
+    prod *= m;
+  }
+  double acc = fma(double(esum), 0.6931471805599453094, log(prod));
+  if (slow) {
+    acc = 0.0;
+    for (ix i = i0; i < i1; ++i) {
+      const double d = double(l.cell(b, 0, i));
+      if (!(d > 0.0) && bad < 0) bad = i;
+      acc += log(d);
+    }
   }
   part[b * chunks + c] = acc;
   if (bad >= 0) atomicMin(reinterpret_cast<unsigned long long*>(fail + b), static_cast<unsigned long long>(bad));

@@ -60,6 +60,30 @@ def test_error_rows(gpu):
     assert st[0] == 3 and row[0] == 1
 
 
+def test_log_det_pivot_ranges(gpu, oracle):
+    """log_det sums one log of a mantissa product per 64-row chunk: pivots
+    across the whole exponent range, near 1 (small log-det), exactly at the
+    sqrt 2 mantissa split, and chunks with subnormal / inf pivots (the per-row
+    loop) against the reference's per-row sum."""
+    rng = np.random.default_rng(11)
+    B, n = 6, 300
+    l = np.zeros((B, n, 3))
+    l[0, :, 0] = 10.0 ** rng.uniform(-300, 300, n)
+    l[1, :, 0] = 1.0 + rng.uniform(-1e-3, 1e-3, n)
+    l[2, :, 0] = np.sqrt(2.0) * (1.0 + rng.choice([-1, 0, 1], n) * 2.0 ** -52)
+    l[3, :, 0] = rng.uniform(0.5, 2.0, n)
+    l[3, 70, 0] = 5e-320  # subnormal: the chunk's per-row loop
+    l[4, :, 0] = rng.uniform(0.1, 10.0, n)
+    l[4, 200, 0] = np.inf
+    l[5, :, 0] = 2.0 ** rng.integers(-1000, 1000, n)
+    got, st, _ = gpu.log_det(l)
+    want, st_o, _ = oracle.log_det(l)
+    assert np.array_equal(st, st_o)
+    for b in (0, 1, 2, 3, 5):
+        assert abs(got[b] - want[b]) <= 1e-12 * max(1.0, np.abs(np.log(l[b, :, 0])).sum()), b
+    assert np.isinf(got[4]) and np.isinf(want[4])
+
+
 def test_known_answers(gpu):
     l, st, _ = gpu.cholesky(np.array([[[4.0, 2.0], [5.0, 0.0]]]))
     assert np.allclose(l[0], [[2.0, 1.0], [2.0, 0.0]], rtol=0, atol=1e-15)
