@@ -70,7 +70,7 @@ struct FwdP {
   const double* y;  // tile 32
   double* lp;       // Lp scratch (tile 32), storage row 0 = 1/Lp(i,i)
   double* w;        // w = Lp^-1 y (tile 32)
-  double* side;     // [unit][SIDE]
+  double* side;     // [tile][segment][SIDE][lane]: coalesced for the writer and the check
   double* part;     // [unit][4]
   int64_t* fail;
   int32_t* flag;    // [batch] matrices for the exact single-unit repair
@@ -215,11 +215,11 @@ __device__ void fwd_unit(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, d
         el += x;
       }
     } else if (side && i >= s - K) {
-      double* sd = side + (i - (s - K)) * (W + 1);
+      double* sd = side + (i - (s - K)) * (W + 1) * 32;
       sd[0] = rs;
 #pragma unroll
-      for (int a = 1; a < W; ++a) sd[a] = c[a];
-      sd[W] = wi;
+      for (int a = 1; a < W; ++a) sd[a * 32] = c[a];
+      sd[W * 32] = wi;
     }
   };
   auto take_y = [&](ix r, double v) {
@@ -393,7 +393,7 @@ __global__ void k_fwd(FwdP P, Geo G) {
   const ix s = ix(u.p) * G.seg;
   const ix e = s + G.seg < G.n ? s + G.seg : G.n;
   const ix i0 = s - G.burn > 0 ? s - G.burn : 0;
-  fwd_unit<K, false>(P, G, u.b, s, e, i0, u.p > 0 ? P.side + u.id * Shape<K>::SIDE : nullptr,
+  fwd_unit<K, false>(P, G, u.b, s, e, i0, u.p > 0 ? P.side + (gt >> 5) * Shape<K>::SIDE * 32 + (gt & 31) : nullptr,
                      P.part + u.id * 4, sm + threadIdx.x, true, nullptr,
                      u.p + 1 < G.nseg ? P.exitf + u.id * Shape<K>::STATEF : nullptr);
 }
@@ -432,41 +432,43 @@ __global__ void k_recheck(const int32_t* uflag, const double* before, const doub
   if (bad) flag[id / G.nseg] = 1;
 }
 
+__device__ __noinline__ void check_fwd_report(ix b, int p, ix col, const double* sd, const double* lp, double w,
+                                              int W) {
+  for (int r = 0; r <= W; ++r)
+    printf("t1 fwd check b=%lld p=%d col=%lld r=%d burn=%.17g real=%.17g\n", (long long)b, p, (long long)col, r,
+           sd[r * 32], r < W ? lp[r * 32] : w);
+}
+
 // One thread per (unit, column): the burn-in copy of the K columns before
-// the segment must equal the neighbour's genuine columns.
+// the segment must equal the neighbour's genuine columns.  Thread layout
+// [tile][segment][column][lane], so every read is one 256-byte warp access.
 template <int K>
 __global__ void k_check_fwd(FwdP P, Geo G) {
   using Sh = Shape<K>;
   constexpr int W = Sh::W;
   const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
-  const ix id = t / K;  // unit id = b * nseg + p
-  const int c = int(t % K);
-  if (id >= G.batch * G.nseg) return;
-  const int p = int(id % G.nseg);
-  if (p == 0) return;
-  const ix b = id / G.nseg, n = G.n, s = ix(p) * G.seg;
-  const double* sd = P.side + id * Sh::SIDE + c * (W + 1);
+  const ix warp = t >> 5;  // (tile * nseg + p) * K + c
+  const int c = int(warp % K);
+  const ix tp = warp / K;
+  const int p = int(tp % G.nseg);
+  const ix b = (tp / G.nseg) * 32 + (t & 31);
+  if (b >= G.batch || p == 0) return;
+  const ix id = b * G.nseg + p, n = G.n, s = ix(p) * G.seg;
+  const double* sd = P.side + tp * Sh::SIDE * 32 + c * (W + 1) * 32 + (t & 31);
   double wscale = 0.0;
   for (int q = 0; q < K; ++q) wscale = fmax(wscale, fabs(P.w[voff(b, n, s - K + q)]));
   const ix col = s - K + c;
-  double ref[W + 1], sc = 0.0;
+  const double* lp = P.lp + boff(b, n, W, col, 0);
+  double sc = 0.0;
 #pragma unroll
-  for (int r = 0; r < W; ++r) {
-    ref[r] = P.lp[boff(b, n, W, col, r)];
-    sc = fmax(sc, fabs(ref[r]));
-  }
-  ref[W] = P.w[voff(b, n, col)];
-  bool bad = false;
+  for (int r = 0; r < W; ++r) sc = fmax(sc, fabs(lp[r * 32]));
+  // |burn - real| <= tol * scale, without a division per cell; the second
+  // read of the column hits L1 (keeps the kernel at ~40 registers)
+  const double tl = kCheckTol * (sc + 1e-300);
+  bool bad = !(fabs(sd[W * 32] - P.w[voff(b, n, col)]) <= kCheckTol * (wscale + 1e-300));
 #pragma unroll
-  for (int r = 0; r <= W; ++r) {
-    const double rel = fabs(sd[r] - ref[r]) / ((r < W ? sc : wscale) + 1e-300);
-    if (!(rel <= kCheckTol)) {
-      if (G.debug && !bad)
-        printf("t1 fwd check b=%lld p=%d col=%lld r=%d burn=%.17g real=%.17g\n", (long long)b, p,
-               (long long)col, r, sd[r], ref[r]);
-      bad = true;
-    }
-  }
+  for (int r = 0; r < W; ++r) bad |= !(fabs(sd[r * 32] - lp[r * 32]) <= tl);
+  if (bad && G.debug) check_fwd_report(b, p, col, sd, lp, P.w[voff(b, n, col)], W);
   if (bad) P.uflag[id] = 1;
 }
 
@@ -682,8 +684,7 @@ __global__ void k_check_bwd(BwdP P, Geo G) {
   us = warp_max(us);
   bool bad = false;
   for (int q = lane; q < Sh::STATE; q += 32) {
-    const double rel = fabs(a[q] - r[q]) / ((q < Sh::NB ? ss : us) + 1e-300);
-    if (!(rel <= kCheckTol)) {
+    if (!(fabs(a[q] - r[q]) <= kCheckTol * ((q < Sh::NB ? ss : us) + 1e-300))) {
       if (G.debug && !bad)
         printf("t1 bwd check b=%lld p=%d slot=%d burn=%.17g real=%.17g\n", (long long)b, p, q, a[q],
                r[q]);
@@ -795,7 +796,7 @@ int run(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, const bg
   const ix uf = G.batch * Gf.nseg, ub = G.batch * Gb.nseg;
 
   const size_t nb = size_t(G.tiles) * 32 * size_t(G.n);
-  const size_t bytes = sizeof(double) * (nb * Sh::W + nb + size_t(uf) * (Sh::SIDE + 4 + 2 * Sh::STATEF) +
+  const size_t bytes = sizeof(double) * (nb * Sh::W + nb + size_t(uf) * (4 + 2 * Sh::STATEF) + size_t(G.tiles) * 32 * Gf.nseg * Sh::SIDE +
                                          size_t(ub) * (3 * Sh::STATE + 2)) +
                        sizeof(int64_t) * size_t(G.batch) + sizeof(int32_t) * (2 * size_t(G.batch) + uf + ub) + 256;
   char* ws = nullptr;
@@ -811,7 +812,7 @@ int run(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, const bg
   F.w = dp;
   dp += nb;
   F.side = dp;
-  dp += size_t(uf) * Sh::SIDE;
+  dp += size_t(G.tiles) * 32 * Gf.nseg * Sh::SIDE;
   F.part = dp;
   dp += size_t(uf) * 4;
   Bp.entry = dp;
@@ -851,7 +852,7 @@ int run(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, const bg
   }
   {
     timing::Scope ts("mlik_check_fwd", s);
-    k_check_fwd<K><<<unsigned((uf * K + 127) / 128), 128, 0, s>>>(F, Gf);
+    k_check_fwd<K><<<unsigned((ix(G.tiles) * Gf.nseg * K * 32 + 127) / 128), 128, 0, s>>>(F, Gf);
   }
   {
     timing::Scope ts("mlik_fix_fwd", s);
