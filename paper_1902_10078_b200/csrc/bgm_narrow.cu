@@ -593,13 +593,19 @@ __global__ void k_subset_repair(SubP<T> C, Geo G) {
   subset_unit<T, K>(C, b, G.n, 0, G.n, G.n - 1, nullptr, sm + threadIdx.x);
 }
 
+// First pivot below the floor per matrix: thread per (matrix, 64-row chunk),
+// one index split per thread (not per element), one atomic per chunk.
 template <class T>
-__global__ void k_diag_small(Band<T> l, ix batch, int64_t* fail) {
+__global__ void k_diag_small(Band<T> l, ix batch, ix chunks, int64_t* fail) {
   const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
-  ix b, i;
-  if (!split_bj(t, batch, l.n, l.s, b, i)) return;
-  if (dabs(l.cell(b, 0, i)) < kPivotFloor)
-    atomicMin(reinterpret_cast<unsigned long long*>(fail + b), static_cast<unsigned long long>(i));
+  ix b, c;
+  if (!split_bj(t, batch, chunks, l.s, b, c)) return;
+  const ix i1 = (c + 1) * 64 < l.n ? (c + 1) * 64 : l.n;
+  ix bad = -1;
+#pragma unroll 8
+  for (ix i = c * 64; i < i1; ++i)
+    if (bad < 0 && dabs(l.cell(b, 0, i)) < kPivotFloor) bad = i;
+  if (bad >= 0) atomicMin(reinterpret_cast<unsigned long long*>(fail + b), static_cast<unsigned long long>(bad));
 }
 
 // ------------------------------------------------------------------ vjp_cholesky
@@ -1034,7 +1040,8 @@ bool run_subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row
   int64_t* fail = reinterpret_cast<int64_t*>(ws.p + (side + 7) / 8 * 8);
   C.flag = reinterpret_cast<int32_t*>(fail + G.batch);
   k_init<<<blocks_for(G.batch, 128), 128, 0, s>>>(fail, C.flag, G.batch, G.n);
-  k_diag_small<T><<<blocks_for(G.tiles * 32 * G.n, 256), 256, 0, s>>>(C.l, G.batch, fail);
+  const ix dchunks = (G.n + 63) / 64;
+  k_diag_small<T><<<blocks_for(G.tiles * 32 * dchunks, 256), 256, 0, s>>>(C.l, G.batch, dchunks, fail);
   {
     timing::Scope t("narrow_subset", s);
     k_subset<T, K><<<unsigned(G.tiles * G.nseg), kThreads, smem, s>>>(C, G);
