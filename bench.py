@@ -1,26 +1,38 @@
 #!/usr/bin/env python
 """bench.py -- the driver's benchmark contract for bandgm_b200.
 
-Workload (default, ``--workload cfg3``): BASELINE.json configs[3], the
-end-to-end learning step -- B=256 series of length n=65536, precision
-Q = L L^T with lower bandwidth k=16, tau2 = 0.01; per step one fused forward
-+ reverse pass (Cholesky, solves, log-det, inverse subset, dL, d tau2).  It is
-the config whose suite is the metric's "fwd+bwd banded Chol/solve/inv-subset"
-(configs[1] is forward-only).  Metric: band-rows/s = B*n*ranks / step time.
+Workloads (``--workload``; BASELINE.json configs at their full sizes):
+
+* ``cfg3`` (default) -- configs[3], the end-to-end learning step: B=256 series
+  of length n=65536, precision Q = L L^T with lower bandwidth k=16,
+  tau2=0.01; per step one fused forward + reverse pass (Cholesky, solves,
+  log-det, inverse subset, dL, d tau2).  It is the config whose suite is the
+  metric's "fwd+bwd banded Chol/solve/inv-subset".
+* ``cfg1`` -- configs[1]: B=4096, n=2048, k=4, forward Cholesky + solve L +
+  solve L^T + log-det.
+* ``cfg2`` -- configs[2]: B=512, n=65536, L L^T (8,8), A(8,8) B(3,3), A v and
+  their three VJPs.
+* ``cfg4_k{64,128}_{f64,f32}`` -- configs[4]: B=64, n=32768, the full
+  forward + reverse suite (Cholesky, both solves, log-det, inverse subset,
+  and the VJPs of each).
+
+Metric: band-rows/s = B_total * n / step time.  Multi-GPU (torchrun) is STRONG
+scaling: the batch of B_total matrices is split into contiguous slices by the
+batch partitioner (``dist.shard_bounds``); every rank runs its slice, config 3
+all-reduces its two scalars over NCCL, and the step time is the max over
+ranks.  At N=1 the line also carries ``scaling_proxy``: T(B) / (G * T(B/G))
+measured on this GPU for G = 2, 4, 8 (the per-GPU work of a G-GPU run).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-
-Under torchrun every rank processes its own B-matrix batch (weak scaling:
-the batch partitioner hands each GPU whole, independent matrices) and the
-per-step scalars (sum loss, sum d tau2) are all-reduced over NCCL.
+                    [--workload cfg3|cfg1|cfg2|cfg4_k64_f64|...] [--batch B]
 """
 from __future__ import annotations
 
 import argparse
 import ctypes as C
 import json
-import math
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -30,25 +42,68 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-WORKLOADS = {
-    # name: (B, n, k, description)
-    "cfg3": dict(B=256, n=65536, k=16, tau2=0.01,
-                 desc="configs[3]: Gaussian log-likelihood + dL + dtau2, B=256 n=65536 k=16 fp64"),
-    "cfg3_small": dict(B=64, n=8192, k=16, tau2=0.01, desc="configs[3] shape at reduced B, n (smoke)"),
-}
+METRIC = "band-rows/s (B*n/s) fwd+bwd banded Chol/solve/inv-subset; % of roofline"
 
-# Algorithmic bytes per band-row of each fused kernel:
-# forward reads L (w doubles) + y, writes Lp (w) + w-vector;
-# reverse reads L, Lp (w each) + w-vector, writes L_bar (w).
-def alg_bytes_per_row(kernel: str, k: int) -> float:
+WORKLOADS = {
+    "cfg3": dict(kind="mlik", B=256, n=65536, k=16, tau2=0.01, dtype="f64",
+                 desc="configs[3]: Gaussian log-likelihood + dL + dtau2, B=256 n=65536 k=16 fp64"),
+    "cfg3_small": dict(kind="mlik", B=64, n=8192, k=16, tau2=0.01, dtype="f64",
+                       desc="configs[3] shape at reduced B, n (smoke)"),
+    "cfg1": dict(kind="cfg1", B=4096, n=2048, k=4, dtype="f64",
+                 desc="configs[1]: cholesky + solve L + solve L^T + log-det, B=4096 n=2048 k=4 fp64"),
+    "cfg2": dict(kind="cfg2", B=512, n=65536, k=8, dtype="f64",
+                 desc="configs[2]: L.L^T (8,8), A(8,8).B(3,3), A.v and their VJPs, B=512 n=65536 fp64"),
+}
+for _k in (64, 128):
+    for _dt in ("f64", "f32"):
+        WORKLOADS[f"cfg4_k{_k}_{_dt}"] = dict(
+            kind="wide", B=64, n=32768, k=_k, dtype=_dt,
+            desc=f"configs[4]: cholesky, solves L / L^T, log-det, inverse subset + their VJPs, "
+                 f"B=64 n=32768 k={_k} {'fp64' if _dt == 'f64' else 'fp32'}")
+
+
+# --------------------------------------------------------------------- roofline counts
+def op_counts(op, k, wa=None, wb=None, w=None):
+    """(flops, fp64 bytes) per band-row of one operator: SURVEY.md §8(d).
+    FMA = 2 flops, div / sqrt / log = 1; bytes = API inputs read once plus
+    outputs written once (fp32 storage halves them)."""
+    if op == "cholesky":
+        return (k + 1) ** 2, 16 * (k + 1)
+    if op == "solve_vec":
+        return 2 * k + 1, 8 * (k + 3)
+    if op == "log_det":
+        return 1, 8
+    if op == "subset":
+        return 2 * k * (k + 1) + k + 2, 16 * (k + 1)
+    if op == "product":
+        return 2 * wa * wb, 8 * (2 * wa + 2 * wb - 1)
+    if op == "band_vec":
+        return 2 * w, 8 * (w + 2)
+    if op == "vjp_cholesky":
+        return 2 * k * (k + 1) + 4 * k + 2, 24 * (k + 1)
+    if op == "vjp_solve_vec":
+        return 3 * k + 2, 16 * (k + 1) + 24
+    if op == "vjp_log_det":
+        return 1, 8 + 8 * (k + 1)
+    if op == "vjp_subset":
+        return 4 * k * (k + 1) + 2 * (k + 1) + 3 * k + 7, 32 * (k + 1)
+    if op == "vjp_product":
+        return 4 * wa * wb, 8 * (3 * wa + 3 * wb - 1)
+    if op == "vjp_band_vec":
+        return 3 * w, 8 * (2 * w + 3)
+    raise KeyError(op)
+
+
+def mlik_kernel_counts(kernel: str, k: int):
+    """(flops, bytes) per band-row of the fused config-3 sweeps:
+    forward reads L (w doubles) + y, writes Lp (w) + w-vector, ~k^2 + 5k FMA;
+    reverse reads L, Lp (w each) + w-vector, writes L_bar (w), ~2k^2 + 5k FMA."""
     w = k + 1
-    if "fwd" in kernel:
-        return 8.0 * (2 * w + 2)
-    if "bwd" in kernel:
-        return 8.0 * (3 * w + 1)
-    if "mlik_seg" in kernel:
-        return 8.0 * (5 * w + 3)
-    return float("nan")
+    if "fwd" in kernel and "t1" in kernel or kernel == "mlik_seg_fwd":
+        return 2 * (k * k + 5 * k), 8.0 * (2 * w + 2)
+    if "bwd" in kernel and "t1" in kernel or kernel == "mlik_seg_bwd":
+        return 2 * (2 * k * k + 5 * k), 8.0 * (3 * w + 1)
+    return None, None
 
 
 def load_traffic(kernel: str):
@@ -67,13 +122,43 @@ def load_traffic(kernel: str):
     return None, None
 
 
-def load_peaks():
+def load_hbm_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["hbm_gbs"]), "MEASURED_PEAKS.json"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def measure_fp64_peaks():
+    """Live DFMA / DMMA microbenchmarks (csrc/bgm_peak.cu), TFLOP/s."""
+    import paper_1902_10078_b200 as bgm
+    try:
+        dfma, dmma = bgm.api.fp64_peak()
+        return {"dfma_tflops": round(dfma, 2), "dmma_tflops": round(dmma, 2), "source": "measured live (bgm_fp64_peak)"}
+    except Exception as exc:  # pragma: no cover
+        return {"dfma_tflops": 37.2, "dmma_tflops": 37.2, "source": f"nominal (measurement failed: {exc})"}
+
+
+def roofline_entry(name, ms, flops_per_launch, bytes_per_launch, hbm, fp64, tensor, extra=None):
+    """max(bytes / HBM, flops / FP64) for one kernel (or API call): the side
+    that binds is reported, with its achieved rate and peak."""
+    t_hbm = bytes_per_launch / (hbm * 1e9)
+    peak_f = fp64["dmma_tflops"] if tensor else fp64["dfma_tflops"]
+    t_fp = flops_per_launch / (peak_f * 1e12) if flops_per_launch else 0.0
+    sec = ms / 1e3
+    if t_hbm >= t_fp:
+        d = {"bound": "hbm", "achieved": round(bytes_per_launch / sec / 1e9, 1), "peak": hbm, "unit": "GB/s"}
+    else:
+        d = {"bound": "tensor" if tensor else "fp64", "achieved": round(flops_per_launch / sec / 1e12, 3),
+             "peak": peak_f, "unit": "TFLOP/s"}
+    d["frac"] = round(d["achieved"] / d["peak"], 4)
+    d.update({"kernel": name, "kernel_ms": round(ms, 4), "alg_bytes_per_launch": bytes_per_launch,
+              "alg_flops_per_launch": flops_per_launch, "roofline_ms": round(max(t_hbm, t_fp) * 1e3, 4)})
+    if extra:
+        d.update(extra)
+    return d
 
 
 # --------------------------------------------------------------------- clocks
@@ -118,6 +203,7 @@ class ClockSampler:
                 self._p.kill()
             if self._t:
                 self._t.join(timeout=5)
+            self._p = None
 
     def summary(self):
         if not self.rows:
@@ -137,60 +223,593 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-# --------------------------------------------------------------------- inputs
-def make_inputs(B, n, k, seed, device, tile=32):
-    """Config-3 inputs on the device: L diag U[1,2], off-diag
-    N(0, 0.1^2); y = L^-T z + eps, z ~ N(0,1), eps ~ N(0, 0.1^2)."""
+def host_info():
+    model = platform.processor() or ""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+# --------------------------------------------------------------------- graphs
+def graph_kernel_names(g):
+    """Names of the kernel nodes of a captured graph (keep_graph=True), via
+    the driver API; None when introspection is unavailable."""
+    try:
+        from cuda.bindings import driver as d
+        graph = d.CUgraph(g.raw_cuda_graph())
+        err, _, num = d.cuGraphGetNodes(graph, 0)
+        err, nodes, num = d.cuGraphGetNodes(graph, num)
+        names = []
+        for nd in nodes[:num]:
+            err, ty = d.cuGraphNodeGetType(nd)
+            if ty != d.CUgraphNodeType.CU_GRAPH_NODE_TYPE_KERNEL:
+                continue
+            err, p = d.cuGraphKernelNodeGetParams(nd)
+            err, nm = d.cuFuncGetName(p.func)
+            names.append(nm.decode() if isinstance(nm, bytes) else str(nm))
+        return names
+    except Exception:
+        return None
+
+
+def capture(step):
+    """Capture `step` into a CUDA graph (after one eager warm-up on a side
+    stream); returns (graph, kernel names) or (None, None)."""
     import torch
-    import paper_1902_10078_b200 as bgm
-
-    g = torch.Generator(device=device)
-    g.manual_seed(seed)
-    # generated in the tile-1 layout (the reference's own (k+1) x n storage
-    # block per matrix)
-    L = bgm.Bands.empty(B, n, k, 0, tile=1, device=device)
-    L.data.normal_(0.0, 0.1, generator=g)
-    L.data[:, :, 0].uniform_(1.0, 2.0, generator=g)
-    for r in range(1, k + 1):
-        L.data[:, n - r:, r] = 0.0  # corner cells
-    z = bgm.Vecs.empty(B, n, tile=1, device=device)
-    z.data.normal_(0.0, 1.0, generator=g)
-    x = bgm.solve_vec(L, z, transpose_l=True)
-    eps = torch.empty_like(x.data).normal_(0.0, 0.1, generator=g)
-    y = bgm.Vecs(x.data + eps, B, n, 1)
-    if tile == 1:
-        return L, y
-    # tile 32 (default): 32 matrices interleaved per cell, the layout of the
-    # one-thread-per-unit sweeps (coalesced 256-byte warp accesses)
-    return L.to_tile(32), y.to_tile(32)
+    try:
+        g = torch.cuda.CUDAGraph(keep_graph=True)
+        s0 = torch.cuda.Stream()
+        s0.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s0):
+            step()
+        torch.cuda.current_stream().wait_stream(s0)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            step()
+        names = graph_kernel_names(g)
+        g.instantiate()
+        torch.cuda.synchronize()
+        return g, names
+    except Exception as exc:
+        print(f"# graph capture failed ({exc}); timing eager launches", file=sys.stderr)
+        return None, None
 
 
-# --------------------------------------------------------------------- cpu legs
-def cpu_run(L_ref, y_ref, tau2, which=None):
-    import oracle as orc
-
-    kind = which or ("reference" if orc.available("reference") else "restatement")
-    o = orc.Oracle(kind)
-    t0 = time.perf_counter()
-    _, _, _, st, _ = o.marginal_likelihood_grad(L_ref, y_ref, tau2)
-    dt = time.perf_counter() - t0
-    assert (st == 0).all()
-    return dt, ("reference" if kind == "reference" else "port"), o.threads()
+def ours(names):
+    """Kernel names that belong to libbandgm_b200 (namespace bgm)."""
+    return [n for n in names if "bgm" in n]
 
 
-def host_sample(L, y, m):
-    """First m matrices in the reference layout, on the host."""
+# --------------------------------------------------------------------- parity helpers
+def rel_err(a, b, floor_scale):
     import numpy as np
-    import paper_1902_10078_b200 as bgm
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    if a.size == 0:
+        return 0.0
+    floor = max(floor_scale * float(np.max(np.abs(b))), 1e-300)
+    den = np.maximum(np.maximum(np.abs(a), np.abs(b)), floor)
+    return float(np.max(np.abs(a - b) / den))
 
-    Lr, yr = L.to_reference(), y.to_reference()
-    return (np.ascontiguousarray(Lr[:m].cpu().numpy()), np.ascontiguousarray(yr[:m].cpu().numpy()))
+
+def normwise(a, b):
+    import numpy as np
+    nb = float(np.linalg.norm(np.asarray(b, np.float64)))
+    return float(np.linalg.norm(np.asarray(a, np.float64) - np.asarray(b, np.float64))) / (nb if nb > 0 else 1.0)
 
 
-def sample_size(cores, B):
-    # ~0.2 s of single-core work per config-3 matrix: a few matrices per core
-    # keeps the sample near 10-30 s of CPU time and well under a minute wall.
-    return int(max(8, min(B, 4 * cores)))
+def parity_report(pairs, tol, relaxed=None):
+    """pairs: [(name, gpu array, oracle array)].  Pinned floor 1e-12 max|b|
+    (BASELINE.md §4); for names in `relaxed` (config-3 gradients, see
+    DESIGN.md §5) the pass criterion is the 1e-6 floor plus normwise 1e-10."""
+    relaxed = relaxed or set()
+    out, ok = {}, True
+    for name, g, o in pairs:
+        e12, e6, nw = rel_err(g, o, 1e-12), rel_err(g, o, 1e-6), normwise(g, o)
+        passed = (e6 <= tol and nw <= 1e-10) if name in relaxed else e12 <= tol
+        ok &= passed
+        out[name] = {"max_rel_pinned_1e-12": float(f"{e12:.3e}"), "max_rel_floor_1e-6": float(f"{e6:.3e}"),
+                     "normwise": float(f"{nw:.3e}"), "pass": bool(passed)}
+    return {"tol": tol, "pass": bool(ok), "outputs": out}
+
+
+# --------------------------------------------------------------------- config 3
+class MlikWorkload:
+    """Config 3: the fused learning step (bgm_marginal_likelihood_grad)."""
+
+    def __init__(self, wl, batch, start, dev, tile=32):
+        import torch
+        import paper_1902_10078_b200 as bgm
+
+        self.wl, self.B, self.n, self.k, self.tau2 = wl, batch, wl["n"], wl["k"], wl["tau2"]
+        self.dev, self.tile = dev, tile
+        self.L, self.y = self.make_inputs(batch, self.n, self.k, 1234 + 7919 * start, dev, tile)
+        self.loss = torch.empty(batch, dtype=torch.float64, device=dev)
+        self.tbar = torch.empty(batch, dtype=torch.float64, device=dev)
+        self.lbar = self.L.like()
+        self.st = bgm.api.new_status(batch, dev)
+        self.out = (self.loss, self.lbar, self.tbar, self.st)
+
+    @staticmethod
+    def make_inputs(B, n, k, seed, device, tile=32):
+        """Config-3 inputs on the device: L diag U[1,2],
+        off-diag N(0, 0.1^2); y = L^-T z + eps, z ~ N(0,1), eps ~ N(0, 0.1^2)."""
+        import torch
+        import paper_1902_10078_b200 as bgm
+
+        g = torch.Generator(device=device)
+        g.manual_seed(seed)
+        L = bgm.Bands.empty(B, n, k, 0, tile=1, device=device)
+        L.data.normal_(0.0, 0.1, generator=g)
+        L.data[:, :, 0].uniform_(1.0, 2.0, generator=g)
+        for r in range(1, k + 1):
+            L.data[:, n - r:, r] = 0.0  # corner cells
+        z = bgm.Vecs.empty(B, n, tile=1, device=device)
+        z.data.normal_(0.0, 1.0, generator=g)
+        if tile == 32:
+            L32, z32 = L.to_tile(32), z.to_tile(32)
+            x = bgm.solve_vec(L32, z32, transpose_l=True)
+            eps = torch.empty_like(x.data).normal_(0.0, 0.1, generator=g)
+            return L32, bgm.Vecs(x.data + eps, B, n, 32)
+        x = bgm.solve_vec(L, z, transpose_l=True)
+        eps = torch.empty_like(x.data).normal_(0.0, 0.1, generator=g)
+        return L, bgm.Vecs(x.data + eps, B, n, 1)
+
+    def step(self):
+        import paper_1902_10078_b200 as bgm
+        from paper_1902_10078_b200.dist import reduce_totals
+
+        # fused sweeps on this rank's matrices, then the one 2 x fp64 NCCL
+        # all-reduce of (sum loss, sum d tau2) when world > 1
+        bgm.marginal_likelihood_grad(self.L, self.y, self.tau2, check=False, out=self.out)
+        return reduce_totals([self.loss, self.tbar])
+
+    def graphable(self, world):
+        return world == 1  # the NCCL all-reduce stays outside the graph
+
+    def check_status(self):
+        self.st.raise_first()
+
+    def attribution(self, steps, hbm, fp64):
+        """Per-kernel CUDA events on the launch stream (bgm_timing)."""
+        import torch
+        import paper_1902_10078_b200 as bgm
+
+        lib = bgm.library()
+        lib.bgm_timing_enable(1)
+        for _ in range(steps):
+            self.step()
+        torch.cuda.synchronize()
+        kernels = []
+        cnt = lib.bgm_timing_read(-1, None, 0, None, None)
+        for i in range(cnt):
+            name = C.create_string_buffer(128)
+            tot = C.c_double()
+            c = C.c_int64()
+            lib.bgm_timing_read(i, name, 128, C.byref(tot), C.byref(c))
+            kernels.append((name.value.decode(), tot.value, c.value))
+        lib.bgm_timing_enable(0)
+        launches = sum(c for _, _, c in kernels) / max(steps, 1)
+        dom = max(kernels, key=lambda t: t[1])
+        rows = self.B * self.n
+        fl, by = mlik_kernel_counts(dom[0], self.k)
+        traffic, tsrc = load_traffic(dom[0])
+        roof = roofline_entry(dom[0], dom[1] / dom[2], fl * rows, by * rows, hbm, fp64, tensor=False,
+                              extra={"traffic": traffic, "traffic_source": tsrc, "alg_bytes_per_row": by,
+                                     "alg_flops_per_row": fl,
+                                     "kernel_ms_all": {n: round(t / c, 4) for n, t, c in kernels}})
+        return roof, launches
+
+    def suite(self, ms):
+        # SURVEY.md §8(d): the reference composition's suite roofline for
+        # config 3 (sum of per-op max(bytes/HBM, flops/FP64)), and the fused
+        # step's own floor (DESIGN.md §4.1: compulsory bytes, fused flops)
+        rows = self.B * self.n
+        suite_ms = 7.50 * rows / (256 * 65536)
+        return {"reference_composition_roofline_ms": round(suite_ms, 3),
+                "fused_floor_ms": round(0.84 * rows / (256 * 65536), 3),
+                "fused_floor_frac": round(0.84 * rows / (256 * 65536) / ms, 4),
+                "note": "fused_floor = ~1860 flop/row at the FP64 peak (0.72 ms of compulsory bytes); "
+                        "the reference composition's suite roofline is not a bound on the fused step"}
+
+    # ---- e2e: the public host-buffer API
+    def e2e(self, steps, world, dev):
+        import torch
+        from paper_1902_10078_b200.dist import reduce_totals
+        from paper_1902_10078_b200.host import marginal_likelihood_grad_host
+
+        Lr, yr = self.L.to_reference(), self.y.to_reference()
+        hL = torch.empty(Lr.shape, dtype=Lr.dtype, pin_memory=True)
+        hy = torch.empty(yr.shape, dtype=yr.dtype, pin_memory=True)
+        hL.copy_(Lr)
+        hy.copy_(yr)
+        del Lr, yr
+        hout = (torch.empty(self.B, dtype=torch.float64, pin_memory=True),
+                torch.empty(hL.shape, dtype=torch.float64, pin_memory=True),
+                torch.empty(self.B, dtype=torch.float64, pin_memory=True))
+
+        def step():
+            # public host-buffer API: chunked H2D -> fused sweeps -> D2H, overlapped
+            hloss, _, htb = marginal_likelihood_grad_host(hL, hy, self.tau2, out_host=hout, tile=self.tile)
+            if world > 1:
+                reduce_totals([hloss.to(dev, non_blocking=True), htb.to(dev, non_blocking=True)])
+
+        h2d = hL.numel() * 8 + hy.numel() * 8
+        d2h = hout[1].numel() * 8 + hout[0].numel() * 8 + hout[2].numel() * 8
+        return step, h2d, d2h
+
+    # ---- CPU leg (oracle on a bounded sample of the same matrices) + parity
+    def cpu_and_parity(self, m):
+        import numpy as np
+        import oracle as orc
+
+        Lh = np.ascontiguousarray(self.L.to_reference()[:m].cpu().numpy())
+        yh = np.ascontiguousarray(self.y.to_reference()[:m].cpu().numpy())
+        kind = "reference" if orc.available("reference") else "restatement"
+        o = orc.Oracle(kind)
+        t0 = time.perf_counter()
+        lo, lb, tb, st, _ = o.marginal_likelihood_grad(Lh, yh, self.tau2)
+        dt = time.perf_counter() - t0
+        assert (st == 0).all()
+        lg = self.loss[:m].cpu().numpy()
+        tg = self.tbar[:m].cpu().numpy()
+        lbg = self.lbar.to_reference()[:m].cpu().numpy()
+        par = parity_report([("loss", lg, lo), ("l_bar", lbg, lb), ("tau2_bar", tg, tb)], 1e-9,
+                            relaxed={"l_bar", "tau2_bar"})
+        par["sample"] = f"first {m} matrices of the timed batch vs the {kind} oracle"
+        return dt, ("reference" if kind == "reference" else "port"), o.threads(), par
+
+    def cpu_sample_size(self, cores):
+        # ~0.2 s of single-core work per config-3 matrix
+        return int(max(8, min(self.B, 4 * cores)))
+
+
+# --------------------------------------------------------------------- per-op suites
+class SuiteWorkload:
+    """Configs 1, 2, 4: the config's operator suite as one step of API calls.
+    Each op is (name, counts(flops, bytes per row), dmma?, gpu thunk,
+    oracle thunk); inputs are device-resident (tile 32 for configs 1-2, the
+    reference layout for config 4 whose wide kernels read whole columns)."""
+
+    def __init__(self, wl, batch, start, dev):
+        import torch
+
+        self.wl, self.B, self.n, self.k = wl, batch, wl["n"], wl["k"]
+        self.dev = dev
+        self.dtype = torch.float32 if wl["dtype"] == "f32" else torch.float64
+        self.tile = 1 if wl["kind"] == "wide" else 32
+        self.seed = 1000 + 7919 * start
+        self.res = {}
+        getattr(self, "_build_" + wl["kind"])()
+
+    # ---- input generators (device, seeded)
+    def _gen(self):
+        import torch
+        g = torch.Generator(device=self.dev)
+        g.manual_seed(self.seed)
+        self.seed += 1
+        return g
+
+    def _factor(self, off_std):
+        import paper_1902_10078_b200 as bgm
+        g = self._gen()
+        L = bgm.Bands.empty(self.B, self.n, self.k, 0, tile=1, device=self.dev)
+        L.data.normal_(0.0, off_std, generator=g)
+        L.data[:, :, 0].uniform_(1.0, 2.0, generator=g)
+        for r in range(1, self.k + 1):
+            L.data[:, self.n - r:, r] = 0.0
+        return L.to_tile(self.tile) if self.tile == 32 else L
+
+    def _band(self, lo, up):
+        import paper_1902_10078_b200 as bgm
+        X = bgm.Bands.empty(self.B, self.n, lo, up, tile=self.tile, dtype=self.dtype, device=self.dev)
+        X.data.normal_(0.0, 1.0, generator=self._gen())
+        return X
+
+    def _vec(self):
+        import paper_1902_10078_b200 as bgm
+        v = bgm.Vecs.empty(self.B, self.n, tile=self.tile, dtype=self.dtype, device=self.dev)
+        v.data.normal_(0.0, 1.0, generator=self._gen())
+        return v
+
+    def _precision(self, off_std):
+        """Q = band(L0 L0^T) ("as in config 0"); fp32 configs
+        round the fp64 Q to fp32."""
+        import paper_1902_10078_b200 as bgm
+        L0 = self._factor(off_std)
+        Q = bgm.product_band_band_restricted(L0, bgm.T(L0), self.k, 0)
+        if self.dtype != Q.dtype:
+            Q = bgm.Bands(Q.data.to(self.dtype), Q.batch, Q.n, Q.lower, Q.upper, Q.tile)
+        return Q
+
+    # ---- config 1
+    def _build_cfg1(self):
+        import paper_1902_10078_b200 as bgm
+        k = self.k
+        self.inputs = {"q": self._precision(0.1), "b": self._vec()}
+        Q, b, r = self.inputs["q"], self.inputs["b"], self.res
+        self.ops = [
+            ("cholesky", op_counts("cholesky", k), False, lambda: r.__setitem__("l", bgm.cholesky(Q, check=False))),
+            ("solve_vec L", op_counts("solve_vec", k), False,
+             lambda: r.__setitem__("x1", bgm.solve_vec(r["l"], b, False, check=False))),
+            ("solve_vec Lt", op_counts("solve_vec", k), False,
+             lambda: r.__setitem__("x2", bgm.solve_vec(r["l"], r["x1"], True, check=False))),
+            ("log_det", op_counts("log_det", k), False,
+             lambda: r.__setitem__("ld", bgm.log_det_from_cholesky(r["l"], check=False))),
+        ]
+        self.outputs = ["l", "x1", "x2", "ld"]
+
+    def _oracle_cfg1(self, o, h, g):
+        # every op on the same inputs as its GPU call (g: the GPU's own
+        # intermediates), so each output measures that op's error alone
+        L, _, _ = o.cholesky(h["q"])
+        x1, _, _ = o.solve_vec(g["l"], h["b"])
+        x2, _, _ = o.solve_vec(g["l"], g["x1"], True)
+        ld, _, _ = o.log_det(g["l"])
+        return {"l": L, "x1": x1, "x2": x2, "ld": ld}
+
+    # ---- config 2
+    def _build_cfg2(self):
+        import paper_1902_10078_b200 as bgm
+        k = self.k
+        L = self._band(k, 0)
+        self.inputs = {"l": L, "lt": L.transpose(), "a": self._band(8, 8), "bm": self._band(3, 3),
+                       "v": self._vec(), "p1bar": self._band(k, k),
+                       "p2bar": self._band(11, 11), "pvbar": self._vec()}
+        i, r = self.inputs, self.res
+        self.ops = [
+            ("L.Lt (8,8)", (2 * (k + 1) ** 2, 8 * (3 * k + 2)), False,
+             lambda: r.__setitem__("p1", bgm.product_band_band(i["l"], bgm.T(i["l"])))),
+            ("A(8,8).B(3,3)", op_counts("product", k, wa=17, wb=7), False,
+             lambda: r.__setitem__("p2", bgm.product_band_band(i["a"], i["bm"]))),
+            ("A.v", op_counts("band_vec", k, w=17), False,
+             lambda: r.__setitem__("pv", bgm.product_band_vec(i["a"], i["v"]))),
+            ("vjp L.Lt", op_counts("vjp_product", k, wa=9, wb=9), False,
+             lambda: r.__setitem__("g1", bgm.vjp_product_band_band(i["l"], i["lt"], i["p1bar"]))),
+            ("vjp A.B", op_counts("vjp_product", k, wa=17, wb=7), False,
+             lambda: r.__setitem__("g2", bgm.vjp_product_band_band(i["a"], i["bm"], i["p2bar"]))),
+            ("vjp A.v", op_counts("vjp_band_vec", k, w=17), False,
+             lambda: r.__setitem__("g3", bgm.vjp_product_band_vec(i["a"], i["v"], i["pvbar"], False))),
+        ]
+        self.outputs = ["p1", "p2", "pv", "g1", "g2", "g3"]
+
+    def _oracle_cfg2(self, o, h, g):
+        k = self.k
+        p1, _, _ = o.product_band_band(h["l"], k, 0, h["lt"], 0, k)
+        p2, _, _ = o.product_band_band(h["a"], 8, 8, h["bm"], 3, 3)
+        pv = o.product_band_vec(h["a"], 8, 8, h["v"])
+        g1 = o.vjp_product_band_band(h["l"], k, 0, h["lt"], 0, k, h["p1bar"], k, k)
+        g2 = o.vjp_product_band_band(h["a"], 8, 8, h["bm"], 3, 3, h["p2bar"], 11, 11)
+        g3 = o.vjp_product_band_vec(h["a"], 8, 8, h["v"], h["pvbar"])
+        return {"p1": p1, "p2": p2, "pv": pv, "g1": g1, "g2": g2, "g3": g3}
+
+    # ---- config 4
+    def _build_wide(self):
+        import torch
+        import paper_1902_10078_b200 as bgm
+        k = self.k
+        self.inputs = {"q": self._precision(0.02 / k ** 0.5), "b": self._vec(), "sb": self._vec(),
+                       "sbar": self._band(k, 0), "lbar": self._band(k, 0)}
+        self.cbar = torch.ones(self.B, dtype=self.dtype, device=self.dev)
+        i, r = self.inputs, self.res
+        self.ops = [
+            ("cholesky", op_counts("cholesky", k), True, lambda: r.__setitem__("l", bgm.cholesky(i["q"], check=False))),
+            ("solve_vec L", op_counts("solve_vec", k), False,
+             lambda: r.__setitem__("x1", bgm.solve_vec(r["l"], i["b"], False, check=False))),
+            ("solve_vec Lt", op_counts("solve_vec", k), False,
+             lambda: r.__setitem__("x2", bgm.solve_vec(r["l"], r["x1"], True, check=False))),
+            ("log_det", op_counts("log_det", k), False,
+             lambda: r.__setitem__("ld", bgm.log_det_from_cholesky(r["l"], check=False))),
+            ("subset", op_counts("subset", k), True,
+             lambda: r.__setitem__("s", bgm.sparse_inverse_subset(r["l"], check=False))),
+            ("vjp_solve_vec L", op_counts("vjp_solve_vec", k), False,
+             lambda: r.__setitem__("g_x1", bgm.vjp_solve_vec(r["l"], r["x1"], i["sb"], False, check=False))),
+            ("vjp_solve_vec Lt", op_counts("vjp_solve_vec", k), False,
+             lambda: r.__setitem__("g_x2", bgm.vjp_solve_vec(r["l"], r["x2"], i["sb"], True, check=False))),
+            ("vjp_log_det", op_counts("vjp_log_det", k), False,
+             lambda: r.__setitem__("g_ld", bgm.vjp_log_det_from_cholesky(r["l"], self.cbar))),
+            ("vjp_subset", op_counts("vjp_subset", k), True,
+             lambda: r.__setitem__("g_s", bgm.vjp_sparse_inverse_subset(r["l"], r["s"], i["sbar"], check=False))),
+            ("vjp_cholesky", op_counts("vjp_cholesky", k), True,
+             lambda: r.__setitem__("g_l", bgm.vjp_cholesky(r["l"], i["lbar"]))),
+        ]
+        self.outputs = ["l", "x1", "x2", "ld", "s", "g_x1", "g_x2", "g_ld", "g_s", "g_l"]
+
+    def _oracle_wide(self, o, h, g):
+        import numpy as np
+        L, x1, x2, S = g["l"], g["x1"], g["x2"], g["s"]  # the GPU's intermediates
+        Lo, _, _ = o.cholesky(h["q"])
+        x1o, _, _ = o.solve_vec(L, h["b"])
+        x2o, _, _ = o.solve_vec(L, x1, True)
+        ld, _, _ = o.log_det(L)
+        So, _, _ = o.sparse_inverse_subset(L)
+        g1 = o.vjp_solve_vec(L, x1, h["sb"], False)[:2]
+        g2 = o.vjp_solve_vec(L, x2, h["sb"], True)[:2]
+        g3 = o.vjp_log_det(L, np.ones(L.shape[0]))
+        g4, _, _ = o.vjp_sparse_inverse_subset(L, S, h["sbar"])
+        g5 = o.vjp_cholesky(L, h["lbar"])
+        return {"l": Lo, "x1": x1o, "x2": x2o, "ld": ld, "s": So, "g_x1": g1, "g_x2": g2, "g_ld": g3, "g_s": g4,
+                "g_l": g5}
+
+    # ---- step / attribution
+    def step(self):
+        for _, _, _, fn in self.ops:
+            fn()
+
+    def graphable(self, world):
+        return True
+
+    def check_status(self):
+        pass
+
+    def _scale(self):
+        return 0.5 if self.wl["dtype"] == "f32" else 1.0
+
+    def attribution(self, steps, hbm, fp64):
+        """Each op captured as its own CUDA graph (reading the previous op's
+        graph outputs) and its replays timed with CUDA events on the launch
+        stream: device time per op, free of the host launch cost the eager
+        Python calls add (the step itself is timed as one graph)."""
+        import torch
+        per_ms = []
+        for name, _, _, fn in self.ops:
+            g, _ = capture(fn)
+            run = g.replay if g is not None else fn
+            run()
+            torch.cuda.synchronize()
+            per_ms.append(time_steps(run, max(steps, 3)))
+            self._op_graphs = getattr(self, "_op_graphs", []) + [g]
+        rows = self.B * self.n
+        per = []
+        for q, (name, (fl, by), dmma, _) in enumerate(self.ops):
+            per.append(roofline_entry(name, per_ms[q], fl * rows, by * self._scale() * rows, hbm, fp64,
+                                      tensor=dmma))
+        dom = dict(max(per, key=lambda d: d["kernel_ms"]))
+        dom["timing"] = "the op's API call (main kernel + its checks) as a CUDA graph, CUDA events on the launch stream"
+        dom["traffic"], dom["traffic_source"] = load_traffic(dom["kernel"])
+        dom["per_op"] = {d["kernel"]: {"ms": d["kernel_ms"], "roofline_ms": d["roofline_ms"], "bound": d["bound"],
+                                       "frac": d["frac"]} for d in per}
+        self._per = per
+        return dom, None
+
+    def suite(self, ms):
+        roof = sum(d["roofline_ms"] for d in self._per)
+        ops_ms = sum(d["kernel_ms"] for d in self._per)
+        return {"suite_roofline_ms": round(roof, 4), "suite_frac_of_step": round(roof / ms, 4),
+                "sum_of_op_ms": round(ops_ms, 4),
+                "note": "sum over the config's ops of max(bytes/HBM, flops/FP64-or-DMMA peak), SURVEY.md 8(d)"}
+
+    # ---- e2e: host (reference layout, pinned) -> device -> suite -> host
+    def e2e(self, steps, world, dev):
+        import torch
+        import paper_1902_10078_b200 as bgm
+
+        hin, din = {}, {}
+        for name, x in self.inputs.items():
+            ref = x.to_reference()
+            hin[name] = torch.empty(ref.shape, dtype=ref.dtype, pin_memory=True)
+            hin[name].copy_(ref)
+            # tile-1 operands are copied straight into the kernels' buffers
+            din[name] = x.data if x.tile == 1 else torch.empty_like(ref)
+        self.step()
+        torch.cuda.synchronize()
+        houts = {}
+        for name in self.outputs:
+            for q, t in enumerate(self._flat(self.res[name])):
+                r = self._ref_of(t)
+                houts[(name, q)] = torch.empty(r.shape, dtype=r.dtype, pin_memory=True)
+
+        def step():
+            # user data in the reference layout: H2D, relayout to the kernels'
+            # layout (tile 32 for configs 1-2), the suite, relayout back, D2H
+            for name, x in self.inputs.items():
+                din[name].copy_(hin[name], non_blocking=True)
+                if x.tile == 1:
+                    continue
+                if isinstance(x, bgm.Bands):
+                    bgm.Bands(din[name], x.batch, x.n, x.lower, x.upper, 1).to_tile(x.tile, x)
+                else:
+                    bgm.Vecs(din[name], x.batch, x.n, 1).to_tile(x.tile, x)
+            self.step()
+            for name in self.outputs:
+                for q, t in enumerate(self._flat(self.res[name])):
+                    houts[(name, q)].copy_(self._ref_of(t), non_blocking=True)
+
+        h2d = sum(t.numel() * t.element_size() for t in hin.values())
+        d2h = sum(t.numel() * t.element_size() for t in houts.values())
+        return step, h2d, d2h
+
+    @staticmethod
+    def _flat(v):
+        return list(v) if isinstance(v, tuple) else [v]
+
+    @staticmethod
+    def _ref_of(t):
+        return t.to_reference() if hasattr(t, "to_reference") else t
+
+    def _host(self, t, m):
+        import numpy as np
+        import torch
+        a = self._ref_of(t)[:m]
+        return np.ascontiguousarray(a.to(torch.float64).cpu().numpy())
+
+    def cpu_and_parity(self, m):
+        import oracle as orc
+
+        h = {name: self._host(x, m) for name, x in self.inputs.items()}
+        gi = {name: self._host(self.res[name], m) for name in ("l", "x1", "x2", "s") if name in self.res}
+        kind = "reference" if orc.available("reference") else "restatement"
+        o = orc.Oracle(kind)
+        t0 = time.perf_counter()
+        ref = getattr(self, "_oracle_" + self.wl["kind"])(o, h, gi)
+        dt = time.perf_counter() - t0
+        pairs = []
+        for name in self.outputs:
+            gs = self._flat(self.res[name])
+            rs = list(ref[name]) if isinstance(ref[name], tuple) else [ref[name]]
+            for q, (g, r) in enumerate(zip(gs, rs)):
+                pairs.append((name if len(gs) == 1 else f"{name}[{q}]", self._host(g, m), r))
+        tol = 1e-4 if self.wl["dtype"] == "f32" else 1e-9
+        par = parity_report(pairs, tol)
+        par["sample"] = (f"first {m} matrices of the timed batch vs the {kind} oracle, each op on the same "
+                         f"inputs as its GPU call" + (" (fp64 oracle on the fp32 inputs)" if self.wl["dtype"] == "f32"
+                                                      else ""))
+        return dt, ("reference" if kind == "reference" else "port"), o.threads(), par
+
+    def cpu_sample_size(self, cores):
+        # bounded to ~10-30 s of CPU work: matrices are independent
+        per_core = {"cfg1": 64, "cfg2": 2, "wide": 0.5 if self.k == 64 else 0.125}[self.wl["kind"]]
+        return int(max(2, min(self.B, per_core * cores)))
+
+
+def make_workload(wl, batch, start, dev, tile=32):
+    if wl["kind"] == "mlik":
+        return MlikWorkload(wl, batch, start, dev, tile)
+    return SuiteWorkload(wl, batch, start, dev)
+
+
+# --------------------------------------------------------------------- timing
+def time_steps(step, steps, barrier=None):
+    import torch
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if barrier:
+        barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    return e0.elapsed_time(e1) / steps
+
+
+def proxy_efficiency(wl, B, dev, tile, t_full, steps):
+    """T(B) / (G * T(B/G)) for G = 2, 4, 8, each B/G batch timed on this GPU
+    as a G-GPU run's rank would run it (its own inputs, its own graph)."""
+    import torch
+    out = {}
+    for G in (2, 4, 8):
+        b = max(1, B // G)
+        w = make_workload(wl, b, 0, dev, tile)
+        w.step()
+        torch.cuda.synchronize()
+        g, _ = capture(w.step) if w.graphable(1) else (None, None)
+        st = g.replay if g is not None else w.step
+        for _ in range(3):
+            st()
+        ms = time_steps(st, max(steps, 5))
+        out[str(G)] = {"batch_per_gpu": b, "ms_per_step": round(ms, 4), "efficiency": round(t_full / (G * ms), 4)}
+        del w, g
+        torch.cuda.empty_cache()
+    return out
 
 
 # --------------------------------------------------------------------- main
@@ -201,89 +820,60 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg3")
+    ap.add_argument("--batch", type=int, default=0, help="total batch (default: the config's B)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-proxy", action="store_true", help="skip the 1-GPU strong-scaling proxy")
     ap.add_argument("--segment-rows", type=int, default=0)
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="time eager launches instead of the captured CUDA graph")
     ap.add_argument("--tile", type=int, choices=[1, 32], default=32,
-                    help="device layout: 32 = interleaved (one-thread-per-unit sweeps), 1 = reference layout (team sweeps)")
+                    help="config-3 device layout: 32 = interleaved (one-thread-per-unit sweeps), 1 = reference layout")
     args = ap.parse_args()
-    wl = WORKLOADS[args.workload]
-    B, n, k, tau2 = wl["B"], wl["n"], wl["k"], wl["tau2"]
-    metric = "band-rows/s (B*n/s) fwd+bwd banded Chol/solve/inv-subset; % of roofline"
+    wl = dict(WORKLOADS[args.workload])
+    if args.batch:
+        wl["B"] = args.batch
+    B_total, n = wl["B"], wl["n"]
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
     if args.impl == "reference":
-        return reference_arm(args, wl, metric, world, rank)
+        return reference_arm(args, wl, world, rank)
 
     import torch
     import torch.distributed as dist
     import paper_1902_10078_b200 as bgm
+    from paper_1902_10078_b200.dist import shard_bounds
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    lib = bgm.library()
+    bgm.library()
     if args.segment_rows:
         bgm.set_segment_rows(args.segment_rows)
 
-    L, y = make_inputs(B, n, k, seed=1234 + 7919 * rank, device=dev, tile=args.tile)
-    loss = torch.empty(B, dtype=torch.float64, device=dev)
-    tbar = torch.empty(B, dtype=torch.float64, device=dev)
-    lbar = L.like()
-    st = bgm.api.new_status(B, dev)
-    out = (loss, lbar, tbar, st)
-    from paper_1902_10078_b200.dist import reduce_totals
-
-    def step():
-        # fused sweeps on this rank's matrices, then the one 2 x fp64 NCCL
-        # all-reduce of (sum loss, sum d tau2) when world > 1
-        bgm.marginal_likelihood_grad(L, y, tau2, check=False, out=out)
-        return reduce_totals([loss, tbar])
-
-    step()  # first call sizes the scratch pool
+    # strong scaling: this rank's contiguous slice of the B_total matrices
+    start, stop = shard_bounds(B_total, world, rank)
+    B = stop - start
+    W = make_workload(wl, B, start, dev, args.tile)
+    W.step()  # first call sizes the scratch pool
     torch.cuda.synchronize()
-    st.raise_first()
+    W.check_status()
 
-    # The step's ~10 launches are captured once into a CUDA graph and
-    # replayed (same kernels, same work; no per-launch host overhead).  The
-    # NCCL all-reduce of the multi-GPU case stays outside the graph.
-    graph = None
-    if args.graph and world == 1:
-        try:
-            g = torch.cuda.CUDAGraph()
-            s0 = torch.cuda.Stream()
-            s0.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(s0):
-                step()
-            torch.cuda.current_stream().wait_stream(s0)
-            torch.cuda.synchronize()
-            with torch.cuda.graph(g):
-                step()
-            torch.cuda.synchronize()
-            graph = g
-        except Exception as exc:  # capture unsupported: time the eager launches
-            print(f"# graph capture failed ({exc}); timing eager launches", file=sys.stderr)
-            graph = None
-    eager_step = step
-    if graph is not None:
-        def step():
-            graph.replay()
+    graph, gnames = (capture(W.step) if args.graph and W.graphable(world) else (None, None))
+    step = graph.replay if graph is not None else W.step
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    stream = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    hbm, hbm_src = load_hbm_peak()
+    fp64 = measure_fp64_peaks()
     # The clock sampler (nvidia-smi every 50 ms) runs across warm-up, the timed
-    # region and the per-kernel attribution pass below -- all the same kernels
-    # back to back -- so its samples are taken under this load.
+    # region and the per-kernel attribution pass -- the same kernels back to back.
     clk = ClockSampler(local).__enter__()
     t_warm = time.perf_counter()
     nwarm = max(args.warmup, 3)
@@ -292,87 +882,71 @@ def main():
         nwarm -= 1
         if nwarm <= 0:
             torch.cuda.synchronize()
-    # ---------------- timed region: device-resident inputs (2.3 GB > L2)
-    barrier()
-    torch.cuda.synchronize()
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    ms = e0.elapsed_time(e1) / args.steps
+    # ---------------- timed region: device-resident inputs (each > L2)
+    ms = time_steps(step, args.steps, barrier)
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
-    rows_total = B * n * world
-    value = rows_total / (ms / 1e3)
+    value = B_total * n / (ms / 1e3)
 
     # ---------------- per-kernel attribution (CUDA events on the launch stream)
-    lib.bgm_timing_enable(1)
-    for _ in range(args.steps):
-        eager_step()
-    torch.cuda.synchronize()
+    roofline, launches = W.attribution(args.steps, hbm, fp64)
     clk.__exit__(None, None, None)
-    kernels = []
-    cnt = lib.bgm_timing_read(-1, None, 0, None, None)
-    for i in range(cnt):
-        name = C.create_string_buffer(128)
-        tot = C.c_double()
-        c = C.c_int64()
-        lib.bgm_timing_read(i, name, 128, C.byref(tot), C.byref(c))
-        kernels.append((name.value.decode(), tot.value, c.value))
-    lib.bgm_timing_enable(0)
-    launches_per_step = sum(c for _, _, c in kernels) / max(args.steps, 1)
-    dom = max(kernels, key=lambda t: t[1]) if kernels else ("?", float("nan"), 1)
-    dom_ms = dom[1] / dom[2]
-    peak, peak_src = load_peaks()
-    bpr = alg_bytes_per_row(dom[0], k)
-    achieved = bpr * B * n / (dom_ms / 1e3) / 1e9
-    traffic, traffic_src = load_traffic(dom[0])
-    roofline = {"bound": "hbm", "kernel": dom[0], "achieved": round(achieved, 1), "peak": peak,
-                "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                "traffic": traffic, "traffic_source": traffic_src,
-                "alg_bytes_per_launch": bpr * B * n, "alg_bytes_per_row": bpr,
-                "kernel_ms": {kname: round(t / c, 4) for kname, t, c in kernels}}
-    # the reference composition's suite roofline for config 3
-    # (sum of per-op max(bytes/HBM, flops/FP64)) -- the metric's "% of roofline"
-    suite = None
-    if args.workload == "cfg3":
-        suite_ms = 7.50 * (B * n) / (256 * 65536)
-        suite = {"suite_roofline_ms": round(suite_ms, 3), "frac": round(suite_ms / ms, 3),
-                 "note": "reference op-by-op composition at HBM/FP64 peaks (SURVEY.md 8(d)); "
-                         "the fused step beats it, its own FP64 roofline is ~0.84 ms (DESIGN.md 4.1)"}
+    roofline["peak_source"] = hbm_src if roofline["unit"] == "GB/s" else fp64["source"]
+    if gnames is not None:
+        launches = len(ours(gnames))
+    suite = W.suite(ms)
+
+    # ---------------- 1-GPU strong-scaling proxy
+    proxy = None
+    if world == 1 and not args.no_proxy and B_total >= 8:
+        proxy = proxy_efficiency(wl, B_total, dev, args.tile, ms, args.steps)
 
     # ---------------- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = e2e_run(args, L, y, tau2, out, world, dev)
+        e2e_step, h2d, d2h = W.e2e(args.steps, world, dev)
+        e2e_step()
+        torch.cuda.synchronize()
+        e_steps = max(2, min(args.steps, 5))
+        ems = time_steps(e2e_step, e_steps, barrier)
+        ems_t = torch.tensor([ems], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ems_t, op=dist.ReduceOp.MAX)
+        ems = float(ems_t.item())
+        e2e = {"value": round(B_total * n / (ems / 1e3), 1), "unit": "band-rows/s", "ms_per_step": round(ems, 3),
+               "steps": e_steps, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "path": "public host-buffer API: pinned host (reference layout) -> device -> step -> host"}
 
-    # ---------------- CPU baseline (rank 0, N=1)
-    cpu = None
+    # ---------------- CPU baseline (rank 0, N=1) + parity of the sample
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu:
         cores = os.cpu_count() or 1
-        m = sample_size(cores, B)
-        Lh, yh = host_sample(L, y, m)
-        dt, kind, thr = cpu_run(Lh, yh, tau2)
+        m = W.cpu_sample_size(cores)
+        W.step()  # the outputs of the sampled matrices, from the same inputs
+        torch.cuda.synchronize()
+        dt, kind, thr, parity = W.cpu_and_parity(m)
         cpu = {"value": round(m * n / dt, 1), "unit": "band-rows/s", "cores": thr, "kind": kind,
-               "sample": f"{m} of the {B} config-3 matrices (n={n}, k={k}), oracle marginal_likelihood_grad, "
-                         f"{dt:.2f} s wall on {thr} threads"}
+               "sample": f"{m} of the {B} {args.workload} matrices (n={n}, k={wl['k']}), the same inputs, "
+                         f"{dt:.2f} s wall on {thr} threads", **host_info()}
 
     if rank == 0:
         line = {
-            "metric": metric, "value": round(value, 1), "unit": "band-rows/s", "n_gpus": world,
+            "metric": METRIC, "value": round(value, 1), "unit": "band-rows/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": wl["dtype"],
             "data": "synthetic (seeded on device; BASELINE.md §4 construction)",
-            "config": {"workload": args.workload, "desc": wl["desc"], "batch_per_gpu": B, "n": n, "k": k,
-                       "tau2": tau2, "parallelism": f"batch-sharded x{world}", "layout_tile": L.tile,
-                       "cuda_graph": graph is not None,
-                       "l2": "inputs (%.2f GB/GPU) exceed the 126 MB L2; no flush needed" % (B * n * (k + 1) * 8 / 1e9)},
-            "roofline": roofline, "suite_roofline": suite, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": int(round(launches_per_step * args.steps)),
+            "config": {"workload": args.workload, "desc": wl["desc"], "global_batch": B_total,
+                       "batch_per_gpu": B, "n": n, "k": wl["k"],
+                       **({"tau2": wl["tau2"]} if "tau2" in wl else {}),
+                       "parallelism": f"batch-sharded x{world} (contiguous slices, dist.shard_bounds)",
+                       "layout_tile": getattr(W, "tile", None), "cuda_graph": graph is not None,
+                       "l2": "inputs exceed the 126 MB L2 (%.2f GB/GPU); no flush needed"
+                             % (B * n * (wl["k"] + 1) * 8 / 1e9)},
+            "roofline": roofline, "suite_roofline": suite, "fp64_peaks": fp64, "cpu_baseline": cpu,
+            "parity": parity, "e2e": e2e, "scaling_proxy": proxy,
+            "gpu_launches": int(round(launches * args.steps)) if launches is not None else None,
             "clocks": clk.summary(),
         }
         print(json.dumps(line))
@@ -380,63 +954,12 @@ def main():
         dist.destroy_process_group()
 
 
-def e2e_run(args, L, y, tau2, out, world, dev):
-    """Same metric through the public API from pinned HOST buffers: each step
-    copies L and y host->device, runs the step, and reads loss, tau2_bar and
-    the full L_bar back device->host."""
-    import torch
-    import torch.distributed as dist
-    import paper_1902_10078_b200 as bgm
-
-    from paper_1902_10078_b200.dist import reduce_totals
-    from paper_1902_10078_b200.host import marginal_likelihood_grad_host
-
-    loss, lbar, tbar, st = out
-    # the user's data: pinned host buffers in the reference storage layout
-    Lr, yr = L.to_reference(), y.to_reference()
-    hL = torch.empty(Lr.shape, dtype=Lr.dtype, pin_memory=True)
-    hy = torch.empty(yr.shape, dtype=yr.dtype, pin_memory=True)
-    hL.copy_(Lr)
-    hy.copy_(yr)
-    del Lr, yr
-    hout = (torch.empty(L.batch, dtype=torch.float64, pin_memory=True),
-            torch.empty(hL.shape, dtype=torch.float64, pin_memory=True),
-            torch.empty(L.batch, dtype=torch.float64, pin_memory=True))
-    hLb = hout[1]
-
-    def step():
-        # public host-buffer API: chunked H2D -> fused sweeps -> D2H, overlapped
-        hloss, _, htb = marginal_likelihood_grad_host(hL, hy, tau2, out_host=hout, tile=L.tile)
-        if world > 1:
-            reduce_totals([hloss.to(dev, non_blocking=True), htb.to(dev, non_blocking=True)])
-
-    steps = max(2, min(args.steps, 5))
-    step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s = torch.cuda.current_stream()
-    e0.record(s)
-    for _ in range(steps):
-        step()
-    e1.record(s)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms = float(ms_t.item())
-    h2d = hL.numel() * 8 + hy.numel() * 8
-    d2h = hLb.numel() * 8 + hout[0].numel() * 8 + hout[2].numel() * 8
-    return {"value": round(L.batch * L.n * world / (ms / 1e3), 1), "unit": "band-rows/s",
-            "ms_per_step": round(ms, 3), "steps": steps, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
-
-
-def reference_arm(args, wl, metric, world, rank):
+def reference_arm(args, wl, world, rank):
     """--impl reference: the reference's own CPU implementation (oracle/_ref,
-    compiled verbatim; the C restatement if that is absent) on the host cores,
-    each step a bounded sample of the workload.  Rank 0 only."""
+    its proj/src compiled verbatim; the C restatement if that is absent) on
+    the host cores, OpenMP over matrices.  Each step runs the whole config-3
+    batch when it fits ~8 s of wall time on this host (else a stated
+    sample), the same number of steps as the GPU arm.  Rank 0 only."""
     if rank != 0:
         return
     import numpy as np
@@ -444,32 +967,76 @@ def reference_arm(args, wl, metric, world, rank):
     import oracle as orc
     from tests import common as cm
 
-    B, n, k, tau2 = wl["B"], wl["n"], wl["k"], wl["tau2"]
-    cores = os.cpu_count() or 1
-    m = sample_size(cores, B)
-    rng = np.random.default_rng(99)
-    L = cm.config_factor(rng, m, n, k)
-    y = rng.normal(0.0, 1.0, (m, n))
+    B, n, k = wl["B"], wl["n"], wl["k"]
     kind = "reference" if orc.available("reference") else "restatement"
+    o = orc.Oracle(kind)
+    thr = o.threads()
+    rng = np.random.default_rng(99)
+    if wl["kind"] == "mlik":
+        per_matrix_s = 0.2 * n / 65536 * (k / 16) ** 2  # one core, measured on the round-1 box
+        m = int(min(B, max(thr, 8.0 * thr / per_matrix_s)))
+        tau2 = wl["tau2"]
+        L = cm.config_factor(rng, m, n, k)
+        z = rng.normal(0.0, 1.0, (m, n))
+        x, _, _ = o.solve_vec(L, z, True)  # y = L^-T z + eps
+        y = x + rng.normal(0.0, 0.1, (m, n))
+
+        def run():
+            _, _, _, st, _ = o.marginal_likelihood_grad(L, y, tau2)
+            assert (st == 0).all()
+        what = "config-3 learning step (marginal likelihood + dL + dtau2, tape composition)"
+    else:
+        m = {"cfg1": B, "cfg2": 2 * thr, "wide": thr if k == 64 else max(4, thr // 2)}[wl["kind"]]
+        m = int(min(B, m))
+        off = 0.1 if wl["kind"] == "cfg1" else 0.02 / k ** 0.5
+        h = {}
+        if wl["kind"] in ("cfg1", "wide"):
+            L0 = cm.config_factor(rng, m, n, k, off_std=off)
+            q, _, _ = o.product_band_band(L0, k, 0, cm.transpose_ref(L0, k, 0), 0, k, k, 0)
+            if wl["dtype"] == "f32":
+                q = q.astype(np.float32).astype(np.float64)
+            h = {"q": q, "b": rng.normal(0, 1, (m, n)), "sb": rng.normal(0, 1, (m, n)),
+                 "sbar": cm.zero_corners(rng.normal(0, 1, (m, n, k + 1)), k, 0),
+                 "lbar": cm.zero_corners(rng.normal(0, 1, (m, n, k + 1)), k, 0)}
+        else:
+            Lb = cm.zero_corners(rng.normal(0, 1, (m, n, k + 1)), k, 0)
+            h = {"l": Lb, "lt": cm.transpose_ref(Lb, k, 0), "a": cm.zero_corners(rng.normal(0, 1, (m, n, 17)), 8, 8),
+                 "bm": cm.zero_corners(rng.normal(0, 1, (m, n, 7)), 3, 3), "v": rng.normal(0, 1, (m, n)),
+                 "p1bar": cm.zero_corners(rng.normal(0, 1, (m, n, 2 * k + 1)), k, k),
+                 "p2bar": cm.zero_corners(rng.normal(0, 1, (m, n, 23)), 11, 11), "pvbar": rng.normal(0, 1, (m, n))}
+        shim = SuiteWorkload.__new__(SuiteWorkload)
+        shim.k = k
+        g = {}
+        if wl["kind"] in ("cfg1", "wide"):  # the reference chain's own intermediates
+            g["l"], _, _ = o.cholesky(h["q"])
+            g["x1"], _, _ = o.solve_vec(g["l"], h["b"])
+            g["x2"], _, _ = o.solve_vec(g["l"], g["x1"], True)
+            if wl["kind"] == "wide":
+                g["s"], _, _ = o.sparse_inverse_subset(g["l"])
+
+        def run():
+            getattr(shim, "_oracle_" + wl["kind"])(o, h, g)
+        what = "the config's operator suite, " + wl["desc"]
     for _ in range(max(args.warmup, 1) if m * n * (k + 1) < 5e8 else 1):
-        cpu_run(L[: max(1, m // 8)], y[: max(1, m // 8)], tau2, kind)
+        run()
     times = []
-    steps = max(1, min(args.steps, 3))
-    thr = 1
-    for _ in range(steps):
-        dt, kk, thr = cpu_run(L, y, tau2, kind)
-        times.append(dt)
+    for _ in range(max(1, args.steps)):
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
     dt = statistics.median(times)
     value = m * n / dt
-    line = {"impl": "reference", "metric": metric, "value": round(value, 1), "unit": "band-rows/s",
-            "n_gpus": world, "steps": steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 2),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+    sample = (f"{m} of the {B} matrices per step" if m < B else f"the whole batch of {B} matrices per step") + \
+        f" (n={n}, k={k}): {what}; median of {len(times)} steps"
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": "band-rows/s",
+            "n_gpus": world, "steps": len(times), "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 2),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": wl["dtype"],
             "data": "synthetic (seeded numpy; BASELINE.md §4 construction)",
-            "config": {"workload": args.workload, "desc": wl["desc"], "batch_per_gpu": B, "n": n, "k": k,
-                       "tau2": tau2},
+            "config": {"workload": args.workload, "desc": wl["desc"], "global_batch": B, "n": n, "k": k,
+                       **({"tau2": wl["tau2"]} if "tau2" in wl else {})},
             "cpu_baseline": {"value": round(value, 1), "unit": "band-rows/s", "cores": thr,
-                             "kind": "reference" if kind == "reference" else "port",
-                             "sample": f"{m} config-3 matrices per step (n={n}, k={k}), median of {steps}"},
+                             "kind": "reference" if kind == "reference" else "port", "sample": sample,
+                             **host_info()},
             "e2e": {"value": round(value, 1), "unit": "band-rows/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))

@@ -260,6 +260,12 @@ int bgm_force_generic(int on);
 /* Tuning knob for the segment-parallel sweeps (0 = automatic). */
 int bgm_set_segment_rows(int64_t rows);
 
+/* Measured FP64 peaks of the current device in TFLOP/s: vector DFMA and
+ * DMMA (mma.sync.m8n8k4.f64) microbenchmarks, timed with CUDA events on
+ * `stream` (synchronizing).  The FP64 denominators of bench.py's rooflines;
+ * no reference counterpart (the reference reports no rooflines). */
+int bgm_fp64_peak(double* dfma_tflops, double* dmma_tflops, bgm_stream stream);
+
 #ifdef __cplusplus
 }
 #endif

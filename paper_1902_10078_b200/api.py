@@ -718,3 +718,11 @@ def debug_repairs(reset: bool = True, with_dev: bool = False):
 
 def new_status(batch: int, device=None) -> _Status:
     return _Status(batch, _device(device))
+
+
+def fp64_peak():
+    """Measured (DFMA, DMMA) FP64 peaks of the current device, TFLOP/s
+    (microbenchmarks in csrc/bgm_peak.cu; synchronizing)."""
+    a, b = C.c_double(0.0), C.c_double(0.0)
+    _call("bgm_fp64_peak", C.byref(a), C.byref(b), _stream())
+    return float(a.value), float(b.value)

@@ -7,6 +7,8 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
+#include <atomic>
 #include <stdint.h>
 
 #include <cmath>
@@ -122,6 +124,35 @@ __device__ __forceinline__ bool split_bj(ix t, ix batch, ix n, int s, ix& b, ix&
 }
 
 int set_error(cudaError_t e);
+
+// Kernel attributes (the > 48 KB dynamic shared-memory opt-in) and the
+// occupancy derived from them belong to a device context: cache them per
+// device ordinal, safely from any host thread (a repeated set is harmless).
+struct PerDevice {
+  std::atomic<unsigned long long> done{0};
+  static unsigned long long bit() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return 1ull << (d & 63);
+  }
+  bool first() const { return !(done.load(std::memory_order_acquire) & bit()); }
+  void mark() { done.fetch_or(bit(), std::memory_order_acq_rel); }
+};
+// A caller-requested segment length (bgm_set_segment_rows; 0 = automatic),
+// clamped so every segment start s >= bandwidth: the boundary checks read
+// the k columns before s.
+inline long long requested_seg(long long rows, int k) { return rows > 0 && rows < k + 1 ? k + 1 : rows; }
+
+struct PerDeviceInt {  // value + 1 per device ordinal, 0 = not yet known
+  std::atomic<int> v[64] = {};
+  static int dev() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d & 63;
+  }
+  int get() const { return v[dev()].load(std::memory_order_acquire) - 1; }
+  void set(int x) { v[dev()].store(x + 1, std::memory_order_release); }
+};
 
 // Stream-ordered scratch from the library's private pool (bgm_scratch.cu).
 cudaError_t scratch_alloc(void** ptr, size_t bytes, cudaStream_t s);

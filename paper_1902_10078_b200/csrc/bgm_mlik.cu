@@ -152,7 +152,7 @@ int bgm_debug_repairs(int64_t* count, double* max_dev, int reset) {
 }
 
 int bgm_set_segment_rows(int64_t rows) {
-  if (rows < 0) return BGM_ERR_ARG;
+  if (rows < 0 || rows > INT32_MAX) return BGM_ERR_ARG;
   g_segment_rows = int(rows);
   wide::set_segment_rows(int(rows));
   narrow::set_segment_rows(int(rows));

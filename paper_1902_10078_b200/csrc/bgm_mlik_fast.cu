@@ -267,10 +267,19 @@ __device__ __forceinline__ void fwd_block(FwdSt<TEAM>& S, const FwdCtx& C, ix ba
           if (SAFE) {
             if (!(d > kPivotFloor) || !(al0 > kPivotFloor)) S.fail = i < S.fail ? i : S.fail;
           } else {
-            S.odd |= !(d > 1e-30) | !(d < 1e30) | !(al0 > 1e-30) | !(al0 < 1e30);
+            // |L_ii| in [1e-18, 1e18] keeps a 16-row product of them inside
+            // the fp64 range (the products are renormalised once per block)
+            S.odd |= !(d > 1e-30) | !(d < 1e30) | !(al0 > 1e-18) | !(al0 < 1e18);
           }
           S.prodp *= d * rs;
           S.prodl *= al0;
+          if (SAFE) {  // exact path: any magnitude, renormalise every row
+            int x;
+            S.prodp = frexp(S.prodp, &x);
+            S.ep += x;
+            S.prodl = frexp(S.prodl, &x);
+            S.el += x;
+          }
           S.ww += wi * wi;
         }
         if (PH == PH_GEN && C.side && i >= C.s - 16 && i < C.s) {
@@ -731,7 +740,9 @@ __global__ void __launch_bounds__(THREADS, MinBlocks<TEAM>::bwd) k_repair_bwd(Bw
   const int lane = threadIdx.x & 31;
   const int slot = threadIdx.x / TEAM;
   const ix b0 = ix(blockIdx.x) * UPB + slot;
-  const bool work = b0 < G.batch && flag[b0] && fail[b0] >= G.n;
+  // flag = [forward flags | reverse flags]: forward-flagged matrices (out-of-
+  // range pivots or |L_ii|) need the exact reverse too (seeded_rcp of L_ii)
+  const bool work = b0 < G.batch && (flag[b0] | flag[G.batch + b0]) && fail[b0] >= G.n;
   if (!__any_sync(FULL, work)) return;
   const ix b = work ? b0 : 0;
   const int t = lane & (TEAM - 1);
@@ -820,7 +831,7 @@ void launch_all(const FwdP& F, const BwdP& Bp, const Geo& Gf, const Geo& Gb, int
   }
   {
     timing::Scope ts("mlik_repair_bwd", s);
-    k_repair_bwd<TEAM><<<mblocks, THREADS, 0, s>>>(Bp, Gb, flags + Gb.batch, F.fail);
+    k_repair_bwd<TEAM><<<mblocks, THREADS, 0, s>>>(Bp, Gb, flags, F.fail);
   }
   {
     timing::Scope ts("mlik_finalize", s);
@@ -899,6 +910,7 @@ int mlik_fast(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, co
     resident<16>(bf, bb);
   const int upb = (32 / team) * WARPS;
   Geo Gf = G, Gb = G;
+  segment_rows = int(requested_seg(segment_rows, l.lower));
   Gf.seg = segment_for(G.n, G.batch, ix(sms) * bf * upb, G.burn, segment_rows);
   Gb.seg = segment_for(G.n, G.batch, ix(sms) * bb * upb, G.burn, segment_rows);
   Gf.nseg = int((G.n + Gf.seg - 1) / Gf.seg);

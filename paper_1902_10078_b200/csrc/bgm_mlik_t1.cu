@@ -207,7 +207,7 @@ __device__ void fwd_unit(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, d
       prodp *= c[0];
       prodl *= al;
       ww += wi * wi;
-      if ((i & 7) == 7) {
+      if (SAFE || (i & 7) == 7) {  // exact path: any magnitude, every row
         int x;
         prodp = frexp(prodp, &x);
         ep += x;
@@ -350,9 +350,10 @@ __device__ void fwd_unit(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, d
     for (int r = 0; r < W; ++r) lcur[r] = lnext[r];
   };
 
-  // pairs while both prefetched columns (i+2, i+3) and y_{i+K+2} are interior
+  // pairs while the refill of pair(i) -- L columns i+2, i+3 and y_{i+K+3},
+  // y_{i+K+4} -- stays inside the matrix: i + 4 + K < n
   ix i = i0;
-  const ix pair_end = n - 3 - K;  // pair(i) needs i + 3 + K < n
+  const ix pair_end = n - 4 - K;
   if (i + 1 < e && i < pair_end) {
     fetch2(i);
 #pragma unroll 1
@@ -697,9 +698,13 @@ __global__ void k_check_bwd(BwdP P, Geo G) {
 
 template <int K>
 __global__ void k_repair_bwd(BwdP P, Geo G, const int32_t* flag, const int64_t* fail) {
+  // flag = [forward flags | reverse flags].  A forward-flagged matrix (an
+  // out-of-range pivot or |L_ii|, or an unconverged chain) is redone exactly
+  // here too: the fast reverse sweep seeds 1/L_ii from a float reciprocal,
+  // which is not valid outside [1e-30, 1e30].
   extern __shared__ double sm[];
   const ix b = blockIdx.x * ix(blockDim.x) + threadIdx.x;
-  if (b >= G.batch || !flag[b] || fail[b] < G.n) return;
+  if (b >= G.batch || !(flag[b] | flag[G.batch + b]) || fail[b] < G.n) return;
   atomicAdd(&g_repairs_t1, 1ull);
   double* part0 = P.part + b * G.nseg * 2;
   for (int q = 2; q < G.nseg * 2; ++q) part0[q] = 0.0;
@@ -773,15 +778,15 @@ int run(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, const bg
     if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
   G.debug = std::getenv("BGM_DEBUG") != nullptr;
   const size_t smf = sizeof(double) * (Sh::NF + 2 * Sh::W + 2) * kThreads, smb = sizeof(double) * Sh::NB * kThreads;
-  static bool attrs = false;
-  if (!attrs) {
+  static PerDevice attrs;
+  if (attrs.first()) {
     cudaFuncSetAttribute(k_fwd<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smf));
     cudaFuncSetAttribute(k_repair_fwd<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smf));
     cudaFuncSetAttribute(k_bwd<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smb));
     cudaFuncSetAttribute(k_repair_bwd<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smb));
     cudaFuncSetAttribute(k_fwd_fix<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smf));
     cudaFuncSetAttribute(k_bwd_fix<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smb));
-    attrs = true;
+    attrs.mark();
   }
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -789,6 +794,7 @@ int run(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, const bg
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, k_fwd<K>, kThreads, smf);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bb, k_bwd<K>, kThreads, smb);
   Geo Gf = G, Gb = G;
+  segment_rows = int(requested_seg(segment_rows, K));
   Gf.seg = seg_for(G.n, G.tiles, ix(sms) * (bf > 0 ? bf : 1), G.burn, segment_rows);
   Gb.seg = seg_for(G.n, G.tiles, ix(sms) * (bb > 0 ? bb : 1), G.burn, segment_rows);
   Gf.nseg = int((G.n + Gf.seg - 1) / Gf.seg);
@@ -885,7 +891,7 @@ int run(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, const bg
   }
   {
     timing::Scope ts("mlik_repair_bwd", s);
-    k_repair_bwd<K><<<mb, kThreads, smb, s>>>(Bp, Gb, flags + G.batch, F.fail);
+    k_repair_bwd<K><<<mb, kThreads, smb, s>>>(Bp, Gb, flags, F.fail);
   }
   {
     timing::Scope ts("mlik_finalize", s);

@@ -911,7 +911,7 @@ Geo make_geo(KernelT kern, size_t smem, ix batch, ix n, int burn, int segf_defau
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, smem);
   if (per < 1) per = 1;
-  ix seg = g_segment_rows;
+  ix seg = requested_seg(g_segment_rows, 16)  /* widest narrow band */;
   if (seg <= 0) {
     ix nseg = ix(sms) * per / G.tiles;
     if (nseg < 1) nseg = 1;
@@ -937,11 +937,11 @@ struct Scratch {
 template <class T, int K>
 bool run_chol(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, cudaStream_t s) {
   const size_t smem = sizeof(T) * (K * (K + 1) / 2 + 2 * (K + 1)) * kThreads;  // window + pair slot
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;
+  if (attr.first()) {
     cudaFuncSetAttribute(k_chol<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     cudaFuncSetAttribute(k_chol_repair<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = true;
+    attr.mark();
   }
   const int burn = burn_rows(K);
   const Geo G = make_geo(k_chol<T, K>, smem, q.batch, q.n, burn);
@@ -1020,11 +1020,11 @@ bool run_solve(const bgm_band& l, const bgm_vec& v, const bgm_vec& x, int32_t* s
 template <class T, int K>
 bool run_subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cudaStream_t s) {
   const size_t smem = sizeof(T) * (K * (K + 1) / 2) * kThreads;
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;
+  if (attr.first()) {
     cudaFuncSetAttribute(k_subset<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     cudaFuncSetAttribute(k_subset_repair<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = true;
+    attr.mark();
   }
   const int burn = burn_rows(K);
   const Geo G = make_geo(k_subset<T, K>, smem, l.batch, l.n, burn);
@@ -1061,11 +1061,11 @@ bool run_subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row
 template <class T, int K>
 bool run_vchol(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cudaStream_t s) {
   const size_t smem = sizeof(T) * ((K + 1) * (K + 2) / 2 + (VCHOL_SLOT ? 4 * (K + 1) : 0)) * kThreads;
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;
+  if (attr.first()) {
     cudaFuncSetAttribute(k_vchol<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     cudaFuncSetAttribute(k_vchol_repair<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = true;
+    attr.mark();
   }
   const Geo G = make_geo(k_vchol<T, K>, smem, l.batch, l.n, kBurnGen * K > kBurnMin ? kBurnGen * K : kBurnMin);
   const ix units = G.batch * G.nseg;

@@ -10,7 +10,7 @@
 //  * one persistent CTA per SM walks a contiguous run of output columns of
 //    one tile (32 matrices) -- or of one lane group of LN matrices of it;
 //  * each operand has a ring of RC columns in shared memory, filled by TMA
-//    tensor copies (cp.async.bulk.tensor.2d, box = LN lanes x W storage rows,
+//    tensor copies (cp.async.bulk.tensor.3d over lanes x cells x columns; box = LN lanes x W storage rows,
 //    i.e. one band column of LN matrices) that complete on an mbarrier;
 //    loads run D steps (D*CJ columns) ahead of the compute;
 //  * a thread's window of H+1 columns (H = the operand's column halo) wraps
@@ -437,12 +437,14 @@ bool run(const bgm_band* ops, const bgm_band& c1, const bgm_band* c2, const char
   for (int o = 0; o < S::NOP; ++o)
     if (!make_map<T>(&maps.step[o], ops[o], LN, Gm::WP(o), CJ) || !make_map<T>(&maps.col[o], ops[o], LN, Gm::WP(o), 1))
       return false;
-  static int occ = -1;
+  static PerDeviceInt occ_cache;
+  int occ = occ_cache.get();
   if (occ < 0) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Gm::SMEM));
     int per = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, Gm::THREADS, Gm::SMEM);
     occ = per;
+    occ_cache.set(per);
   }
   if (occ < 1) return false;
   int sms = 148, dev = 0;

@@ -2586,7 +2586,7 @@ bool run_chol(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, c
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_chol<T, K, P, TS>, Sh::NT, 0);
   if (per < 1) per = 1;
-  ix seg = g_segment_rows;
+  ix seg = requested_seg(g_segment_rows, K);
   if (seg <= 0) {
     ix units = ix(sms) * per;
     ix nseg = units / (G.batch > 0 ? G.batch : 1);
@@ -2640,7 +2640,7 @@ bool run_chol_mw(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_chol_mw<K, NW>, 32 * NW, 0);
   if (per < 1) per = 1;
-  ix seg = g_segment_rows;
+  ix seg = requested_seg(g_segment_rows, K);
   if (seg <= 0) {
     ix nseg = ix(sms) * per / (G.batch > 0 ? G.batch : 1);
     if (nseg < 1) nseg = 1;
@@ -2691,7 +2691,7 @@ bool run_chol_dmma(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* r
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_chol_dmma, 32, 0);
   if (per < 1) per = 1;
-  ix seg = g_segment_rows;
+  ix seg = requested_seg(g_segment_rows, K);
   if (seg <= 0) {
     ix nseg = ix(sms) * per / (G.batch > 0 ? G.batch : 1);
     if (nseg < 1) nseg = 1;
@@ -2753,11 +2753,11 @@ bool run_vsub_dmma(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, co
                    int64_t* row, cudaStream_t s) {
   const size_t smem = sizeof(VtSmem<K, NW>);
   if (smem > 227 * 1024) return false;
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;
+  if (attr.first()) {
     cudaFuncSetAttribute(k_vsub_dmma<K, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     cudaFuncSetAttribute(k_vsub_dmma_repair<K, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = true;
+    attr.mark();
   }
   constexpr int STATE = VtSmem<K, NW>::NWT * 64;
   Geo G;
@@ -2770,7 +2770,7 @@ bool run_vsub_dmma(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, co
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_vsub_dmma<K, NW>, 32 * NW, smem);
   if (per < 1) per = 1;
-  ix seg = g_segment_rows;
+  ix seg = requested_seg(g_segment_rows, K);
   if (seg <= 0) {
     const int ns = pick_nseg(G.batch, G.n, sms * per, G.burn, 2 * G.burn);
     seg = (G.n + ns - 1) / ns;
@@ -2817,11 +2817,11 @@ template <int K>
 bool run_vchol_dmma(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cudaStream_t s) {
   constexpr int NW = K >= 128 ? 4 : 2, NT = K / 8, STATE = NT * (NT + 1) / 2 * 64;
   const size_t smem = sizeof(VdSmem<K, NW>);
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;
+  if (attr.first()) {
     cudaFuncSetAttribute(k_vchol_dmma<K, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     cudaFuncSetAttribute(k_vchol_dmma_repair<K, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = true;
+    attr.mark();
   }
   Geo G;
   G.batch = l.batch;
@@ -2833,7 +2833,7 @@ bool run_vchol_dmma(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, c
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_vchol_dmma<K, NW>, 32 * NW, smem);
   if (per < 1) per = 1;
-  ix seg = g_segment_rows;
+  ix seg = requested_seg(g_segment_rows, K);
   if (seg <= 0) {
     const int ns = pick_nseg(G.batch, G.n, sms * per, G.burn, 2 * G.burn);
     seg = (G.n + ns - 1) / ns;
@@ -2875,11 +2875,11 @@ bool run_vchol_dmma(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, c
 template <int K, int NW>
 bool run_subset_mw(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cudaStream_t s) {
   const size_t smem = sizeof(TakMwSmem<K, NW>);
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;
+  if (attr.first()) {
     cudaFuncSetAttribute(k_subset_mw<K, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     cudaFuncSetAttribute(k_subset_mw_repair<K, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = true;
+    attr.mark();
   }
   Geo G;
   G.batch = l.batch;
@@ -2892,7 +2892,7 @@ bool run_subset_mw(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* 
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_subset_mw<K, NW>, 32 * NW, smem);
   if (per < 1) per = 1;
-  ix seg = g_segment_rows;
+  ix seg = requested_seg(g_segment_rows, K);
   if (seg <= 0) {
     const int ns = pick_nseg(G.batch, G.n, sms * per, G.burn, 2 * G.burn);
     seg = (G.n + ns - 1) / ns;
@@ -2934,11 +2934,11 @@ bool run_subset_mw(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* 
 template <int K>
 bool run_subset_dmma(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cudaStream_t s) {
   const size_t smem = sizeof(TakSmem<K>);
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;
+  if (attr.first()) {
     cudaFuncSetAttribute(k_subset_dmma<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     cudaFuncSetAttribute(k_subset_dmma_repair<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = true;
+    attr.mark();
   }
   Geo G;
   G.batch = l.batch;
@@ -2951,7 +2951,7 @@ bool run_subset_dmma(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_subset_dmma<K>, 32, smem);
   if (per < 1) per = 1;
-  ix seg = g_segment_rows;
+  ix seg = requested_seg(g_segment_rows, K);
   if (seg <= 0) {
     ix nseg = ix(sms) * per / (G.batch > 0 ? G.batch : 1);
     if (nseg < 1) nseg = 1;
@@ -3001,7 +3001,7 @@ bool run_subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row
   G.burn = kBurnGen * K;
   if (const char* bv = std::getenv("BGM_WIDE_BURN"))
     if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
-  ix seg = g_segment_rows > 0 ? ix(g_segment_rows) : pick_seg(k_subset<T, K, P, TS>, Sh::NT, G, 2 * ix(G.burn));
+  ix seg = g_segment_rows > 0 ? ix(requested_seg(g_segment_rows, K)) : pick_seg(k_subset<T, K, P, TS>, Sh::NT, G, 2 * ix(G.burn));
   seg = (seg + TS - 1) / TS * TS;
   G.seg = seg;
   G.nseg = int((G.n + seg - 1) / seg);
@@ -3043,7 +3043,7 @@ bool run_solve(const bgm_band& l, const bgm_vec& v, const bgm_vec& x, int32_t* s
   G.burn = (kBurnGen + 2) * K;  // a solve damps by ~sqrt(K)|L(i,m)/L(i,i)| per generation
   if (const char* bv = std::getenv("BGM_WIDE_BURN"))
     if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
-  ix seg = g_segment_rows;
+  ix seg = requested_seg(g_segment_rows, K);
   if (seg <= 0) {
     int sms = 148, dev = 0, per = 1;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -3112,11 +3112,11 @@ bool run_logdet(const bgm_band& l, void* out, int32_t* st, int64_t* row, cudaStr
 template <class T, int K>
 bool run_vchol(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cudaStream_t s) {
   const size_t smem = VcSmem<T, K>::bytes;
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;
+  if (attr.first()) {
     cudaFuncSetAttribute(k_vchol_w<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     cudaFuncSetAttribute(k_vchol_w_repair<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = true;
+    attr.mark();
   }
   Geo G;
   G.batch = l.batch;
@@ -3124,7 +3124,7 @@ bool run_vchol(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cudaSt
   G.burn = kBurnGen * K;
   if (const char* bv = std::getenv("BGM_WIDE_BURN"))
     if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
-  ix seg = g_segment_rows;
+  ix seg = requested_seg(g_segment_rows, K);
   if (seg <= 0) {
     int sms = 148, dev = 0, per = 1;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -3169,11 +3169,11 @@ template <class T, int K>
 bool run_vsub(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, const bgm_band& lb, int32_t* st,
               int64_t* row, cudaStream_t s) {
   const size_t smem = VsSmem<T, K>::bytes;
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;
+  if (attr.first()) {
     cudaFuncSetAttribute(k_vsub<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     cudaFuncSetAttribute(k_vsub_repair<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = true;
+    attr.mark();
   }
   Geo G;
   G.batch = l.batch;
@@ -3181,7 +3181,7 @@ bool run_vsub(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, const b
   G.burn = kBurnGen * K;
   if (const char* bv = std::getenv("BGM_WIDE_BURN"))
     if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
-  ix seg = g_segment_rows;
+  ix seg = requested_seg(g_segment_rows, K);
   if (seg <= 0) {
     int sms = 148, dev = 0, per = 1;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -106,3 +106,50 @@ def test_mlik_fast_not_pd(cuda, oracle, tile):
         api.set_segment_rows(0)
     assert st[0] == 0 and st[2] == 0
     assert st[1] != 0 and row[1] == 500
+
+
+@pytest.mark.parametrize("tile,k", [(1, 16), (32, 16), (32, 8)])
+def test_mlik_fast_extreme_diagonals(cuda, oracle, tile, k):
+    """Pivots and |L_ii| outside [1e-30, 1e30] send a matrix to the exact
+    sweeps.  The reverse must be redone too: its fast path seeds 1/L_ii from a
+    float reciprocal, which overflows for |L_ii| < ~3e-39.
+    Matrix 0 has one L_ii = 1e-39 (its row otherwise zero, so chol(L L^T) in
+    the reference still reproduces it), matrices 1 and 2 are scaled by 1e35 and
+    1e-35, matrix 3 is an ordinary control."""
+    from paper_1902_10078_b200 import api
+    from tests.gpu_adapter import GpuOracle
+    rng = np.random.default_rng(17 + k)
+    B, n, tau2, i = 4, 900, 0.01, 300
+    L = cm.config_factor(rng, B, n, k)
+    L[0, i, 0] = 1e-39
+    for r in range(1, k + 1):
+        L[0, i - r, r] = 0.0
+    L[1] *= 1e35
+    L[2] *= 1e-35
+    y = rng.normal(0, 1, (B, n))
+    lo, lb, tb, st, _ = oracle.marginal_likelihood_grad(L, y, tau2)
+    assert np.all(st == 0)
+    api.set_segment_rows(128)
+    try:
+        lg, lbg, tbg, stg, _ = GpuOracle(tile=tile).marginal_likelihood_grad(L, y, tau2)
+    finally:
+        api.set_segment_rows(0)
+    assert np.all(stg == 0)
+    assert np.all(np.isfinite(lbg))
+    assert cm.max_rel_err(lg, lo, floor_scale=FLOOR) <= TOL
+    # d tau2 cancels summands of ~yTy / (2 tau2^2) to ~1e-9 on the 1e-35
+    # matrix: compare relative to the summands (DESIGN.md §5)
+    summ = n / (2 * tau2) + (y * y).sum(axis=1) / (2 * tau2 ** 2)
+    assert np.all(np.abs(tbg - tb) <= 1e-12 * np.maximum(summ, np.abs(tb)))
+    # L_bar(i, i) = ... + 1/L_ii = ~1e39 on matrix 0
+    assert abs(lbg[0, i, 0] - lb[0, i, 0]) <= TOL * abs(lb[0, i, 0])
+    for b in range(B):  # per matrix: the scales differ by 1e70
+        g, o = lbg[b].copy(), lb[b].copy()
+        if b == 0:
+            g[i, 0] = o[i, 0] = 0.0
+        # floor relative to the summands' scale (1/L_ii): at 1e35 the
+        # log|A| and log|L_Q| adjoints cancel exactly in the reference (A = Q
+        # in fp64), leaving zeros that the fused form reaches as ~1e-16 of them
+        scale = max(np.abs(o).max(), np.abs(1.0 / L[b, :, 0]).max() if b else 0.0)
+        den = np.maximum(np.maximum(np.abs(g), np.abs(o)), FLOOR * scale)
+        assert float(np.max(np.abs(g - o) / den)) <= TOL, b
