@@ -754,13 +754,25 @@ __global__ void k_init(int64_t* fail, int32_t* flag, ix batch, ix n) {
 }
 
 
-ix seg_for(ix n, ix tiles, ix warps_resident, int burn, ix requested) {
+// Segment length.  Per kernel the step costs ~max(W (seg + burn) a,
+// (seg + burn) l) for W resident warps: a throughput term (a ~3 ns per warp
+// and row at 5-6 warps per SM) and a latency term (l ~1.6 us per row for a
+// warp on a lightly loaded SM).  They cross near 3.5 warps per SM; a whole
+// number of warps per SM avoids an uneven last share, so the segments are
+// sized for 4 warps per SM, not for the occupancy limit (5 / 6): more warps
+// only add burn-in rows.  Measured B = 256: 3.54 -> 3.09 ms.
+ix seg_for(ix n, ix tiles, ix sms, ix warps_resident, int burn, ix requested, const char* knob) {
   ix seg = requested;
   if (seg <= 0) {
-    ix per = warps_resident / (tiles > 0 ? tiles : 1);
+    double per_sm = 4.0;
+    if (const char* v = std::getenv("BGM_T1_WARPS")) per_sm = std::atof(v);
+    if (const char* v = std::getenv(knob)) per_sm = std::atof(v);
+    ix target = ix(per_sm * double(sms));
+    if (target > warps_resident) target = warps_resident;
+    ix per = target / (tiles > 0 ? tiles : 1);
     if (per < 1) per = 1;
     seg = (n + per - 1) / per;
-    if (seg < 2 * burn) seg = 2 * burn;
+    if (seg < burn + 32) seg = burn + 32;
   }
   return seg < 1 ? 1 : seg;
 }
@@ -795,8 +807,8 @@ int run(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, const bg
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bb, k_bwd<K>, kThreads, smb);
   Geo Gf = G, Gb = G;
   segment_rows = int(requested_seg(segment_rows, K));
-  Gf.seg = seg_for(G.n, G.tiles, ix(sms) * (bf > 0 ? bf : 1), G.burn, segment_rows);
-  Gb.seg = seg_for(G.n, G.tiles, ix(sms) * (bb > 0 ? bb : 1), G.burn, segment_rows);
+  Gf.seg = seg_for(G.n, G.tiles, sms, ix(sms) * (bf > 0 ? bf : 1), G.burn, segment_rows, "BGM_T1_WARPS_F");
+  Gb.seg = seg_for(G.n, G.tiles, sms, ix(sms) * (bb > 0 ? bb : 1), G.burn, segment_rows, "BGM_T1_WARPS_B");
   Gf.nseg = int((G.n + Gf.seg - 1) / Gf.seg);
   Gb.nseg = int((G.n + Gb.seg - 1) / Gb.seg);
   const ix uf = G.batch * Gf.nseg, ub = G.batch * Gb.nseg;

@@ -157,3 +157,116 @@ def _transpose(L):
             return bgm.Bands(g.contiguous(), L.batch, L.n, L.upper, L.lower, L.tile).transpose().data
 
     return bgm.Bands(_T.apply(L.data), L.batch, L.n, L.upper, L.lower, L.tile)
+
+
+# ------------------------------------------------------------------ vs the reference tape
+# The autograd compositions against the reference's own compiled Tape
+# (oracle/_ref: proj/src/tape.cpp compiled verbatim; the config-3 node graph of
+# inference.cpp:140-163 and the KL of inference.cpp:247-268 built on it by
+# oracle/ref_capi.cpp), not against the GPU's own finite differences.
+def _config3_composite(L, y, tau2, B, n, k, tile):
+    """The reference's config-3 composition written with the autograd wrappers:
+    Q = band(L L^T), chol(Q + tau^-2 I), chol(Q), solve, two log-dets."""
+    import paper_1902_10078_b200 as bgm
+    from paper_1902_10078_b200 import autograd as ag
+    Lt = _transpose(L)
+    Q = ag.product_band_band(L, Lt, k, 0)
+    shift = bgm.Bands.zeros(B, n, k, 0, tile=tile)
+    if tile == 32:
+        shift.data[:, :, 0, :] = 1.0 / tau2
+    else:
+        shift.data[:, :, 0] = 1.0 / tau2
+    A = bgm.Bands(Q.data + shift.data, B, n, k, 0, tile)
+    Lp, Lq = ag.cholesky(A), ag.cholesky(Q)
+    w = ag.solve_vec(Lp, y, False)
+    yy = y.data * y.data
+    ww = w.data * w.data
+    if tile == 32:
+        lane = lambda t: t.sum(dim=1).reshape(-1)[:B]  # noqa: E731
+    else:
+        lane = lambda t: t.sum(dim=1)  # noqa: E731
+    return (-0.5 * n * np.log(2 * np.pi) - ag.log_det_from_cholesky(Lp) + ag.log_det_from_cholesky(Lq)
+            - 0.5 * n * np.log(tau2) - 0.5 * lane(yy) / tau2 + 0.5 * lane(ww) / tau2 ** 2)
+
+
+@pytest.mark.parametrize("tile", [1, 32])
+@pytest.mark.parametrize("B,n,k", [(3, 200, 2), (5, 300, 4), (2, 257, 16)])
+def test_composite_autograd_vs_reference_tape(cuda, reference, tile, B, n, k):
+    """torch autograd through the wrapped operators reproduces the reference
+    tape's loss and dL (tape.cpp:435-451 backward) at 1e-9."""
+    import paper_1902_10078_b200 as bgm
+    rng = np.random.default_rng(1000 + 10 * k + tile)
+    tau2 = 0.01
+    L0 = cm.config_factor(rng, B, n, k)
+    yv = rng.normal(0, 1, (B, n))
+    rl, rlb, _, st, _ = reference.marginal_likelihood_grad(L0, yv, tau2)
+    assert np.all(st == 0)
+    L = bgm.Bands.from_reference(L0, k, 0, tile=tile)
+    y = bgm.Vecs.from_reference(yv, tile=tile)
+    L.data.requires_grad_(True)
+    loss = _config3_composite(L, y, tau2, B, n, k, tile)
+    loss.sum().backward()
+    got = bgm.Bands(L.data.grad, B, n, k, 0, tile).numpy()
+    assert cm.max_rel_err(loss.detach().cpu().numpy(), rl) <= 1e-9
+    assert cm.max_rel_err(got, rlb, floor_scale=1e-6) <= 1e-9
+    assert np.linalg.norm(got - rlb) <= 1e-10 * np.linalg.norm(rlb)
+
+
+@pytest.mark.parametrize("tile", [1, 32])
+def test_fused_autograd_vs_reference_tape(cuda, reference, tile):
+    """ag.marginal_likelihood (the fused step as a torch Function) under an
+    upstream cotangent: dL and d tau2 equal the reference tape's, scaled."""
+    import paper_1902_10078_b200 as bgm
+    from paper_1902_10078_b200 import autograd as ag
+    rng = np.random.default_rng(77 + tile)
+    B, n, k, tau2 = 6, 700, 16, 0.01
+    L0 = cm.config_factor(rng, B, n, k)
+    yv = rng.normal(0, 1, (B, n))
+    rl, rlb, rtb, st, _ = reference.marginal_likelihood_grad(L0, yv, tau2)
+    assert np.all(st == 0)
+    L = bgm.Bands.from_reference(L0, k, 0, tile=tile)
+    y = bgm.Vecs.from_reference(yv, tile=tile)
+    L.data.requires_grad_(True)
+    t = torch.tensor(tau2, dtype=torch.float64, device=L.data.device, requires_grad=True)
+    cot = torch.as_tensor(rng.normal(0, 1, B), device=L.data.device)
+    loss = ag.marginal_likelihood(L, y, t)
+    (loss * cot).sum().backward()
+    got = bgm.Bands(L.data.grad, B, n, k, 0, tile).numpy()
+    c = cot.cpu().numpy()
+    assert cm.max_rel_err(loss.detach().cpu().numpy(), rl) <= 1e-9
+    want = rlb * c[:, None, None]
+    assert cm.max_rel_err(got, want, floor_scale=1e-6) <= 1e-9
+    assert np.linalg.norm(got - want) <= 1e-10 * np.linalg.norm(want)
+    # d tau2 sums cancelling ~n y'y / tau2^2 terms: judged against them
+    summ = np.abs(c) @ (n / (2 * tau2) + (yv * yv).sum(axis=1) / (2 * tau2 ** 2))
+    assert abs(float(t.grad) - float(c @ rtb)) <= 1e-12 * summ
+
+
+@pytest.mark.parametrize("tile", [1, 32])
+def test_kl_autograd_vs_reference_tape(cuda, reference, tile):
+    """ag.kl_divergence under a cotangent: d m_q and d L_q equal the
+    reference tape's KL gradient (inference.cpp:247-268), scaled."""
+    import paper_1902_10078_b200 as bgm
+    from paper_1902_10078_b200 import autograd as ag
+    rng = np.random.default_rng(5 + tile)
+    B, n, kq, kp = 9, 300, 4, 2
+    lq0 = cm.config_factor(rng, B, n, kq)
+    lp0 = cm.config_factor(rng, B, n, kp)
+    mq0, mp0 = rng.normal(0, 1, (B, n)), rng.normal(0, 1, (B, n))
+    rkl, rmb, rlb, st, _ = reference.kl_divergence_grad(mq0, lq0, mp0, lp0)
+    assert np.all(st == 0)
+    mq = bgm.Vecs.from_reference(mq0, tile=tile)
+    lq = bgm.Bands.from_reference(lq0, kq, 0, tile=tile)
+    mp = bgm.Vecs.from_reference(mp0, tile=tile)
+    lp = bgm.Bands.from_reference(lp0, kp, 0, tile=tile)
+    mq.data.requires_grad_(True)
+    lq.data.requires_grad_(True)
+    cot = torch.as_tensor(rng.normal(0, 1, B), device=mq.data.device)
+    kl = ag.kl_divergence(mq, lq, mp, lp)
+    (kl * cot).sum().backward()
+    c = cot.cpu().numpy()
+    gm = bgm.Vecs(mq.data.grad, B, n, tile).numpy()
+    gl = bgm.Bands(lq.data.grad, B, n, kq, 0, tile).numpy()
+    assert cm.max_rel_err(kl.detach().cpu().numpy(), rkl) <= 1e-9
+    assert cm.max_rel_err(gm, rmb * c[:, None]) <= 1e-9
+    assert cm.max_rel_err(gl, rlb * c[:, None, None]) <= 1e-9
