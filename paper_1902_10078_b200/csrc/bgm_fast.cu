@@ -34,12 +34,14 @@ namespace fast {
 
 bool cholesky(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, cudaStream_t s) {
   if (disabled()) return false;
-  return narrow::cholesky(q, l, st, row, s) || wide::cholesky(q, l, st, row, s);
+  return narrow::cholesky(q, l, st, row, s) || wide::cholesky(q, l, st, row, s) ||
+         promote::cholesky(q, l, st, row, s);
 }
 bool solve_vec(const bgm_band& l, const bgm_vec& v, int tr, const bgm_vec& x, int32_t* st, int64_t* row,
                cudaStream_t s) {
   if (disabled()) return false;
-  return narrow::solve_vec(l, v, tr, x, st, row, s) || wide::solve_vec(l, v, tr, x, st, row, s);
+  return narrow::solve_vec(l, v, tr, x, st, row, s) || wide::solve_vec(l, v, tr, x, st, row, s) ||
+         promote::solve_vec(l, v, tr, x, st, row, s);
 }
 bool log_det(const bgm_band& l, void* out, int32_t* st, int64_t* row, cudaStream_t s) {
   if (disabled()) return false;
@@ -47,7 +49,7 @@ bool log_det(const bgm_band& l, void* out, int32_t* st, int64_t* row, cudaStream
 }
 bool subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cudaStream_t s) {
   if (disabled()) return false;
-  return narrow::subset(l, sb, st, row, s) || wide::subset(l, sb, st, row, s);
+  return narrow::subset(l, sb, st, row, s) || wide::subset(l, sb, st, row, s) || promote::subset(l, sb, st, row, s);
 }
 bool product(const bgm_band& a, int ta, const bgm_band& b, int tb, const bgm_band& c, cudaStream_t s) {
   if (disabled()) return false;
@@ -59,12 +61,13 @@ bool band_vec(const bgm_band& b, const bgm_vec& v, int tr, const bgm_vec& y, cud
 }
 bool vjp_cholesky(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cudaStream_t s) {
   if (disabled()) return false;
-  return narrow::vjp_cholesky(l, lb, qb, s) || wide::vjp_cholesky(l, lb, qb, s);
+  return narrow::vjp_cholesky(l, lb, qb, s) || wide::vjp_cholesky(l, lb, qb, s) ||
+         promote::vjp_cholesky(l, lb, qb, s);
 }
 bool vjp_subset(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, const bgm_band& lb, int32_t* st,
                 int64_t* row, cudaStream_t s) {
   if (disabled()) return false;
-  return wide::vjp_subset(l, sm, sb, lb, st, row, s);
+  return wide::vjp_subset(l, sm, sb, lb, st, row, s) || promote::vjp_subset(l, sm, sb, lb, st, row, s);
 }
 bool vjp_product(const bgm_band& a, const bgm_band& b, const bgm_band& pb, const bgm_band& ab,
                  const bgm_band& bb, cudaStream_t s) {

@@ -32,6 +32,17 @@ bool vjp_cholesky(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cud
 void set_segment_rows(int rows);
 }  // namespace narrow
 
+// Other bandwidths / layouts staged onto the compiled ones (bgm_promote.cu).
+namespace promote {
+bool cholesky(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, cudaStream_t s);
+bool solve_vec(const bgm_band& l, const bgm_vec& v, int tr, const bgm_vec& x, int32_t* st, int64_t* row,
+               cudaStream_t s);
+bool subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cudaStream_t s);
+bool vjp_cholesky(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cudaStream_t s);
+bool vjp_subset(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, const bgm_band& lb, int32_t* st,
+                int64_t* row, cudaStream_t s);
+}  // namespace promote
+
 // Band x band products with strided operand walks (bgm_product.cu).
 namespace prod {
 bool product(const bgm_band& a, int ta, const bgm_band& b, int tb, const bgm_band& c, cudaStream_t s);

@@ -46,3 +46,26 @@ def test_reference_tape_and_gradcheck_on_the_dropin(cuda):
     print(r.stdout[-3000:])
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert r.stdout.count("[PASS]") >= 27
+
+
+SCALE_DROPIN = os.path.join(ROOT, "oracle", "_ref", "scaling_dropin")
+SCALE_REF = os.path.join(ROOT, "oracle", "_ref", "scaling_ref")
+
+
+@pytest.mark.gpu
+def test_dropin_check_scaling_workload(cuda):
+    """acceptance.cpp:302-325's banded leg (bw = 5, n = 5e4 / 1e5 / 2e5, the
+    reference Tape's chol -> log-det -> backward) through the drop-in: no
+    super-linear growth, and faster than the reference kernels on this host
+    (the drop-in's narrow bands stage onto the segment-parallel kernels,
+    csrc/bgm_promote.cu, instead of one GPU thread per matrix)."""
+    import json
+    if not (os.path.exists(SCALE_DROPIN) and os.path.exists(SCALE_REF)):
+        pytest.skip("oracle/_ref/scaling_* not built (needs /root/reference at build time)")
+    got = json.loads(subprocess.run([SCALE_DROPIN], capture_output=True, text=True, timeout=900).stdout)["ms"]
+    ref = json.loads(subprocess.run([SCALE_REF], capture_output=True, text=True, timeout=900).stdout)["ms"]
+    print("drop-in", got, "reference", ref)
+    g = [got[k] for k in ("50000", "100000", "200000")]
+    r = [ref[k] for k in ("50000", "100000", "200000")]
+    assert g[1] / g[0] <= 2.8 and g[2] / g[1] <= 2.8
+    assert g[2] < r[2]
