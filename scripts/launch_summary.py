@@ -16,7 +16,14 @@ for r in rows:
     a = agg.setdefault(r["Kernel Name"][:70], [0, 0.0])
     a[0] += 1
     a[1] += v
-setup = lambda k: k.startswith("void at::") or "relayout" in k or "k_solve_vec" in k  # noqa: E731
+import os
+import re
+
+# kernels of the timed step (default: the fused config-3 sweeps); everything
+# else -- torch's input generation, the inputs' solve and relayout, the FP64
+# peak microbenchmarks -- runs outside the timed region
+STEP = re.compile(os.environ.get("STEP_RE", r"t1::|mlik"))
+setup = lambda k: not STEP.search(k)  # noqa: E731
 step = {k: t / c for k, (c, t) in agg.items() if not setup(k)}
 per_step = sum(step.values())
 print(sys.argv[2] if len(sys.argv) > 2 else "")

@@ -12,7 +12,7 @@ B = int(os.environ.get("PROF_B", "256"))
 n = int(os.environ.get("PROF_N", "65536"))
 reps = int(os.environ.get("PROF_REPS", "2"))
 dev = torch.device("cuda", 0)
-L, y = bench.make_inputs(B, n, 16, 1234, dev)
+L, y = bench.MlikWorkload.make_inputs(B, n, 16, 1234, dev)
 for _ in range(reps):
     loss, lbar, tb = bgm.marginal_likelihood_grad(L, y, 0.01)
 torch.cuda.synchronize()
