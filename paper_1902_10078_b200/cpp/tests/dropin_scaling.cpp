@@ -5,14 +5,19 @@
 // median of 5 after one warm-up, at n = 5e4, 1e5, 2e5.  oracle/Makefile builds
 // it twice from the same source: linked with the B200 drop-in
 // (_ref/scaling_dropin) and with the reference kernels compiled verbatim
-// (_ref/scaling_ref).  Prints one JSON line.
+// (_ref/scaling_ref).  A second leg times the operators alone, without the
+// Tape's host bookkeeping: ops::cholesky, ops::log_det_from_cholesky,
+// grad::vjp_log_det_from_cholesky, grad::vjp_cholesky on host buffers.
+// Prints one JSON line.
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <random>
 #include <vector>
 
+#include "bandgm/grad.hpp"
 #include "bandgm/gradcheck.hpp"
+#include "bandgm/kernels.hpp"
 #include "bandgm/tape.hpp"
 
 using namespace bandgm;
@@ -34,7 +39,25 @@ int main(int argc, char** argv) {
   const long bw = 5;
   std::vector<long> ns = {50000, 100000, 200000};
   if (argc > 1) ns = {std::atol(argv[1])};
-  std::printf("{\"bw\": %ld, \"ms\": {", bw);
+  std::printf("{\"bw\": %ld, \"ops_ms\": {", bw);
+  for (size_t q = 0; q < ns.size(); ++q) {
+    const long n = ns[q];
+    std::mt19937_64 rng(4000 + n);
+    const SymmetricBandedMatrix qm = gradcheck::random_spd_band(rng, n, bw);
+    const double ms = median_ms(
+        [&] {
+          const BandedMatrix l = ops::cholesky(qm);
+          volatile double v = ops::log_det_from_cholesky(l);
+          (void)v;
+          const BandedMatrix lb = grad::vjp_log_det_from_cholesky(l, 1.0);
+          const SymmetricBandedMatrix qb = grad::vjp_cholesky(l, lb);
+          volatile double z = qb(0, 0);
+          (void)z;
+        },
+        5);
+    std::printf("%s\"%ld\": %.4f", q ? ", " : "", n, ms);
+  }
+  std::printf("}, \"ms\": {");
   for (size_t q = 0; q < ns.size(); ++q) {
     const long n = ns[q];
     std::mt19937_64 rng(4000 + n);

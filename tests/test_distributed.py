@@ -62,3 +62,28 @@ def test_sharded_allreduce_matches_single_process(oracle):
     mp.spawn(_worker, args=(world, _free_port(), L, y, tau2, out), nprocs=world, join=True)
     for r in range(world):
         np.testing.assert_allclose(out[r], want, rtol=1e-13)
+
+
+def _bench_worker(rank, world, port, out):
+    """bench.py's strong-scaling arithmetic: each rank's slice of the batch,
+    the max-over-ranks step time, B_total * n / that time."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    a, b = bench.strong_slice(256, world, rank)
+    local_ms = 1.0 + rank  # rank 1 is the slow one
+    ms = bench.rank_max(local_ms, "cpu")
+    out[rank] = (a, b, ms, 256 * 65536 / (ms / 1e3))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_bench_strong_split_and_rank_max():
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_bench_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    assert (out[0][0], out[0][1], out[1][0], out[1][1]) == (0, 128, 128, 256)
+    assert out[0][2] == out[1][2] == 2.0  # both ranks report the slowest rank's time
+    assert out[0][3] == 256 * 65536 / 2e-3
