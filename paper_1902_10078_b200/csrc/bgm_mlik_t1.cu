@@ -39,6 +39,9 @@ constexpr int kThreads = 32;
 #ifndef T1_FWD_AHEAD
 #define T1_FWD_AHEAD 1  // forward L2 prefetch distance, in column pairs (measured best of 0-4)
 #endif
+#ifndef T1_FWD_SLOTS
+#define T1_FWD_SLOTS 2  // forward cp.async column-pair slots (prefetch distance in pairs)
+#endif
 #ifndef T1_BWD_PROGRESSIVE
 #define T1_BWD_PROGRESSIVE 0  // reverse: load the next row cell by cell inside the mat-vecs
 #endif
@@ -164,7 +167,11 @@ __device__ void fwd_unit(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, d
   constexpr int W = Sh::W;
   const ix n = G.n;
   auto Wr = [&](int a, int c) -> double& { return win[tri(a, c) * ts]; };
-  double* slot = win + Sh::NF * ts;  // [2 columns][W][thread], then [2 y][thread]
+  // T1_FWD_SLOTS slots of [2 columns][W][thread] + [2 y][thread]; pair(i)
+  // consumes one and refills it T1_FWD_SLOTS pairs ahead
+  constexpr int NS = T1_FWD_SLOTS, SLOTSZ = (2 * W + 2) * ts;
+  double* const slot0 = win + Sh::NF * ts;
+  double* slot = slot0;
   // per-thread bases: cell (r, column i) at Lt[i * cstep + r * 32], y_i at yt[i * 32]
   const ix cstep = ix(W) * 32;  // one column of one tile
   const ix tile0 = (b >> 5) * n, lane = b & 31;
@@ -231,23 +238,27 @@ __device__ void fwd_unit(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, d
   // written once per two rows with both rank-2 corrections applied:
   //   W''(a-2, b-2) = W(a, b) + l_a l_b - c_a c_b + m_{a-1} m_{b-1} - d_{a-1} d_{b-1}
   // (l, c: column i and its Cholesky column; m, d: the same for column i+1).
-  auto fetch2 = [&](ix i) {  // L columns i, i+1 and y_{i+K+1}, y_{i+K+2} -> slot (interior only)
+  // L columns i, i+1 and y_{i+K+1}, y_{i+K+2} -> slot dst (interior only)
+  auto fetch2 = [&](ix i, double* dst) {
     const double* Lq = Lt + i * cstep;
 #pragma unroll
     for (int r = 0; r < W; ++r) {
-      cpa8(slot + r * ts, Lq + r * 32);
-      cpa8(slot + (W + r) * ts, Lq + cstep + r * 32);
+      cpa8(dst + r * ts, Lq + r * 32);
+      cpa8(dst + (W + r) * ts, Lq + cstep + r * 32);
     }
-    cpa8(slot + 2 * W * ts, yt + (i + W) * 32);
-    cpa8(slot + (2 * W + 1) * ts, yt + (i + W + 1) * 32);
+    cpa8(dst + 2 * W * ts, yt + (i + W) * 32);
+    cpa8(dst + (2 * W + 1) * ts, yt + (i + W + 1) * 32);
     cpa_commit();
   };
   auto pair = [&](ix i) {
-    if ((threadIdx.x & 31) == 0 && i + W + 3 + 2 * kAhead < n) {
-      l2_prefetch(Lt + (i + 2 + 2 * kAhead) * cstep, 2 * W * 256);
-      l2_prefetch(yt + (i + W + 2 + 2 * kAhead) * 32, 512);
+    if ((threadIdx.x & 31) == 0 && i + W + 1 + 2 * (NS + kAhead) < n) {
+      l2_prefetch(Lt + (i + 2 * (NS + kAhead)) * cstep, 2 * W * 256);
+      l2_prefetch(yt + (i + W + 2 * (NS + kAhead)) * 32, 512);
     }
-    cpa_wait();
+    if (NS == 2)
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // this pair's slot; the next may be in flight
+    else
+      cpa_wait();
     const double y1 = slot[2 * W * ts], y2 = slot[(2 * W + 1) * ts];
     double l[W], m[W];
 #pragma unroll
@@ -284,8 +295,9 @@ __device__ void fwd_unit(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, d
 #pragma unroll
     for (int a = 1; a < W; ++a) res[a - 1] = fma(-dd[a], w1, res[a]);
     res[K] = y2;
-    // the slot's values have all been consumed: refill it two columns ahead
-    fetch2(i + 2);
+    // the slot's values have all been consumed: refill it NS pairs ahead
+    fetch2(i + 2 * NS, slot);
+    if (NS == 2) slot = slot == slot0 ? slot0 + SLOTSZ : slot0;
     // bulk: old rows 2..K-1, ascending packed index = in-place memmove order
 #pragma unroll
     for (int a = 2; a < K; ++a) {
@@ -350,12 +362,13 @@ __device__ void fwd_unit(const FwdP& P, const Geo& G, ix b, ix s, ix e, ix i0, d
     for (int r = 0; r < W; ++r) lcur[r] = lnext[r];
   };
 
-  // pairs while the refill of pair(i) -- L columns i+2, i+3 and y_{i+K+3},
-  // y_{i+K+4} -- stays inside the matrix: i + 4 + K < n
+  // pairs while the refill of pair(i) -- L columns i+2NS, i+2NS+1 and
+  // y_{i+2NS+K+1}, y_{i+2NS+K+2} -- stays inside the matrix
   ix i = i0;
-  const ix pair_end = n - 4 - K;
+  const ix pair_end = n - K - 2 - 2 * NS;
   if (i + 1 < e && i < pair_end) {
-    fetch2(i);
+    fetch2(i, slot0);
+    if (NS == 2) fetch2(i + 2, slot0 + SLOTSZ);
 #pragma unroll 1
     for (; i + 1 < e && i < pair_end; i += 2) pair(i);
     cpa_wait();
@@ -789,7 +802,8 @@ int run(const bgm_band& l, const bgm_vec& y, double tau2, double* loss, const bg
   if (const char* bv = std::getenv("BGM_BURN"))
     if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
   G.debug = std::getenv("BGM_DEBUG") != nullptr;
-  const size_t smf = sizeof(double) * (Sh::NF + 2 * Sh::W + 2) * kThreads, smb = sizeof(double) * Sh::NB * kThreads;
+  const size_t smf = sizeof(double) * (Sh::NF + T1_FWD_SLOTS * (2 * Sh::W + 2)) * kThreads,
+               smb = sizeof(double) * Sh::NB * kThreads;
   static PerDevice attrs;
   if (attrs.first()) {
     cudaFuncSetAttribute(k_fwd<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smf));
