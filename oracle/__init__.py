@@ -292,6 +292,19 @@ class Oracle:
         return el, mb, lb, st, row
 
     # ---------------------------------------------------------- reference only
+    def mlik_exact_ld(self, L, y, tau2):
+        """Config-3 loss, L_bar, tau2_bar along the banded route in x87 long
+        double (restatement library only; the yardstick of tests/test_exact.py),
+        rounded to float64."""
+        if self.which != "restatement":
+            raise RuntimeError("the long-double yardstick lives in the restatement library")
+        L, y = _f64(L), _f64(y)
+        B, n, w = L.shape
+        loss, lbar, tbar = np.zeros(B), np.zeros_like(L), np.zeros(B)
+        self._fn("mlik_exact_ld")(_i64(B), _i64(n), _i64(w - 1), _ptr(L), _ptr(y), C.c_double(tau2), _ptr(loss),
+                                   _ptr(lbar), _ptr(tbar))
+        return loss, lbar, tbar
+
     def run_grad_suite(self, seed: int, instances: int):
         if self.which != "reference":
             raise RuntimeError("gradcheck suite lives in the compiled reference only")

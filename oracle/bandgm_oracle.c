@@ -710,3 +710,108 @@ int orc_marginal_likelihood_grad(ix batch, ix n, ix bw, const double* L, const d
 }
 
 int orc_abi_version(void) { return 1; }
+
+/* ------------------------------------------------------------------------
+ * Accuracy yardstick (tests only): the config-3 quantities along the banded
+ * route in x87 long double (64-bit mantissa) -- the same mathematics as
+ * tests/exact.py (and bgm_mlik.cu's header), in C so that the full config-3
+ * size (n = 65536) takes seconds:
+ *   A = band(L L^T) + I/tau2 = Lp Lp^T, w = Lp^-1 y, u = Lp^-T w,
+ *   S = band(A^-1) by the Takahashi recursion (kernels_serial.cpp:80-104),
+ *   L_bar = -band_lower[(S + u u^T / tau2^2) L] + diag(1/L_ii),
+ *   loss and d tau2 as inference.cpp:140-163 differentiated.
+ * Outputs are rounded to double.  One matrix at a time, reference layout.
+ * ---------------------------------------------------------------------- */
+typedef long double ld_t;
+
+static void mlik_exact1(ix n, ix k, const double* L, const double* y, double tau2, double* loss,
+                        double* lbar, double* tbar) {
+  const ix w = k + 1;
+  const ld_t s = 1.0L / (ld_t)tau2, c4 = s * s;
+  ld_t* A = (ld_t*)calloc((size_t)(n * w), sizeof(ld_t));
+  ld_t* P = (ld_t*)calloc((size_t)(n * w), sizeof(ld_t));
+  ld_t* S = (ld_t*)calloc((size_t)(n * w), sizeof(ld_t));
+  ld_t* wv = (ld_t*)calloc((size_t)n, sizeof(ld_t));
+  ld_t* u = (ld_t*)calloc((size_t)n, sizeof(ld_t));
+#define LL(i, j) ((ld_t)L[(j) * w + ((i) - (j))]) /* lower band entry, i - j in [0, k] */
+#define AA(i, j) A[(j) * w + ((i) - (j))]
+#define PP(i, j) P[(j) * w + ((i) - (j))]
+#define SS(i, j) S[(j) * w + ((i) - (j))]
+  for (ix j = 0; j < n; ++j) /* A = band(L L^T) + s I */
+    for (ix r = 0; r < w && j + r < n; ++r) {
+      const ix i = j + r;
+      ld_t acc = 0;
+      for (ix m = imax(0, i - k); m <= j; ++m) acc += LL(i, m) * LL(j, m);
+      AA(i, j) = acc + (r == 0 ? s : 0);
+    }
+  for (ix i = 0; i < n; ++i) { /* Cholesky, kernels_serial.cpp:12-32 order */
+    const ix j0 = imax(0, i - k);
+    for (ix j = j0; j <= i; ++j) {
+      ld_t acc = 0;
+      for (ix m = j0; m < j; ++m) acc += PP(i, m) * PP(j, m);
+      if (i == j) PP(i, i) = sqrtl(AA(i, i) - acc);
+      else PP(i, j) = (AA(i, j) - acc) / PP(j, j);
+    }
+  }
+  for (ix i = 0; i < n; ++i) {
+    ld_t acc = 0;
+    for (ix m = imax(0, i - k); m < i; ++m) acc += PP(i, m) * wv[m];
+    wv[i] = ((ld_t)y[i] - acc) / PP(i, i);
+  }
+  for (ix i = n - 1; i >= 0; --i) {
+    ld_t acc = 0;
+    for (ix m = i + 1; m < imin(n, i + k + 1); ++m) acc += PP(m, i) * u[m];
+    u[i] = (wv[i] - acc) / PP(i, i);
+  }
+  for (ix j = n - 1; j >= 0; --j) /* Takahashi */
+    for (ix i = j; i >= imax(0, j - k); --i) {
+      ld_t acc = 0;
+      for (ix m = i + 1; m < imin(n, i + k + 1); ++m) {
+        const ld_t smj = m >= j ? SS(m, j) : SS(j, m);
+        acc += (PP(m, i) / PP(i, i)) * smj;
+      }
+      SS(j, i) = -acc + (i == j ? 1.0L / (PP(i, i) * PP(i, i)) : 0);
+    }
+  ld_t yy = 0, ww = 0, uu = 0, tr = 0, ldp = 0, ldl = 0;
+  for (ix j = 0; j < n; ++j) {
+    for (ix r = 0; r < w; ++r) {
+      const ix i = j + r;
+      if (i >= n) {
+        lbar[j * w + r] = 0.0;
+        continue;
+      }
+      ld_t acc = 0;
+      for (ix m = j; m < imin(n, j + k + 1); ++m) {
+        const ix d = i > m ? i - m : m - i;
+        const ld_t sim = d <= k ? (i >= m ? SS(i, m) : SS(m, i)) : 0;
+        acc += sim * LL(m, j) + c4 * u[i] * u[m] * LL(m, j);
+      }
+      lbar[j * w + r] = (double)(-acc + (r == 0 ? 1.0L / LL(j, j) : 0));
+    }
+    yy += (ld_t)y[j] * (ld_t)y[j];
+    ww += wv[j] * wv[j];
+    uu += u[j] * u[j];
+    tr += SS(j, j);
+    ldp += logl(PP(j, j));
+    ldl += logl(fabsl(LL(j, j)));
+  }
+  const ld_t nn = (ld_t)n, log2pi = 1.837877066409345483560659472811235279722794947275566825634L;
+  *loss = (double)(-0.5L * nn * log2pi - ldp + ldl - 0.5L * nn * logl((ld_t)tau2) - 0.5L * yy * s + 0.5L * ww * c4);
+  *tbar = (double)(-nn * 0.5L * s + 0.5L * yy * c4 + 0.5L * c4 * tr - ww * c4 * s + 0.5L * uu * c4 * c4);
+#undef LL
+#undef AA
+#undef PP
+#undef SS
+  free(A);
+  free(P);
+  free(S);
+  free(wv);
+  free(u);
+}
+
+int orc_mlik_exact_ld(ix batch, ix n, ix k, const double* L, const double* y, double tau2, double* loss,
+                      double* lbar, double* tbar) {
+  for (ix b = 0; b < batch; ++b)
+    mlik_exact1(n, k, L + b * n * (k + 1), y + b * n, tau2, loss + b, lbar + b * n * (k + 1), tbar + b);
+  return 0;
+}
