@@ -223,6 +223,19 @@ int bgm_elbo_poisson_grad(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p, 
                           int quad_points, double* elbo, double* kl, bgm_vec m_q_bar, bgm_band l_q_bar,
                           int32_t* status, int64_t* row, bgm_stream stream);
 
+/* The two ELBOs with a partial models::SelectionIndex (models.hpp:122-131,
+ * inference.cpp:45-100): `observed` is a 0/1 fp64 mask of the observed latents
+ * (same batch, n and tile as y); y (and weight) are scattered to full length
+ * (models::scatter), their unobserved entries ignored.  Only observed latents
+ * contribute to the expected log-likelihood and its gradients; the KL is over
+ * every latent, as in the reference. */
+int bgm_elbo_gaussian_grad_sel(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p, bgm_vec y, bgm_vec observed,
+                               double tau2, double* elbo, double* kl, bgm_vec m_q_bar, bgm_band l_q_bar,
+                               double* tau2_bar, int32_t* status, int64_t* row, bgm_stream stream);
+int bgm_elbo_poisson_grad_sel(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p, bgm_vec y, bgm_vec weight,
+                              bgm_vec observed, int quad_points, double* elbo, double* kl, bgm_vec m_q_bar,
+                              bgm_band l_q_bar, int32_t* status, int64_t* row, bgm_stream stream);
+
 /* infer::gauss_hermite (inference.cpp:120-137): quad_points ascending nodes x
  * and weights w (host arrays), by the Golub-Welsch eigen-decomposition. */
 int bgm_gauss_hermite(int quad_points, double* x, double* w);

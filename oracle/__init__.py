@@ -55,6 +55,20 @@ def _ptr(a: np.ndarray):
     return a.ctypes.data_as(_dp)
 
 
+def _opt(a):
+    """Pointer to an optional float64 array (None -> NULL); the array is kept
+    alive by the module-level holder until the next call."""
+    global _HOLD
+    if a is None:
+        _HOLD = None
+        return _dp()
+    _HOLD = np.ascontiguousarray(a, dtype=np.float64)
+    return _HOLD.ctypes.data_as(_dp)
+
+
+_HOLD = None
+
+
 def _f64(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.float64)
 
@@ -259,9 +273,11 @@ class Oracle:
                                        row.ctypes.data_as(_i64p))
         return kl, mb, lb, st, row
 
-    def elbo_gaussian_grad(self, mq, lq, mp, lp, y, tau2):
-        """infer::elbo (inference.cpp:276-287), GaussianLik, full observation;
-        reference (verbatim tape) only.  -> elbo, m_bar, l_bar, tau2_bar, st, row."""
+    def elbo_gaussian_grad(self, mq, lq, mp, lp, y, tau2, observed=None):
+        """infer::elbo (inference.cpp:276-287), GaussianLik; reference
+        (verbatim tape) only.  observed: optional (B, n) 0/1 mask of the
+        SelectionIndex (y scattered to full length); None = every latent.
+        -> elbo, m_bar, l_bar, tau2_bar, st, row."""
         if self.which != "reference":
             raise RuntimeError("elbo lives in the compiled reference tape only")
         mq, lq, mp, lp, y = _f64(mq), _f64(lq), _f64(mp), _f64(lp), _f64(y)
@@ -271,12 +287,13 @@ class Oracle:
         st, row = self._status(B)
         self._fn("elbo_gaussian_grad")(_i64(B), _i64(n), _i64(wq - 1), _i64(wp - 1), _ptr(mq), _ptr(lq), _ptr(mp),
                                        _ptr(lp), _ptr(y), C.c_double(tau2), _ptr(el), _ptr(mb), _ptr(lb), _ptr(tb),
-                                       st.ctypes.data_as(_i32p), row.ctypes.data_as(_i64p))
+                                       st.ctypes.data_as(_i32p), row.ctypes.data_as(_i64p), _opt(observed))
         return el, mb, lb, tb, st, row
 
-    def elbo_poisson_grad(self, mq, lq, mp, lp, y, weight, quad_points=20):
-        """infer::elbo (inference.cpp:276-287), PoissonLik, full observation,
-        Gauss-Hermite nodes from numpy's hermgauss; reference tape only."""
+    def elbo_poisson_grad(self, mq, lq, mp, lp, y, weight, quad_points=20, observed=None):
+        """infer::elbo (inference.cpp:276-287), PoissonLik, Gauss-Hermite
+        nodes from numpy's hermgauss; observed as in elbo_gaussian_grad;
+        reference tape only."""
         if self.which != "reference":
             raise RuntimeError("elbo lives in the compiled reference tape only")
         gx, gw = np.polynomial.hermite.hermgauss(quad_points)
@@ -288,7 +305,7 @@ class Oracle:
         self._fn("elbo_poisson_grad")(_i64(B), _i64(n), _i64(wq - 1), _i64(wp - 1), _ptr(mq), _ptr(lq), _ptr(mp),
                                       _ptr(lp), _ptr(y), _ptr(weight), _i64(quad_points), _ptr(_f64(gx)),
                                       _ptr(_f64(gw)), _ptr(el), _ptr(mb), _ptr(lb), st.ctypes.data_as(_i32p),
-                                      row.ctypes.data_as(_i64p))
+                                      row.ctypes.data_as(_i64p), _opt(observed))
         return el, mb, lb, st, row
 
     # ---------------------------------------------------------- reference only

@@ -337,7 +337,7 @@ int ref_marginal_likelihood_grad(ix batch, ix n, ix bw, const double* L, const d
 // (stored cells) come from Tape::backward.
 int ref_kl_divergence_grad(ix batch, ix n, ix bq, ix bp, const double* mq, const double* lq,
                            const double* mp, const double* lp, double* kl, double* mq_bar,
-                           double* lq_bar, std::int32_t* status, ix* row) {
+                           double* lq_bar, std::int32_t* status, ix* row, const double* obs) {
   over_batch(batch, [&](ix b) {
     status[b] = guarded(
         [&] {
@@ -370,15 +370,15 @@ int ref_kl_divergence_grad(ix batch, ix n, ix bq, ix bp, const double* mq, const
   return 0;
 }
 
-// infer::elbo (inference.cpp:276-287) for a GaussianLik observing every
-// latent: the Gaussian branch of expected_loglik (inference.cpp:52-63,
+// infer::elbo (inference.cpp:276-287) for a GaussianLik observing the
+// latents marked in obs (every latent when obs is null): the Gaussian branch of expected_loglik (inference.cpp:52-63,
 // anonymous in the reference, restated) joins the compiled reference Tape as
 // a linearized scalar over (m_q, diag_sym(subset(L_q))), minus the KL built
 // node for node as in ref_kl_divergence_grad.
 int ref_elbo_gaussian_grad(ix batch, ix n, ix bq, ix bp, const double* mq, const double* lq,
                            const double* mp, const double* lp, const double* y, double tau2,
                            double* elbo, double* mq_bar, double* lq_bar, double* tau2_bar,
-                           std::int32_t* status, ix* row) {
+                           std::int32_t* status, ix* row, const double* obs) {
   over_batch(batch, [&](ix b) {
     status[b] = guarded(
         [&] {
@@ -401,6 +401,10 @@ int ref_elbo_gaussian_grad(ix batch, ix n, ix bq, ix bp, const double* mq, const
           double value = 0.0, d_tau2 = 0.0;
           Eigen::VectorXd d_mean = Eigen::VectorXd::Zero(n), d_var = Eigen::VectorXd::Zero(n);
           for (ix i = 0; i < n; ++i) {
+            // SelectionIndex (models.hpp:122-128): the reference loops over
+            // sel.observed with y in selection order; here y is scattered to
+            // full length and obs marks the observed latents (null = all)
+            if (obs && obs[b * n + i] == 0.0) continue;
             const double r = yv(i) - mean(i);
             value += -0.5 * (std::log(tau2) + kLog2Pi) - (r * r + var(i)) / (2.0 * tau2);
             d_mean(i) = r / tau2;
@@ -429,15 +433,15 @@ int ref_elbo_gaussian_grad(ix batch, ix n, ix bq, ix bp, const double* mq, const
   return 0;
 }
 
-// infer::elbo (inference.cpp:276-287) for a PoissonLik observing every
-// latent: the Poisson branch of expected_loglik (inference.cpp:65-100,
+// infer::elbo (inference.cpp:276-287) for a PoissonLik observing the
+// latents marked in obs (every latent when obs is null): the Poisson branch of expected_loglik (inference.cpp:65-100,
 // restated) with the Gauss-Hermite rule passed in by the caller (the tests
 // use numpy's hermgauss, independent of the library's own Golub-Welsch),
 // joined to the compiled reference Tape as in ref_elbo_gaussian_grad.
 int ref_elbo_poisson_grad(ix batch, ix n, ix bq, ix bp, const double* mq, const double* lq,
                           const double* mp, const double* lp, const double* y, const double* wt,
                           ix nq, const double* ghx, const double* ghw, double* elbo, double* mq_bar,
-                          double* lq_bar, std::int32_t* status, ix* row) {
+                          double* lq_bar, std::int32_t* status, ix* row, const double* obs) {
   over_batch(batch, [&](ix b) {
     status[b] = guarded(
         [&] {
@@ -459,6 +463,7 @@ int ref_elbo_poisson_grad(ix batch, ix n, ix bq, ix bp, const double* mq, const 
           double value = 0.0;
           Eigen::VectorXd d_mean = Eigen::VectorXd::Zero(n), d_var = Eigen::VectorXd::Zero(n);
           for (ix i = 0; i < n; ++i) {
+            if (obs && obs[b * n + i] == 0.0) continue;  // SelectionIndex, as in the Gaussian case
             const double w = wv(i);
             if (w <= 0.0) throw std::invalid_argument("weight");
             const double m = mean(i), v = var(i);

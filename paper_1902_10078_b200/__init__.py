@@ -35,6 +35,7 @@ from .api import (  # noqa: F401
     product_band_band_restricted,
     prior_natural_params,
     product_band_vec,
+    selection,
     set_segment_rows,
     solve_mat,
     solve_vec,

@@ -576,9 +576,30 @@ def kl_divergence_grad(m_q: Vecs, l_q: Bands, m_p: Vecs, l_p: Bands, check: bool
     return kl, m_bar, l_bar
 
 
-def elbo_gaussian_grad(m_q: Vecs, l_q: Bands, m_p: Vecs, l_p: Bands, y: Vecs, tau2: float, check: bool = True):
-    """infer::elbo (inference.cpp:276-287) for a Gaussian likelihood that
-    observes every latent: E_q log N(y | F, tau2 I) - KL(q || p) per matrix.
+def selection(observed, batch: int, n: int, tile: int = 32, device=None) -> Vecs:
+    """models::SelectionIndex (models.hpp:122-128) as the device's 0/1 mask:
+    ``observed`` = sorted latent indices observed in every matrix of the batch
+    (or a (batch, n) boolean array).  Pair it with y / weight scattered to full
+    length (models::scatter, models.hpp:131); unobserved entries are ignored."""
+    obs = np.asarray(observed)
+    if obs.ndim == 2:
+        if obs.shape != (batch, n):
+            raise DimensionMismatch("selection mask shape")
+        mask = obs.astype(np.float64)
+    else:
+        idx = obs.astype(np.int64)
+        if idx.size and (idx.min() < 0 or idx.max() >= n or np.any(np.diff(idx) <= 0)):
+            raise BandgmError("selection indices must be sorted, unique and inside [0, n)")
+        mask = np.zeros((batch, n))
+        mask[:, idx] = 1.0
+    return Vecs.from_reference(mask, tile=tile, device=device)
+
+
+def elbo_gaussian_grad(m_q: Vecs, l_q: Bands, m_p: Vecs, l_p: Bands, y: Vecs, tau2: float, check: bool = True,
+                       observed: Vecs | None = None):
+    """infer::elbo (inference.cpp:276-287) for a Gaussian likelihood:
+    E_q log N(y | F, tau2 I) - KL(q || p) per matrix, over every latent or,
+    with ``observed`` (a ``selection`` mask), over the observed ones only.
     Returns (elbo[B], kl[B], m_q_bar, l_q_bar, tau2_bar[B]) -- the ELBO's
     gradient in the variational parameters and its tau2 partial."""
     if l_q.lower < l_p.lower:
@@ -592,15 +613,21 @@ def elbo_gaussian_grad(m_q: Vecs, l_q: Bands, m_p: Vecs, l_p: Bands, y: Vecs, ta
     elbo, kl, tb = (torch.empty(l_q.batch, dtype=torch.float64, device=dev) for _ in range(3))
     m_bar, l_bar = m_q.like(), l_q.like()
     st = _status_for(l_q.batch, dev, check)
-    _call("bgm_elbo_gaussian_grad", m_q.desc(), l_q.desc(), m_p.desc(), l_p.desc(), y.desc(), C.c_double(tau2),
-          C.c_void_p(elbo.data_ptr()), C.c_void_p(kl.data_ptr()), m_bar.desc(), l_bar.desc(),
-          C.c_void_p(tb.data_ptr()), *st.ptrs(), _stream())
+    if observed is None:
+        _call("bgm_elbo_gaussian_grad", m_q.desc(), l_q.desc(), m_p.desc(), l_p.desc(), y.desc(), C.c_double(tau2),
+              C.c_void_p(elbo.data_ptr()), C.c_void_p(kl.data_ptr()), m_bar.desc(), l_bar.desc(),
+              C.c_void_p(tb.data_ptr()), *st.ptrs(), _stream())
+    else:
+        _same(l_q, observed)
+        _call("bgm_elbo_gaussian_grad_sel", m_q.desc(), l_q.desc(), m_p.desc(), l_p.desc(), y.desc(),
+              observed.desc(), C.c_double(tau2), C.c_void_p(elbo.data_ptr()), C.c_void_p(kl.data_ptr()),
+              m_bar.desc(), l_bar.desc(), C.c_void_p(tb.data_ptr()), *st.ptrs(), _stream())
     _check(st, check)
     return elbo, kl, m_bar, l_bar, tb
 
 
 def elbo_poisson_grad(m_q: Vecs, l_q: Bands, m_p: Vecs, l_p: Bands, y: Vecs, weight: Vecs, quad_points: int = 20,
-                      check: bool = True):
+                      check: bool = True, observed: Vecs | None = None):
     """infer::elbo (inference.cpp:276-287) for a Poisson likelihood with
     exposure weights observing every latent; the expectation by
     ``quad_points``-node Gauss-Hermite quadrature (inference.cpp:65-100).
@@ -616,9 +643,15 @@ def elbo_poisson_grad(m_q: Vecs, l_q: Bands, m_p: Vecs, l_p: Bands, y: Vecs, wei
     elbo, kl = (torch.empty(l_q.batch, dtype=torch.float64, device=dev) for _ in range(2))
     m_bar, l_bar = m_q.like(), l_q.like()
     st = _status_for(l_q.batch, dev, check)
-    _call("bgm_elbo_poisson_grad", m_q.desc(), l_q.desc(), m_p.desc(), l_p.desc(), y.desc(), weight.desc(),
-          C.c_int(quad_points), C.c_void_p(elbo.data_ptr()), C.c_void_p(kl.data_ptr()), m_bar.desc(), l_bar.desc(),
-          *st.ptrs(), _stream())
+    if observed is None:
+        _call("bgm_elbo_poisson_grad", m_q.desc(), l_q.desc(), m_p.desc(), l_p.desc(), y.desc(), weight.desc(),
+              C.c_int(quad_points), C.c_void_p(elbo.data_ptr()), C.c_void_p(kl.data_ptr()), m_bar.desc(),
+              l_bar.desc(), *st.ptrs(), _stream())
+    else:  # partial SelectionIndex: only observed latents' weights are vetted
+        _same(l_q, observed)
+        _call("bgm_elbo_poisson_grad_sel", m_q.desc(), l_q.desc(), m_p.desc(), l_p.desc(), y.desc(), weight.desc(),
+              observed.desc(), C.c_int(quad_points), C.c_void_p(elbo.data_ptr()), C.c_void_p(kl.data_ptr()),
+              m_bar.desc(), l_bar.desc(), *st.ptrs(), _stream())
     if check:
         stn = st.st.cpu().numpy()
         bad = np.nonzero(stn == BGM_ERR_ARG)[0]

@@ -191,7 +191,7 @@ constexpr double kLog2Pi = 1.8378770664093454836;  // inference.cpp:15
 // per matrix sum_i -1/2 (log tau2 + log 2 pi) - ((y_i - m_i)^2 + v_i) / (2 tau2)
 // with v_i = S(i, i); d_mean_i = r_i / tau2 goes to dm, the tau2 partial to part2.
 __global__ void k_gauss_part(Vec<double> y, Vec<double> m, Band<double> S, double t2, ix batch, double* part,
-                             double* part2, Vec<double> dm) {
+                             double* part2, Vec<double> dm, Vec<double> obs, Vec<double> dv) {
   const ix nch = chunks(y.n);
   const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
   if (t >= batch * nch) return;
@@ -200,10 +200,18 @@ __global__ void k_gauss_part(Vec<double> y, Vec<double> m, Band<double> S, doubl
   const double lt = -0.5 * (log(t2) + kLog2Pi);
   double v = 0.0, dt = 0.0;
   for (ix i = c * kChunk; i < j1; ++i) {
+    // partial SelectionIndex (obs.p set): unobserved latents add nothing
+    // (inference.cpp:55-62 loops over sel.observed only)
+    if (obs.p && obs(mb, i) == 0.0) {
+      dm(mb, i) = 0.0;
+      dv(mb, i) = 0.0;
+      continue;
+    }
     const double r = y(mb, i) - m(mb, i), var = S.cell(mb, 0, i);
     v += lt - (r * r + var) / (2.0 * t2);
     dt += (r * r + var) / (2.0 * t2 * t2) - 0.5 / t2;
     dm(mb, i) = r / t2;
+    if (obs.p) dv(mb, i) = -0.5 / t2;
   }
   part[mb * nch + c] = v;
   part2[mb * nch + c] = dt;
@@ -246,6 +254,7 @@ struct GH {  // Gauss-Hermite rule, ascending nodes (inference.cpp:120-137)
 struct LikTerm {
   int kind;  // 0 Gaussian (tau2), 1 Poisson (weight, Gauss-Hermite)
   bgm_vec y, weight;
+  bgm_vec obs;  // 0/1 mask of the observed latents; data == null: all
   double tau2;
   GH gh;
   double* elbo;
@@ -257,7 +266,8 @@ struct LikTerm {
 // y log w - lgamma(y + 1), its mean / variance partials to dm / dv; the first
 // non-positive weight per matrix is recorded in bad (NonPositiveParam).
 __global__ void k_poisson_part(Vec<double> y, Vec<double> wt, Vec<double> m, Band<double> S, const GH gh, ix batch,
-                               double* part, Vec<double> dm, Vec<double> dv, unsigned long long* bad) {
+                               double* part, Vec<double> dm, Vec<double> dv, unsigned long long* bad,
+                               Vec<double> obs) {
   const ix nch = chunks(y.n);
   const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
   if (t >= batch * nch) return;
@@ -266,6 +276,11 @@ __global__ void k_poisson_part(Vec<double> y, Vec<double> wt, Vec<double> m, Ban
   const double norm = 1.0 / sqrt(3.14159265358979323846);
   double val = 0.0;
   for (ix i = c * kChunk; i < j1; ++i) {
+    if (obs.p && obs(mb, i) == 0.0) {  // unobserved latent (partial SelectionIndex)
+      dm(mb, i) = 0.0;
+      dv(mb, i) = 0.0;
+      continue;
+    }
     const double w = wt(mb, i), yi = y(mb, i), mi = m(mb, i), v = S.cell(mb, 0, i);
     if (!(w > 0.0)) {
       atomicMin(bad + mb, static_cast<unsigned long long>(i));
@@ -405,16 +420,19 @@ int vi_core(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p, double* kl, bg
   if (g && !ok_vec(g->y)) return BGM_ERR_ARG;
   if (g && g->kind == 0 && !(g->tau2 > 0.0)) return BGM_ERR_ARG;  // NonPositiveParam("tau2")
   if (g && g->kind == 1 && !ok_vec(g->weight)) return BGM_ERR_ARG;
+  const bool sel = g && g->obs.data;
+  if (sel && (!ok_vec(g->obs) || g->obs.dtype != BGM_F64)) return BGM_ERR_ARG;
   const ix B = l_q.batch, n = l_q.n;
   if (B > 0 && (!kl || (g && !g->elbo))) return BGM_ERR_ARG;
   const bool same = l_p.batch == B && m_q.batch == B && m_p.batch == B && m_q_bar.batch == B && l_q_bar.batch == B &&
                     l_p.n == n && m_q.n == n && m_p.n == n && m_q_bar.n == n && l_q_bar.n == n &&
                     (!g || (g->y.batch == B && g->y.n == n)) &&
-                    (!g || g->kind != 1 || (g->weight.batch == B && g->weight.n == n));
+                    (!g || g->kind != 1 || (g->weight.batch == B && g->weight.n == n)) &&
+                    (!sel || (g->obs.batch == B && g->obs.n == n));
   const int tile = l_q.tile;
   const bool tiles = l_p.tile == tile && m_q.tile == tile && m_p.tile == tile && m_q_bar.tile == tile &&
                      l_q_bar.tile == tile && (!g || g->y.tile == tile) &&
-                     (!g || g->kind != 1 || g->weight.tile == tile);
+                     (!g || g->kind != 1 || g->weight.tile == tile) && (!sel || g->obs.tile == tile);
   if (!same || !tiles || l_q.upper != 0 || l_p.upper != 0 || l_q_bar.lower != l_q.lower || l_q_bar.upper != 0 ||
       l_q.lower < l_p.lower)  // inference.cpp:252-253
     return BGM_ERR_DIM;
@@ -479,17 +497,22 @@ int vi_core(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p, double* kl, bg
   if ((rc = bgm_vjp_trace_product_sym(S, Qp, cb, Sb, none, stream))) return rc;
   const ix bwork = (B + tile - 1) / tile * tile * n;
   if (g) {
+    Vec<double> ov{};
+    if (sel) ov = view<double>(g->obs);
     if (g->kind == 0) {
       k_gauss_part<<<blocks_for(B * nch, kThreads), kThreads, 0, s>>>(view<double>(g->y), view<double>(m_q),
                                                                        view<double>(S), g->tau2, B, part, part2,
-                                                                       view<double>(dm));
+                                                                       view<double>(dm), ov, view<double>(dvv));
       if (g->tau2_bar) k_sum_parts<<<blocks_for(B, kThreads), kThreads, 0, s>>>(part2, nch, B, g->tau2_bar);
-      k_add_diag<<<blocks_for(bwork, kThreads), kThreads, 0, s>>>(view<double>(Sb), -0.5 / g->tau2, B);
+      if (sel)  // d_var = -1/(2 tau2) on the observed latents only
+        k_add_diag_vec<<<blocks_for(bwork, kThreads), kThreads, 0, s>>>(view<double>(Sb), view<double>(dvv), B);
+      else
+        k_add_diag<<<blocks_for(bwork, kThreads), kThreads, 0, s>>>(view<double>(Sb), -0.5 / g->tau2, B);
     } else {
       k_bad_init<<<blocks_for(B, kThreads), kThreads, 0, s>>>(bad, B, n);
       k_poisson_part<<<blocks_for(B * nch, kThreads), kThreads, 0, s>>>(
           view<double>(g->y), view<double>(g->weight), view<double>(m_q), view<double>(S), g->gh, B, part,
-          view<double>(dm), view<double>(dvv), bad);
+          view<double>(dm), view<double>(dvv), bad, ov);
       k_add_diag_vec<<<blocks_for(bwork, kThreads), kThreads, 0, s>>>(view<double>(Sb), view<double>(dvv), B);
     }
     k_sum_parts<<<blocks_for(B, kThreads), kThreads, 0, s>>>(part, nch, B, ve);
@@ -539,6 +562,34 @@ int bgm_elbo_poisson_grad(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p, 
   g.y = y;
   g.weight = weight;
   if (!vi::gauss_hermite(quad_points, g.gh)) return BGM_ERR_ARG;  // NonPositiveParam("quad_points")
+  g.elbo = elbo;
+  return vi::vi_core(m_q, l_q, m_p, l_p, kl, m_q_bar, l_q_bar, status, row, stream, &g);
+}
+
+int bgm_elbo_gaussian_grad_sel(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p, bgm_vec y, bgm_vec observed,
+                               double tau2, double* elbo, double* kl, bgm_vec m_q_bar, bgm_band l_q_bar,
+                               double* tau2_bar, int32_t* status, int64_t* row, bgm_stream stream) {
+  if (!observed.data) return BGM_ERR_ARG;
+  vi::LikTerm g{};
+  g.kind = 0;
+  g.y = y;
+  g.obs = observed;
+  g.tau2 = tau2;
+  g.elbo = elbo;
+  g.tau2_bar = tau2_bar;
+  return vi::vi_core(m_q, l_q, m_p, l_p, kl, m_q_bar, l_q_bar, status, row, stream, &g);
+}
+
+int bgm_elbo_poisson_grad_sel(bgm_vec m_q, bgm_band l_q, bgm_vec m_p, bgm_band l_p, bgm_vec y, bgm_vec weight,
+                              bgm_vec observed, int quad_points, double* elbo, double* kl, bgm_vec m_q_bar,
+                              bgm_band l_q_bar, int32_t* status, int64_t* row, bgm_stream stream) {
+  if (!observed.data) return BGM_ERR_ARG;
+  vi::LikTerm g{};
+  g.kind = 1;
+  g.y = y;
+  g.weight = weight;
+  g.obs = observed;
+  if (!vi::gauss_hermite(quad_points, g.gh)) return BGM_ERR_ARG;
   g.elbo = elbo;
   return vi::vi_core(m_q, l_q, m_p, l_p, kl, m_q_bar, l_q_bar, status, row, stream, &g);
 }

@@ -148,3 +148,57 @@ def test_elbo_poisson_vs_reference_tape(cuda, ref, tile, quad):
     with pytest.raises(bgm.BandgmError, match="weight"):
         bgm.elbo_poisson_grad(V(mq), bgm.Bands.from_reference(lq, kq, 0, tile=tile), V(mp),
                               bgm.Bands.from_reference(lp, kp, 0, tile=tile), V(y), V(wt), quad)
+
+
+# ---------------------------------------------------------------- partial SelectionIndex
+@pytest.mark.parametrize("tile", [1, 32])
+@pytest.mark.parametrize("frac", [0.0, 0.3, 1.0])
+def test_elbo_gaussian_partial_selection(cuda, ref, tile, frac):
+    """models::SelectionIndex observing a subset of the latents
+    (inference.cpp:45-63, 276-287): only observed latents enter the expected
+    log-likelihood; the GPU mask path against the reference tape."""
+    import paper_1902_10078_b200 as bgm
+    rng = np.random.default_rng(int(100 * frac) + tile)
+    B, n, kq, kp, tau2 = 9, 300, 4, 2, 0.3
+    mq, lq, mp, lp = _kl_inputs(rng, B, n, kq, kp)
+    idx = np.sort(rng.choice(n, int(frac * n), replace=False))
+    y = rng.normal(0, 1, (B, n))  # scattered to full length; unobserved entries ignored
+    obs = np.zeros((B, n))
+    obs[:, idx] = 1.0
+    V = lambda a: bgm.Vecs.from_reference(a, tile=tile)  # noqa: E731
+    el, kl, mb, lb, tb = bgm.elbo_gaussian_grad(V(mq), bgm.Bands.from_reference(lq, kq, 0, tile=tile), V(mp),
+                                                bgm.Bands.from_reference(lp, kp, 0, tile=tile), V(y), tau2,
+                                                observed=bgm.selection(idx, B, n, tile=tile))
+    rel, rmb, rlb, rtb, st, _ = ref.elbo_gaussian_grad(mq, lq, mp, lp, y, tau2, observed=obs)
+    assert np.all(st == 0)
+    assert cm.max_rel_err(el.cpu().numpy(), rel) <= TOL
+    assert cm.max_rel_err(mb.numpy(), rmb) <= TOL
+    assert cm.max_rel_err(lb.numpy(), rlb) <= TOL
+    assert cm.max_rel_err(tb.cpu().numpy(), rtb) <= TOL
+
+
+@pytest.mark.parametrize("tile", [1, 32])
+def test_elbo_poisson_partial_selection(cuda, ref, tile):
+    """Poisson with a partial selection: unobserved latents' weights are not
+    vetted (the reference only reads weight(i) for i in the selection)."""
+    import paper_1902_10078_b200 as bgm
+    rng = np.random.default_rng(41 + tile)
+    B, n, kq, kp, quad = 9, 257, 4, 2, 20
+    mq, lq, mp, lp = _kl_inputs(rng, B, n, kq, kp)
+    mq *= 0.3
+    idx = np.sort(rng.choice(n, 100, replace=False))
+    y = rng.poisson(1.5, (B, n)).astype(np.float64)
+    wt = rng.uniform(0.5, 2.0, (B, n))
+    unobs = np.setdiff1d(np.arange(n), idx)
+    wt[:, unobs[:5]] = 0.0  # invalid weights at unobserved latents: ignored
+    obs = np.zeros((B, n))
+    obs[:, idx] = 1.0
+    V = lambda a: bgm.Vecs.from_reference(a, tile=tile)  # noqa: E731
+    el, kl, mb, lb = bgm.elbo_poisson_grad(V(mq), bgm.Bands.from_reference(lq, kq, 0, tile=tile), V(mp),
+                                           bgm.Bands.from_reference(lp, kp, 0, tile=tile), V(y), V(wt), quad,
+                                           observed=bgm.selection(idx, B, n, tile=tile))
+    rel, rmb, rlb, st, _ = ref.elbo_poisson_grad(mq, lq, mp, lp, y, wt, quad, observed=obs)
+    assert np.all(st == 0)
+    assert cm.max_rel_err(el.cpu().numpy(), rel) <= TOL
+    assert cm.max_rel_err(mb.numpy(), rmb) <= TOL
+    assert cm.max_rel_err(lb.numpy(), rlb) <= TOL
