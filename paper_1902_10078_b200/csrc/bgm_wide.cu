@@ -488,6 +488,9 @@ struct SolveP {
 };
 
 constexpr int kSolveWarps = 4;  // units per CTA
+#ifndef WSOLVE_PF
+#define WSOLVE_PF 96  // L2 bulk-prefetch distance of the wide solves, rows
+#endif
 #ifndef WSOLVE_RING64
 #define WSOLVE_RING64 12
 #endif
@@ -531,7 +534,7 @@ __device__ void solve_unit(const SolveP<T>& C, ix b, ix n, ix s, ix e, ix start,
   const int dir = TR ? -1 : 1;
   const ix stop = TR ? s - 1 : e;
   // L2 prefetch of PB columns (and their v entries) PF columns ahead of the sweep
-  constexpr int PF = 96, PB = 16;
+  constexpr int PF = WSOLVE_PF, PB = 16;
   auto l2pf = [&](ix j0) {
     ix a = j0 < 0 ? 0 : j0, z = j0 + PB < n ? j0 + PB : n;
     if (a >= z) return;
