@@ -1,9 +1,9 @@
 """Operand bounds under guard pages (compute-sanitizer is closed on this GPU
 pool; tests/guarded.py places every operand flush against an unmapped guard
 region, after it or before it).  Each fast path runs on guarded copies of its
-operands and must neither fault nor change its result: this is how the
-round-2 y over-read in the paired forward sweep would have been caught
-(bgm_mlik_t1.cu, pair_end)."""
+operands and must neither fault nor change its result.  Checked to bite: on a
+build whose paired forward runs one pair row too far (the round-2 y over-read,
+bgm_mlik_t1.cu pair_end) the fused-step cases fail with an illegal address."""
 import numpy as np
 import pytest
 import torch
