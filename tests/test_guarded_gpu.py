@@ -103,3 +103,58 @@ def test_products_guarded(cuda, where):
     torch.cuda.synchronize()
     for a, b in zip(got, want):
         _same(a, b)
+
+
+@pytest.mark.parametrize("where", ["tail", "head"])
+@pytest.mark.parametrize("tile", [1, 32])
+def test_generic_and_misc_guarded(cuda, oracle, where, tile):
+    """The reference-loop kernels (forced, bgm_force_generic), solve_mat and
+    outer_band on guarded operands."""
+    import paper_1902_10078_b200 as bgm
+    lib = bgm.library()
+    rng = np.random.default_rng(11 + tile)
+    B, n, k = 5, 300, 3
+    q = cm.precision(oracle, cm.config_factor(rng, B, n, k), k)
+    Q = bgm.Bands.from_reference(q, k, 0, tile=tile)
+    v = bgm.Vecs.from_reference(rng.normal(0, 1, (B, n)), tile=tile)
+    R = bgm.Bands.from_reference(cm.zero_corners(rng.normal(0, 1, (B, n, 4)), 1, 2), 1, 2, tile=tile)
+
+    def run(Q, v, R):
+        L = bgm.cholesky(Q)
+        return [L, bgm.solve_vec(L, v, True), bgm.sparse_inverse_subset(L), bgm.solve_mat(L, R, 4, 2),
+                bgm.outer_band(v, v, 2, 1), bgm.log_det_from_cholesky(L)]
+
+    lib.bgm_force_generic(1)
+    try:
+        want = run(Q, v, R)
+        got = run(*(_guard(x, where) for x in (Q, v, R)))
+        torch.cuda.synchronize()
+    finally:
+        lib.bgm_force_generic(0)
+    for a, b in zip(got, want):
+        _same(a, b)
+
+
+@pytest.mark.parametrize("where", ["tail", "head"])
+def test_vi_objectives_guarded(cuda, where):
+    """KL and both ELBOs (with a partial selection) on guarded operands."""
+    import paper_1902_10078_b200 as bgm
+    rng = np.random.default_rng(5)
+    B, n, kq, kp = 33, 257, 4, 2
+    mq = bgm.Vecs.from_reference(rng.normal(0, 1, (B, n)) * 0.3)
+    lq = bgm.Bands.from_reference(cm.config_factor(rng, B, n, kq), kq, 0)
+    mp = bgm.Vecs.from_reference(rng.normal(0, 1, (B, n)))
+    lp = bgm.Bands.from_reference(cm.config_factor(rng, B, n, kp), kp, 0)
+    y = bgm.Vecs.from_reference(rng.poisson(1.5, (B, n)).astype(np.float64))
+    wt = bgm.Vecs.from_reference(rng.uniform(0.5, 2.0, (B, n)))
+    obs = bgm.selection(np.arange(0, n, 3), B, n)
+
+    def run(mq, lq, mp, lp, y, wt, obs):
+        return [*bgm.kl_divergence_grad(mq, lq, mp, lp), *bgm.elbo_gaussian_grad(mq, lq, mp, lp, y, 0.5, observed=obs),
+                *bgm.elbo_poisson_grad(mq, lq, mp, lp, y, wt, 20, observed=obs)]
+
+    want = run(mq, lq, mp, lp, y, wt, obs)
+    got = run(*(_guard(x, where) for x in (mq, lq, mp, lp, y, wt, obs)))
+    torch.cuda.synchronize()
+    for a, b in zip(got, want):
+        _same(a, b)
