@@ -253,6 +253,18 @@ int bgm_prior_natural_params(int64_t batch, int d, int64_t steps, const double* 
                              const double* q, const double* mu0, const double* sigma0, bgm_band lambda,
                              bgm_vec eta, int32_t* status, int64_t* row, bgm_stream stream);
 
+/* Reverse of bgm_prior_natural_params, the analytic replacement of the
+ * reference's central-difference compose_precision_gradient
+ * (inference.cpp:360-380) for this assembly: cotangents of Lambda (stored
+ * lower cells, grad.hpp:4-8) and eta -> cotangents of a, b, q, mu0, sigma0
+ * (device arrays shaped as the inputs).  Q_t and Sigma0 are read through their
+ * lower triangles (models.cpp:25-29), so their adjoints are lower-folded
+ * (upper entries 0).  Status as the forward (SingularBlock). */
+int bgm_vjp_prior_natural_params(int64_t batch, int d, int64_t steps, const double* a, const double* b,
+                                 const double* q, const double* mu0, const double* sigma0, bgm_band lambda_bar,
+                                 bgm_vec eta_bar, double* a_bar, double* b_bar, double* q_bar, double* mu0_bar,
+                                 double* sigma0_bar, int32_t* status, int64_t* row, bgm_stream stream);
+
 /* ------------------------------------------------- instrumentation */
 /* Per-kernel CUDA-event timing on the launching stream (off by default).
  * bgm_timing_enable(1) clears and starts recording; bgm_timing_read(i, ...)

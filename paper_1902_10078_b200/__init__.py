@@ -44,6 +44,7 @@ from .api import (  # noqa: F401
     vjp_cholesky,
     vjp_log_det_from_cholesky,
     vjp_outer_band,
+    vjp_prior_natural_params,
     vjp_product_band_band,
     vjp_product_band_vec,
     vjp_solve_mat,

@@ -697,6 +697,8 @@ def prior_natural_params(a, b, q, mu0, sigma0, tile: int = 32, check: bool = Tru
     n = (T + 1) * d
     lam = Bands.empty(B, n, 2 * d - 1, 0, tile, torch.float64, dev)
     eta = Vecs.empty(B, n, tile, torch.float64, dev)
+    if B % tile:
+        eta.data.zero_()  # padding lanes of a partial tile (lambda's are cleared on the device)
     st = _status_for(B, dev, check)
     _call("bgm_prior_natural_params", C.c_int64(B), C.c_int(d), C.c_int64(T), *(C.c_void_p(x.data_ptr()) for x in t),
           lam.desc(), eta.desc(), *st.ptrs(), _stream())
@@ -707,6 +709,34 @@ def prior_natural_params(a, b, q, mu0, sigma0, tile: int = 32, check: bool = Tru
             m = int(bad[0])
             raise SingularBlock(int(st.row[m]), m)
     return lam, eta
+
+
+def vjp_prior_natural_params(a, b, q, mu0, sigma0, lam_bar: Bands, eta_bar: Vecs, check: bool = True):
+    """Reverse of prior_natural_params: cotangents of (Lambda, eta) -> those
+    of (a, b, q, mu0, sigma0), analytically -- the replacement of the
+    reference's finite-difference compose_precision_gradient
+    (inference.cpp:360-380) for this assembly.  Lambda's cotangent follows the
+    stored-cell convention (grad.hpp:4-8); q and sigma0 are read through their
+    lower triangles, so their cotangents are lower-folded."""
+    dev = _device()
+    t = [torch.as_tensor(x, dtype=torch.float64).to(dev).contiguous() for x in (a, b, q, mu0, sigma0)]
+    a, b, q, mu0, sigma0 = t
+    B, T, d, _ = a.shape
+    n = (T + 1) * d
+    if (lam_bar.batch, lam_bar.n, lam_bar.lower, lam_bar.upper) != (B, n, 2 * d - 1, 0) or eta_bar.n != n:
+        raise DimensionMismatch("vjp_prior_natural_params: cotangent shapes do not agree")
+    bars = [torch.empty_like(x) for x in t]
+    st = _status_for(B, dev, check)
+    _call("bgm_vjp_prior_natural_params", C.c_int64(B), C.c_int(d), C.c_int64(T),
+          *(C.c_void_p(x.data_ptr()) for x in t), lam_bar.desc(), eta_bar.desc(),
+          *(C.c_void_p(x.data_ptr()) for x in bars), *st.ptrs(), _stream())
+    if check:
+        stn = st.st.cpu().numpy()
+        bad = np.nonzero(stn)[0]
+        if bad.size:
+            m = int(bad[0])
+            raise SingularBlock(int(st.row[m]), m)
+    return tuple(bars)
 
 
 # --------------------------------------------------------------------- config 3

@@ -293,3 +293,32 @@ def kl_divergence(m_q: Vecs, l_q: Bands, m_p: Vecs, l_p: Bands) -> torch.Tensor:
     differentiable in the variational parameters m_q and L_q (stored cells);
     the prior (m_p, L_p) is constant, as in the reference's VI objective."""
     return _KL.apply(m_q.data, l_q.data, m_p.data, l_p.data, (m_q.batch, m_q.n, m_q.tile), _meta(l_q), _meta(l_p))
+
+
+class _PriorNaturalParams(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, a, b, q, mu0, sigma0, tile):
+        lam, eta = api.prior_natural_params(a, b, q, mu0, sigma0, tile=tile)
+        ctx.save_for_backward(a, b, q, mu0, sigma0)
+        ctx.meta = (_meta(lam), (eta.batch, eta.n, eta.tile))
+        return lam.data, eta.data
+
+    @staticmethod
+    def backward(ctx, glam, geta):
+        a, b, q, mu0, sigma0 = ctx.saved_tensors
+        lmeta, vmeta = ctx.meta
+        lb = _bands(_g(glam).contiguous(), lmeta)
+        eb = _vecs(_g(geta).contiguous(), vmeta)
+        bars = api.vjp_prior_natural_params(a, b, q, mu0, sigma0, lb, eb)
+        return (*bars, None)
+
+
+def prior_natural_params(a, b, q, mu0, sigma0, tile: int = 32):
+    """models::prior_natural_params (models.cpp:165-189) as a torch Function:
+    (Lambda, eta) differentiable in a, b, q, mu0, sigma0 through the analytic
+    device VJP (bgm_vjp_prior_natural_params) -- with it, the gradient of any
+    objective of (Lambda, eta) with respect to model hyperparameters theta
+    follows by autograd through the user's theta -> (a, q, ...) map, replacing
+    the reference's finite-difference compose_precision_gradient
+    (inference.cpp:360-380).  Returns the Bands / Vecs storage tensors."""
+    return _PriorNaturalParams.apply(a, b, q, mu0, sigma0, tile)
