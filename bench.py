@@ -368,13 +368,11 @@ class MlikWorkload:
         return L, bgm.Vecs(x.data + eps, B, n, 1)
 
     def step(self):
-        import paper_1902_10078_b200 as bgm
-        from paper_1902_10078_b200.dist import reduce_totals
+        from paper_1902_10078_b200.dist import marginal_likelihood_grad_sharded
 
         # fused sweeps on this rank's matrices, then the one 2 x fp64 NCCL
         # all-reduce of (sum loss, sum d tau2) when world > 1
-        bgm.marginal_likelihood_grad(self.L, self.y, self.tau2, check=False, out=self.out)
-        return reduce_totals([self.loss, self.tbar])
+        return marginal_likelihood_grad_sharded(self.L, self.y, self.tau2, check=False, out=self.out)[0]
 
     def graphable(self, world):
         return world == 1  # the NCCL all-reduce stays outside the graph

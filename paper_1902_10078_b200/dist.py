@@ -32,10 +32,13 @@ def reduce_totals(per_matrix: list[torch.Tensor], group=None) -> torch.Tensor:
     return local
 
 
-def marginal_likelihood_grad_sharded(L, y, tau2: float, group=None, check: bool = True):
-    """Config-3 step on this rank's shard: local fused sweeps, then the global
-    (sum loss, sum tau2_bar).  Returns (totals[2], loss[B_local], l_bar, tau2_bar[B_local])."""
+def marginal_likelihood_grad_sharded(L, y, tau2: float, group=None, check: bool = True, out=None):
+    """Config-3 step on this rank's shard (the matrices shard_bounds gave it):
+    local fused sweeps, then the global (sum loss, sum tau2_bar) -- the one
+    16-byte all-reduce of the step.  ``out`` = preallocated (loss, l_bar,
+    tau2_bar, status) as for api.marginal_likelihood_grad (bench.py reuses
+    them across steps).  Returns (totals[2], loss[B_local], l_bar, tau2_bar[B_local])."""
     from .api import marginal_likelihood_grad
 
-    loss, l_bar, t_bar = marginal_likelihood_grad(L, y, tau2, check=check)
+    loss, l_bar, t_bar = marginal_likelihood_grad(L, y, tau2, check=check, out=out)
     return reduce_totals([loss, t_bar], group), loss, l_bar, t_bar
