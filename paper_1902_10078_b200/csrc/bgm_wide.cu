@@ -1601,19 +1601,21 @@ __device__ void subset_dmma_unit(const SubP<double>& C, ix b, ix n, ix s, ix e, 
     // (1) Linv = L_PP^-1 by forward substitution in the fragment layout
     {
       double M0 = rr == c2 ? 1.0 : 0.0, M1 = rr == c2 + 1 ? 1.0 : 0.0;
+      const double rme = 1.0 / lp[rr][rr];  // off the 8-step chain (see k_vsub_dmma)
+      double lr[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) lr[k] = rr > k ? lp[rr][k] : 0.0;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         if (rr == k) {
-          const double ri = 1.0 / lp[k][k];
-          M0 *= ri;
-          M1 *= ri;
+          M0 *= rme;
+          M1 *= rme;
         }
         const double mk0 = __shfl_sync(0xffffffffu, M0, 4 * k + q);
         const double mk1 = __shfl_sync(0xffffffffu, M1, 4 * k + q);
         if (rr > k) {
-          const double lrk = lp[rr][k];
-          M0 = fma(-lrk, mk0, M0);
-          M1 = fma(-lrk, mk1, M1);
+          M0 = fma(-lr[k], mk0, M0);
+          M1 = fma(-lr[k], mk1, M1);
         }
       }
       sm.linv[rr][c2] = M0;
@@ -1907,19 +1909,23 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
     // ---- (1) Linv (per warp), Y and Z_TP for the warp's tile rows
     {
       double M0 = rr == c2 ? 1.0 : 0.0, M1 = rr == c2 + 1 ? 1.0 : 0.0;
+      // this lane's row pivot reciprocal and row of L_PP, loaded / divided
+      // up front: only the shuffles and FMAs stay on the 8-step chain
+      const double rme = 1.0 / lp[sw8(rr, rr)];
+      double lr[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) lr[k] = rr > k ? lp[sw8(rr, k)] : 0.0;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         if (rr == k) {
-          const double ri = 1.0 / lp[sw8(k, k)];
-          M0 *= ri;
-          M1 *= ri;
+          M0 *= rme;
+          M1 *= rme;
         }
         const double mk0 = __shfl_sync(0xffffffffu, M0, 4 * k + q);
         const double mk1 = __shfl_sync(0xffffffffu, M1, 4 * k + q);
         if (rr > k) {
-          const double lrk = lp[sw8(rr, k)];
-          M0 = fma(-lrk, mk0, M0);
-          M1 = fma(-lrk, mk1, M1);
+          M0 = fma(-lr[k], mk0, M0);
+          M1 = fma(-lr[k], mk1, M1);
         }
       }
       put(lin, M0, M1);
@@ -2233,19 +2239,23 @@ __device__ void vchol_dmma_unit(const VdP<double>& C, ix b, ix n, ix s, ix e, ix
     double* lin = sm.lin[warp];
     {  // Linv (per warp)
       double M0 = rr == c2 ? 1.0 : 0.0, M1 = rr == c2 + 1 ? 1.0 : 0.0;
+      // this lane's row pivot reciprocal and row of L_PP, loaded / divided
+      // up front: only the shuffles and FMAs stay on the 8-step chain
+      const double rme = 1.0 / lp[sw8(rr, rr)];
+      double lr[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) lr[k] = rr > k ? lp[sw8(rr, k)] : 0.0;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         if (rr == k) {
-          const double ri = 1.0 / lp[sw8(k, k)];
-          M0 *= ri;
-          M1 *= ri;
+          M0 *= rme;
+          M1 *= rme;
         }
         const double mk0 = __shfl_sync(0xffffffffu, M0, 4 * k + q);
         const double mk1 = __shfl_sync(0xffffffffu, M1, 4 * k + q);
         if (rr > k) {
-          const double lrk = lp[sw8(rr, k)];
-          M0 = fma(-lrk, mk0, M0);
-          M1 = fma(-lrk, mk1, M1);
+          M0 = fma(-lr[k], mk0, M0);
+          M1 = fma(-lr[k], mk1, M1);
         }
       }
       put(lin, M0, M1);
@@ -2482,19 +2492,23 @@ __device__ void subset_mw_unit(const SubP<double>& C, ix b, ix n, ix s, ix e, ix
     double* lin = sm.lin[warp];
     {  // Linv (per warp)
       double M0 = rr == c2 ? 1.0 : 0.0, M1 = rr == c2 + 1 ? 1.0 : 0.0;
+      // this lane's row pivot reciprocal and row of L_PP, loaded / divided
+      // up front: only the shuffles and FMAs stay on the 8-step chain
+      const double rme = 1.0 / lp[sw8(rr, rr)];
+      double lr[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) lr[k] = rr > k ? lp[sw8(rr, k)] : 0.0;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         if (rr == k) {
-          const double ri = 1.0 / lp[sw8(k, k)];
-          M0 *= ri;
-          M1 *= ri;
+          M0 *= rme;
+          M1 *= rme;
         }
         const double mk0 = __shfl_sync(0xffffffffu, M0, 4 * k + q);
         const double mk1 = __shfl_sync(0xffffffffu, M1, 4 * k + q);
         if (rr > k) {
-          const double lrk = lp[sw8(rr, k)];
-          M0 = fma(-lrk, mk0, M0);
-          M1 = fma(-lrk, mk1, M1);
+          M0 = fma(-lr[k], mk0, M0);
+          M1 = fma(-lr[k], mk1, M1);
         }
       }
       put(lin, M0, M1);
