@@ -1248,8 +1248,10 @@ __device__ void chol_dmma_unit(const CholP<double>& C, ix b, ix n, ix s, ix e, i
     for (int p = 0; p < 8; ++p) {
       const double dpp = __shfl_sync(0xffffffffu, pick(D, p & 1), 4 * p + (p >> 1));
       if (lane == 0 && g + p >= s && g + p < n && !(dpp > kPivotFloor)) fail = fail < g + p ? fail : g + p;
-      const double piv = sqrt(dpp);
-      rinv[p] = 1.0 / piv;
+      // 1/sqrt by the reciprocal square root, the pivot from it: one MUFU
+      // sequence on the 8-step chain instead of a sqrt and a division
+      const double ri = rsqrt(dpp), piv = dpp * ri;
+      rinv[p] = ri;
       if (q == (p >> 1)) {
         if (rr > p) D[p & 1] *= rinv[p];
         else if (rr == p) D[p & 1] = piv;
@@ -1411,7 +1413,7 @@ __device__ void chol_mw_unit(const CholP<double>& C, ix b, ix n, ix s, ix e, ix 
       for (int p = 0; p < 8; ++p) {
         const double dpp = __shfl_sync(0xffffffffu, pick(D, p & 1), 4 * p + (p >> 1));
         if (lane == 0 && g + p >= s && g + p < n && !(dpp > kPivotFloor)) fail = fail < g + p ? fail : g + p;
-        const double piv = sqrt(dpp), ri = 1.0 / piv;
+        const double ri = rsqrt(dpp), piv = dpp * ri;  // one MUFU sequence on the chain (see k_chol_dmma)
         if (lane == 0) sm.rinv[p] = ri;
         if (q == (p >> 1)) {
           if (rr > p) D[p & 1] *= ri;
