@@ -82,6 +82,11 @@ __device__ __forceinline__ void cpa(T* dst, const T* src) {
   else
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
 }
+// 1 / sqrt(x) by the reciprocal square root: the Cholesky pivot chains take
+// one MUFU sequence per row instead of a square root and a division
+__device__ __forceinline__ double rsq_t(double x) { return rsqrt(x); }
+__device__ __forceinline__ float rsq_t(float x) { return rsqrtf(x); }
+
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
@@ -149,7 +154,7 @@ __device__ void chol_unit(const CholP<T>& C, ix b, ix n, ix s, ix e, ix i0, T* s
     }
     const T d0 = Wr(0, 0);
     if (!(double(d0) > kPivotFloor) && i >= s) fail = fail < i ? fail : i;
-    const T p0 = sqrt(d0), r0 = T(1) / p0;
+    const T r0 = rsq_t(d0), p0 = d0 * r0;  // one MUFU sequence on the pivot chain
     T c[W];
     c[0] = p0;
 #pragma unroll
@@ -159,7 +164,7 @@ __device__ void chol_unit(const CholP<T>& C, ix b, ix n, ix s, ix e, ix i0, T* s
     auto v = [&](int a1) { return a1 + 1 < K ? fma(-c[a1 + 1], c[1], Wr(a1 + 1, 1)) : fma(-c[K], c[1], q0[1]); };
     const T d1 = v(0);
     if (!(double(d1) > kPivotFloor) && i + 1 >= s) fail = fail < i + 1 ? fail : i + 1;
-    const T p1 = sqrt(d1), r1 = T(1) / p1;
+    const T r1 = rsq_t(d1), p1 = d1 * r1;
     T dd[W];
     dd[0] = p1;
 #pragma unroll
@@ -195,7 +200,7 @@ __device__ void chol_unit(const CholP<T>& C, ix b, ix n, ix s, ix e, ix i0, T* s
     load_row(i + K + 1, qn);  // one row ahead
     const T d = Wr(0, 0);
     if (!(double(d) > kPivotFloor) && i >= s) fail = fail < i ? fail : i;
-    const T piv = sqrt(d), rinv = T(1) / piv;
+    const T rinv = rsq_t(d), piv = d * rinv;
     T l[W];
     l[0] = piv;
 #pragma unroll
