@@ -19,6 +19,9 @@ bool vjp_cholesky(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, cud
 bool vjp_subset(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, const bgm_band& lb, int32_t* st,
                 int64_t* row, cudaStream_t s);
 void set_segment_rows(int rows);
+// look-ahead DMMA Cholesky, k = 64 / 128, fp64 (bgm_wide_la.cu)
+bool cholesky_la(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, cudaStream_t s,
+                 int segment_rows);
 
 }  // namespace wide
 
