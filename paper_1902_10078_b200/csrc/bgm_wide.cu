@@ -3364,9 +3364,9 @@ bool cholesky(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, c
           const char* e = std::getenv("BGM_WIDE_DMMA_WARPS");
           return e ? std::atoi(e) : 0;  // 0: look-ahead kernel
         }();
+        if (nw == 0 && cholesky_la(q, l, st, row, s, g_segment_rows)) return true;
         if (nw == 2) return run_chol_mw<64, 2>(q, l, st, row, s);
-        if (nw == 1) return run_chol_dmma(q, l, st, row, s);
-        return cholesky_la(q, l, st, row, s, g_segment_rows);
+        return run_chol_dmma(q, l, st, row, s);
       }
       return f64 ? run_chol<double, 64, 8, 9>(q, l, st, row, s) : run_chol<float, 64, 8, 9>(q, l, st, row, s);
     }
@@ -3381,9 +3381,9 @@ bool cholesky(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, c
           return e ? std::atoi(e) : 0;  // 0: look-ahead kernel
         }();
         if (nw == 8) return run_chol_mw<128, 8>(q, l, st, row, s);
+        if (nw == 0 && cholesky_la(q, l, st, row, s, g_segment_rows)) return true;
         if (nw == 2) return run_chol_mw<128, 2>(q, l, st, row, s);
-        if (nw == 4) return run_chol_mw<128, 4>(q, l, st, row, s);
-        return cholesky_la(q, l, st, row, s, g_segment_rows);
+        return run_chol_mw<128, 4>(q, l, st, row, s);
       }
       return f64 ? run_chol<double, 128, 16, 9>(q, l, st, row, s) : run_chol<float, 128, 16, 9>(q, l, st, row, s);
     }

@@ -122,11 +122,19 @@ __device__ __forceinline__ int ppos(int c) { return (c & 3) * 2 + (c >> 2); }
 
 template <int K, int NW>
 struct LASmem {
-  double dt[64];    // minus the next diagonal tile, on its way to the sequential factorisation
+  double dt[64];    // the next diagonal tile, on its way to the sequential factorisation
   double l00[64];   // L00, row-major, lower part
-  double nlinv[64]; // -L00^-1, row-major, upper part zero
-  double pft[K / 8 + 1][64];  // panel tiles, permuted rows
+  double linv[64];  // L00^-1, row-major, upper part zero
+  double pft[K / 8 + 1][64];   // panel tiles, permuted rows
+  double npft[K / 8 + 1][64];  // minus the panel tiles (the A operands of the update)
+  double fresh[2][32];         // warp 0's fresh diagonal tile, per lane, by cp.async
 };
+
+__device__ __forceinline__ void cpa8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(unsigned(__cvta_generic_to_shared(dst))), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ void dmma4(double& d0, double& d1, double a, double b, double c0, double c1) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%4, %5};"
@@ -150,19 +158,19 @@ __device__ __forceinline__ double rsqrt_nr(double d) {
   return h + h;
 }
 
-// Every lane factors minus the 8x8 tile in `dt` (lower part) and publishes L00
-// and minus its inverse.  `piv(j, d)` sees pivot j before its square root;
+// Every lane factors the 8x8 tile in `dt` (lower part) and publishes L00 and
+// its inverse.  `piv(j, d)` sees pivot j before its square root;
 // `hook(j)` runs after elimination step j (independent work to interleave).
 template <class F, class H>
-__device__ __forceinline__ void chol8_seq(const double* dt, double* l00, double* nlinv, F&& piv, H&& hook) {
+__device__ __forceinline__ void chol8_seq(const double* dt, double* l00, double* linv, F&& piv, H&& hook) {
   double a[8][8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j <= i; j += 2) {
       const double2 v = *reinterpret_cast<const double2*>(dt + i * 8 + j);
-      a[i][j] = -v.x;
-      if (j + 1 <= i) a[i][j + 1] = -v.y;
+      a[i][j] = v.x;
+      if (j + 1 <= i) a[i][j + 1] = v.y;
     }
   double ri[8];
 #pragma unroll
@@ -184,13 +192,13 @@ __device__ __forceinline__ void chol8_seq(const double* dt, double* l00, double*
 #pragma unroll
     for (int j = 0; j <= i; j += 2)
       *reinterpret_cast<double2*>(l00 + i * 8 + j) = make_double2(a[i][j], j + 1 <= i ? a[i][j + 1] : 0.0);
-  // minus the inverse, two columns at a time: w(i, j) = -(L^-1)(i, j)
+  // the inverse, two columns at a time
 #pragma unroll
   for (int jp = 0; jp < 8; jp += 2) {
     double w0[8], w1[8];
-    w0[jp] = -ri[jp];
+    w0[jp] = ri[jp];
     w1[jp] = 0.0;
-    w1[jp + 1] = -ri[jp + 1];
+    w1[jp + 1] = ri[jp + 1];
 #pragma unroll
     for (int i = jp + 1; i < 8; ++i) {
       double s0 = a[i][jp] * w0[jp];
@@ -205,7 +213,7 @@ __device__ __forceinline__ void chol8_seq(const double* dt, double* l00, double*
       }
     }
 #pragma unroll
-    for (int i = jp; i < 8; ++i) *reinterpret_cast<double2*>(nlinv + i * 8 + jp) = make_double2(w0[i], w1[i]);
+    for (int i = jp; i < 8; ++i) *reinterpret_cast<double2*>(linv + i * 8 + jp) = make_double2(w0[i], w1[i]);
   }
 }
 
@@ -215,7 +223,7 @@ struct Mode {
 };
 
 template <int K, int NW, int W>
-__device__ void chol_la_unit(const CholP& C, ix b, ix n, ix s, ix e, ix i0, double* side, LASmem<K, NW>& sm) {
+__device__ void chol_la_unit(const CholP& C, ix b, int n, int s, int e, int i0, double* side, LASmem<K, NW>& sm) {
   using M = LA<K, NW>;
   constexpr int T = M::T;
   const int lane = threadIdx.x & 31, rr = lane >> 2, q = lane & 3, c2 = 2 * q;
@@ -231,15 +239,15 @@ __device__ void chol_la_unit(const CholP& C, ix b, ix n, ix s, ix e, ix i0, doub
     if (r >= n) return r == c ? 1.0 : 0.0;
     return Q.cell(b, int(r - c), c);
   };
-  auto store_l = [&](ix g, int I, double x0, double x1) {  // general: rows 8I + rr of columns g + c2 + v
+  auto store_l = [&](int g, int I, double x0, double x1) {  // general: rows 8I + rr of columns g + c2 + v
 #pragma unroll
     for (int v = 0; v < 2; ++v) {
       const int c = c2 + v, cell = 8 * I + rr - c;
-      const ix col = g + c;
+      const int col = g + c;
       if (cell >= 0 && cell <= K && col < n) {
         const double val = (col + cell < n) ? (v ? x1 : x0) : 0.0;
         if (col >= s) L.cell(b, cell, col) = val;
-        else if (side && col >= s - K) side[(col - (s - K)) * (K + 1) + cell] = val;
+        else if (side && col >= s - K) side[ix(col - (s - K)) * (K + 1) + cell] = val;
       }
     }
   };
@@ -250,40 +258,45 @@ __device__ void chol_la_unit(const CholP& C, ix b, ix n, ix s, ix e, ix i0, doub
   double* const lb = &L.cell(b, 0, 0);
   const int pw0 = rr * 8 + ppos(c2), pw1 = rr * 8 + ppos(c2 + 1), pr = rr * 8 + c2;
   constexpr int NTW = M::ntiles(W) > 0 ? M::ntiles(W) : 1;
-  double wt[NTW][2];  // MINUS the Schur window (so the update is a plain accumulate)
+  double wt[NTW][2];  // the Schur window
 #pragma unroll
   for (int d = 0; d < T; ++d)
     if (M::owner(d) == W)
 #pragma unroll
       for (int J = 0; J < T - d; ++J)
 #pragma unroll
-        for (int v = 0; v < 2; ++v) wt[M::slot(W, d, J)][v] = -qval(i0 + 8 * (J + d) + rr, i0 + 8 * J + c2 + v);
-  ix fail = n;
-  auto piv = [&](ix gp) {
-    return [&fail, gp, s, n](int j, double d) {
-      if (!(d > kPivotFloor) && gp + j >= s && gp + j < n) fail = fail < gp + j ? fail : gp + j;
-    };
+        for (int v = 0; v < 2; ++v) wt[M::slot(W, d, J)][v] = qval(i0 + 8 * (J + d) + rr, i0 + 8 * J + c2 + v);
+  int fail = n;
+  unsigned bad = 0;  // pivots of the tile being factored that are not above the floor
+  auto piv = [&bad](int j, double d) { bad |= unsigned(!(d > kPivotFloor)) << j; };
+  auto settle = [&](int gp) {  // first bad pivot of panel gp inside [s, n)
+    if (bad) {
+      for (int j = 7; j >= 0; --j)
+        if ((bad >> j & 1) && gp + j >= s && gp + j < n) fail = fail < gp + j ? fail : gp + j;
+      bad = 0;
+    }
   };
-  if (threadIdx.x < 64) sm.nlinv[threadIdx.x] = 0.0;
+  if (threadIdx.x < 64) sm.linv[threadIdx.x] = 0.0;
   __syncthreads();
   if (W == 0) {
     const double* D = wt[M::slot(W, 0, 0)];
     *reinterpret_cast<double2*>(sm.dt + pr) = make_double2(D[0], D[1]);
     __syncwarp();
-    chol8_seq(sm.dt, sm.l00, sm.nlinv, piv(i0), [](int) {});
+    chol8_seq(sm.dt, sm.l00, sm.linv, piv, [](int) {});
+    settle(i0);
   }
   __syncthreads();
 
   // MODE 0: interior, burn-in columns that nobody reads (no stores); 1: interior, L stores; 2: general
-  auto panel = [&](const ix g, auto mode) -> bool {
+  auto panel = [&](const int g, auto mode) -> bool {
     constexpr int MODE = decltype(mode)::value;
     // (B) warp 0 writes L00; the others solve their panel tiles on the tensor cores (X = W L00^-T with
-    // -L00^-1 as the B fragments and the stored -W as A), write them and publish them
+    // L00^-1 as the B fragments), write them and publish them
     if (W == 0) {
       if (MODE != 0) {
         const double2 x2 = *reinterpret_cast<const double2*>(sm.l00 + pr);
         if (MODE == 1) {
-          double* p = lb + (((g + c2) * L.w + (rr - c2)) << lsh);
+          double* p = lb + ((ix(g + c2) * L.w + (rr - c2)) << lsh);
           if (rr >= c2) p[0] = x2.x;
           if (rr >= c2 + 1) p[lw1] = x2.y;
         } else {
@@ -291,7 +304,7 @@ __device__ void chol_la_unit(const CholP& C, ix b, ix n, ix s, ix e, ix i0, doub
         }
       }
     } else {
-      const double nb0 = sm.nlinv[rr * 8 + q], nb1 = sm.nlinv[rr * 8 + 4 + q];
+      const double nb0 = sm.linv[rr * 8 + q], nb1 = sm.linv[rr * 8 + 4 + q];
 #pragma unroll
       for (int d = 1; d < T; ++d)
         if (M::owner(d) == W) {
@@ -300,95 +313,114 @@ __device__ void chol_la_unit(const CholP& C, ix b, ix n, ix s, ix e, ix i0, doub
           sm.pft[d][pw1] = X[1];
         }
       __syncwarp();
-      double y[T][2];
 #pragma unroll
       for (int d = 1; d < T; ++d)
         if (M::owner(d) == W) {
+          double* Y = wt[M::slot(W, d, 0)];  // the slot is dead once X is staged
           const double2 af = *reinterpret_cast<const double2*>(sm.pft[d] + pr);
-          dmma4(y[d][0], y[d][1], af.x, nb0, 0.0, 0.0);
-          dmma(y[d][0], y[d][1], af.y, nb1);
+          dmma4(Y[0], Y[1], af.x, nb0, 0.0, 0.0);
+          dmma(Y[0], Y[1], af.y, nb1);
         }
       __syncwarp();
 #pragma unroll
       for (int d = 1; d < T; ++d)
         if (M::owner(d) == W) {
-          sm.pft[d][pw0] = y[d][0];
-          sm.pft[d][pw1] = y[d][1];
+          const double* Y = wt[M::slot(W, d, 0)];
+          sm.pft[d][pw0] = Y[0];
+          sm.pft[d][pw1] = Y[1];
+          sm.npft[d][pw0] = -Y[0];
+          sm.npft[d][pw1] = -Y[1];
           if (MODE == 1) {
-            double* p = lb + (((g + c2) * L.w + (8 * d + rr - c2)) << lsh);
-            if (8 * d + rr - c2 <= K) p[0] = y[d][0];
-            if (8 * d + rr - c2 - 1 <= K) p[lw1] = y[d][1];
+            double* p = lb + ((ix(g + c2) * L.w + (8 * d + rr - c2)) << lsh);
+            if (8 * d + rr - c2 <= K) p[0] = Y[0];
+            if (8 * d + rr - c2 - 1 <= K) p[lw1] = Y[1];
           } else if (MODE == 2) {
-            store_l(g, d, y[d][0], y[d][1]);
+            store_l(g, d, Y[0], Y[1]);
           }
         }
     }
     __syncthreads();
-    const ix g2 = g + 8;
+    const int g2 = g + 8;
     if (g2 >= e) return false;  // the unit's last panel: nothing left to update
-    // (C) trailing update into the shifted slots (minus-window += X_I X_J^T), the look-ahead
+    // (C) trailing update into the shifted slots (window += (-X_I) X_J^T), the look-ahead
     // factorisation of the next diagonal tile (warp 0), the fresh tile row of Q
     if (W == 0) {
       auto upd = [&](int Ja, int Jb) {  // tiles (Ja, Ja), (Jb, Jb) of diagonal 0, interleaved
         const double2 fa = *reinterpret_cast<const double2*>(sm.pft[Ja] + pr);
+        const double2 na = *reinterpret_cast<const double2*>(sm.npft[Ja] + pr);
         double* ta = wt[M::slot(W, 0, Ja - 1)];
         const double* oa = wt[M::slot(W, 0, Ja)];
-        dmma4(ta[0], ta[1], fa.x, fa.x, oa[0], oa[1]);
+        dmma4(ta[0], ta[1], na.x, fa.x, oa[0], oa[1]);
         if (Jb < T) {
           const double2 fb = *reinterpret_cast<const double2*>(sm.pft[Jb] + pr);
+          const double2 nb = *reinterpret_cast<const double2*>(sm.npft[Jb] + pr);
           double* tb = wt[M::slot(W, 0, Jb - 1)];
           const double* ob = wt[M::slot(W, 0, Jb)];
-          dmma4(tb[0], tb[1], fb.x, fb.x, ob[0], ob[1]);
-          dmma(ta[0], ta[1], fa.y, fa.y);
-          dmma(tb[0], tb[1], fb.y, fb.y);
+          dmma4(tb[0], tb[1], nb.x, fb.x, ob[0], ob[1]);
+          dmma(ta[0], ta[1], na.y, fa.y);
+          dmma(tb[0], tb[1], nb.y, fb.y);
         } else {
-          dmma(ta[0], ta[1], fa.y, fa.y);
+          dmma(ta[0], ta[1], na.y, fa.y);
         }
       };
+      if (MODE != 2) {  // the fresh diagonal tile (rows / columns g2 + K ..) by cp.async: no register
+                        // scoreboard is held across the factorisation (a hoisted LDG stalled it for ~1200 clk)
+        const int r = g2 + K + rr;
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int c = g2 + K + c2 + v;
+          const double* src = r >= c ? qb + ((ix(c) * Q.w + (r - c)) << qsh) : qb + ((ix(r) * Q.w + (c - r)) << qsh);
+          cpa8(&sm.fresh[v][lane], src);
+        }
+        cpa_commit();
+      }
       upd(1, T);  // tile (1, 1) alone: the next diagonal tile
       const double* D = wt[M::slot(W, 0, 0)];
       *reinterpret_cast<double2*>(sm.dt + pr) = make_double2(D[0], D[1]);
       __syncwarp();
-      chol8_seq(sm.dt, sm.l00, sm.nlinv, piv(g2), [&](int j) {
+      chol8_seq(sm.dt, sm.l00, sm.linv, piv, [&](int j) {
         if (2 * j + 2 < T) upd(2 * j + 2, 2 * j + 3);
       });
+      settle(g2);
     } else {
 #pragma unroll
       for (int J = 1; J < T; ++J) {
         const double2 fb = *reinterpret_cast<const double2*>(sm.pft[J] + pr);
-        double2 fa[T];
+        double fay[T];
 #pragma unroll
         for (int d = 1; d < T; ++d)
           if (M::owner(d) == W && J < T - d) {
-            fa[d] = *reinterpret_cast<const double2*>(sm.pft[J + d] + pr);
+            const double2 fa = *reinterpret_cast<const double2*>(sm.npft[J + d] + pr);
+            fay[d] = fa.y;
             double* tn = wt[M::slot(W, d, J - 1)];
             const double* to = wt[M::slot(W, d, J)];
-            dmma4(tn[0], tn[1], fa[d].x, fb.x, to[0], to[1]);
+            dmma4(tn[0], tn[1], fa.x, fb.x, to[0], to[1]);
           }
 #pragma unroll
         for (int d = 1; d < T; ++d)
           if (M::owner(d) == W && J < T - d) {
             double* tn = wt[M::slot(W, d, J - 1)];
-            dmma(tn[0], tn[1], fa[d].y, fb.y);
+            dmma(tn[0], tn[1], fay[d], fb.y);
           }
       }
     }
     // fresh tile (T-1, T-1-d): rows g2 + K + rr, columns g2 + 8 (T-1-d) + c2 + v
     if (MODE != 2) {
-      const double* const qp = qb + (((g2 + c2) * Q.w + (K + rr - c2)) << qsh);  // (row g2+K+rr, column g2+c2)
+      const double* const qp = qb + ((ix(g2 + c2) * Q.w + (K + rr - c2)) << qsh);  // (row g2+K+rr, column g2+c2)
 #pragma unroll
       for (int d = 0; d < T; ++d)
         if (M::owner(d) == W) {
           double* tf = wt[M::slot(W, d, T - 1 - d)];
+          if (d > 0) {
 #pragma unroll
-          for (int v = 0; v < 2; ++v) {
-            const int cell = 8 * d + rr - c2 - v;
-            if (d > 0) {
-              tf[v] = cell <= K ? -__ldg(qp + (8 * (T - 1 - d) + v) * qw1) : 0.0;
-            } else {  // diagonal tile: mirror the upper part
-              const ix r = g2 + K + rr, c = g2 + K + c2 + v;
-              tf[v] = -(cell >= 0 ? __ldg(qp + (8 * (T - 1) + v) * qw1) : __ldg(qb + ((r * Q.w + (c - r)) << qsh)));
+            for (int v = 0; v < 2; ++v) {
+              const int cell = 8 * d + rr - c2 - v;
+              tf[v] = cell <= K ? __ldg(qp + (8 * (T - 1 - d) + v) * qw1) : 0.0;
             }
+          } else {
+            cpa_wait0();
+            tf[0] = sm.fresh[0][lane];
+            tf[1] = sm.fresh[1][lane];
           }
         }
     } else {
@@ -397,14 +429,14 @@ __device__ void chol_la_unit(const CholP& C, ix b, ix n, ix s, ix e, ix i0, doub
         if (M::owner(d) == W) {
           double* tf = wt[M::slot(W, d, T - 1 - d)];
 #pragma unroll
-          for (int v = 0; v < 2; ++v) tf[v] = -qval(g2 + 8 * (T - 1) + rr, g2 + 8 * (T - 1 - d) + c2 + v);
+          for (int v = 0; v < 2; ++v) tf[v] = qval(g2 + 8 * (T - 1) + rr, g2 + 8 * (T - 1 - d) + c2 + v);
         }
     }
     __syncthreads();
     return true;
   };
 
-  ix g = i0;
+  int g = i0;
   while (g < e) {
     const bool inner = g + K + 16 <= n;
     if (inner && g + 8 + K <= s) {
@@ -433,7 +465,7 @@ __device__ void chol_la_unit(const CholP& C, ix b, ix n, ix s, ix e, ix i0, doub
 }
 
 template <int K, int NW, int W>
-__device__ __forceinline__ void chol_la_dispatch(int w, const CholP& C, ix b, ix n, ix s, ix e, ix i0,
+__device__ __forceinline__ void chol_la_dispatch(int w, const CholP& C, ix b, int n, int s, int e, int i0,
                                                  double* side, LASmem<K, NW>& sm) {
   if (w == W) chol_la_unit<K, NW, W>(C, b, n, s, e, i0, side, sm);
   if constexpr (W + 1 < NW) chol_la_dispatch<K, NW, W + 1>(w, C, b, n, s, e, i0, side, sm);
@@ -441,7 +473,7 @@ __device__ __forceinline__ void chol_la_dispatch(int w, const CholP& C, ix b, ix
 
 // repair != 0: one CTA per flagged matrix, a single exact unit over the whole matrix
 template <int K, int NW>
-__global__ void __launch_bounds__(32 * NW) k_chol_la(CholP C, Geo G, int repair) {
+__global__ void __launch_bounds__(32 * NW, K == 64 ? 4 : 2) k_chol_la(CholP C, Geo G, int repair) {
   __shared__ __align__(16) LASmem<K, NW> sm;
   ix b, s, e, i0;
   double* side = nullptr;
@@ -463,7 +495,9 @@ __global__ void __launch_bounds__(32 * NW) k_chol_la(CholP C, Geo G, int repair)
     i0 -= i0 % 8;
     if (p > 0) side = C.side + unit * ix(K) * (K + 1);
   }
-  chol_la_dispatch<K, NW, 0>(threadIdx.x >> 5, C, b, G.n, s, e, i0, side, sm);
+  // co-resident CTAs swap roles so the heavy (tile) warps do not all share one SM sub-partition's tensor pipe
+  const int role = NW == 2 ? int((threadIdx.x >> 5) ^ (blockIdx.x & 1)) : int(threadIdx.x >> 5);
+  chol_la_dispatch<K, NW, 0>(role, C, b, int(G.n), int(s), int(e), int(i0), side, sm);
 }
 
 template <int K, int NW>
@@ -520,6 +554,7 @@ bool run_chol_la(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row
 
 bool cholesky_la(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, cudaStream_t s, int segment_rows) {
   if (q.dtype != BGM_F64 || l.dtype != BGM_F64) return false;
+  if (q.n * ix(q.lower + 1) >= (ix(1) << 31) - 4096) return false;  // 32-bit row / cell indices inside
   if (q.lower == 64) return run_chol_la<64, 2>(q, l, st, row, s, segment_rows);
   if (q.lower == 128) return run_chol_la<128, 4>(q, l, st, row, s, segment_rows);
   return false;
