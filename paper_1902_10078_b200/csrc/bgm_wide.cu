@@ -3433,6 +3433,11 @@ bool subset(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* row, cu
 bool solve_vec(const bgm_band& l, const bgm_vec& v, int tr, const bgm_vec& x, int32_t* st, int64_t* row,
                cudaStream_t s) {
   if (l.upper != 0 || l.batch == 0 || l.n == 0 || l.n < 8 * l.lower) return false;
+  static const bool blocked = [] {
+    const char* e = std::getenv("BGM_WSOLVE_BLK");
+    return !(e && e[0] == '0');
+  }();
+  if (blocked && solve_vec_blk(l, v, tr, x, st, row, s, g_segment_rows)) return true;
   const bool f64 = l.dtype == BGM_F64;
   switch (l.lower) {
 #define BGM_SOLVE(KK)                                                                           \

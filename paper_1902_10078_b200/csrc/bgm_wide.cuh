@@ -22,6 +22,9 @@ void set_segment_rows(int rows);
 // look-ahead DMMA Cholesky, k = 64 / 128, fp64 (bgm_wide_la.cu)
 bool cholesky_la(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, cudaStream_t s,
                  int segment_rows);
+// blocked solves, k = 64 / 128, reference layout, n % 8 == 0 (bgm_wide_solve.cu)
+bool solve_vec_blk(const bgm_band& l, const bgm_vec& v, int tr, const bgm_vec& x, int32_t* st, int64_t* row,
+                   cudaStream_t s, int segment_rows);
 
 }  // namespace wide
 
