@@ -1780,6 +1780,35 @@ struct BRow {
 };
 __device__ __forceinline__ BRow brow(const Band<double>& X, ix b) { return BRow{&X.cell(b, 0, 0), X.w, X.s}; }
 
+// L_PP^-1 in the MMA accumulator layout by forward substitution on the identity: lane (rr, q) holds
+// columns 2q, 2q+1 of row rr.  The 8 steps are separate calls so a caller can interleave them with
+// independent DMMAs (the shuffles' latency then hides behind the tensor pipe).
+struct LinvChain {
+  double M0, M1, rme, lr[8];
+  int rr, q;
+  __device__ __forceinline__ void init(const double* lp, int rr_, int q_) {
+    rr = rr_;
+    q = q_;
+    M0 = rr == 2 * q ? 1.0 : 0.0;
+    M1 = rr == 2 * q + 1 ? 1.0 : 0.0;
+    rme = 1.0 / lp[sw8(rr, rr)];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) lr[k] = rr > k ? lp[sw8(rr, k)] : 0.0;
+  }
+  __device__ __forceinline__ void step(int k) {
+    if (rr == k) {
+      M0 *= rme;
+      M1 *= rme;
+    }
+    const double mk0 = __shfl_sync(0xffffffffu, M0, 4 * k + q);
+    const double mk1 = __shfl_sync(0xffffffffu, M1, 4 * k + q);
+    if (rr > k) {
+      M0 = fma(-lr[k], mk0, M0);
+      M1 = fma(-lr[k], mk1, M1);
+    }
+  }
+};
+
 template <int K, int NW>
 struct VtSmem {
   static constexpr int NT = K / 8;
@@ -1909,40 +1938,24 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
     cpa_commit();
     const double* lp = sm.lp[buf];
     double* lin = sm.lin[warp];
-    // ---- (1) Linv (per warp), Y and Z_TP for the warp's tile rows
+    // ---- (1) Linv (per warp), Y and Z_TP for the warp's tile rows; the Linv chain is interleaved
+    //          with the Y products (tile column outer: the warp's rows give independent accumulators)
     {
-      double M0 = rr == c2 ? 1.0 : 0.0, M1 = rr == c2 + 1 ? 1.0 : 0.0;
-      // this lane's row pivot reciprocal and row of L_PP, loaded / divided
-      // up front: only the shuffles and FMAs stay on the 8-step chain
-      const double rme = 1.0 / lp[sw8(rr, rr)];
-      double lr[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) lr[k] = rr > k ? lp[sw8(rr, k)] : 0.0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        if (rr == k) {
-          M0 *= rme;
-          M1 *= rme;
-        }
-        const double mk0 = __shfl_sync(0xffffffffu, M0, 4 * k + q);
-        const double mk1 = __shfl_sync(0xffffffffu, M1, 4 * k + q);
-        if (rr > k) {
-          M0 = fma(-lr[k], mk0, M0);
-          M1 = fma(-lr[k], mk1, M1);
-        }
-      }
-      put(lin, M0, M1);
-    }
-    {
+      LinvChain ch;
+      ch.init(lp, rr, q);
       double ya[TPW][2][2];
 #pragma unroll
-      for (int i = 0; i < TPW; ++i) {
-        const int t = warp + NW * i;
-        ya[i][0][0] = ya[i][0][1] = ya[i][1][0] = ya[i][1][1] = 0.0;
+      for (int i = 0; i < TPW; ++i) ya[i][0][0] = ya[i][0][1] = ya[i][1][0] = ya[i][1][1] = 0.0;
 #pragma unroll
-        for (int u = 0; u < NT; ++u)
+      for (int u = 0; u < NT; ++u) {
+#pragma unroll
+        for (int i = 0; i < TPW; ++i) {
+          const int t = warp + NW * i;
           mm(ya[i][u & 1], &sm.z[0][0] + sm.zs[t * NT + u], t < u, lp + (8 + 8 * u) * 8, false);
+        }
+        if ((u + 1) % (NT / 8) == 0) ch.step((u + 1) / (NT / 8) - 1);
       }
+      put(lin, ch.M0, ch.M1);
 #pragma unroll
       for (int i = 0; i < TPW; ++i) put(sm.y[warp + NW * i], ya[i][0][0] + ya[i][1][0], ya[i][0][1] + ya[i][1][1]);
       __syncwarp();
@@ -2023,14 +2036,24 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
     row_issue(&sm.w[0][0], grow, false, pb + NT + 1, NT + 1);
     cpa_commit();
     // Ltpb = -Z_TP Ab^T + Z_TT Yb -> L-bar rows 8pb+8+8t+rr, columns 8pb+c2+v
+    double lacc[TPW][2][2];
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) {
+      lacc[i][0][0] = -la[i][0];
+      lacc[i][0][1] = -la[i][1];
+      lacc[i][1][0] = lacc[i][1][1] = 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < NT; ++u)
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) {
+        const int t = warp + NW * i;
+        mm(lacc[i][u & 1], &sm.z[0][0] + sm.zs[t * NT + u], t < u, sm.yb[u], false);
+      }
 #pragma unroll
     for (int i = 0; i < TPW; ++i) {
       const int t = warp + NW * i;
-      double acc[2] = {-la[i][0], -la[i][1]}, acc2[2] = {0.0, 0.0};
-#pragma unroll
-      for (int u = 0; u < NT; ++u) mm(u & 1 ? acc2 : acc, &sm.z[0][0] + sm.zs[t * NT + u], t < u, sm.yb[u], false);
-      acc[0] += acc2[0];
-      acc[1] += acc2[1];
+      const double acc[2] = {lacc[i][0][0] + lacc[i][1][0], lacc[i][0][1] + lacc[i][1][1]};
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const ix col = 8 * pb + c2 + v;
@@ -2240,31 +2263,15 @@ __device__ void vchol_dmma_unit(const VdP<double>& C, ix b, ix n, ix s, ix e, ix
     load_lb(pb > pb_end ? pb - 1 : -1, nbt, nbp);
     const double* lp = sm.lp[buf];
     double* lin = sm.lin[warp];
-    {  // Linv (per warp)
-      double M0 = rr == c2 ? 1.0 : 0.0, M1 = rr == c2 + 1 ? 1.0 : 0.0;
-      // this lane's row pivot reciprocal and row of L_PP, loaded / divided
-      // up front: only the shuffles and FMAs stay on the 8-step chain
-      const double rme = 1.0 / lp[sw8(rr, rr)];
-      double lr[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) lr[k] = rr > k ? lp[sw8(rr, k)] : 0.0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        if (rr == k) {
-          M0 *= rme;
-          M1 *= rme;
-        }
-        const double mk0 = __shfl_sync(0xffffffffu, M0, 4 * k + q);
-        const double mk1 = __shfl_sync(0xffffffffu, M1, 4 * k + q);
-        if (rr > k) {
-          M0 = fma(-lr[k], mk0, M0);
-          M1 = fma(-lr[k], mk1, M1);
-        }
-      }
-      put(lin, M0, M1);
-    }
-    // Lb_TP = Lbar_TP - 2 G_TT L_TP (own tile rows)
+    // Linv (per warp), then Lb_TP = Lbar_TP - 2 G_TT L_TP (own tile rows).  (Interleaving the chain with
+    // the products and running them tile-column outer, as the subset kernels do, was slower here:
+    // 7.73 vs 7.14 ms at k = 128.)
     {
+      LinvChain ch;
+      ch.init(lp, rr, q);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) ch.step(k);
+      put(lin, ch.M0, ch.M1);
       double ga[TPW][2];
 #pragma unroll
       for (int i = 0; i < TPW; ++i) {
@@ -2493,38 +2500,22 @@ __device__ void subset_mw_unit(const SubP<double>& C, ix b, ix n, ix s, ix e, ix
     const double* lp = sm.lp[buf];
     const int* zs = sm.zs[pb & 1];
     double* lin = sm.lin[warp];
-    {  // Linv (per warp)
-      double M0 = rr == c2 ? 1.0 : 0.0, M1 = rr == c2 + 1 ? 1.0 : 0.0;
-      // this lane's row pivot reciprocal and row of L_PP, loaded / divided
-      // up front: only the shuffles and FMAs stay on the 8-step chain
-      const double rme = 1.0 / lp[sw8(rr, rr)];
-      double lr[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) lr[k] = rr > k ? lp[sw8(rr, k)] : 0.0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        if (rr == k) {
-          M0 *= rme;
-          M1 *= rme;
-        }
-        const double mk0 = __shfl_sync(0xffffffffu, M0, 4 * k + q);
-        const double mk1 = __shfl_sync(0xffffffffu, M1, 4 * k + q);
-        if (rr > k) {
-          M0 = fma(-lr[k], mk0, M0);
-          M1 = fma(-lr[k], mk1, M1);
-        }
-      }
-      put(lin, M0, M1);
-    }
-    {
+    {  // Linv (per warp) interleaved with Y = Z_TT L_TP (tile column outer)
+      LinvChain ch;
+      ch.init(lp, rr, q);
       double ya[TPW][2][2];
 #pragma unroll
-      for (int i = 0; i < TPW; ++i) {
-        const int t = warp + NW * i;
-        ya[i][0][0] = ya[i][0][1] = ya[i][1][0] = ya[i][1][1] = 0.0;
+      for (int i = 0; i < TPW; ++i) ya[i][0][0] = ya[i][0][1] = ya[i][1][0] = ya[i][1][1] = 0.0;
 #pragma unroll
-        for (int u = 0; u < NT; ++u) mm(ya[i][u & 1], &sm.z[0][0] + zs[t * NT + u], t < u, lp + (8 + 8 * u) * 8, false);
+      for (int u = 0; u < NT; ++u) {
+#pragma unroll
+        for (int i = 0; i < TPW; ++i) {
+          const int t = warp + NW * i;
+          mm(ya[i][u & 1], &sm.z[0][0] + zs[t * NT + u], t < u, lp + (8 + 8 * u) * 8, false);
+        }
+        if ((u + 1) % (NT / 8) == 0) ch.step((u + 1) / (NT / 8) - 1);
       }
+      put(lin, ch.M0, ch.M1);
 #pragma unroll
       for (int i = 0; i < TPW; ++i) put(sm.y[warp + NW * i], ya[i][0][0] + ya[i][1][0], ya[i][0][1] + ya[i][1][1]);
       __syncwarp();
