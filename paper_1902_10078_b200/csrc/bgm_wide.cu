@@ -26,6 +26,7 @@
 
 #include <cmath>
 #include <initializer_list>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -1780,6 +1781,19 @@ struct BRow {
 };
 __device__ __forceinline__ BRow brow(const Band<double>& X, ix b) { return BRow{&X.cell(b, 0, 0), X.w, X.s}; }
 
+// Calls f(integral_constant<int, w>) for the CTA's warp w, so a unit can resolve its warp-dependent
+// indices (tile rows, transposition of a tile read, table offsets) at compile time.  NOT used by the
+// kernels below: measured on the B200, eight warp-specialised copies of the subset / adjoint loops
+// (WI >= 0) thrash the instruction cache -- k = 128 subset 6.3 -> 20.5 ms, adjoint 17.1 -> 66 ms,
+// vjp_cholesky 7.7 -> 11.8 ms -- although each copy has ~half the instructions.  The runtime-warp
+// version (WI = -1) stays; its ~10-14 instructions per DMMA (IMAD / LEA / ISETP / FSEL index math)
+// are the price of one shared loop body.
+template <int NW, int WI = 0, class F>
+__device__ __forceinline__ void warp_dispatch(int w, F&& f) {
+  if (w == WI) f(std::integral_constant<int, WI>{});
+  if constexpr (WI + 1 < NW) warp_dispatch<NW, WI + 1>(w, f);
+}
+
 // L_PP^-1 in the MMA accumulator layout by forward substitution on the identity: lane (rr, q) holds
 // columns 2q, 2q+1 of row rr.  The 8 steps are separate calls so a caller can interleave them with
 // independent DMMAs (the shuffles' latency then hides behind the tensor pipe).
@@ -1824,12 +1838,13 @@ struct VtSmem {
   unsigned mg[NT + 2];           // mod_small multipliers
 };
 
-template <int K, int NW>
+template <int K, int NW, int WI = -1>  // WI >= 0: the warp index as a compile-time constant
 __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix i0, double* side, double* tail,
                                VtSmem<K, NW>& sm) {
   constexpr int NT = K / 8, NTH = 32 * NW, TPW = NT / NW, NWT = VtSmem<K, NW>::NWT;
   static_assert(NT % NW == 0, "warps must divide the tile rows");
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, rr = lane >> 2, q = lane & 3, c2 = 2 * q;
+  const int tid = threadIdx.x, warp = WI >= 0 ? WI : tid >> 5, lane = tid & 31, rr = lane >> 2, q = lane & 3,
+            c2 = 2 * q;
   const int o0[2] = {sw8(rr, q), sw8(rr, 4 + q)}, o1[2] = {sw8(q, rr), sw8(4 + q, rr)};
   const int oc = sw8(rr, c2);
   const Band<double>& L = C.l;
@@ -2194,12 +2209,13 @@ struct VdSmem {
   unsigned mg[NT + 2];
 };
 
-template <int K, int NW>
+template <int K, int NW, int WI = -1>  // WI >= 0: the warp index as a compile-time constant
 __device__ void vchol_dmma_unit(const VdP<double>& C, ix b, ix n, ix s, ix e, ix iend, double* side, double* tail,
                                 VdSmem<K, NW>& sm) {
   constexpr int NT = K / 8, NTH = 32 * NW, TPW = NT / NW, NST = NT * (NT + 1) / 2;
   static_assert(NT % NW == 0, "warps must divide the tile rows");
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, rr = lane >> 2, q = lane & 3, c2 = 2 * q;
+  const int tid = threadIdx.x, warp = WI >= 0 ? WI : tid >> 5, lane = tid & 31, rr = lane >> 2, q = lane & 3,
+            c2 = 2 * q;
   const int o0[2] = {sw8(rr, q), sw8(rr, 4 + q)}, o1[2] = {sw8(q, rr), sw8(4 + q, rr)};
   const int oc = sw8(rr, c2);
   const Band<double>& L = C.l;
@@ -2431,12 +2447,13 @@ struct TakMwSmem {
   unsigned mg[NT + 2];
 };
 
-template <int K, int NW>
+template <int K, int NW, int WI = -1>  // WI >= 0: the warp index as a compile-time constant
 __device__ void subset_mw_unit(const SubP<double>& C, ix b, ix n, ix s, ix e, ix jend, double* side,
                                TakMwSmem<K, NW>& sm) {
   constexpr int NT = K / 8, NTH = 32 * NW, TPW = NT / NW;
   static_assert(NT % NW == 0, "warps must divide the tile rows");
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, rr = lane >> 2, q = lane & 3, c2 = 2 * q;
+  const int tid = threadIdx.x, warp = WI >= 0 ? WI : tid >> 5, lane = tid & 31, rr = lane >> 2, q = lane & 3,
+            c2 = 2 * q;
   const int o0[2] = {sw8(rr, q), sw8(rr, 4 + q)}, o1[2] = {sw8(q, rr), sw8(4 + q, rr)};
   const int oc = sw8(rr, c2);
   auto mm = [&](double* acc, const double* X, bool tx, const double* Y, bool ty) {
