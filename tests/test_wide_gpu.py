@@ -170,6 +170,57 @@ def test_wide_solve_repair_singular_fp32(cuda, oracle, segrows, monkeypatch, tr)
     _fp32_ok(GpuOracle(tile=1, dtype=torch.float32).solve_vec(l32, v32, tr)[0], oracle.solve_vec(l32, v32, tr)[0])
 
 
+@pytest.mark.parametrize("k,n", [(64, 1504), (128, 2048)])
+@pytest.mark.parametrize("tr", [False, True])
+def test_wide_solve_blocked_panels(cuda, oracle, segrows, monkeypatch, k, n, tr):
+    """n a multiple of 8 in the reference layout runs the blocked solves (csrc/bgm_wide_solve.cu):
+    whole matrix in one unit, forced segments with the regular burn-in, a burn-in too short to
+    converge (check + exact repair), singular rows in the first and last segment, and fp32 storage."""
+    from tests.gpu_adapter import GpuOracle
+    rng = np.random.default_rng(5 * k + n + tr)
+    l = oracle.cholesky(_q(oracle, rng, 3, n, k, "dominant"))[0]
+    v = cm.random_vec(rng, 3, n)
+    x_o = oracle.solve_vec(l, v, tr)[0]
+    for seg in (0, 8 * k + 8, 3 * k):
+        segrows(seg)
+        x_g, st, _ = GpuOracle(tile=1).solve_vec(l, v, tr)
+        assert not st.any()
+        assert cm.max_rel_err(x_g, x_o) <= 1e-9, seg
+    monkeypatch.setenv("BGM_WIDE_BURN", "8")
+    segrows(3 * k)
+    ls = l.copy()
+    ls[1, 40, 0] = 0.0
+    ls[1, n - 9, 0] = 0.0
+    x_g, st, row = GpuOracle(tile=1).solve_vec(ls, v, tr)
+    x_s, st_o, row_o = oracle.solve_vec(ls, v, tr)
+    assert list(st) == list(st_o) and st[1] != 0 and row[1] == row_o[1] == (n - 9 if tr else 40)
+    for b in (0, 2):
+        assert cm.max_rel_err(x_g[b], x_s[b]) <= 1e-9
+    monkeypatch.delenv("BGM_WIDE_BURN")
+    segrows(0)
+    l32 = oracle.cholesky(_q(oracle, rng, 2, n, k, "cfg4"))[0].astype(np.float32).astype(np.float64)
+    v32 = v[1:].astype(np.float32).astype(np.float64)
+    _fp32_ok(GpuOracle(tile=1, dtype=torch.float32).solve_vec(l32, v32, tr)[0], oracle.solve_vec(l32, v32, tr)[0])
+
+
+@pytest.mark.parametrize("k,n", [(64, 1600), (128, 2304)])
+def test_wide_cholesky_lookahead_interior(cuda, oracle, segrows, k, n):
+    """n a multiple of 8 with several segments: the look-ahead kernel's interior loops (no stores during
+    the burn-in, fast stores / loads inside), the tail panels, both warp-role assignments at k = 64
+    (odd and even CTAs) and a failing pivot in the last panel."""
+    from tests.gpu_adapter import GpuOracle
+    rng = np.random.default_rng(11 * k + n)
+    q = _q(oracle, rng, 5, n, k, "cfg4")
+    q[3, n - 3, 0] = -0.5
+    l_o, st_o, row_o = oracle.cholesky(q)
+    for seg in (0, 8 * k, 5 * k + 8):
+        segrows(seg)
+        l_g, st, row = GpuOracle(tile=1).cholesky(q)
+        assert list(st) == list(st_o) and row[3] == row_o[3] == n - 3
+        for b in (0, 1, 2, 4):
+            assert cm.max_rel_err(l_g[b], l_o[b]) <= 1e-9, (seg, b)
+
+
 @pytest.mark.parametrize("k,n", [(64, 700), (128, 1100)])
 @pytest.mark.parametrize("tile", [1, 32])
 @pytest.mark.parametrize("seg", [0, 270])
