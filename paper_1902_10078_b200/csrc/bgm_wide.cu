@@ -1900,18 +1900,19 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
       elem(sm.w[ring_slot<K>(d, pb + j, sm.mg)], grow, false, pb + j + d, pb + j, x & 63);
     }
   };
-  // L rows [8pb, 8pb+K+8) x cols [8pb, 8pb+8), identity past n; thread column fc
-  const int fc = tid & 7, fr = tid >> 3;
-  auto fill = [&](int buf, ix pb) {
-    const ix col = 8 * pb + fc;
-    const double* colp = lrow.at(0, col);
+  // L rows [8pb, 8pb+K+8) x cols [8pb, 8pb+8), identity past n
+  auto fill = [&](int buf, ix pb) {  // a warp copies whole columns, lanes consecutive rows (coalesced)
 #pragma unroll
-    for (int i = 0; i < (K + 8 + NTH / 8 - 1) / (NTH / 8); ++i) {
-      const int r = fr + (NTH / 8) * i, cell = r - fc;
-      if (r < K + 8) {
-        double* dst = sm.lp[buf] + sw8(r, fc);
-        if (cell >= 0 && cell <= K && 8 * pb + r < n) cpa(dst, colp + (ix(cell) << lrow.s));
-        else *dst = (cell == 0) ? 1.0 : 0.0;
+    for (int c = warp; c < 8; c += NW) {
+      const double* colp = lrow.at(0, 8 * pb + c);
+#pragma unroll
+      for (int i = 0; i < (K + 8 + 31) / 32; ++i) {
+        const int r = lane + 32 * i, cell = r - c;
+        if (r < K + 8) {
+          double* dst = sm.lp[buf] + sw8(r, c);
+          if (cell >= 0 && cell <= K && 8 * pb + r < n) cpa(dst, colp + (ix(cell) << lrow.s));
+          else *dst = (cell == 0) ? 1.0 : 0.0;
+        }
       }
     }
   };
@@ -2225,6 +2226,7 @@ __device__ void vchol_dmma_unit(const VdP<double>& C, ix b, ix n, ix s, ix e, ix
     for (int kc = 0; kc < 2; ++kc) dmma(acc[0], acc[1], X[tx ? o1[kc] : o0[kc]], Y[ty ? o0[kc] : o1[kc]]);
   };
   auto put = [&](double* Tt, double v0, double v1) { *reinterpret_cast<double2*>(Tt + oc) = make_double2(v0, v1); };
+  // (kept as is: a division-free warp-per-column version of this copy measured 4% slower here)
   auto fill = [&](int buf, ix pb) {  // L rows [8pb, 8pb+K+8) x cols [8pb, 8pb+8), identity past n
     for (int x = tid; x < 8 * (K + 8); x += NTH) {
       const int c = x / (K + 8), r = x % (K + 8), cell = r - c;
@@ -2283,11 +2285,29 @@ __device__ void vchol_dmma_unit(const VdP<double>& C, ix b, ix n, ix s, ix e, ix
     // the products and running them tile-column outer, as the subset kernels do, was slower here:
     // 7.73 vs 7.14 ms at k = 128.)
     {
-      LinvChain ch;
-      ch.init(lp, rr, q);
+      double M0 = rr == c2 ? 1.0 : 0.0, M1 = rr == c2 + 1 ? 1.0 : 0.0;
+      // this lane's row pivot reciprocal and row of L_PP, loaded / divided
+      // up front: only the shuffles and FMAs stay on the 8-step chain
+      const double rme = 1.0 / lp[sw8(rr, rr)];
+      double lr[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) ch.step(k);
-      put(lin, ch.M0, ch.M1);
+      for (int k = 0; k < 8; ++k) lr[k] = rr > k ? lp[sw8(rr, k)] : 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (rr == k) {
+          M0 *= rme;
+          M1 *= rme;
+        }
+        const double mk0 = __shfl_sync(0xffffffffu, M0, 4 * k + q);
+        const double mk1 = __shfl_sync(0xffffffffu, M1, 4 * k + q);
+        if (rr > k) {
+          M0 = fma(-lr[k], mk0, M0);
+          M1 = fma(-lr[k], mk1, M1);
+        }
+      }
+      put(lin, M0, M1);
+    }
+    {
       double ga[TPW][2];
 #pragma unroll
       for (int i = 0; i < TPW; ++i) {
@@ -2470,17 +2490,20 @@ __device__ void subset_mw_unit(const SubP<double>& C, ix b, ix n, ix s, ix e, ix
     const int t = x >> 6, m = (x >> 3) & 7, c = x & 7;
     (&sm.z[0][0])[x] = (exact_top && t <= NT && m == c) ? 1.0 : 0.0;
   }
-  const int fc = tid & 7, fr = tid >> 3;
-  auto fill = [&](int buf, ix pb) {  // L rows [8pb, 8pb+K+8) x cols [8pb, 8pb+8), identity past n
-    const ix col = 8 * pb + fc;
-    const double* colp = lrow.at(0, col);
+  // L rows [8pb, 8pb+K+8) x cols [8pb, 8pb+8), identity past n: a warp copies whole columns, lanes
+  // consecutive rows (coalesced)
+  auto fill = [&](int buf, ix pb) {
 #pragma unroll
-    for (int i = 0; i < (K + 8 + NTH / 8 - 1) / (NTH / 8); ++i) {
-      const int r = fr + (NTH / 8) * i, cell = r - fc;
-      if (r < K + 8) {
-        double* dst = sm.lp[buf] + sw8(r, fc);
-        if (cell >= 0 && cell <= K && 8 * pb + r < n) cpa(dst, colp + (ix(cell) << lrow.s));
-        else *dst = (cell == 0) ? 1.0 : 0.0;
+    for (int c = warp; c < 8; c += NW) {
+      const double* colp = lrow.at(0, 8 * pb + c);
+#pragma unroll
+      for (int i = 0; i < (K + 8 + 31) / 32; ++i) {
+        const int r = lane + 32 * i, cell = r - c;
+        if (r < K + 8) {
+          double* dst = sm.lp[buf] + sw8(r, c);
+          if (cell >= 0 && cell <= K && 8 * pb + r < n) cpa(dst, colp + (ix(cell) << lrow.s));
+          else *dst = (cell == 0) ? 1.0 : 0.0;
+        }
       }
     }
   };
