@@ -1877,7 +1877,7 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
   // tab[d (NT+1)] / 64 of the current panel; each thread owns the element
   // (em, ec) of tiles et, et + NTH/64, ...  (NTH is a multiple of 64)
   static_assert(NTH % 64 == 0, "block size");
-  const int em = (tid & 63) >> 3, ec = tid & 7, et = tid >> 6;
+  const int em = tid & 7, ec = (tid & 63) >> 3, et = tid >> 6;  // lanes run down a column: 64-byte source runs
   auto row_issue = [&](double* ring, const BRow& X, bool ident, ix bn, int ntile) {
     const double* rowp = X.p + ((8 * bn * X.w) << X.s);
 #pragma unroll
