@@ -303,6 +303,23 @@ def normwise(a, b):
     return float(np.linalg.norm(np.asarray(a, np.float64) - np.asarray(b, np.float64))) / (nb if nb > 0 else 1.0)
 
 
+def solve_summands(L, v, x, transpose):
+    """Per-row magnitude of a triangular solve's terms, (|v_i| + sum_j |L_ij| |x_j|) / |L_ii|, for the
+    reference layout L[b, column, cell] (cell r of column j = L(j + r, j)): rounding in ANY evaluation
+    order moves x_i by a few ulp of this, not of |x_i| -- rows whose terms cancel (|x_i| ~ 1e-7 of the
+    largest) are judged against it, like the cancelling sum of config 3's d tau2."""
+    import numpy as np
+    L, v, x = (np.abs(np.asarray(a, np.float64)) for a in (L, v, x))
+    n, k = L.shape[1], L.shape[2] - 1
+    s = v.copy()
+    for a in range(1, k + 1):
+        if transpose:
+            s[:, :n - a] += L[:, :n - a, a] * x[:, a:]
+        else:
+            s[:, a:] += L[:, :n - a, a] * x[:, :n - a]
+    return s / np.maximum(L[:, :, 0], 1e-300)
+
+
 def parity_report(pairs, tol, relaxed=None, normwise_tol=1e-10):
     """pairs: [(name, gpu array, oracle array)].  Pinned floor 1e-12 max|b|
     (BASELINE.md §4); for names in `relaxed` (config-3 gradients, see
@@ -559,7 +576,9 @@ class SuiteWorkload:
         x1, _, _ = o.solve_vec(g["l"], h["b"])
         x2, _, _ = o.solve_vec(g["l"], g["x1"], True)
         ld, _, _ = o.log_det(g["l"])
-        return {"l": L, "x1": x1, "x2": x2, "ld": ld}
+        return {"l": L, "x1": x1, "x2": x2, "ld": ld,
+                "_summands": {"x1": solve_summands(g["l"], h["b"], x1, False),
+                              "x2": solve_summands(g["l"], g["x1"], x2, True)}}
 
     # ---- config 2
     def _build_cfg2(self):
@@ -642,7 +661,8 @@ class SuiteWorkload:
         g4, _, _ = o.vjp_sparse_inverse_subset(L, S, h["sbar"])
         g5 = o.vjp_cholesky(L, h["lbar"])
         return {"l": Lo, "x1": x1o, "x2": x2o, "ld": ld, "s": So, "g_x1": g1, "g_x2": g2, "g_ld": g3, "g_s": g4,
-                "g_l": g5}
+                "g_l": g5, "_summands": {"x1": solve_summands(L, h["b"], x1o, False),
+                                         "x2": solve_summands(L, x1, x2o, True)}}
 
     # ---- step / attribution
     # Independent operators of a suite run concurrently: op -> (stream lane,
@@ -801,11 +821,13 @@ class SuiteWorkload:
         ref = getattr(self, "_oracle_" + self.wl["kind"])(o, h, gi)
         dt = time.perf_counter() - t0
         pairs = []
+        summ = ref.get("_summands", {})
         for name in self.outputs:
             gs = self._flat(self.res[name])
             rs = list(ref[name]) if isinstance(ref[name], tuple) else [ref[name]]
             for q, (g, r) in enumerate(zip(gs, rs)):
-                pairs.append((name if len(gs) == 1 else f"{name}[{q}]", self._host(g, m), r))
+                item = (name if len(gs) == 1 else f"{name}[{q}]", self._host(g, m), r)
+                pairs.append(item + (summ[name],) if name in summ else item)
         f32 = self.wl["dtype"] == "f32"
         # fp32 storage: the adjoint of the inverse subset combines the fp32-
         # rounded S and L, which agree only to ~6e-8 -- entries that cancel
