@@ -3381,6 +3381,16 @@ bool cholesky(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, c
   if (q.lower != l.lower || q.upper != 0 || l.upper != 0 || q.batch == 0 || q.n == 0) return false;
   if (q.n < 4 * q.lower) return false;  // short matrices: the generic sweep is fine
   const bool f64 = q.dtype == BGM_F64;
+  // fp32 storage: the look-ahead kernel reads / writes fp32 directly (fp64 arithmetic); only if it
+  // declines is the band widened into an fp64 scratch copy for the fp64 DMMA kernels
+  static const bool la32 = [] {
+    const char* e = std::getenv("BGM_WIDE_DMMA_WARPS");
+    const char* d = std::getenv("BGM_WIDE_DMMA");
+    return !(e && std::atoi(e) != 0) && !(d && d[0] == '0');
+  }();
+  if (!f64 && (q.lower == 64 || q.lower == 128) && wide32() && la32 &&
+      cholesky_la(q, l, st, row, s, g_segment_rows))
+    return true;
   if (!f64 && (q.lower == 64 || q.lower == 128) && wide32() &&
       via_f64({&q}, {&l}, s, [&](bgm_band* d) { return cholesky(d[0], d[1], st, row, s); }))
     return true;

@@ -45,10 +45,11 @@ struct Geo {
   int nseg, burn;
 };
 
-struct CholP {
-  Band<double> q;  // symmetric lower store
-  Band<double> l;  // output factor
-  double* side;    // [unit][K][K+1] burn-in copies of the K columns before the segment
+template <class ST>  // storage type; the arithmetic is fp64 for both (an fp32 factorisation rounds only
+struct CholP {        // its inputs and outputs)
+  Band<ST> q;  // symmetric lower store
+  Band<ST> l;  // output factor
+  ST* side;    // [unit][K][K+1] burn-in copies of the K columns before the segment
   int64_t* fail;
   int32_t* flag;
 };
@@ -67,8 +68,8 @@ __global__ void k_la_init(int64_t* fail, int32_t* flag, ix batch, ix n) {
 }
 
 // burn-in copies of the K columns before each segment against the neighbour's genuine columns
-template <int K>
-__global__ void k_la_check(CholP C, Geo G) {
+template <class ST, int K>
+__global__ void k_la_check(CholP<ST> C, Geo G) {
   const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
   const ix unit = t / K;
   const int c = int(t % K);
@@ -76,11 +77,13 @@ __global__ void k_la_check(CholP C, Geo G) {
   const int p = int(unit % G.nseg);
   if (p == 0) return;
   const ix b = unit / G.nseg, s = ix(p) * G.seg, col = s - K + c;
-  const double* sd = C.side + (unit * K + c) * (K + 1);
+  const ST* sd = C.side + (unit * K + c) * (K + 1);
   double sc = 0.0;
-  for (int r = 0; r <= K; ++r) sc = fmax(sc, fabs(C.l.cell(b, r, col)));
+  for (int r = 0; r <= K; ++r) sc = fmax(sc, fabs(double(C.l.cell(b, r, col))));
   bool bad = false;
-  for (int r = 0; r <= K; ++r) bad |= !(fabs(sd[r] - C.l.cell(b, r, col)) <= kCheckTol * (sc + 1e-300));
+  const double tol = sizeof(ST) == 8 ? kCheckTol : 1e-5;
+  for (int r = 0; r <= K; ++r)
+    bad |= !(fabs(double(sd[r]) - double(C.l.cell(b, r, col))) <= tol * (sc + 1e-300));
   if (bad) C.flag[b] = 1;
 }
 
@@ -120,18 +123,22 @@ struct LA {
 // elements of lane (r, q) -- columns q and 4 + q -- are one 16-byte load.
 __device__ __forceinline__ int ppos(int c) { return (c & 3) * 2 + (c >> 2); }
 
-template <int K, int NW>
+template <class ST, int K, int NW>
 struct LASmem {
   double dt[64];    // the next diagonal tile, on its way to the sequential factorisation
   double l00[64];   // L00, row-major, lower part
   double linv[64];  // L00^-1, row-major, upper part zero
   double pft[K / 8 + 1][64];   // panel tiles, permuted rows
   double npft[K / 8 + 1][64];  // minus the panel tiles (the A operands of the update)
-  double fresh[2][32];         // warp 0's fresh diagonal tile, per lane, by cp.async
+  ST fresh[2][32];             // warp 0's fresh diagonal tile, per lane, by cp.async
 };
 
-__device__ __forceinline__ void cpa8(double* dst, const double* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(unsigned(__cvta_generic_to_shared(dst))), "l"(src) : "memory");
+template <class ST>
+__device__ __forceinline__ void cpa8(ST* dst, const ST* src) {
+  if (sizeof(ST) == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(unsigned(__cvta_generic_to_shared(dst))), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(unsigned(__cvta_generic_to_shared(dst))), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cpa_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
@@ -222,13 +229,14 @@ struct Mode {
   static constexpr int value = N;
 };
 
-template <int K, int NW, int W>
-__device__ void chol_la_unit(const CholP& C, ix b, int n, int s, int e, int i0, double* side, LASmem<K, NW>& sm) {
+template <class ST, int K, int NW, int W>
+__device__ void chol_la_unit(const CholP<ST>& C, ix b, int n, int s, int e, int i0, ST* side,
+                             LASmem<ST, K, NW>& sm) {
   using M = LA<K, NW>;
   constexpr int T = M::T;
   const int lane = threadIdx.x & 31, rr = lane >> 2, q = lane & 3, c2 = 2 * q;
-  const Band<double>& Q = C.q;
-  const Band<double>& L = C.l;
+  const Band<ST>& Q = C.q;
+  const Band<ST>& L = C.l;
   auto qval = [&](ix r, ix c) -> double {  // symmetric Q(r, c), identity past n
     if (r < c) {
       const ix t = r;
@@ -237,7 +245,7 @@ __device__ void chol_la_unit(const CholP& C, ix b, int n, int s, int e, int i0, 
     }
     if (r - c > K || c < 0) return 0.0;
     if (r >= n) return r == c ? 1.0 : 0.0;
-    return Q.cell(b, int(r - c), c);
+    return double(Q.cell(b, int(r - c), c));
   };
   auto store_l = [&](int g, int I, double x0, double x1) {  // general: rows 8I + rr of columns g + c2 + v
 #pragma unroll
@@ -246,16 +254,16 @@ __device__ void chol_la_unit(const CholP& C, ix b, int n, int s, int e, int i0, 
       const int col = g + c;
       if (cell >= 0 && cell <= K && col < n) {
         const double val = (col + cell < n) ? (v ? x1 : x0) : 0.0;
-        if (col >= s) L.cell(b, cell, col) = val;
-        else if (side && col >= s - K) side[ix(col - (s - K)) * (K + 1) + cell] = val;
+        if (col >= s) L.cell(b, cell, col) = ST(val);
+        else if (side && col >= s - K) side[ix(col - (s - K)) * (K + 1) + cell] = ST(val);
       }
     }
   };
   // interior fast paths: element (cell r, column j) of matrix b sits at base + ((j w + r) << sh)
   const int qsh = Q.s, lsh = L.s;
   const ix qw1 = ix(Q.w - 1) << qsh, lw1 = ix(L.w - 1) << lsh;
-  const double* const qb = &Q.cell(b, 0, 0);
-  double* const lb = &L.cell(b, 0, 0);
+  const ST* const qb = &Q.cell(b, 0, 0);
+  ST* const lb = &L.cell(b, 0, 0);
   const int pw0 = rr * 8 + ppos(c2), pw1 = rr * 8 + ppos(c2 + 1), pr = rr * 8 + c2;
   constexpr int NTW = M::ntiles(W) > 0 ? M::ntiles(W) : 1;
   double wt[NTW][2];  // the Schur window
@@ -296,9 +304,9 @@ __device__ void chol_la_unit(const CholP& C, ix b, int n, int s, int e, int i0, 
       if (MODE != 0) {
         const double2 x2 = *reinterpret_cast<const double2*>(sm.l00 + pr);
         if (MODE == 1) {
-          double* p = lb + ((ix(g + c2) * L.w + (rr - c2)) << lsh);
-          if (rr >= c2) p[0] = x2.x;
-          if (rr >= c2 + 1) p[lw1] = x2.y;
+          ST* p = lb + ((ix(g + c2) * L.w + (rr - c2)) << lsh);
+          if (rr >= c2) p[0] = ST(x2.x);
+          if (rr >= c2 + 1) p[lw1] = ST(x2.y);
         } else {
           store_l(g, 0, x2.x, c2 + 1 <= rr ? x2.y : 0.0);
         }
@@ -331,9 +339,9 @@ __device__ void chol_la_unit(const CholP& C, ix b, int n, int s, int e, int i0, 
           sm.npft[d][pw0] = -Y[0];
           sm.npft[d][pw1] = -Y[1];
           if (MODE == 1) {
-            double* p = lb + ((ix(g + c2) * L.w + (8 * d + rr - c2)) << lsh);
-            if (8 * d + rr - c2 <= K) p[0] = Y[0];
-            if (8 * d + rr - c2 - 1 <= K) p[lw1] = Y[1];
+            ST* p = lb + ((ix(g + c2) * L.w + (8 * d + rr - c2)) << lsh);
+            if (8 * d + rr - c2 <= K) p[0] = ST(Y[0]);
+            if (8 * d + rr - c2 - 1 <= K) p[lw1] = ST(Y[1]);
           } else if (MODE == 2) {
             store_l(g, d, Y[0], Y[1]);
           }
@@ -369,7 +377,7 @@ __device__ void chol_la_unit(const CholP& C, ix b, int n, int s, int e, int i0, 
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
           const int c = g2 + K + c2 + v;
-          const double* src = r >= c ? qb + ((ix(c) * Q.w + (r - c)) << qsh) : qb + ((ix(r) * Q.w + (c - r)) << qsh);
+          const ST* src = r >= c ? qb + ((ix(c) * Q.w + (r - c)) << qsh) : qb + ((ix(r) * Q.w + (c - r)) << qsh);
           cpa8(&sm.fresh[v][lane], src);
         }
         cpa_commit();
@@ -406,7 +414,7 @@ __device__ void chol_la_unit(const CholP& C, ix b, int n, int s, int e, int i0, 
     }
     // fresh tile (T-1, T-1-d): rows g2 + K + rr, columns g2 + 8 (T-1-d) + c2 + v
     if (MODE != 2) {
-      const double* const qp = qb + ((ix(g2 + c2) * Q.w + (K + rr - c2)) << qsh);  // (row g2+K+rr, column g2+c2)
+      const ST* const qp = qb + ((ix(g2 + c2) * Q.w + (K + rr - c2)) << qsh);  // (row g2+K+rr, column g2+c2)
 #pragma unroll
       for (int d = 0; d < T; ++d)
         if (M::owner(d) == W) {
@@ -415,12 +423,12 @@ __device__ void chol_la_unit(const CholP& C, ix b, int n, int s, int e, int i0, 
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
               const int cell = 8 * d + rr - c2 - v;
-              tf[v] = cell <= K ? __ldg(qp + (8 * (T - 1 - d) + v) * qw1) : 0.0;
+              tf[v] = cell <= K ? double(__ldg(qp + (8 * (T - 1 - d) + v) * qw1)) : 0.0;
             }
           } else {
             cpa_wait0();
-            tf[0] = sm.fresh[0][lane];
-            tf[1] = sm.fresh[1][lane];
+            tf[0] = double(sm.fresh[0][lane]);
+            tf[1] = double(sm.fresh[1][lane]);
           }
         }
     } else {
@@ -464,19 +472,19 @@ __device__ void chol_la_unit(const CholP& C, ix b, int n, int s, int e, int i0, 
     atomicMin(reinterpret_cast<unsigned long long*>(C.fail + b), static_cast<unsigned long long>(fail));
 }
 
-template <int K, int NW, int W>
-__device__ __forceinline__ void chol_la_dispatch(int w, const CholP& C, ix b, int n, int s, int e, int i0,
-                                                 double* side, LASmem<K, NW>& sm) {
-  if (w == W) chol_la_unit<K, NW, W>(C, b, n, s, e, i0, side, sm);
-  if constexpr (W + 1 < NW) chol_la_dispatch<K, NW, W + 1>(w, C, b, n, s, e, i0, side, sm);
+template <class ST, int K, int NW, int W>
+__device__ __forceinline__ void chol_la_dispatch(int w, const CholP<ST>& C, ix b, int n, int s, int e, int i0,
+                                                 ST* side, LASmem<ST, K, NW>& sm) {
+  if (w == W) chol_la_unit<ST, K, NW, W>(C, b, n, s, e, i0, side, sm);
+  if constexpr (W + 1 < NW) chol_la_dispatch<ST, K, NW, W + 1>(w, C, b, n, s, e, i0, side, sm);
 }
 
 // repair != 0: one CTA per flagged matrix, a single exact unit over the whole matrix
-template <int K, int NW>
-__global__ void __launch_bounds__(32 * NW, K == 64 ? 4 : 2) k_chol_la(CholP C, Geo G, int repair) {
-  __shared__ __align__(16) LASmem<K, NW> sm;
+template <class ST, int K, int NW>
+__global__ void __launch_bounds__(32 * NW, K == 64 ? 4 : 2) k_chol_la(CholP<ST> C, Geo G, int repair) {
+  __shared__ __align__(16) LASmem<ST, K, NW> sm;
   ix b, s, e, i0;
-  double* side = nullptr;
+  ST* side = nullptr;
   if (repair) {
     b = blockIdx.x;
     if (b >= G.batch || !C.flag[b]) return;
@@ -497,10 +505,10 @@ __global__ void __launch_bounds__(32 * NW, K == 64 ? 4 : 2) k_chol_la(CholP C, G
   }
   // co-resident CTAs swap roles so the heavy (tile) warps do not all share one SM sub-partition's tensor pipe
   const int role = NW == 2 ? int((threadIdx.x >> 5) ^ (blockIdx.x & 1)) : int(threadIdx.x >> 5);
-  chol_la_dispatch<K, NW, 0>(role, C, b, int(G.n), int(s), int(e), int(i0), side, sm);
+  chol_la_dispatch<ST, K, NW, 0>(role, C, b, int(G.n), int(s), int(e), int(i0), side, sm);
 }
 
-template <int K, int NW>
+template <class ST, int K, int NW>
 bool run_chol_la(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, cudaStream_t s, int segment_rows) {
   Geo G;
   G.batch = q.batch;
@@ -510,7 +518,7 @@ bool run_chol_la(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row
     if (std::atoi(bv) >= 1) G.burn = std::atoi(bv);
   int sms = 148, dev = 0, per = 1;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_chol_la<K, NW>, 32 * NW, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_chol_la<ST, K, NW>, 32 * NW, 0);
   if (per < 1) per = 1;
   ix seg = requested_seg(segment_rows, K);
   if (seg <= 0) {
@@ -523,27 +531,27 @@ bool run_chol_la(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row
   G.seg = seg;
   G.nseg = int((G.n + seg - 1) / seg);
   const ix units = G.batch * G.nseg;
-  const size_t sb = sizeof(double) * size_t(units) * K * (K + 1);
+  const size_t sb = (sizeof(ST) * size_t(units) * K * (K + 1) + 15) / 16 * 16;
   char* ws = nullptr;
   if (scratch_alloc(reinterpret_cast<void**>(&ws), sb + 12 * size_t(G.batch) + 64, s) != cudaSuccess) return false;
-  CholP C;
-  C.q = view<double>(q);
-  C.l = view<double>(l);
-  C.side = reinterpret_cast<double*>(ws);
+  CholP<ST> C;
+  C.q = view<ST>(q);
+  C.l = view<ST>(l);
+  C.side = reinterpret_cast<ST*>(ws);
   C.fail = reinterpret_cast<int64_t*>(ws + sb);
   C.flag = reinterpret_cast<int32_t*>(C.fail + G.batch);
   k_la_init<<<blocks_for(G.batch, 128), 128, 0, s>>>(C.fail, C.flag, G.batch, G.n);
   {
     timing::Scope ts("wide_chol_dmma", s);
-    k_chol_la<K, NW><<<unsigned(units), 32 * NW, 0, s>>>(C, G, 0);
+    k_chol_la<ST, K, NW><<<unsigned(units), 32 * NW, 0, s>>>(C, G, 0);
   }
   {
     timing::Scope ts("wide_chol_check", s);
-    k_la_check<K><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
+    k_la_check<ST, K><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
   }
   {
     timing::Scope ts("wide_chol_repair", s);
-    k_chol_la<K, NW><<<unsigned(G.batch), 32 * NW, 0, s>>>(C, G, 1);
+    k_chol_la<ST, K, NW><<<unsigned(G.batch), 32 * NW, 0, s>>>(C, G, 1);
   }
   k_la_status<<<blocks_for(G.batch, 128), 128, 0, s>>>(C.fail, G.batch, G.n, st, row);
   scratch_free(ws, s);
@@ -553,10 +561,15 @@ bool run_chol_la(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row
 }  // namespace
 
 bool cholesky_la(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* row, cudaStream_t s, int segment_rows) {
-  if (q.dtype != BGM_F64 || l.dtype != BGM_F64) return false;
+  if (q.dtype != l.dtype) return false;
   if (q.n * ix(q.lower + 1) >= (ix(1) << 31) - 4096) return false;  // 32-bit row / cell indices inside
-  if (q.lower == 64) return run_chol_la<64, 2>(q, l, st, row, s, segment_rows);
-  if (q.lower == 128) return run_chol_la<128, 4>(q, l, st, row, s, segment_rows);
+  const bool f64 = q.dtype == BGM_F64;
+  if (q.lower == 64)
+    return f64 ? run_chol_la<double, 64, 2>(q, l, st, row, s, segment_rows)
+               : run_chol_la<float, 64, 2>(q, l, st, row, s, segment_rows);
+  if (q.lower == 128)
+    return f64 ? run_chol_la<double, 128, 4>(q, l, st, row, s, segment_rows)
+               : run_chol_la<float, 128, 4>(q, l, st, row, s, segment_rows);
   return false;
 }
 
