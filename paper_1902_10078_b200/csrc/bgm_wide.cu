@@ -51,7 +51,27 @@ constexpr int kBurnGen = 6;
 struct Geo {
   ix batch, n, seg;
   int nseg, burn;
+  // Row-span mode (span_rows > 0): instead of nseg equal segments per matrix, the batch's rows --
+  // matrices laid end to end, each padded to n8 = round_up(n, 8) -- are cut into equal runs of
+  // span_rows, one CTA each, so every resident CTA slot gets the same number of rows whatever the
+  // batch size (64 matrices x 2 segments leave 20 of 148 one-CTA SMs idle).  A run that crosses a
+  // matrix end gives its CTA several pieces (at most span_kmax); only a piece that starts inside a
+  // matrix needs a burn-in and a check against its predecessor, the last piece of the CTA before.
+  ix span_rows = 0, n8 = 0;
+  int span_kmax = 0;
 };
+
+// piece k of the run of CTA c: matrix b, rows [s, e) (false: no such piece)
+__device__ __forceinline__ bool span_piece(const Geo& G, ix c, int k, ix& b, ix& s, ix& e) {
+  const ix g0 = c * G.span_rows, g1 = g0 + G.span_rows;
+  b = g0 / G.n8 + k;
+  if (b >= G.batch || b * G.n8 >= g1) return false;
+  s = g0 - b * G.n8;
+  if (s < 0) s = 0;
+  e = g1 - b * G.n8;
+  if (e > G.n) e = G.n;
+  return s < e;
+}
 
 template <class T>
 struct CholP {
@@ -2132,6 +2152,20 @@ __global__ void __launch_bounds__(32 * NW) k_vsub_dmma(VsP<double> C, Geo G) {
   extern __shared__ __align__(16) unsigned char smraw[];
   VtSmem<K, NW>& sm = *reinterpret_cast<VtSmem<K, NW>*>(smraw);
   constexpr int STATE = VtSmem<K, NW>::NWT * 64;
+  if (G.span_rows > 0) {
+    for (int k = 0; k < G.span_kmax; ++k) {
+      ix b, s, e;
+      if (!span_piece(G, blockIdx.x, k, b, s, e)) continue;  // uniform across the CTA
+      ix i0 = s - G.burn;
+      if (i0 < 0) i0 = 0;
+      i0 -= i0 % 8;
+      const ix slot = (ix(blockIdx.x) * G.span_kmax + k) * ix(STATE);
+      vsub_dmma_unit<K, NW>(C, b, G.n, s, e, i0, s > 0 ? C.side + slot : nullptr, e < G.n ? C.tail + slot : nullptr,
+                            sm);
+      __syncthreads();  // the next piece reuses the shared windows
+    }
+    return;
+  }
   const ix unit = blockIdx.x;
   const ix b = unit / G.nseg;
   const int p = int(unit % G.nseg);
@@ -2149,11 +2183,23 @@ __global__ void k_vsub_dmma_check(VsP<double> C, Geo G) {
   constexpr int STATE = VtSmem<K, NW>::NWT * 64;
   const ix id = (blockIdx.x * ix(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (id >= G.batch * G.nseg) return;
-  const int p = int(id % G.nseg);
-  if (p == 0) return;
-  const double* a = C.side + id * ix(STATE);
-  const double* r = C.tail + (id - 1) * ix(STATE);
+  const double *a, *r;
+  ix bflag;
+  if (G.span_rows > 0) {  // id = CTA: its first piece, if it starts inside a matrix, against the
+    ix b, s, e;           // last piece of the CTA before (same matrix)
+    if (id < 1 || !span_piece(G, id, 0, b, s, e) || s == 0) return;
+    const int kprev = int(b - ((id - 1) * G.span_rows) / G.n8);
+    a = C.side + (id * G.span_kmax) * ix(STATE);
+    r = C.tail + ((id - 1) * G.span_kmax + kprev) * ix(STATE);
+    bflag = b;
+  } else {
+    if (id >= G.batch * G.nseg) return;
+    const int p = int(id % G.nseg);
+    if (p == 0) return;
+    a = C.side + id * ix(STATE);
+    r = C.tail + (id - 1) * ix(STATE);
+    bflag = id / G.nseg;
+  }
   double sc = 0.0;
   for (int i = lane; i < STATE; i += 32) sc = fmax(sc, fabs(r[i]));
 #pragma unroll
@@ -2161,7 +2207,7 @@ __global__ void k_vsub_dmma_check(VsP<double> C, Geo G) {
   bool bad = false;
   for (int i = lane; i < STATE; i += 32) bad |= !(fabs(a[i] - r[i]) <= kCheckTol * (sc + 1e-300));
   bad = __any_sync(0xffffffffu, bad);
-  if (bad && lane == 0) C.flag[id / G.nseg] = 1;
+  if (bad && lane == 0) C.flag[bflag] = 1;
 }
 
 template <int K, int NW>
@@ -2780,6 +2826,27 @@ bool run_chol_dmma(const bgm_band& q, const bgm_band& l, int32_t* st, int64_t* r
   return true;
 }
 
+// Row-span geometry (see Geo): equal runs of rows over `ctas` CTAs (BGM_WIDE_SPAN_CTAS overrides the
+// count, BGM_WIDE_SPAN=0 disables).  Declined when a run would be shorter than min_rows (small
+// batches keep the per-matrix segments) or when the uniform segments already fill the slots.
+inline bool span_rows(Geo& G, ix ctas, ix min_rows) {
+  static const int off = [] {
+    const char* e = std::getenv("BGM_WIDE_SPAN");
+    return e && e[0] == '0';
+  }();
+  if (off) return false;
+  if (const char* cv = std::getenv("BGM_WIDE_SPAN_CTAS"))
+    if (std::atoi(cv) >= 1) ctas = std::atoi(cv);
+  const ix n8 = (G.n + 7) / 8 * 8;
+  ix rows = (G.batch * n8 + ctas - 1) / ctas;
+  rows = (rows + 7) / 8 * 8;
+  if (rows < min_rows || rows >= G.batch * n8) return false;
+  G.span_rows = rows;
+  G.n8 = n8;
+  G.span_kmax = int((rows + n8 - 1) / n8) + 1;
+  return true;
+}
+
 // segments per matrix: fill the resident CTA slots in whole waves, burn-in
 // overhead counted (the k_vsub_dmma grid is one short launch)
 inline int pick_nseg(ix batch, ix n, int slots, int burn, int seg_min) {
@@ -2829,8 +2896,12 @@ bool run_vsub_dmma(const bgm_band& l, const bgm_band& sm, const bgm_band& sb, co
   seg = (seg + 7) / 8 * 8;
   G.seg = seg;
   G.nseg = int((G.n + seg - 1) / seg);
-  const ix units = G.batch * G.nseg;
-  const size_t sb_bytes = sizeof(double) * size_t(units) * STATE;
+  ix units = G.batch * G.nseg, slots = units;
+  if (g_segment_rows <= 0 && span_rows(G, ix(sms) * per, 2 * ix(G.burn))) {
+    units = (G.batch * G.n8 + G.span_rows - 1) / G.span_rows;
+    slots = units * G.span_kmax;
+  }
+  const size_t sb_bytes = sizeof(double) * size_t(slots) * STATE;
   char* ws = nullptr;
   if (scratch_alloc(reinterpret_cast<void**>(&ws), 2 * sb_bytes + 12 * size_t(G.batch) + 64, s) != cudaSuccess)
     return false;

@@ -267,6 +267,32 @@ def test_wide_vjp_subset(cuda, oracle, segrows, k, n, tile, seg, kind):
     assert cm.max_rel_err(g, o) <= 1e-9
 
 
+@pytest.mark.parametrize("k,n,ctas", [(64, 1000, 7), (64, 1203, 5), (128, 2000, 3)])
+def test_wide_vjp_subset_row_spans(cuda, oracle, segrows, monkeypatch, k, n, ctas):
+    """Row-span geometry: the batch's rows, matrices end to end, cut into equal runs over a forced
+    number of CTAs, so runs cross matrix ends (several pieces per CTA) and pieces start inside
+    matrices (burn-in + check against the previous CTA's last piece); n % 8 != 0 pads each matrix."""
+    from tests.gpu_adapter import GpuOracle
+    rng = np.random.default_rng(17 * k + n)
+    B = 5
+    l = oracle.cholesky(_q(oracle, rng, B, n, k, "cfg4"))[0]
+    s = oracle.sparse_inverse_subset(l)[0]
+    sbar = cm.random_band(rng, B, n, k, 0)
+    o = oracle.vjp_sparse_inverse_subset(l, s, sbar)[0]
+    monkeypatch.setenv("BGM_WIDE_SPAN_CTAS", str(ctas))
+    segrows(0)
+    g, st, _ = GpuOracle(tile=1).vjp_sparse_inverse_subset(l, s, sbar)
+    assert not st.any()
+    assert cm.max_rel_err(g, o) <= 1e-9
+    sub, st, _ = GpuOracle(tile=1).sparse_inverse_subset(l)
+    assert not st.any()
+    assert cm.max_rel_err(sub, s) <= 1e-9
+    # a burn-in too short to converge: the span check must flag it and the exact path repair it
+    monkeypatch.setenv("BGM_WIDE_BURN", "8")
+    g, st, _ = GpuOracle(tile=1).vjp_sparse_inverse_subset(l, s, sbar)
+    assert cm.max_rel_err(g, o) <= 1e-9
+
+
 def test_wide_vjp_subset_fp32_repair_singular(cuda, oracle, segrows, monkeypatch):
     from tests.gpu_adapter import GpuOracle
     rng = np.random.default_rng(78)
