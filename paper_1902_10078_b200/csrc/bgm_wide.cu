@@ -1851,8 +1851,8 @@ struct VtSmem {
   double z[NZ][64];
   double w[NWT][64];
   double lp[2][(K + 8) * 8];
-  double y[NT][64], zt[NT][64], yb[NT][64];
-  double lin[NW][64], am[NW][64], ab[NW][64], part[NW][64], ph[NW][64];
+  double y[NT][64], zt[NT][64], yb[NT][64], gb[NT][64];
+  double lin[NW][64], am[NW][64], ab[NW][64], part[NW][64], ph[NW][64], hm[64];
   int zs[NT * NT];               // element offset of Z_TT tile (t, u) in z (lower-stored)
   int ws[(NT + 1) * (NT + 1)];   // element offset of W tile (t1, t2) in w, window of the panel
   unsigned mg[NT + 2];           // mod_small multipliers
@@ -1974,24 +1974,81 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
     cpa_commit();
     const double* lp = sm.lp[buf];
     double* lin = sm.lin[warp];
-    // ---- (1) Linv (per warp), Y and Z_TP for the warp's tile rows; the Linv chain is interleaved
-    //          with the Y products (tile column outer: the warp's rows give independent accumulators)
+    // ---- (1) Linv (per warp) and everything that does not need Y = Z_TT L_TP:
+    //          Ab = Linv Zb_PP^T, G = L_TP Ab - W2(T,P) (= -Zb_TP), Yb = G Linv^T for the warp's tile rows.
+    //          With Yb known first, ONE pass over the Z_TT tiles serves both big products (2): each
+    //          tile's fragments are read from shared memory once instead of twice -- these kernels
+    //          are bound by shared-memory bandwidth (a DMMA whose two operands come from shared memory
+    //          needs 4 wavefronts per 17 clk and pipe: 93% of the bandwidth at the full tensor rate).
     {
       LinvChain ch;
       ch.init(lp, rr, q);
-      double ya[TPW][2][2];
 #pragma unroll
-      for (int i = 0; i < TPW; ++i) ya[i][0][0] = ya[i][0][1] = ya[i][1][0] = ya[i][1][1] = 0.0;
+      for (int k = 0; k < 8; ++k) ch.step(k);
+      put(lin, ch.M0, ch.M1);
+      __syncwarp();
+    }
+    const double* wpp = &sm.w[0][0] + sm.ws[0];  // Zb_PP = (W2_PP + diag(S-bar_ii)) / 2
+    {
+      const double2 l2 = get(lin);
+      double a[2] = {0.0, 0.0};
+      mm(a, lin, false, wpp, true);
+      a[0] = 0.5 * fma(l2.x, dl0, a[0]);
+      a[1] = 0.5 * fma(l2.y, dl1, a[1]);
+      put(sm.ab[warp], a[0], a[1]);
+      if (warp == NW - 1) {  // W2_PP for the panel algebra at the end: its ring slot is refilled below
+        const double2 w2 = get(wpp);
+        put(sm.am[warp], w2.x, w2.y);
+      }
+      __syncwarp();
+      double g[TPW][2];
 #pragma unroll
-      for (int u = 0; u < NT; ++u) {
+      for (int i = 0; i < TPW; ++i) {
+        const int t = warp + NW * i;
+        const double2 w2 = get(&sm.w[0][0] + sm.ws[(t + 1) * (NT + 1)]);
+        g[i][0] = -w2.x;
+        g[i][1] = -w2.y;
+        mm(g[i], lp + (8 + 8 * t) * 8, false, sm.ab[warp], false);
+      }
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) put(sm.gb[warp + NW * i], g[i][0], g[i][1]);
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) {
+        g[i][0] = g[i][1] = 0.0;
+        mm(g[i], sm.gb[warp + NW * i], false, lin, true);
+      }
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) put(sm.yb[warp + NW * i], g[i][0], g[i][1]);
+    }
+    __syncthreads();
+    // W block row pb+NT+1 enters the slots of column pb (read for the last time above)
+    row_issue(&sm.w[0][0], grow, false, pb + NT + 1, NT + 1);
+    cpa_commit();
+    // ---- (2) Y = Z_TT L_TP and Q = Z_TT Yb in one pass (tile column outer), then Z_TP = -Y Linv,
+    //          L-bar(T,P) = Q - Z_TP Ab^T, and the partial sums L_TP^T Z_TP (for A) and Y^T G (for Linvb)
+    {
+      double ya[TPW][2][2], qa[TPW][2][2];
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) {
+        ya[i][0][0] = ya[i][0][1] = ya[i][1][0] = ya[i][1][1] = 0.0;
+        qa[i][0][0] = qa[i][0][1] = qa[i][1][0] = qa[i][1][1] = 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < NT; ++u)
 #pragma unroll
         for (int i = 0; i < TPW; ++i) {
           const int t = warp + NW * i;
-          mm(ya[i][u & 1], &sm.z[0][0] + sm.zs[t * NT + u], t < u, lp + (8 + 8 * u) * 8, false);
+          const double* zt = &sm.z[0][0] + sm.zs[t * NT + u];
+          const double* y1 = lp + (8 + 8 * u) * 8;
+          const double* y2 = sm.yb[u];
+#pragma unroll
+          for (int kc = 0; kc < 2; ++kc) {  // the tile's fragment is read once for both products
+            const double xa = zt[t < u ? o1[kc] : o0[kc]];
+            dmma(ya[i][u & 1][0], ya[i][u & 1][1], xa, y1[o1[kc]]);
+            dmma(qa[i][u & 1][0], qa[i][u & 1][1], xa, y2[o1[kc]]);
+          }
         }
-        if ((u + 1) % (NT / 8) == 0) ch.step((u + 1) / (NT / 8) - 1);
-      }
-      put(lin, ch.M0, ch.M1);
 #pragma unroll
       for (int i = 0; i < TPW; ++i) put(sm.y[warp + NW * i], ya[i][0][0] + ya[i][1][0], ya[i][0][1] + ya[i][1][1]);
       __syncwarp();
@@ -2003,98 +2060,27 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
 #pragma unroll
       for (int i = 0; i < TPW; ++i) put(sm.zt[warp + NW * i], -ya[i][0][0], -ya[i][0][1]);
       __syncwarp();
-      double h[2] = {0.0, 0.0};  // this warp's share of L_TP^T Z_TP
+      double h[2] = {0.0, 0.0}, pa[2] = {0.0, 0.0};
 #pragma unroll
-      for (int i = 0; i < TPW; ++i) mm(h, lp + (8 + 8 * (warp + NW * i)) * 8, true, sm.zt[warp + NW * i], false);
+      for (int i = 0; i < TPW; ++i) {
+        const int t = warp + NW * i;
+        mm(h, lp + (8 + 8 * t) * 8, true, sm.zt[t], false);
+        mm(pa, sm.y[t], true, sm.gb[t], false);
+      }
       put(sm.ph[warp], h[0], h[1]);
-    }
-    __syncthreads();
-    // ---- (2) A = Linv - L_TP^T Z_TP; Ab = Linv Zb_PP^T; Linvb0 = A Zb_PP + Ab (per warp)
-    double lvb[2];
-    {
-      double h0 = 0.0, h1 = 0.0;
-#pragma unroll
-      for (int w2 = 0; w2 < NW; ++w2) {
-        const double2 p2 = get(sm.ph[w2]);
-        h0 += p2.x;
-        h1 += p2.y;
-      }
-      const double2 l2 = get(lin);
-      put(sm.am[warp], l2.x - h0, l2.y - h1);
-      __syncwarp();
-      // Zb_PP = (W2_PP + diag(S-bar_ii)) / 2
-      const double* wpp = &sm.w[0][0] + sm.ws[0];
-      double a[2] = {0.0, 0.0}, v[2] = {0.0, 0.0};
-      mm(a, lin, false, wpp, true);
-      mm(v, sm.am[warp], false, wpp, false);
-      const double2 am2 = get(sm.am[warp]);
-      a[0] = 0.5 * fma(l2.x, dl0, a[0]);
-      a[1] = 0.5 * fma(l2.y, dl1, a[1]);
-      v[0] = 0.5 * fma(am2.x, dl0, v[0]);
-      v[1] = 0.5 * fma(am2.y, dl1, v[1]);
-      lvb[0] = v[0] + a[0];
-      lvb[1] = v[1] + a[1];
-      put(sm.ab[warp], a[0], a[1]);
-      __syncwarp();
-    }
-    // ---- (3) per tile row: G = L_TP Ab - W2(T,P) (= -Zb_TP), Z_TP Ab^T (= -Ltpb part),
-    //          Linvb partial sum Y^T G, Yb = G Linv^T
-    double la[TPW][2];
-    {
-      double g[TPW][2], pa[2] = {0.0, 0.0};
-#pragma unroll
-      for (int i = 0; i < TPW; ++i) {
-        const int t = warp + NW * i;
-        la[i][0] = la[i][1] = 0.0;
-        mm(la[i], sm.zt[t], false, sm.ab[warp], true);
-        const double2 w2 = get(&sm.w[0][0] + sm.ws[(t + 1) * (NT + 1)]);
-        g[i][0] = -w2.x;
-        g[i][1] = -w2.y;
-        mm(g[i], lp + (8 + 8 * t) * 8, false, sm.ab[warp], false);
-      }
-#pragma unroll
-      for (int i = 0; i < TPW; ++i) put(sm.yb[warp + NW * i], g[i][0], g[i][1]);
-      __syncwarp();
-#pragma unroll
-      for (int i = 0; i < TPW; ++i) {
-        const int t = warp + NW * i;
-        mm(pa, sm.y[t], true, sm.yb[t], false);
-        g[i][0] = g[i][1] = 0.0;
-        mm(g[i], sm.yb[t], false, lin, true);
-      }
-      __syncwarp();
-#pragma unroll
-      for (int i = 0; i < TPW; ++i) put(sm.yb[warp + NW * i], g[i][0], g[i][1]);
       put(sm.part[warp], pa[0], pa[1]);
-    }
-    __syncthreads();
-    // ---- (4) W block row pb+NT+1 enters the slots of column pb (read for the last time above)
-    row_issue(&sm.w[0][0], grow, false, pb + NT + 1, NT + 1);
-    cpa_commit();
-    // Ltpb = -Z_TP Ab^T + Z_TT Yb -> L-bar rows 8pb+8+8t+rr, columns 8pb+c2+v
-    double lacc[TPW][2][2];
-#pragma unroll
-    for (int i = 0; i < TPW; ++i) {
-      lacc[i][0][0] = -la[i][0];
-      lacc[i][0][1] = -la[i][1];
-      lacc[i][1][0] = lacc[i][1][1] = 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < NT; ++u)
 #pragma unroll
       for (int i = 0; i < TPW; ++i) {
         const int t = warp + NW * i;
-        mm(lacc[i][u & 1], &sm.z[0][0] + sm.zs[t * NT + u], t < u, sm.yb[u], false);
-      }
+        double la[2] = {0.0, 0.0};
+        mm(la, sm.zt[t], false, sm.ab[warp], true);
+        const double acc[2] = {qa[i][0][0] + qa[i][1][0] - la[0], qa[i][0][1] + qa[i][1][1] - la[1]};
 #pragma unroll
-    for (int i = 0; i < TPW; ++i) {
-      const int t = warp + NW * i;
-      const double acc[2] = {lacc[i][0][0] + lacc[i][1][0], lacc[i][0][1] + lacc[i][1][1]};
-#pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const ix col = 8 * pb + c2 + v;
-        const int cell = 8 + 8 * t + rr - c2 - v;
-        if (col >= s && col < e && cell <= K) *orow.at(cell, col) = (col + cell < n) ? acc[v] : 0.0;
+        for (int v = 0; v < 2; ++v) {
+          const ix col = 8 * pb + c2 + v;
+          const int cell = 8 + 8 * t + rr - c2 - v;
+          if (col >= s && col < e && cell <= K) *orow.at(cell, col) = (col + cell < n) ? acc[v] : 0.0;
+        }
       }
     }
     // W2(T,T) += Yb L_TP^T + L_TP Yb^T: tile rows pp and NT-1-pp together (NT+1 tiles)
@@ -2116,27 +2102,44 @@ __device__ void vsub_dmma_unit(const VsP<double>& C, ix b, ix n, ix s, ix e, ix 
         put(&sm.w[0][0] + sm.ws[(t1 + 1) * (NT + 1) + t2 + 1], wa[j][0], wa[j][1]);
       }
     }
-    // Lppb = -Linv^T (Linvb Linv^T), Linvb = Linvb0 + sum of the warps' partials
+    __syncthreads();
+    // ---- (3) the panel's own 8x8 algebra on the last warp: A = Linv - L_TP^T Z_TP,
+    //          Linvb = A Zb_PP + Ab - Y^T Zb_TP, Lppb = -Linv^T (Linvb Linv^T)
     if (warp == NW - 1) {
+      double h0 = 0.0, h1 = 0.0, p0 = 0.0, p1 = 0.0;
 #pragma unroll
       for (int w2 = 0; w2 < NW; ++w2) {
-        const double2 p2 = get(sm.part[w2]);
-        lvb[0] += p2.x;
-        lvb[1] += p2.y;
+        const double2 hh = get(sm.ph[w2]);
+        const double2 pp2 = get(sm.part[w2]);
+        h0 += hh.x;
+        h1 += hh.y;
+        p0 += pp2.x;
+        p1 += pp2.y;
       }
-      put(sm.am[warp], lvb[0], lvb[1]);
+      const double2 l2 = get(lin);
+      const double2 ab2 = get(sm.ab[warp]);
+      const double am0 = l2.x - h0, am1 = l2.y - h1;
+      put(sm.hm, am0, am1);
+      __syncwarp();
+      double v[2] = {0.0, 0.0};
+      mm(v, sm.hm, false, sm.am[warp], false);  // A W2_PP (the copy taken in (1))
+      v[0] = 0.5 * fma(am0, dl0, v[0]);
+      v[1] = 0.5 * fma(am1, dl1, v[1]);
+      __syncwarp();
+      put(sm.hm, v[0] + ab2.x + p0, v[1] + ab2.y + p1);  // Linvb
       __syncwarp();
       double t2[2] = {0.0, 0.0};
-      mm(t2, sm.am[warp], false, lin, true);
-      put(sm.ab[warp], t2[0], t2[1]);
+      mm(t2, sm.hm, false, lin, true);
+      __syncwarp();
+      put(sm.hm, t2[0], t2[1]);
       __syncwarp();
       double p2[2] = {0.0, 0.0};
-      mm(p2, lin, true, sm.ab[warp], false);
+      mm(p2, lin, true, sm.hm, false);
 #pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const ix col = 8 * pb + c2 + v;
-        const int cell = rr - c2 - v;
-        if (col >= s && col < e && cell >= 0) *orow.at(cell, col) = (col + cell < n) ? -p2[v] : 0.0;
+      for (int v2 = 0; v2 < 2; ++v2) {
+        const ix col = 8 * pb + c2 + v2;
+        const int cell = rr - c2 - v2;
+        if (col >= s && col < e && cell >= 0) *orow.at(cell, col) = (col + cell < n) ? -p2[v2] : 0.0;
       }
     }
     __syncthreads();
