@@ -2456,6 +2456,18 @@ __global__ void __launch_bounds__(32 * NW) k_vchol_dmma(VdP<double> C, Geo G) {
   extern __shared__ __align__(16) unsigned char smraw[];
   VdSmem<K, NW>& sm = *reinterpret_cast<VdSmem<K, NW>*>(smraw);
   constexpr int NT = K / 8, STATE = NT * (NT + 1) / 2 * 64;
+  if (G.span_rows > 0) {  // row spans (see Geo): the sweep runs upwards, so a piece that ENDS inside a
+    for (int k = 0; k < G.span_kmax; ++k) {  // matrix burns in from below its end
+      ix b, s, e;
+      if (!span_piece(G, blockIdx.x, k, b, s, e)) continue;  // uniform across the CTA
+      const ix iend = e + G.burn < G.n ? e + G.burn : G.n;
+      const ix slot = (ix(blockIdx.x) * G.span_kmax + k) * ix(STATE);
+      vchol_dmma_unit<K, NW>(C, b, G.n, s, e, iend, e < G.n ? C.side + slot : nullptr, s > 0 ? C.tail + slot : nullptr,
+                             sm);
+      __syncthreads();  // the next piece reuses the shared windows
+    }
+    return;
+  }
   const ix unit = blockIdx.x;
   const ix b = unit / G.nseg;
   const int p = int(unit % G.nseg);
@@ -2471,11 +2483,23 @@ __global__ void k_vchol_dmma_check(VdP<double> C, Geo G) {
   constexpr int NT = K / 8, STATE = NT * (NT + 1) / 2 * 64;
   const ix id = (blockIdx.x * ix(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (id >= G.batch * G.nseg) return;
-  const int p = int(id % G.nseg);
-  if (p + 1 >= G.nseg) return;
-  const double* a = C.side + id * ix(STATE);
-  const double* r = C.tail + (id + 1) * ix(STATE);
+  const double *a, *r;
+  ix bflag;
+  if (G.span_rows > 0) {  // id = CTA whose first piece starts inside a matrix: its genuine state against
+    ix b, s, e;           // the burn-in state of the previous CTA's last piece (same matrix)
+    if (id < 1 || !span_piece(G, id, 0, b, s, e) || s == 0) return;
+    const int kprev = int(b - ((id - 1) * G.span_rows) / G.n8);
+    a = C.side + ((id - 1) * G.span_kmax + kprev) * ix(STATE);
+    r = C.tail + (id * G.span_kmax) * ix(STATE);
+    bflag = b;
+  } else {
+    if (id >= G.batch * G.nseg) return;
+    const int p = int(id % G.nseg);
+    if (p + 1 >= G.nseg) return;
+    a = C.side + id * ix(STATE);
+    r = C.tail + (id + 1) * ix(STATE);
+    bflag = id / G.nseg;
+  }
   double sc = 0.0;
   for (int i = lane; i < STATE; i += 32) sc = fmax(sc, fabs(r[i]));
 #pragma unroll
@@ -2483,7 +2507,7 @@ __global__ void k_vchol_dmma_check(VdP<double> C, Geo G) {
   bool bad = false;
   for (int i = lane; i < STATE; i += 32) bad |= !(fabs(a[i] - r[i]) <= kCheckTol * (sc + 1e-300));
   bad = __any_sync(0xffffffffu, bad);
-  if (bad && lane == 0) C.flag[id / G.nseg] = 1;
+  if (bad && lane == 0) C.flag[bflag] = 1;
 }
 
 template <int K, int NW>
@@ -2966,8 +2990,12 @@ bool run_vchol_dmma(const bgm_band& l, const bgm_band& lb, const bgm_band& qb, c
   seg = (seg + 7) / 8 * 8;
   G.seg = seg;
   G.nseg = int((G.n + seg - 1) / seg);
-  const ix units = G.batch * G.nseg;
-  const size_t sb_bytes = sizeof(double) * size_t(units) * STATE;
+  ix units = G.batch * G.nseg, slots = units;
+  if (g_segment_rows <= 0 && span_rows(G, ix(sms) * per, 2 * ix(G.burn))) {
+    units = (G.batch * G.n8 + G.span_rows - 1) / G.span_rows;
+    slots = units * G.span_kmax;
+  }
+  const size_t sb_bytes = sizeof(double) * size_t(slots) * STATE;
   char* ws = nullptr;
   if (scratch_alloc(reinterpret_cast<void**>(&ws), 2 * sb_bytes + 4 * size_t(G.batch) + 64, s) != cudaSuccess)
     return false;

@@ -287,10 +287,14 @@ def test_wide_vjp_subset_row_spans(cuda, oracle, segrows, monkeypatch, k, n, cta
     sub, st, _ = GpuOracle(tile=1).sparse_inverse_subset(l)
     assert not st.any()
     assert cm.max_rel_err(sub, s) <= 1e-9
+    lbar = cm.random_band(rng, B, n, k, 0)
+    qb_o = oracle.vjp_cholesky(l, lbar)
+    assert cm.max_rel_err(GpuOracle(tile=1).vjp_cholesky(l, lbar), qb_o) <= 1e-9
     # a burn-in too short to converge: the span check must flag it and the exact path repair it
     monkeypatch.setenv("BGM_WIDE_BURN", "8")
     g, st, _ = GpuOracle(tile=1).vjp_sparse_inverse_subset(l, s, sbar)
     assert cm.max_rel_err(g, o) <= 1e-9
+    assert cm.max_rel_err(GpuOracle(tile=1).vjp_cholesky(l, lbar), qb_o) <= 1e-9
 
 
 def test_wide_vjp_subset_fp32_repair_singular(cuda, oracle, segrows, monkeypatch):
