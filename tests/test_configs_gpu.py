@@ -187,3 +187,15 @@ def test_config4(cuda, oracle, k, dtype):
     B, n = 1, 32768
     L0 = cm.config_factor(rng, B, n, k, off_std=0.02 / np.sqrt(k))
     _suite(GpuOracle(tile=1, dtype=dtype), oracle, L0, k, rng.normal(0, 1, (B, n)), rng, dtype=dtype)
+
+
+def test_config4_batch_row_spans(cuda, oracle, monkeypatch):
+    """configs[4] at its full length with several matrices (k = 64, fp64): the full suite, with the
+    adjoints' row-span geometry forced to 37 CTAs so their runs cross matrix ends at config size."""
+    from tests.gpu_adapter import GpuOracle
+    monkeypatch.setenv("BGM_WIDE_SPAN_CTAS", "37")
+    rng = np.random.default_rng(4464)
+    B, n, k = 5, 32768, 64
+    L0 = cm.config_factor(rng, B, n, k, off_std=0.02 / np.sqrt(k))
+    _suite(GpuOracle(tile=1, dtype=torch.float64), oracle, L0, k, rng.normal(0, 1, (B, n)), rng, dtype=torch.float64)
+
