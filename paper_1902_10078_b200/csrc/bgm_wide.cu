@@ -438,11 +438,18 @@ __global__ void k_subset_check(SubP<T> C, Geo G) {
   const ix t = blockIdx.x * ix(blockDim.x) + threadIdx.x;
   const ix unit = t / K;
   const int c = int(t % K);
-  if (unit >= G.batch * G.nseg) return;
-  const int p = int(unit % G.nseg);
-  if (p + 1 >= G.nseg) return;
-  const ix b = unit / G.nseg;
-  const ix e = ix(p + 1) * G.seg, col = e + c;
+  ix b, e;
+  if (G.span_rows > 0) {  // unit = side slot (CTA, piece): pieces that end inside a matrix burned in from below
+    ix s0;
+    if (!span_piece(G, unit / G.span_kmax, int(unit % G.span_kmax), b, s0, e) || e >= G.n) return;
+  } else {
+    if (unit >= G.batch * G.nseg) return;
+    const int p = int(unit % G.nseg);
+    if (p + 1 >= G.nseg) return;
+    b = unit / G.nseg;
+    e = ix(p + 1) * G.seg;
+  }
+  const ix col = e + c;
   if (col >= G.n) return;
   const T* sd = C.side + (unit * K + c) * (K + 1);
   double sc = 0.0;
@@ -2677,6 +2684,17 @@ template <int K, int NW>
 __global__ void __launch_bounds__(32 * NW) k_subset_mw(SubP<double> C, Geo G) {
   extern __shared__ __align__(16) unsigned char smraw[];
   TakMwSmem<K, NW>& sm = *reinterpret_cast<TakMwSmem<K, NW>*>(smraw);
+  if (G.span_rows > 0) {  // row spans (see Geo); the sweep runs upwards: a piece that ends inside a matrix
+    for (int k = 0; k < G.span_kmax; ++k) {  // burns in from below its end
+      ix b, s, e;
+      if (!span_piece(G, blockIdx.x, k, b, s, e)) continue;  // uniform across the CTA
+      const ix jend = e + G.burn < G.n ? e + G.burn : G.n;
+      const ix slot = ix(blockIdx.x) * G.span_kmax + k;
+      subset_mw_unit<K, NW>(C, b, G.n, s, e, jend, e < G.n ? C.side + slot * ix(K) * (K + 1) : nullptr, sm);
+      __syncthreads();  // the next piece reuses the shared windows
+    }
+    return;
+  }
   const ix unit = blockIdx.x;
   const ix b = unit / G.nseg;
   const int p = int(unit % G.nseg);
@@ -3054,8 +3072,17 @@ bool run_subset_mw(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* 
   if (seg < K) seg = (K + 7) / 8 * 8;
   G.seg = seg;
   G.nseg = int((G.n + seg - 1) / seg);
-  const ix units = G.batch * G.nseg;
-  const size_t side_bytes = sizeof(double) * size_t(units) * K * (K + 1);
+  ix units = G.batch * G.nseg, slots = units;
+  // Row spans are opt-in here (BGM_WIDE_SPAN_SUBSET=1, or a forced CTA count): alone the kernel gains
+  // 14% (k = 128: 5.79 -> 4.96 ms), but in the config-4 suite it runs beside two other stream lanes that
+  // were using the SMs its 128 CTAs leave free, and the step got 0.5 ms slower.
+  const char* sv = std::getenv("BGM_WIDE_SPAN_SUBSET");
+  const bool want_span = (sv && sv[0] == '1') || std::getenv("BGM_WIDE_SPAN_CTAS") != nullptr;
+  if (g_segment_rows <= 0 && want_span && span_rows(G, ix(sms) * per, 2 * ix(G.burn))) {
+    units = (G.batch * G.n8 + G.span_rows - 1) / G.span_rows;
+    slots = units * G.span_kmax;
+  }
+  const size_t side_bytes = sizeof(double) * size_t(slots) * K * (K + 1);
   char* ws = nullptr;
   if (scratch_alloc(reinterpret_cast<void**>(&ws), side_bytes + 12 * size_t(G.batch) + 64, s) != cudaSuccess)
     return false;
@@ -3073,7 +3100,7 @@ bool run_subset_mw(const bgm_band& l, const bgm_band& sb, int32_t* st, int64_t* 
   }
   {
     timing::Scope ts("wide_subset_check", s);
-    k_subset_check<double, K><<<blocks_for(units * K, 128), 128, 0, s>>>(C, G);
+    k_subset_check<double, K><<<blocks_for(slots * K, 128), 128, 0, s>>>(C, G);
   }
   {
     timing::Scope ts("wide_subset_repair", s);
